@@ -1,0 +1,264 @@
+/*
+ * volpg_b200.h — C ABI of libvolpg_b200.so, the sm_100a implementation of the
+ * path-graph hot path of arXiv 2404.11894 ("Rendering Participating Media
+ * Using Path Graphs").
+ *
+ * The reference (`volpg` 0.1.0, /root/reference/pkg/src/volpg) is a pure
+ * Python/numba package with no FFI of its own; its boundary is the Python API
+ * re-exported at pathgraph/__init__.py:1-21 and transport/__init__.py:1-15.
+ * Each entry point below is the native half of one of those Python calls; the
+ * Python half lives in paper_2404_11894_b200/{pathgraph,transport}/ and is
+ * bound with ctypes (paper_2404_11894_b200/_native.py).  The binding a
+ * maintainer of the reference would add is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Return value: 0 on success, a negative VPG_E* code on failure; the
+ *    message is available from vpg_last_error() (thread-local).
+ *  - Pointers documented "device" are CUDA device pointers (the Python layer
+ *    passes torch tensor storage); "host" pointers are ordinary memory.
+ *  - Every call that launches work takes a `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and is stream-ordered.  Calls that
+ *    return host data synchronise that stream before returning.
+ *  - Layouts follow the reference's RecordSoA / PathSoA exactly
+ *    (transport/records.py:27-64): vec3 fields are row-major (n, 3) float64.
+ *  - No torch types cross this boundary.
+ */
+#ifndef VOLPG_B200_H
+#define VOLPG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPG_ABI_VERSION 1
+
+/* error codes (mapped to the reference's exception types by the Python layer) */
+#define VPG_OK 0
+#define VPG_EINVAL -1    /* ValueError  (clustering.py:34-35, tracer.py:86-87,111-112) */
+#define VPG_ECUDA -2     /* RuntimeError: CUDA failure or no device                    */
+#define VPG_EDIVERGED -3 /* SolveDivergence (solve.py:28-29,84-90)                     */
+#define VPG_ENOMEM -4    /* MemoryError                                                */
+#define VPG_ELIMIT -5    /* ValueError: input exceeds a compiled limit                 */
+
+/* ---------------------------------------------------------------- basics */
+int vpg_abi_version(void);
+const char* vpg_last_error(void);
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t vpg_launch_count(void);
+/* sizeof() of the ABI structs, for binding self-checks:
+ * 0 vpg_pcg64, 1 vpg_records, 2 vpg_paths, 3 vpg_graph_info, 4 vpg_scene, 5 vpg_trace_cfg */
+size_t vpg_struct_size(int32_t which);
+
+/* ------------------------------------------------- numpy Generator replica
+ * Bit-exact replica of numpy.random.Generator(PCG64) for the two calls the
+ * reference's clustering makes: Generator.choice(n, m, replace=False)
+ * (clustering.py:51 -> numpy tail-shuffle / Floyd branches) and
+ * Generator.integers(k) (clustering.py:68).  The state is the one numpy
+ * exposes as `bit_generator.state`; the Python layer copies it in and back
+ * so a caller's Generator advances exactly as with the reference. */
+typedef struct vpg_pcg64 {
+  uint64_t state_hi, state_lo; /* 128-bit LCG state */
+  uint64_t inc_hi, inc_lo;     /* 128-bit increment (odd) */
+  int32_t has_uint32;          /* buffered upper half available */
+  uint32_t uinteger;           /* the buffered half */
+} vpg_pcg64;
+
+/* out[0..m) = Generator.choice(n, m, replace=False) (host memory). */
+int vpg_rng_choice(vpg_pcg64* rng, int64_t n, int64_t m, int64_t* out);
+/* out[i] = Generator.integers(k) for i in [0, count) (host memory). */
+int vpg_rng_integers(vpg_pcg64* rng, int64_t k, int64_t count, int64_t* out);
+
+/* Host split loop of clustering.py:58-85 (exposed for tests; the device build
+ * calls the same code).  Input: groups as CSR over ascending member indices
+ * into `pos` (n_pos x 3, float64, host), their centers, the oversize bound
+ * `max_size` (= 2K).  Output: the final group list in the reference's order
+ * (original groups first, split-off groups appended), as CSR written to
+ * caller buffers of capacity `cap_groups` / `n_members`. */
+int vpg_split_groups(vpg_pcg64* rng, const double* pos, int64_t n_groups,
+                     const int64_t* grp_off, const int64_t* grp_members,
+                     const int64_t* grp_center, int64_t max_size,
+                     int64_t cap_groups, int64_t* out_n_groups,
+                     int64_t* out_off, int64_t* out_members, int64_t* out_center);
+
+/* ------------------------------------------------------- vertex records
+ * Device SoA mirroring RecordSoA (records.py:75-126).  `n` records, stored
+ * contiguous per path and depth-ordered (records.py:3-5). */
+typedef struct vpg_records {
+  int64_t n;
+  double* pos;               /* (n,3) */
+  double* omega_out;         /* (n,3) toward previous vertex */
+  double* normal;            /* (n,3) oriented shading normal (surface) */
+  double* coeff;             /* (n,3) sigma_s(x) or albedo */
+  double* g;                 /* (n)   HG anisotropy (volume) */
+  double* phase_dir;         /* (n,3) */
+  double* pdf_phase;         /* (n)   */
+  double* pdf_emit_at_phase; /* (n)   */
+  double* emit_dir;          /* (n,3) */
+  double* pdf_emit;          /* (n)   */
+  double* d_emit;            /* (n,3) raw NEE radiance */
+  double* d_phase;           /* (n,3) raw phase-hit radiance */
+  double* i_pt;              /* (n,3) path-traced incoming indirect */
+  double* w_cont;            /* (n,3) Tr/p_t of the arriving segment */
+  uint8_t* kind;             /* (n)   0 volume, 1 surface */
+  uint8_t* emit_delta;       /* (n)   */
+  int32_t* class_id;         /* (n)   medium or surface index */
+  int64_t* path_idx;         /* (n)   */
+  int32_t* depth;            /* (n)   */
+} vpg_records;
+
+/* Device SoA mirroring PathSoA (records.py:144-176). */
+typedef struct vpg_paths {
+  int64_t n;
+  int64_t* pixel_idx;
+  int64_t* rec_start;
+  int32_t* rec_count;
+  double* cam_weight;    /* (n,3) */
+  double* d_cam;         /* (n,3) */
+  double* direct0;       /* (n,3) */
+  double* direct0_nee;   /* (n,3) */
+  double* direct0_phase; /* (n,3) */
+  double* extra_direct;  /* (n,3) */
+  double* pt_estimate;   /* (n,3) */
+} vpg_paths;
+
+/* ------------------------------------------------------------ path graph
+ * Replaces build_graph (graph.py:56-69) = cluster_points (clustering.py:28-148)
+ * + RecordSoA.next_index (records.py:128-140) + compute_marginals
+ * (graph.py:94-120) + _build_operators (graph.py:123-168).  The graph keeps
+ * its device buffers (cluster-major permutation, dense per-cluster kernel
+ * blocks, solve vectors) until vpg_graph_free. */
+typedef struct vpg_graph vpg_graph;
+
+typedef struct vpg_graph_info {
+  int64_t n_records;
+  int64_t n_clusters;
+  int64_t nnz;         /* sum over clusters of size^2 (= w_indirect.nnz) */
+  int64_t n_classes;
+  int64_t n_splits;    /* split-loop iterations performed (clustering.py:58-85) */
+  int64_t n_fallback;  /* points resolved by the exact global search (clustering.py:142-147) */
+  double build_ms[8];  /* per-stage device/host timings of the last build (diagnostic) */
+} vpg_graph_info;
+
+/* flags for vpg_graph_build */
+#define VPG_BUILD_TIMINGS 1       /* record per-stage timings (adds stream syncs) */
+#define VPG_BUILD_CLUSTERS_ONLY 2 /* cluster_points only: reads pos, kind, class_id */
+
+/* Cluster the records (class keys kind<<32|class_id, graph.py:59), draw
+ * centers with `rng` (advanced in place), and build the aggregation operators.
+ * `cluster_size` is K (ValueError if < 1).  The graph borrows `rec`'s device
+ * arrays (solve, splat and exports read them): keep them alive and unchanged
+ * until vpg_graph_free. */
+int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng,
+                    int32_t flags, void* stream, vpg_graph** out);
+int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out);
+int vpg_graph_free(vpg_graph* g);
+
+/* Host exports (each synchronises `stream`).  All arrays are in record order.
+ * cluster_id: (n) int64; cl_off: (n_clusters+1) int64 offsets into
+ * cl_members: (n) int64 member record indices, ascending within a cluster;
+ * cl_center: (n_clusters) int64 center record index (clustering.py:23-25). */
+int vpg_graph_export_clusters(const vpg_graph* g, int64_t* cluster_id, int64_t* cl_off,
+                              int64_t* cl_members, int64_t* cl_center, void* stream);
+/* phat_* : (n) float64 marginals (graph.py:94-120). */
+int vpg_graph_export_marginals(const vpg_graph* g, double* phat_ind, double* phat_dir_phase,
+                               double* phat_dir_emit, void* stream);
+/* w_indirect as CSR (graph.py:167): indptr (n+1), indices (nnz), data (nnz);
+ * d_bar (n,3) float64 (graph.py:168). Any pointer may be NULL to skip it. */
+int vpg_graph_export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices,
+                               double* data, double* d_bar, void* stream);
+
+/* ----------------------------------------------------------------- solve
+ * Replaces solve (solve.py:64-98): device-resident fixed point
+ * I <- P A+ I + P Ao D with the residual, tol break and 3-growth divergence
+ * rule evaluated on the device.  residuals: host, capacity `iterations`.
+ * Returns VPG_EDIVERGED (after filling residuals/performed) on divergence. */
+int vpg_solve(vpg_graph* g, int32_t iterations, double tol, double* residuals,
+              int32_t* performed, void* stream);
+/* incoming, i_bar: (n,3) float64 host, record order (SolveResult fields). */
+int vpg_solve_export(const vpg_graph* g, double* incoming, double* i_bar, void* stream);
+
+/* aggregate_indirect (operators.py:17-19): out = coeff * (W @ incoming).
+ * propagate / propagate_linear (operators.py:27-47): out[r] = w_cont[r+1] *
+ * l_bar[r+1] on continuation edges, i_pt (linear=0) or 0 (linear=1) elsewhere.
+ * All (n,3) float64 device arrays in record order. */
+int vpg_aggregate_indirect(const vpg_graph* g, const double* incoming, double* out, void* stream);
+int vpg_propagate(const vpg_records* rec, const double* l_bar, double* out, int32_t linear,
+                  void* stream);
+
+/* ----------------------------------------------------------------- splat
+ * Replaces splat_output (solve.py:101-132). direct_mode: 0 = direct0,
+ * 1 = extra_direct, 2 = aggregated D-bar.  image: (height,width,3) float64
+ * device.  Uses the last solve's i_bar. */
+#define VPG_DIRECT_PT 0
+#define VPG_DIRECT_EXTRA 1
+#define VPG_DIRECT_AGGREGATED 2
+int vpg_splat(const vpg_graph* g, const vpg_paths* paths, int32_t width, int32_t height,
+              int32_t spp, int32_t direct_mode, double* image, void* stream);
+/* splat_pt_image (records.py:259-265): per-pixel mean of pt_estimate. */
+int vpg_splat_pt(const vpg_paths* paths, int32_t width, int32_t height, int32_t spp,
+                 double* image, void* stream);
+
+/* ---------------------------------------------------------------- tracer
+ * Packed scene (flatten.py:87-195 equivalent), passed by value to kernels. */
+#define VPG_MAX_SURF 32
+#define VPG_MAX_EMIT 16
+#define VPG_MAX_MED 8
+typedef struct vpg_scene {
+  int32_t n_surf, n_emit, n_med, width, height, _pad0;
+  int32_t surf_type[VPG_MAX_SURF];  /* 0 sphere, 1 box, 2 quad */
+  int32_t mat_type[VPG_MAX_SURF];   /* 0 lambertian, 1 black, 2 emitter */
+  int32_t emitter_id[VPG_MAX_SURF];
+  double surf_params[VPG_MAX_SURF][9];
+  double albedo[VPG_MAX_SURF][3];
+  int32_t em_type[VPG_MAX_EMIT];    /* 0 point, 1 area, 2 directional */
+  double em_value[VPG_MAX_EMIT][3];
+  double em_pos[VPG_MAX_EMIT][3];   /* point position / unit travel direction */
+  double em_quad[VPG_MAX_EMIT][9];
+  double em_normal[VPG_MAX_EMIT][3];
+  double em_area[VPG_MAX_EMIT];
+  int32_t med_kind[VPG_MAX_MED];    /* 0 homogeneous, 1 grid */
+  int32_t grid_dims[VPG_MAX_MED][3];/* nx, ny, nz */
+  double med_sigma_t[VPG_MAX_MED][3];
+  double med_sigma_s[VPG_MAX_MED][3];
+  double med_g[VPG_MAX_MED];
+  double med_bounds[VPG_MAX_MED][6];
+  double med_majorant[VPG_MAX_MED];
+  double med_scale[VPG_MAX_MED];
+  int64_t grid_offset[VPG_MAX_MED];
+  const float* grid_data;           /* device, concatenated (z,y,x) float32 volumes */
+  double cam[15];                   /* origin, forward, right, up, tan_half, W, H */
+} vpg_scene;
+
+typedef struct vpg_trace_cfg {
+  int32_t spp;
+  int32_t max_depth;
+  int32_t rr_start;
+  int32_t _pad;
+  double rr_floor;
+  int64_t seed;
+  int64_t path_begin; /* first path id of this launch (multi-GPU row partition) */
+  int64_t path_count; /* number of paths (global ids path_begin..) */
+} vpg_trace_cfg;
+
+/* Record-free render (render_image_kernel, kernels.py:433-460): image
+ * (height,width,3) float64 device. */
+int vpg_trace_image(const vpg_scene* scene, const vpg_trace_cfg* cfg, double* image, void* stream);
+/* Pass 1 (count_records_kernel, kernels.py:463-479): counts (path_count) int64
+ * device, plus the path-table estimates. */
+int vpg_trace_count(const vpg_scene* scene, const vpg_trace_cfg* cfg, int64_t* counts,
+                    const vpg_paths* paths, void* stream);
+/* Pass 2 (fill_records_kernel, kernels.py:482-496): writes records at
+ * paths->rec_start offsets (relative to `rec`), and the path table. */
+int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* rec,
+                   const vpg_paths* paths, void* stream);
+/* extra_direct_kernel (kernels.py:499-553). */
+int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
+                     int64_t seed, int32_t n_extra, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLPG_B200_H */

@@ -1,0 +1,834 @@
+// Path-graph clustering on the device, bit-exact with the reference.
+//
+// Reference: pathgraph/clustering.py:28-148 (+ graph.py:59-60 for the class
+// keys and RNG).  Per compatibility class (ascending key kind<<32|class_id):
+//   1. host: m = ceil(n/K) centers = Generator.choice(n, m)          (:51)
+//   2. device: uniform grid with the reference's lo/cell (:102-106); centers
+//      radix-sorted by cell key into an open-addressing cell table; one
+//      thread per point scans the 27-cell neighbourhood with fp64 distances
+//      rounded like numpy ((dx*dx+dy*dy)+dz*dz, no FMA) and lowest-center
+//      ties (:121-137)
+//   3. device: points with an empty neighbourhood or best >= cell fall back to
+//      the exact global argmin (:129-131,138-147), one warp per point
+//   4. device: stable radix sort (center, record) = groups in ascending record
+//      order (:55)
+//   5. host: LIFO split loop over groups > 2K (:58-85) with the same RNG
+//   6. device: clusters numbered in group order, skipping empty groups,
+//      continuing across classes (:87-93); cluster-major permutation.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "graph.cuh"
+#include "host_rng.hpp"
+
+namespace vpg {
+namespace {
+
+constexpr uint64_t kEmpty = 0xFFFFFFFFFFFFFFFFull;
+constexpr int kMaxClasses = 256;
+constexpr int kSlotsPerKind = 65536;
+
+struct CellEntry {
+  unsigned long long key;
+  int32_t start, end;
+};
+
+// order-preserving unsigned encoding of a double (for atomic min/max)
+__host__ __device__ inline uint64_t order_key(double x) {
+#ifdef __CUDA_ARCH__
+  uint64_t b = uint64_t(__double_as_longlong(x));
+#else
+  uint64_t b;
+  memcpy(&b, &x, 8);
+#endif
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+inline double order_key_inv(uint64_t k) {
+  uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double x;
+  memcpy(&x, &b, 8);
+  return x;
+}
+
+__device__ __forceinline__ double dist2_exact(double ax, double ay, double az, double bx,
+                                              double by, double bz) {
+  const double dx = __dsub_rn(ax, bx), dy = __dsub_rn(ay, by), dz = __dsub_rn(az, bz);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+__device__ __forceinline__ long long cell_coord(double p, double lo, double cell) {
+  return (long long)floor(__ddiv_rn(__dsub_rn(p, lo), cell));
+}
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct GridParams {
+  double lo[3];
+  double cell;
+  double slack;        // bound on fp error of a cell index, in cells
+  long long dims[3];   // cells per axis covering the class bounding box
+  long long max_dim;
+  int packed;  // 1: key = packed (x+1,y+1,z+1) in 21 bits each; 0: hashed triple
+  int m;       // centers in this class
+  uint64_t table_mask;
+};
+
+__device__ __forceinline__ uint64_t cell_key(const GridParams& gp, long long x, long long y,
+                                             long long z) {
+  if (gp.packed)
+    return (uint64_t(x + 1) << 42) | (uint64_t(y + 1) << 21) | uint64_t(z + 1);
+  uint64_t h = mix64(uint64_t(x) * 0x9E3779B97F4A7C15ull ^ mix64(uint64_t(y) + 0x632BE59BD9B4E019ull) ^
+                     mix64(uint64_t(z) * 0xD1342543DE82EF95ull + 7));
+  return h & 0x7FFFFFFFFFFFFFFFull;
+}
+
+__device__ __forceinline__ uint64_t table_slot(uint64_t key, uint64_t mask) {
+  return mix64(key) & mask;
+}
+
+// ------------------------------------------------------------ kernels
+
+__global__ void k_class_bitmap(const uint8_t* __restrict__ kind, const int32_t* __restrict__ cls,
+                               int64_t n, uint32_t* bitmap, int32_t* err) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int k = kind[r];
+    const int c = cls[r];
+    if (k > 1 || c < 0 || c >= kSlotsPerKind) {
+      atomicExch(err, 1);
+      continue;
+    }
+    const uint32_t slot = uint32_t(k * kSlotsPerKind + c);
+    const unsigned peers = __match_any_sync(__activemask(), slot);
+    if ((__ffs(peers) - 1) == int(threadIdx.x & 31)) atomicOr(&bitmap[slot >> 5], 1u << (slot & 31));
+  }
+}
+
+// Per-class counts and position bounds; also the class index of each record.
+__global__ void k_class_stats(const uint8_t* __restrict__ kind, const int32_t* __restrict__ cls,
+                              const double* __restrict__ pos, int64_t n,
+                              const uint32_t* __restrict__ slots, int n_cls,
+                              uint8_t* __restrict__ cls_idx, unsigned long long* counts,
+                              unsigned long long* mins, unsigned long long* maxs) {
+  __shared__ uint32_t s_slots[kMaxClasses];
+  __shared__ unsigned long long s_cnt[kMaxClasses], s_mn[kMaxClasses * 3], s_mx[kMaxClasses * 3];
+  for (int i = threadIdx.x; i < n_cls; i += blockDim.x) {
+    s_slots[i] = slots[i];
+    s_cnt[i] = 0;
+    for (int a = 0; a < 3; ++a) {
+      s_mn[i * 3 + a] = ~0ull;
+      s_mx[i * 3 + a] = 0ull;
+    }
+  }
+  __syncthreads();
+  int cur = -1;
+  unsigned long long cnt = 0, mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+  auto flush = [&]() {
+    if (cur < 0 || cnt == 0) return;
+    atomicAdd(&s_cnt[cur], cnt);
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&s_mn[cur * 3 + a], mn[a]);
+      atomicMax(&s_mx[cur * 3 + a], mx[a]);
+      mn[a] = ~0ull;
+      mx[a] = 0;
+    }
+    cnt = 0;
+  };
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t slot = uint32_t(kind[r]) * kSlotsPerKind + uint32_t(cls[r]);
+    int lo = 0, hi = n_cls - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_slots[mid] < slot) lo = mid + 1; else hi = mid;
+    }
+    if (lo != cur) {
+      flush();
+      cur = lo;
+    }
+    if (cls_idx) cls_idx[r] = uint8_t(lo);
+    ++cnt;
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t k = order_key(pos[r * 3 + a]);
+      mn[a] = mn[a] < k ? mn[a] : k;
+      mx[a] = mx[a] > k ? mx[a] : k;
+    }
+  }
+  flush();
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_cls; i += blockDim.x) {
+    if (s_cnt[i] == 0) continue;
+    atomicAdd(&counts[i], s_cnt[i]);
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&mins[i * 3 + a], s_mn[i * 3 + a]);
+      atomicMax(&maxs[i * 3 + a], s_mx[i * 3 + a]);
+    }
+  }
+}
+
+__global__ void k_iota(int32_t* out, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = int32_t(i);
+}
+
+__device__ __forceinline__ int64_t class_row(const int32_t* rows, int64_t row_off, int64_t i) {
+  return rows ? int64_t(rows[row_off + i]) : row_off + i;
+}
+
+// Center positions, record ids and cell keys.
+__global__ void k_center_setup(const int32_t* __restrict__ local, int m, const int32_t* rows,
+                               int64_t row_off, const double* __restrict__ pos, GridParams gp,
+                               double* __restrict__ cpos, int32_t* __restrict__ crec,
+                               unsigned long long* __restrict__ keys, int32_t* __restrict__ ids) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    const int64_t r = class_row(rows, row_off, local[j]);
+    const double x = pos[r * 3], y = pos[r * 3 + 1], z = pos[r * 3 + 2];
+    cpos[j * 3] = x;
+    cpos[j * 3 + 1] = y;
+    cpos[j * 3 + 2] = z;
+    crec[j] = int32_t(r);
+    keys[j] = cell_key(gp, cell_coord(x, gp.lo[0], gp.cell), cell_coord(y, gp.lo[1], gp.cell),
+                       cell_coord(z, gp.lo[2], gp.cell));
+    ids[j] = j;
+  }
+}
+
+// Sorted centers -> packed positions; run heads inserted into the cell table.
+__global__ void k_center_table(const unsigned long long* __restrict__ skeys,
+                               const int32_t* __restrict__ sids, const double* __restrict__ cpos,
+                               int m, GridParams gp, double4* __restrict__ spos,
+                               CellEntry* table) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int j = sids[i];
+    spos[i] = make_double4(cpos[j * 3], cpos[j * 3 + 1], cpos[j * 3 + 2], __longlong_as_double((long long)j));
+    const unsigned long long key = skeys[i];
+    if (i == 0 || skeys[i - 1] != key) {
+      uint64_t slot = table_slot(key, gp.table_mask);
+      while (true) {
+        const unsigned long long prev = atomicCAS(&table[slot].key, kEmpty, key);
+        if (prev == kEmpty) {
+          table[slot].start = i;
+          break;
+        }
+        slot = (slot + 1) & gp.table_mask;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ const CellEntry* table_find(const CellEntry* table, uint64_t key,
+                                                       uint64_t mask) {
+  uint64_t slot = table_slot(key, mask);
+  while (true) {
+    const CellEntry* e = &table[slot];
+    const unsigned long long k = e->key;
+    if (k == key) return e;
+    if (k == kEmpty) return nullptr;
+    slot = (slot + 1) & mask;
+  }
+}
+
+__global__ void k_center_table_ends(const unsigned long long* __restrict__ skeys, int m,
+                                    GridParams gp, CellEntry* table) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long key = skeys[i];
+    if (i == m - 1 || skeys[i + 1] != key) {
+      CellEntry* e = const_cast<CellEntry*>(table_find(table, key, gp.table_mask));
+      e->end = i + 1;
+    }
+  }
+}
+
+struct Best {
+  double d2;
+  int j;
+};
+__device__ __forceinline__ void best_update(Best& b, double d2, int j) {
+  if (d2 < b.d2 || (d2 == b.d2 && j < b.j)) {
+    b.d2 = d2;
+    b.j = j;
+  }
+}
+
+// Scan the centers of one cell (key) into `b`.
+__device__ __forceinline__ void scan_cell(const GridParams& gp, const CellEntry* table,
+                                          const double4* __restrict__ spos, long long cx,
+                                          long long cy, long long cz, double px, double py,
+                                          double pz, Best& b) {
+  const CellEntry* e = table_find(table, cell_key(gp, cx, cy, cz), gp.table_mask);
+  if (!e) return;
+  const int start = e->start, end = e->end;
+  for (int t = start; t < end; ++t) {
+    const double4 c = spos[t];
+    if (!gp.packed) {  // hashed keys: confirm the cell really matches
+      if (cell_coord(c.x, gp.lo[0], gp.cell) != cx || cell_coord(c.y, gp.lo[1], gp.cell) != cy ||
+          cell_coord(c.z, gp.lo[2], gp.cell) != cz)
+        continue;
+    }
+    best_update(b, dist2_exact(px, py, pz, c.x, c.y, c.z), int(__double_as_longlong(c.w)));
+  }
+}
+
+// One thread per point: the reference's 27-cell candidate argmin.
+__global__ void k_assign(const int32_t* rows, int64_t row_off, int64_t n,
+                         const double* __restrict__ pos, GridParams gp,
+                         const CellEntry* __restrict__ table, const double4* __restrict__ spos,
+                         int32_t* __restrict__ assign, int32_t* __restrict__ fb_list,
+                         int32_t* fb_count) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = class_row(rows, row_off, i);
+    const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
+    const long long cx = cell_coord(px, gp.lo[0], gp.cell);
+    const long long cy = cell_coord(py, gp.lo[1], gp.cell);
+    const long long cz = cell_coord(pz, gp.lo[2], gp.cell);
+    Best b{INFINITY, 0x7FFFFFFF};
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz)
+          scan_cell(gp, table, spos, cx + dx, cy + dy, cz + dz, px, py, pz, b);
+    if (b.j == 0x7FFFFFFF || !(__dsqrt_rn(b.d2) < gp.cell)) {
+      fb_list[atomicAdd(fb_count, 1)] = int32_t(i);
+      assign[i] = -1;
+    } else {
+      assign[i] = b.j;
+    }
+  }
+}
+
+__device__ __forceinline__ void warp_best(Best& b) {
+  for (int off = 16; off; off >>= 1) {
+    const double od = __shfl_xor_sync(0xFFFFFFFFu, b.d2, off);
+    const int oj = __shfl_xor_sync(0xFFFFFFFFu, b.j, off);
+    best_update(b, od, oj);
+  }
+}
+
+// Exact global argmin (ties -> lowest center) for the points the reference
+// sends to its brute-force scan (clustering.py:129-147).  One warp per point
+// grows Chebyshev shells of grid cells around the point's cell; after shell R
+// every unvisited center is farther than (R - slack) * cell, so the search
+// stops as soon as the best squared distance is below that bound (with a
+// relative margin covering fp rounding of the cell indices and distances).
+// When the next shell would hold more cells than there are centers the warp
+// scans all centers instead.  Either way the result equals np.argmin over all
+// centers.
+__global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
+                                  const double* __restrict__ pos, GridParams gp,
+                                  const CellEntry* __restrict__ table,
+                                  const double4* __restrict__ spos,
+                                  const int32_t* __restrict__ fb_list, const int32_t* fb_count,
+                                  int32_t* __restrict__ assign) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *fb_count;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
+    const int64_t i = fb_list[w];
+    const int64_t r = class_row(rows, row_off, i);
+    const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
+    const long long cx = cell_coord(px, gp.lo[0], gp.cell);
+    const long long cy = cell_coord(py, gp.lo[1], gp.cell);
+    const long long cz = cell_coord(pz, gp.lo[2], gp.cell);
+    Best b{INFINITY, 0x7FFFFFFF};
+    if (lane < 27)
+      scan_cell(gp, table, spos, cx + lane / 9 - 1, cy + (lane / 3) % 3 - 1, cz + lane % 3 - 1,
+                px, py, pz, b);
+    warp_best(b);
+    for (int R = 1;; ++R) {
+      const double lim = (double(R) - gp.slack) * gp.cell;
+      if (b.j != 0x7FFFFFFF && b.d2 < lim * lim * (1.0 - 1e-9)) break;
+      const long long side = 2LL * R + 3;
+      const long long cube = side * side * side;
+      const long long shell = cube - (side - 2) * (side - 2) * (side - 2);
+      if (shell > gp.m || R > gp.max_dim + 1) {
+        for (int t = lane; t < gp.m; t += 32) {
+          const double4 c = spos[t];
+          best_update(b, dist2_exact(px, py, pz, c.x, c.y, c.z), int(__double_as_longlong(c.w)));
+        }
+        warp_best(b);
+        break;
+      }
+      const int Rn = R + 1;
+      for (long long t = lane; t < cube; t += 32) {
+        const int dx = int(t / (side * side)) - Rn;
+        const int dy = int((t / side) % side) - Rn;
+        const int dz = int(t % side) - Rn;
+        if (max(abs(dx), max(abs(dy), abs(dz))) != Rn) continue;
+        const long long nx = cx + dx, ny = cy + dy, nz = cz + dz;
+        if (nx < 0 || ny < 0 || nz < 0 || nx >= gp.dims[0] || ny >= gp.dims[1] ||
+            nz >= gp.dims[2])
+          continue;  // no center lives outside the class bounding grid
+        scan_cell(gp, table, spos, nx, ny, nz, px, py, pz, b);
+      }
+      warp_best(b);
+    }
+    if (lane == 0) assign[i] = b.j;
+  }
+}
+
+__global__ void k_group_values(const int32_t* rows, int64_t row_off, int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = int32_t(class_row(rows, row_off, i));
+}
+
+__global__ void k_histogram(const int32_t* __restrict__ assign, int64_t n, int32_t* counts) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&counts[assign[i]], 1);
+}
+
+// Gather members (record id + position) of the oversize groups for the host.
+__global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
+                                  const int64_t* __restrict__ seg, int n_seg,
+                                  const double* __restrict__ pos, int32_t* __restrict__ out_rec,
+                                  double* __restrict__ out_pos) {
+  // seg[k*3+0] = source offset, seg[k*3+1] = count, seg[k*3+2] = destination offset
+  for (int k = blockIdx.x; k < n_seg; k += gridDim.x) {
+    const int64_t src = seg[k * 3], cnt = seg[k * 3 + 1], dst = seg[k * 3 + 2];
+    for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int32_t r = grp_rec[src + t];
+      out_rec[dst + t] = r;
+      out_pos[(dst + t) * 3] = pos[int64_t(r) * 3];
+      out_pos[(dst + t) * 3 + 1] = pos[int64_t(r) * 3 + 1];
+      out_pos[(dst + t) * 3 + 2] = pos[int64_t(r) * 3 + 2];
+    }
+  }
+}
+
+__global__ void k_square_sizes(const int32_t* __restrict__ size, int64_t m,
+                               int64_t* __restrict__ sq) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k <= m;
+       k += int64_t(gridDim.x) * blockDim.x)
+    sq[k] = k < m ? int64_t(size[k]) * size[k] : 0;
+}
+
+// Cluster-major permutation: warp per cluster copies its member list.
+__global__ void k_fill_perm(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ cl_src,
+                            int64_t m, const int32_t* __restrict__ grp_rec,
+                            const int32_t* __restrict__ split_rec, int32_t* __restrict__ perm,
+                            int32_t* __restrict__ clpos, int32_t* __restrict__ cluster_id) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < m; k += warps) {
+    const int32_t q0 = cl_off[k], q1 = cl_off[k + 1];
+    const int64_t src = cl_src[k];
+    const int32_t* from = src >= 0 ? grp_rec + src : split_rec + (-1 - src);
+    for (int32_t t = lane; t < q1 - q0; t += 32) {
+      const int32_t r = from[t];
+      perm[q0 + t] = r;
+      clpos[r] = q0 + t;
+      cluster_id[r] = int32_t(k);
+    }
+  }
+}
+
+template <class T>
+void to_host(std::vector<T>& h, const T* d, size_t n, cudaStream_t s) {
+  h.resize(n);
+  if (n) VPG_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+template <class T>
+void to_device(T* d, const std::vector<T>& h, cudaStream_t s) {
+  if (!h.empty())
+    VPG_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+int bits_for(uint64_t max_value) {
+  int b = 1;
+  while (b < 64 && (max_value >> b)) ++b;
+  return b;
+}
+
+struct StageClock {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0;
+  double* slots;
+  StageClock(bool enabled, cudaStream_t st, double* out) : on(enabled), s(st), slots(out) {
+    if (on) {
+      cudaStreamSynchronize(s);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(int slot) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto t1 = std::chrono::steady_clock::now();
+    slots[slot] += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+  }
+};
+
+template <class F>
+void cub_call(F&& f, cudaStream_t s) {
+  size_t bytes = 0;
+  VPG_CUDA(f(nullptr, bytes));
+  DBuf<char> tmp(bytes, s);
+  VPG_CUDA(f(tmp.get(), bytes));
+  count_launch(2);
+}
+
+}  // namespace
+
+void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng_state,
+                    bool timings, cudaStream_t s) {
+  const int64_t n = rec.n;
+  VPG_REQUIRE(K >= 1, VPG_EINVAL, "cluster size K must be >= 1");
+  VPG_REQUIRE(n < (int64_t(1) << 31) - 1, VPG_ELIMIT, "more than 2^31-2 records per device");
+  g->n = n;
+  g->K = K;
+  for (double& t : g->info.build_ms) t = 0.0;
+  StageClock clk(timings, s, g->info.build_ms);
+  Pcg64 rng(*rng_state);
+  const int block = 256;
+
+  g->perm.alloc(n, s);
+  g->clpos.alloc(n, s);
+  g->cluster_id.alloc(n, s);
+  if (n == 0) {
+    g->m = 0;
+    g->cl_off.alloc(1, s);
+    g->w_off.alloc(1, s);
+    g->cl_center.alloc(1, s);
+    VPG_CUDA(cudaMemsetAsync(g->cl_off.get(), 0, sizeof(int32_t), s));
+    VPG_CUDA(cudaMemsetAsync(g->w_off.get(), 0, sizeof(int64_t), s));
+    rng.store(rng_state);
+    return;
+  }
+
+  // ---- classes (np.unique order of kind<<32 | class_id)
+  const int nbits_words = 2 * kSlotsPerKind / 32;
+  DBuf<uint32_t> bitmap(nbits_words + 1, s);
+  VPG_CUDA(cudaMemsetAsync(bitmap.get(), 0, bitmap.bytes(), s));
+  int32_t* d_err = reinterpret_cast<int32_t*>(bitmap.get() + nbits_words);
+  VPG_LAUNCH(k_class_bitmap, grid_for(n, block), block, 0, s, rec.kind, rec.class_id, n,
+             bitmap.get(), d_err);
+  std::vector<uint32_t> h_bitmap;
+  to_host(h_bitmap, bitmap.get(), nbits_words + 1, s);
+  VPG_CUDA(cudaStreamSynchronize(s));
+  VPG_REQUIRE(h_bitmap[nbits_words] == 0, VPG_ELIMIT,
+              "record kind must be 0/1 and class_id in [0, 65536)");
+  std::vector<uint32_t> slots;
+  for (uint32_t w = 0; w < uint32_t(nbits_words); ++w)
+    for (uint32_t b = 0; b < 32; ++b)
+      if (h_bitmap[w] >> b & 1u) slots.push_back(w * 32 + b);
+  const int n_cls = int(slots.size());
+  VPG_REQUIRE(n_cls <= kMaxClasses, VPG_ELIMIT, "more than 256 compatibility classes");
+  g->info.n_classes = n_cls;
+
+  DBuf<uint32_t> d_slots(n_cls, s);
+  to_device(d_slots.get(), slots, s);
+  DBuf<unsigned long long> stats(n_cls * 7, s);
+  {
+    std::vector<unsigned long long> init(n_cls * 7);
+    for (int c = 0; c < n_cls; ++c) {
+      init[c] = 0;
+      for (int a = 0; a < 3; ++a) {
+        init[n_cls + c * 3 + a] = ~0ull;
+        init[4 * n_cls + c * 3 + a] = 0ull;
+      }
+    }
+    to_device(stats.get(), init, s);
+  }
+  DBuf<uint8_t> cls_idx;
+  if (n_cls > 1) cls_idx.alloc(n, s);
+  VPG_LAUNCH(k_class_stats, grid_for(n, block, sm_count() * 4), block, 0, s, rec.kind,
+             rec.class_id, rec.pos, n, d_slots.get(), n_cls, cls_idx.get(), stats.get(),
+             stats.get() + n_cls, stats.get() + 4 * n_cls);
+  std::vector<unsigned long long> h_stats;
+  to_host(h_stats, stats.get(), n_cls * 7, s);
+
+  // stable partition of record ids by class (np.nonzero(class_keys == key))
+  DBuf<int32_t> rows;
+  if (n_cls > 1) {
+    DBuf<int32_t> iota(n, s);
+    DBuf<uint8_t> cls_sorted(n, s);
+    rows.alloc(n, s);
+    VPG_LAUNCH(k_iota, grid_for(n, block), block, 0, s, iota.get(), n);
+    const int end_bit = bits_for(uint64_t(n_cls - 1));
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, cls_idx.get(), cls_sorted.get(), iota.get(),
+                                             rows.get(), int(n), 0, end_bit, s);
+    }, s);
+  }
+  VPG_CUDA(cudaStreamSynchronize(s));
+  clk.mark(0);
+
+  struct ClassPlan {
+    int64_t n, row_off, m, center_off;
+    double lo[3], hi[3];
+  };
+  std::vector<ClassPlan> plan(n_cls);
+  int64_t row_off = 0, center_total = 0;
+  for (int c = 0; c < n_cls; ++c) {
+    ClassPlan& p = plan[c];
+    p.n = int64_t(h_stats[c]);
+    p.row_off = row_off;
+    row_off += p.n;
+    p.m = (p.n + K - 1) / K;
+    p.center_off = center_total;
+    center_total += p.m;
+    for (int a = 0; a < 3; ++a) {
+      p.lo[a] = order_key_inv(h_stats[n_cls + c * 3 + a]);
+      p.hi[a] = order_key_inv(h_stats[4 * n_cls + c * 3 + a]);
+    }
+  }
+
+  // group storage for all classes (records grouped by center, class by class)
+  DBuf<int32_t> grp_rec(n, s), assign(n, s), values(n, s), fb_list(n, s);
+  DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s);
+  DBuf<int32_t> fb_count(1, s);
+  VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
+
+  // host-side final group lists
+  struct SplitOut {
+    std::vector<int64_t> modified_idx;               // original group index (class-local)
+    std::vector<std::vector<int64_t>> groups;        // modified first, then appended
+    std::vector<int64_t> centers;                    // record ids, same order
+  };
+  std::vector<SplitOut> splits(n_cls);
+  std::vector<std::vector<int32_t>> counts_h(n_cls), crec_h(n_cls);
+  int64_t n_splits = 0;
+  std::vector<int32_t> zero1(1, 0);
+
+  for (int c = 0; c < n_cls; ++c) {
+    const ClassPlan& p = plan[c];
+    const int m = int(p.m);
+    std::vector<int64_t> picks(m);
+    rng_choice(rng, p.n, p.m, picks.data());
+    std::vector<int32_t> picks32(picks.begin(), picks.end());
+    DBuf<int32_t> d_local(m, s);
+    to_device(d_local.get(), picks32, s);
+    int32_t* assign_c = assign.get() + p.row_off;
+    const int32_t* rows_p = rows.get();
+
+    DBuf<double> cpos(size_t(m) * 3, s);
+    DBuf<unsigned long long> keys(m, s), skeys(m, s);
+    DBuf<int32_t> ids(m, s), sids(m, s);
+    DBuf<double4> spos(m, s);
+    GridParams gp{};
+    gp.m = m;
+    if (m == 1) {
+      // a single center takes every point (clustering.py:100-101)
+      gp.cell = 1.0;
+      gp.packed = 1;
+      VPG_LAUNCH(k_center_setup, 1, 32, 0, s, d_local.get(), m, rows_p, p.row_off, rec.pos, gp,
+                 cpos.get(), crec_all.get() + p.center_off, keys.get(), ids.get());
+      VPG_CUDA(cudaMemsetAsync(assign_c, 0, sizeof(int32_t) * p.n, s));
+    } else {
+      double volume = 1.0;
+      double extent[3];
+      for (int a = 0; a < 3; ++a) {
+        extent[a] = p.hi[a] - p.lo[a];
+        gp.lo[a] = p.lo[a];
+      }
+      volume = std::max(extent[0], 1e-12) * std::max(extent[1], 1e-12);
+      volume = volume * std::max(extent[2], 1e-12);
+      gp.cell = std::max(std::pow(volume / double(m), 1.0 / 3.0), 1e-9);
+      bool fits = true;
+      gp.max_dim = 0;
+      for (int a = 0; a < 3; ++a) {
+        const double d = std::floor(extent[a] / gp.cell) + 2.0;
+        fits = fits && (d + 2.0 < 2097152.0);
+        gp.dims[a] = d < 9.0e18 ? (long long)d : (long long)9.0e18;
+        gp.max_dim = std::max(gp.max_dim, gp.dims[a]);
+      }
+      gp.packed = fits ? 1 : 0;
+      // u = (p-lo)/cell carries a relative error of a few ulp; allow 2^-44 * |u|
+      gp.slack = 2.0 * (double(std::min<long long>(gp.max_dim, 1LL << 52)) + 4.0) * 5.7e-14;
+      uint64_t cap = 1024;
+      while (cap < uint64_t(m) * 2) cap <<= 1;
+      gp.table_mask = cap - 1;
+      DBuf<CellEntry> table(cap, s);
+      VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+      VPG_LAUNCH(k_center_setup, grid_for(m, block), block, 0, s, d_local.get(), m, rows_p,
+                 p.row_off, rec.pos, gp, cpos.get(), crec_all.get() + p.center_off, keys.get(),
+                 ids.get());
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(),
+                                               sids.get(), m, 0, 64, s);
+      }, s);
+      VPG_LAUNCH(k_center_table, grid_for(m, block), block, 0, s, skeys.get(), sids.get(),
+                 cpos.get(), m, gp, spos.get(), table.get());
+      VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
+                 table.get());
+      to_device(fb_count.get(), zero1, s);
+      VPG_LAUNCH(k_assign, grid_for(p.n, block, sm_count() * 16), block, 0, s, rows_p, p.row_off,
+                 p.n, rec.pos, gp, table.get(), spos.get(), assign_c, fb_list.get(),
+                 fb_count.get());
+      VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
+                 table.get(), spos.get(), fb_list.get(), fb_count.get(), assign_c);
+      std::vector<int32_t> h_fb;
+      to_host(h_fb, fb_count.get(), 1, s);
+      VPG_CUDA(cudaStreamSynchronize(s));
+      g->info.n_fallback += h_fb[0];
+    }
+    clk.mark(1);
+
+    // groups: stable sort of this class's records by center
+    VPG_LAUNCH(k_group_values, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
+               values.get() + p.row_off);
+    {
+      DBuf<int32_t> sorted_keys(p.n, s);
+      const int end_bit = bits_for(uint64_t(m > 1 ? m - 1 : 1));
+      const int64_t nn = p.n;
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, reinterpret_cast<uint32_t*>(assign_c),
+                                               reinterpret_cast<uint32_t*>(sorted_keys.get()),
+                                               values.get() + p.row_off, grp_rec.get() + p.row_off,
+                                               int(nn), 0, end_bit, s);
+      }, s);
+    }
+    int32_t* counts_c = counts_all.get() + p.center_off;
+    VPG_LAUNCH(k_histogram, grid_for(p.n, block), block, 0, s, assign_c, p.n, counts_c);
+    to_host(counts_h[c], counts_c, m, s);
+    to_host(crec_h[c], crec_all.get() + p.center_off, m, s);
+    VPG_CUDA(cudaStreamSynchronize(s));
+    clk.mark(2);
+
+    // ---- split loop on the oversize groups (host, exact RNG order)
+    const int64_t max_size = 2 * int64_t(K);
+    std::vector<int64_t> seg;  // (src, count, dst)
+    std::vector<int64_t> over_idx;
+    int64_t off = 0, staged = 0;
+    for (int j = 0; j < m; ++j) {
+      const int64_t cnt = counts_h[c][j];
+      if (cnt > max_size) {
+        over_idx.push_back(j);
+        seg.push_back(p.row_off + off);
+        seg.push_back(cnt);
+        seg.push_back(staged);
+        staged += cnt;
+      }
+      off += cnt;
+    }
+    SplitOut& so = splits[c];
+    if (!over_idx.empty()) {
+      DBuf<int64_t> d_seg(seg.size(), s);
+      to_device(d_seg.get(), seg, s);
+      DBuf<int32_t> d_srec(staged, s);
+      DBuf<double> d_spos(staged * 3, s);
+      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(int64_t(over_idx.size()), 65535), 128, 0, s,
+                 grp_rec.get(), d_seg.get(), int(over_idx.size()), rec.pos, d_srec.get(),
+                 d_spos.get());
+      std::vector<int32_t> h_srec;
+      std::vector<double> h_spos, h_cpos;
+      to_host(h_srec, d_srec.get(), staged, s);
+      to_host(h_spos, d_spos.get(), staged * 3, s);
+      to_host(h_cpos, cpos.get(), size_t(m) * 3, s);
+      VPG_CUDA(cudaStreamSynchronize(s));
+      // ids in the split loop: staged member index (>= 0) or -(1+j) for an
+      // original center that is not among the staged members.
+      std::vector<std::vector<int64_t>> groups(over_idx.size());
+      std::vector<int64_t> centers(over_idx.size());
+      std::vector<int64_t> id_rec;  // staged index -> record id
+      id_rec.assign(h_srec.begin(), h_srec.end());
+      for (size_t k = 0; k < over_idx.size(); ++k) {
+        const int64_t base = seg[k * 3 + 2], cnt = seg[k * 3 + 1];
+        groups[k].resize(cnt);
+        for (int64_t t = 0; t < cnt; ++t) groups[k][t] = base + t;
+        // the center compares by record id: find it among the members
+        const int32_t crec = crec_h[c][over_idx[k]];
+        int64_t cid = -(1 + over_idx[k]);
+        for (int64_t t = 0; t < cnt; ++t)
+          if (h_srec[base + t] == crec) {
+            cid = base + t;
+            break;
+          }
+        centers[k] = cid;
+      }
+      auto pos_of = [&](int64_t id) -> const double* {
+        return id >= 0 ? &h_spos[size_t(id) * 3] : &h_cpos[size_t(-1 - id) * 3];
+      };
+      n_splits += split_oversize(rng, groups, centers, max_size, pos_of);
+      so.modified_idx = over_idx;
+      so.groups.resize(groups.size());
+      so.centers.resize(groups.size());
+      for (size_t k = 0; k < groups.size(); ++k) {
+        so.groups[k].resize(groups[k].size());
+        for (size_t t = 0; t < groups[k].size(); ++t) so.groups[k][t] = id_rec[groups[k][t]];
+        const int64_t cid = centers[k];
+        so.centers[k] = cid >= 0 ? id_rec[cid] : crec_h[c][-1 - cid];
+      }
+    }
+    clk.mark(3);
+  }
+  g->info.n_splits = n_splits;
+  rng.store(rng_state);
+
+  // ---- final cluster table (clustering.py:87-93)
+  std::vector<int32_t> cl_size;
+  std::vector<int64_t> cl_src;
+  std::vector<int32_t> cl_center;
+  std::vector<int32_t> split_rec;
+  cl_size.reserve(center_total + n_splits);
+  cl_src.reserve(center_total + n_splits);
+  cl_center.reserve(center_total + n_splits);
+  for (int c = 0; c < n_cls; ++c) {
+    const ClassPlan& p = plan[c];
+    const SplitOut& so = splits[c];
+    size_t next_mod = 0;
+    int64_t off = 0;
+    auto emit_split = [&](size_t k) {
+      const std::vector<int64_t>& mem = so.groups[k];
+      cl_size.push_back(int32_t(mem.size()));
+      cl_src.push_back(-1 - int64_t(split_rec.size()));
+      cl_center.push_back(int32_t(so.centers[k]));
+      for (int64_t r : mem) split_rec.push_back(int32_t(r));
+    };
+    for (int64_t j = 0; j < p.m; ++j) {
+      const int64_t cnt = counts_h[c][j];
+      if (next_mod < so.modified_idx.size() && so.modified_idx[next_mod] == j) {
+        emit_split(next_mod);  // modified original keeps its slot
+        ++next_mod;
+      } else if (cnt > 0) {
+        cl_size.push_back(int32_t(cnt));
+        cl_src.push_back(p.row_off + off);
+        cl_center.push_back(crec_h[c][j]);
+      }
+      off += cnt;
+    }
+    for (size_t k = so.modified_idx.size(); k < so.groups.size(); ++k) emit_split(k);
+  }
+  const int64_t M = int64_t(cl_size.size());
+  g->m = M;
+  g->max_cluster = cl_size.empty() ? 0 : *std::max_element(cl_size.begin(), cl_size.end());
+
+  DBuf<int32_t> d_size(M + 1, s);
+  DBuf<int64_t> d_src(M, s), d_sq(M + 1, s);
+  DBuf<int32_t> d_split(split_rec.size() + 1, s);
+  to_device(d_size.get(), cl_size, s);
+  VPG_CUDA(cudaMemsetAsync(d_size.get() + M, 0, sizeof(int32_t), s));
+  to_device(d_src.get(), cl_src, s);
+  to_device(d_split.get(), split_rec, s);
+  g->cl_center.alloc(M, s);
+  to_device(g->cl_center.get(), cl_center, s);
+  g->cl_off.alloc(M + 1, s);
+  g->w_off.alloc(M + 1, s);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, d_size.get(), g->cl_off.get(), int(M + 1), s);
+  }, s);
+  VPG_LAUNCH(k_square_sizes, grid_for(M + 1, block), block, 0, s, d_size.get(), M, d_sq.get());
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, d_sq.get(), g->w_off.get(), int(M + 1), s);
+  }, s);
+  VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), d_src.get(), M,
+             grp_rec.get(), d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
+  std::vector<int64_t> nnz_h;
+  to_host(nnz_h, g->w_off.get() + M, 1, s);
+  VPG_CUDA(cudaStreamSynchronize(s));
+  g->nnz = nnz_h[0];
+  clk.mark(4);
+}
+
+}  // namespace vpg

@@ -1,0 +1,110 @@
+// Shared runtime pieces of libvolpg_b200: error state, launch accounting,
+// stream-ordered scratch allocation.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/volpg_b200.h"
+
+namespace vpg {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+void count_launch(uint64_t n = 1);
+
+#define VPG_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::vpg::Error(VPG_ECUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e) + \
+                                        " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define VPG_REQUIRE(cond, code, msg)                 \
+  do {                                               \
+    if (!(cond)) throw ::vpg::Error((code), (msg));  \
+  } while (0)
+
+// Launch wrapper: counts the launch and surfaces configuration errors.
+#define VPG_LAUNCH(kernel, grid, block, smem, stream, ...)            \
+  do {                                                                \
+    if ((grid) > 0) {                                                 \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
+      ::vpg::count_launch();                                          \
+      VPG_CUDA(cudaGetLastError());                                   \
+    }                                                                 \
+  } while (0)
+
+// Run `body`, translating exceptions into the C ABI's error codes.
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    return VPG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return VPG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return VPG_ECUDA;
+  }
+}
+
+// ------------------------------------------------------ device scratch
+// Stream-ordered allocation from the device's default memory pool; the pool
+// keeps freed blocks (release threshold raised once), so repeated builds of
+// the same size do not return to the driver.
+void* dalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+
+template <class T>
+struct DBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : ptr(o.ptr), n(o.n), s(o.s) { o.ptr = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); ptr = o.ptr; n = o.n; s = o.s; o.ptr = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    ptr = static_cast<T*>(dalloc(count * sizeof(T) + 16, stream));
+  }
+  void release() {
+    if (ptr) dfree(ptr, s);
+    ptr = nullptr;
+    n = 0;
+  }
+  T* get() const { return ptr; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
+  int64_t g = (work + block - 1) / block;
+  if (g > max_blocks) g = max_blocks;
+  return int(g);
+}
+
+int sm_count();
+
+}  // namespace vpg

@@ -1,0 +1,51 @@
+// Device-resident path graph (the native half of PathGraph, graph.py:29-53).
+//
+// Layout in HBM (N records, M clusters, nnz = sum of size^2):
+//   perm[q]      int32   cluster-major position q -> record index; clusters are
+//                        contiguous, members ascending (clustering.py:87-93)
+//   clpos[r]     int32   record -> cluster-major position (inverse of perm)
+//   cluster_id[r]int32   record -> cluster number (reference numbering)
+//   cl_off[k]    int32   (M+1) start of cluster k in cluster-major order
+//   w_off[k]     int64   (M+1) start of cluster k's dense kernel block
+//   wt[]         float   nnz   per cluster an s x s block stored transposed:
+//                        wt[w_off + j*s + r] = W[r, j] = rho_r(w_j)/phat_ind[j]
+//                        (graph.py:143-148), columns implicit
+//   phat[3][N]   double  phat_ind / phat_dir_phase / phat_dir_emit, cluster-major
+//   Solve vectors, cluster-major float4 (xyz = RGB):
+//     i0   = i_pt, a = w_cont*coeff, b = w_cont*D-bar, dbar = D-bar, coeff
+//     par[q] int32: position of the continuation parent (record r-1 on the same
+//     path), -1 for a path's first record.  Row q propagates into par[q]:
+//       I[par] = w_cont[q] * (coeff[q] * (W I)[q] + D-bar[q]) = a*acc + b
+//   ibuf[2], acc[2]: double-buffered I and W*I (acc = i_bar / coeff).
+#pragma once
+#include "common.cuh"
+
+struct vpg_graph {
+  cudaStream_t stream = nullptr;
+  int64_t n = 0, m = 0, nnz = 0;
+  int32_t K = 0;
+  vpg::DBuf<int32_t> perm, clpos, cluster_id, cl_off, cl_center, par;
+  vpg::DBuf<int64_t> w_off;
+  vpg::DBuf<float> wt;
+  vpg::DBuf<double> phat;
+  vpg::DBuf<float4> i0, a, b, dbar, coeff, ibuf[2], acc[2];
+  vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows
+  // solve state (device): red[t*8 + 0..5] float bits, ctl = {performed, stop, grow, diverged}
+  vpg::DBuf<uint32_t> red;
+  vpg::DBuf<double> resid;
+  vpg::DBuf<int32_t> ctl;
+  int32_t red_cap = 0;
+  int32_t performed = -1;  // -1 = no solve yet
+  int32_t max_cluster = 0;
+  vpg_graph_info info{};
+  // the records the graph was built from (borrowed; the caller keeps them alive)
+  vpg_records rec{};
+};
+
+namespace vpg {
+// cluster.cu: fills perm/clpos/cluster_id/cl_off/w_off/cl_center.
+void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng,
+                    bool timings, cudaStream_t s);
+// operators.cu: marginals, kernel blocks, D-bar and solve vectors.
+void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s);
+}  // namespace vpg

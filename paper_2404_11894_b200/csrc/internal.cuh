@@ -1,0 +1,29 @@
+// Cross-translation-unit entry points behind the C ABI (capi.cu).
+#pragma once
+#include "graph.cuh"
+
+namespace vpg {
+void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
+           double* residuals, int32_t* performed, cudaStream_t s);
+void solve_export(const vpg_graph* g, const vpg_records& rec, double* incoming, double* i_bar,
+                  cudaStream_t s);
+void aggregate_indirect(const vpg_graph* g, const vpg_records& rec, const double* incoming,
+                        double* out, cudaStream_t s);
+void propagate(const vpg_records& rec, const double* lbar, double* out, int linear, cudaStream_t s);
+void export_clusters(const vpg_graph* g, int64_t* cluster_id, int64_t* cl_off, int64_t* members,
+                     int64_t* centers, cudaStream_t s);
+void export_marginals(const vpg_graph* g, double* p0, double* p1, double* p2, cudaStream_t s);
+void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, double* data,
+                      double* d_bar, cudaStream_t s);
+void splat(const vpg_graph* g, const vpg_records& rec, const vpg_paths& P, int w, int h, int spp,
+           int mode, double* image, cudaStream_t s);
+void splat_pt(const vpg_paths& P, int w, int h, int spp, double* image, cudaStream_t s);
+
+void trace_image(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* image, cudaStream_t s);
+void trace_count(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t* counts,
+                 const vpg_paths& pth, cudaStream_t s);
+void trace_fill(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& rec,
+                const vpg_paths& pth, cudaStream_t s);
+void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
+                  int n_extra, cudaStream_t s);
+}  // namespace vpg

@@ -1,0 +1,789 @@
+// Volumetric path tracer with record capture (transport/kernels.py).
+//
+// One thread per camera path, persistent grid-stride over paths.  The
+// arithmetic restates trace_one (kernels.py:86-430) and the scenecore njit
+// cores it calls in fp64, in the reference's evaluation order, and this
+// translation unit is compiled with -fmad=false: with the same splitmix64
+// streams (rng.py:19-51) the device reproduces the reference's records up to
+// the last-ulp differences of the libm transcendentals.
+//
+// Record capture is two-pass like the reference (count -> prefix sum ->
+// fill, tracer.py:58-70); the backward i_pt sweep (kernels.py:393-408) runs
+// over the just-written rows instead of a per-thread stack: the D-bar
+// partial sums are staged in the i_pt slot and the f/p factor is recomputed
+// from the stored coeff and pdf_phase.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace vpg {
+namespace {
+
+constexpr double kNoHit = 1e30;
+constexpr double kTEps = 1e-7;
+constexpr double kSurfOffset = 1e-6;
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kInvPi = 1.0 / kPi;
+constexpr double kInv4Pi = 1.0 / (4.0 * kPi);
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kSaltTrace = 0x7E;
+constexpr uint64_t kSaltExtra = 0xED;
+
+enum Mode { kOff = 0, kCount = 1, kFill = 2 };
+
+// ---------------------------------------------------------- rng (rng.py)
+struct Rng {
+  uint64_t s;
+  __device__ uint64_t next_u64() {
+    s += kGamma;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  __device__ double next() { return double(next_u64() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+__device__ Rng make_stream(int64_t seed, int64_t key, uint64_t salt) {
+  Rng r{uint64_t(seed) ^ (uint64_t(key) * 0xD1342543DE82EF95ull)};
+  r.s += salt * kGamma;
+  const uint64_t z1 = r.next_u64();
+  const uint64_t z2 = r.next_u64();
+  return Rng{z1 ^ (z2 >> 1)};
+}
+
+struct V3 {
+  double x, y, z;
+};
+// Python's max(a, b) / min(a, b): keep the first unless the second is strictly beyond it
+__device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
+__device__ __forceinline__ double pymin(double a, double b) { return b < a ? b : a; }
+
+// ------------------------------------------------------ geometry.py
+__device__ void ray_aabb(const V3& o, const V3& d, const double* bd, double& t0, double& t1) {
+  t0 = -kNoHit;
+  t1 = kNoHit;
+  const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+  for (int a = 0; a < 3; ++a) {
+    if (dd[a] != 0.0) {
+      const double inv = 1.0 / dd[a];
+      double lo = (bd[a] - oo[a]) * inv, hi = (bd[3 + a] - oo[a]) * inv;
+      if (lo > hi) {
+        const double t = lo;
+        lo = hi;
+        hi = t;
+      }
+      t0 = pymax(t0, lo);
+      t1 = pymin(t1, hi);
+    } else if (oo[a] < bd[a] || oo[a] > bd[3 + a]) {
+      t0 = 1.0;
+      t1 = -1.0;
+      return;
+    }
+  }
+}
+
+__device__ V3 quad_normal(double ux, double uy, double uz, double vx, double vy, double vz) {
+  const double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+  const double inv = 1.0 / sqrt(nx * nx + ny * ny + nz * nz);
+  return V3{nx * inv, ny * inv, nz * inv};
+}
+
+__device__ double ray_surface(const vpg_scene& sc, int i, const V3& o, const V3& d, double t_min) {
+  const double* p = sc.surf_params[i];
+  const int type = sc.surf_type[i];
+  if (type == 0) {
+    const double lx = o.x - p[0], ly = o.y - p[1], lz = o.z - p[2];
+    const double b = lx * d.x + ly * d.y + lz * d.z;
+    const double c = lx * lx + ly * ly + lz * lz - p[3] * p[3];
+    const double disc = b * b - c;
+    if (disc < 0.0) return kNoHit;
+    const double s = sqrt(disc);
+    const double t0 = -b - s;
+    if (t0 > t_min) return t0;
+    const double t1 = -b + s;
+    if (t1 > t_min) return t1;
+    return kNoHit;
+  }
+  if (type == 1) {
+    double t0, t1;
+    ray_aabb(o, d, p, t0, t1);
+    if (t0 > t1) return kNoHit;
+    if (t0 > t_min) return t0;
+    if (t1 > t_min) return t1;
+    return kNoHit;
+  }
+  const V3 n = quad_normal(p[3], p[4], p[5], p[6], p[7], p[8]);
+  const double denom = d.x * n.x + d.y * n.y + d.z * n.z;
+  if (fabs(denom) < 1e-12) return kNoHit;
+  const double t = ((p[0] - o.x) * n.x + (p[1] - o.y) * n.y + (p[2] - o.z) * n.z) / denom;
+  if (t <= t_min) return kNoHit;
+  const double hx = o.x + t * d.x - p[0], hy = o.y + t * d.y - p[1], hz = o.z + t * d.z - p[2];
+  const double uu = p[3] * p[3] + p[4] * p[4] + p[5] * p[5];
+  const double vv = p[6] * p[6] + p[7] * p[7] + p[8] * p[8];
+  const double a = (hx * p[3] + hy * p[4] + hz * p[5]) / uu;
+  const double b = (hx * p[6] + hy * p[7] + hz * p[8]) / vv;
+  if (a < 0.0 || a > 1.0 || b < 0.0 || b > 1.0) return kNoHit;
+  return t;
+}
+
+// nearest hit, lowest id on ties (geometry.py:145-163)
+__device__ double intersect(const vpg_scene& sc, const V3& o, const V3& d, double t_min,
+                            double t_max, int& sid) {
+  double best = t_max;
+  sid = -1;
+  for (int i = 0; i < sc.n_surf; ++i) {
+    const double t = ray_surface(sc, i, o, d, t_min);
+    if (t < best) {
+      best = t;
+      sid = i;
+    }
+  }
+  return best;
+}
+
+__device__ V3 surface_normal_at(const vpg_scene& sc, int i, const V3& x) {
+  const double* p = sc.surf_params[i];
+  if (sc.surf_type[i] == 0) {
+    const double inv = 1.0 / p[3];
+    return V3{(x.x - p[0]) * inv, (x.y - p[1]) * inv, (x.z - p[2]) * inv};
+  }
+  if (sc.surf_type[i] == 1) {
+    double best = fabs(x.x - p[0]);
+    V3 n{-1.0, 0.0, 0.0};
+    double dd = fabs(x.x - p[3]);
+    if (dd < best) { best = dd; n = V3{1.0, 0.0, 0.0}; }
+    dd = fabs(x.y - p[1]);
+    if (dd < best) { best = dd; n = V3{0.0, -1.0, 0.0}; }
+    dd = fabs(x.y - p[4]);
+    if (dd < best) { best = dd; n = V3{0.0, 1.0, 0.0}; }
+    dd = fabs(x.z - p[2]);
+    if (dd < best) { best = dd; n = V3{0.0, 0.0, -1.0}; }
+    dd = fabs(x.z - p[5]);
+    if (dd < best) { n = V3{0.0, 0.0, 1.0}; }
+    return n;
+  }
+  return quad_normal(p[3], p[4], p[5], p[6], p[7], p[8]);
+}
+
+// ---------------------------------------------------------- medium.py
+__device__ double grid_density(const vpg_scene& sc, int k, const V3& x) {
+  const double* bd = sc.med_bounds[k];
+  const int nx = sc.grid_dims[k][0], ny = sc.grid_dims[k][1], nz = sc.grid_dims[k][2];
+  long long ix = (long long)((x.x - bd[0]) / (bd[3] - bd[0]) * nx);
+  long long iy = (long long)((x.y - bd[1]) / (bd[4] - bd[1]) * ny);
+  long long iz = (long long)((x.z - bd[2]) / (bd[5] - bd[2]) * nz);
+  ix = ix < 0 ? 0 : (ix > nx - 1 ? nx - 1 : ix);
+  iy = iy < 0 ? 0 : (iy > ny - 1 ? ny - 1 : iy);
+  iz = iz < 0 ? 0 : (iz > nz - 1 ? nz - 1 : iz);
+  return double(__ldg(sc.grid_data + sc.grid_offset[k] + (iz * ny + iy) * nx + ix));
+}
+
+struct Flight {
+  bool scattered;
+  double t;
+  double w[3];
+};
+
+__device__ Flight flight_one_medium(const vpg_scene& sc, int k, const V3& o, const V3& d,
+                                    double a, double b, Rng& rng) {
+  const double* st = sc.med_sigma_t[k];
+  const double length = b - a;
+  Flight f{false, b, {1.0, 1.0, 1.0}};
+  if (sc.med_kind[k] == 0) {
+    const double sbar = (st[0] + st[1] + st[2]) / 3.0;
+    if (sbar <= 0.0) return f;
+    const double u = rng.next();
+    const double dist = -log1p(-u) / sbar;
+    if (dist >= length) {
+      for (int c = 0; c < 3; ++c) f.w[c] = exp(-(st[c] - sbar) * length);
+      return f;
+    }
+    for (int c = 0; c < 3; ++c) f.w[c] = exp(-(st[c] - sbar) * dist) / sbar;
+    f.scattered = true;
+    f.t = a + dist;
+    return f;
+  }
+  const double mu = sc.med_majorant[k];
+  if (mu <= 0.0) return f;
+  const double scale = sc.med_scale[k];
+  double t = a;
+  while (true) {
+    const double u = rng.next();
+    t += -log1p(-u) / mu;
+    if (t >= b) return f;
+    const V3 x{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+    const double dens = grid_density(sc, k, x) * scale;
+    const double s0 = st[0] * dens, s1 = st[1] * dens, s2 = st[2] * dens;
+    const double sbar = (s0 + s1 + s2) / 3.0;
+    const double u2 = rng.next();
+    if (u2 * mu < sbar) {
+      const double inv = 1.0 / sbar;
+      for (int c = 0; c < 3; ++c) f.w[c] *= inv;
+      f.scattered = true;
+      f.t = t;
+      return f;
+    }
+    const double denom = mu - sbar;
+    f.w[0] *= (mu - s0) / denom;
+    f.w[1] *= (mu - s1) / denom;
+    f.w[2] *= (mu - s2) / denom;
+  }
+}
+
+__device__ void transmittance_one_medium(const vpg_scene& sc, int k, const V3& o, const V3& d,
+                                         double a, double b, Rng& rng, double* w) {
+  const double* st = sc.med_sigma_t[k];
+  const double length = b - a;
+  w[0] = w[1] = w[2] = 1.0;
+  if (length <= 0.0) return;
+  if (sc.med_kind[k] == 0) {
+    for (int c = 0; c < 3; ++c) w[c] = exp(-st[c] * length);
+    return;
+  }
+  const double mu = sc.med_majorant[k];
+  if (mu <= 0.0) return;
+  const double scale = sc.med_scale[k];
+  double t = a;
+  while (true) {
+    const double u = rng.next();
+    t += -log1p(-u) / mu;
+    if (t >= b) return;
+    const V3 x{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+    const double dens = grid_density(sc, k, x) * scale;
+    for (int c = 0; c < 3; ++c) w[c] *= 1.0 - st[c] * dens / mu;
+    if (w[0] == 0.0 && w[1] == 0.0 && w[2] == 0.0) {
+      w[0] = w[1] = w[2] = 0.0;
+      return;
+    }
+  }
+}
+
+struct MediaFlight {
+  bool scattered;
+  double t;
+  int medium;
+  double w[3];
+};
+
+__device__ MediaFlight media_flight(const vpg_scene& sc, const V3& o, const V3& d, double t_lo,
+                                    double t_hi, Rng& rng) {
+  MediaFlight mf{false, t_hi, -1, {1.0, 1.0, 1.0}};
+  double cur = t_lo;
+  for (int it = 0; it < 2 * sc.n_med + 1; ++it) {
+    int best_k = -1;
+    double best_a = t_hi, best_b = t_hi;
+    for (int k = 0; k < sc.n_med; ++k) {
+      double t0, t1;
+      ray_aabb(o, d, sc.med_bounds[k], t0, t1);
+      const double a = pymax(t0, cur), b = pymin(t1, t_hi);
+      if (b > a + 1e-12 && a < best_a) {
+        best_a = a;
+        best_k = k;
+        best_b = b;
+      }
+    }
+    if (best_k < 0) return mf;
+    const Flight f = flight_one_medium(sc, best_k, o, d, best_a, best_b, rng);
+    for (int c = 0; c < 3; ++c) mf.w[c] *= f.w[c];
+    if (f.scattered) {
+      mf.scattered = true;
+      mf.t = f.t;
+      mf.medium = best_k;
+      return mf;
+    }
+    cur = best_b + 1e-12;
+  }
+  return mf;
+}
+
+__device__ void media_transmittance(const vpg_scene& sc, const V3& o, const V3& d, double t_lo,
+                                    double t_hi, Rng& rng, double* w) {
+  w[0] = w[1] = w[2] = 1.0;
+  for (int k = 0; k < sc.n_med; ++k) {
+    double t0, t1;
+    ray_aabb(o, d, sc.med_bounds[k], t0, t1);
+    const double a = pymax(t0, t_lo), b = pymin(t1, t_hi);
+    if (b > a + 1e-12) {
+      double tr[3];
+      transmittance_one_medium(sc, k, o, d, a, b, rng, tr);
+      for (int c = 0; c < 3; ++c) w[c] *= tr[c];
+    }
+  }
+}
+
+// ----------------------------------------------------------- phase.py
+__device__ double hg_pdf(double cs, double g) {
+  const double g2 = g * g;
+  const double denom = 1.0 + g2 - 2.0 * g * cs;
+  return kInv4Pi * (1.0 - g2) / (denom * sqrt(denom));
+}
+
+__device__ void make_frame(const V3& n, V3& t, V3& s) {
+  double bx = 1.0, by = 0.0, bz = 0.0;
+  if (fabs(n.x) > 0.9) {
+    bx = 0.0;
+    by = 1.0;
+  }
+  double tx = by * n.z - bz * n.y, ty = bz * n.x - bx * n.z, tz = bx * n.y - by * n.x;
+  const double inv = 1.0 / sqrt(tx * tx + ty * ty + tz * tz);
+  tx *= inv;
+  ty *= inv;
+  tz *= inv;
+  t = V3{tx, ty, tz};
+  s = V3{n.y * tz - n.z * ty, n.z * tx - n.x * tz, n.x * ty - n.y * tx};
+}
+
+__device__ V3 orient(const V3& t, const V3& s, const V3& n, double a, double b, double c) {
+  const double dx = a * t.x + b * s.x + c * n.x;
+  const double dy = a * t.y + b * s.y + c * n.y;
+  const double dz = a * t.z + b * s.z + c * n.z;
+  const double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  return V3{dx * inv, dy * inv, dz * inv};
+}
+
+__device__ V3 hg_sample_dir(double g, const V3& ax, double u1, double u2) {
+  double ct;
+  if (fabs(g) < 1e-6) {
+    ct = 1.0 - 2.0 * u1;
+  } else {
+    const double s = (1.0 - g * g) / (1.0 - g + 2.0 * g * u1);
+    const double c = (1.0 + g * g - s * s) / (2.0 * g);
+    ct = pymin(1.0, pymax(-1.0, c));
+  }
+  const double st = sqrt(pymax(0.0, 1.0 - ct * ct));
+  const double phi = 2.0 * kPi * u2;
+  V3 t, s;
+  make_frame(ax, t, s);
+  const double cp = cos(phi), sp = sin(phi);
+  return orient(t, s, ax, st * cp, st * sp, ct);
+}
+
+__device__ V3 cosine_sample_dir(const V3& n, double u1, double u2) {
+  const double z = sqrt(pymax(1e-12, 1.0 - u2));
+  const double r = sqrt(pymax(0.0, u2));
+  const double phi = 2.0 * kPi * u1;
+  V3 t, s;
+  make_frame(n, t, s);
+  const double cp = cos(phi), sp = sin(phi);
+  return orient(t, s, n, r * cp, r * sp, z);
+}
+
+// -------------------------------------------------------- emitters.py
+struct EmitterSample {
+  V3 w;
+  double pdf;
+  bool delta;
+  double rad[3];
+};
+
+__device__ EmitterSample sample_emitter(const vpg_scene& sc, const V3& p, Rng& rng) {
+  const int n_em = sc.n_emit;
+  const double u = rng.next();
+  long long e = (long long)(u * n_em);
+  if (e > n_em - 1) e = n_em - 1;
+  const double* val = sc.em_value[e];
+  const double sel = double(n_em);
+  EmitterSample out{V3{0.0, 0.0, 1.0}, 1.0, false, {0.0, 0.0, 0.0}};
+  const int type = sc.em_type[e];
+  if (type == 1) {
+    const double* q = sc.em_quad[e];
+    const double u1 = rng.next(), u2 = rng.next();
+    const double qx = q[0] + u1 * q[3] + u2 * q[6];
+    const double qy = q[1] + u1 * q[4] + u2 * q[7];
+    const double qz = q[2] + u1 * q[5] + u2 * q[8];
+    const double dx = qx - p.x, dy = qy - p.y, dz = qz - p.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    if (d2 < 1e-16) return out;
+    const double dist = sqrt(d2);
+    out.w = V3{dx / dist, dy / dist, dz / dist};
+    const double* nq = sc.em_normal[e];
+    const double cos_q = -(nq[0] * out.w.x + nq[1] * out.w.y + nq[2] * out.w.z);
+    out.pdf = d2 / (sc.em_area[e] * pymax(fabs(cos_q), 1e-12) * sel);
+    if (cos_q <= 0.0) return out;
+    const double clear = dist - 1e-6 * pymax(1.0, dist);
+    int sid;
+    if (intersect(sc, p, out.w, kTEps, clear, sid) < clear) return out;
+    double tr[3];
+    media_transmittance(sc, p, out.w, 0.0, dist, rng, tr);
+    for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c];
+    return out;
+  }
+  out.delta = true;
+  if (type == 0) {
+    const double* lp = sc.em_pos[e];
+    const double dx = lp[0] - p.x, dy = lp[1] - p.y, dz = lp[2] - p.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    if (d2 < 1e-16) return out;
+    const double dist = sqrt(d2);
+    out.w = V3{dx / dist, dy / dist, dz / dist};
+    const double clear = dist - 1e-6 * pymax(1.0, dist);
+    int sid;
+    if (intersect(sc, p, out.w, kTEps, clear, sid) < clear) return out;
+    double tr[3];
+    media_transmittance(sc, p, out.w, 0.0, dist, rng, tr);
+    const double inv_d2 = sel / d2;
+    for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c] * inv_d2;
+    return out;
+  }
+  const double* ld = sc.em_pos[e];
+  out.w = V3{-ld[0], -ld[1], -ld[2]};
+  int sid;
+  if (intersect(sc, p, out.w, kTEps, kNoHit, sid) < kNoHit) return out;
+  double tr[3];
+  media_transmittance(sc, p, out.w, 0.0, kNoHit, rng, tr);
+  for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c] * sel;
+  return out;
+}
+
+__device__ double emitter_dir_pdf_from_hit(const vpg_scene& sc, int sid, double t_hit,
+                                           const V3& w) {
+  if (sid < 0 || sc.mat_type[sid] != 2) return 0.0;
+  const int e = sc.emitter_id[sid];
+  if (sc.em_type[e] != 1) return 0.0;
+  const double* nq = sc.em_normal[e];
+  const double cos_q = fabs(nq[0] * w.x + nq[1] * w.y + nq[2] * w.z);
+  if (cos_q < 1e-12) return 0.0;
+  return t_hit * t_hit / (sc.em_area[e] * cos_q * sc.n_emit);
+}
+
+__device__ __forceinline__ void put3(double* a, int64_t row, double x, double y, double z) {
+  a[row * 3] = x;
+  a[row * 3 + 1] = y;
+  a[row * 3 + 2] = z;
+}
+
+struct PathResult {
+  int n_rec;
+  double est[3];
+};
+
+// ------------------------------------------------------- kernels.py
+template <int kMode>
+__device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
+                                int64_t py, int64_t path_id, int64_t rec_offset,
+                                const vpg_records& rec, const vpg_paths& pth, int64_t slot) {
+  Rng rng = make_stream(cfg.seed, path_id, kSaltTrace);
+  const double jx = rng.next();
+  const double jy = rng.next();
+  const double* cam = sc.cam;
+  const double width = cam[13], height = cam[14];
+  const double aspect = width / height;
+  const double sx = (2.0 * (double(px) + jx) / width - 1.0) * cam[12] * aspect;
+  const double sy = (1.0 - 2.0 * (double(py) + jy) / height) * cam[12];
+  double dx = cam[3] + sx * cam[6] + sy * cam[9];
+  double dy = cam[4] + sx * cam[7] + sy * cam[10];
+  double dz = cam[5] + sx * cam[8] + sy * cam[11];
+  const double inv0 = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  V3 d{dx * inv0, dy * inv0, dz * inv0};
+  V3 o{cam[0], cam[1], cam[2]};
+
+  double est[3] = {0, 0, 0}, beta[3] = {1, 1, 1};
+  double dcam[3] = {0, 0, 0}, camw[3] = {0, 0, 0}, d0n[3] = {0, 0, 0}, d0p[3] = {0, 0, 0};
+  double ext_fs[3] = {0, 0, 0};
+  double ext_pdf = 1.0, rr_inv = 1.0;
+  bool from_camera = true, allow_record = true;
+  int n_rec = 0;
+  const int max_depth = cfg.max_depth;
+
+  while (true) {
+    int sid;
+    const double t_hit = intersect(sc, o, d, kTEps, kNoHit, sid);
+    const double pe_at_dir = emitter_dir_pdf_from_hit(sc, sid, t_hit, d);
+    if (kMode == kFill && !from_camera) rec.pdf_emit_at_phase[rec_offset + n_rec - 1] = pe_at_dir;
+    const MediaFlight mf = media_flight(sc, o, d, 0.0, t_hit, rng);
+    V3 v{o.x + mf.t * d.x, o.y + mf.t * d.y, o.z + mf.t * d.z};
+    bool volume = false;
+    double k[3] = {0, 0, 0};
+    double gpar = 0.0;
+    V3 nrm{0.0, 0.0, 0.0};
+    int class_id = -1;
+
+    if (mf.scattered) {
+      if (!allow_record || n_rec >= max_depth) break;
+      const int mid = mf.medium;
+      const double* ss = sc.med_sigma_s[mid];
+      if (sc.med_kind[mid] == 0) {
+        k[0] = ss[0];
+        k[1] = ss[1];
+        k[2] = ss[2];
+      } else {
+        const double dens = grid_density(sc, mid, v) * sc.med_scale[mid];
+        k[0] = ss[0] * dens;
+        k[1] = ss[1] * dens;
+        k[2] = ss[2] * dens;
+      }
+      if (k[0] == 0.0 && k[1] == 0.0 && k[2] == 0.0) break;  // pure absorption
+      volume = true;
+      gpar = sc.med_g[mid];
+      class_id = mid;
+    } else {
+      if (sid < 0) break;
+      const int mat = sc.mat_type[sid];
+      v = V3{o.x + t_hit * d.x, o.y + t_hit * d.y, o.z + t_hit * d.z};
+      if (mat == 2) {
+        const V3 gn = surface_normal_at(sc, sid, v);
+        if (gn.x * d.x + gn.y * d.y + gn.z * d.z < 0.0) {
+          const double* ev = sc.em_value[sc.emitter_id[sid]];
+          if (from_camera) {
+            for (int c = 0; c < 3; ++c) {
+              dcam[c] = mf.w[c] * ev[c];
+              est[c] += dcam[c];
+            }
+          } else {
+            const double denom = ext_pdf + pe_at_dir;
+            double cc[3];
+            for (int c = 0; c < 3; ++c) {
+              cc[c] = ext_fs[c] * mf.w[c] * ev[c] / denom;
+              est[c] += beta[c] * cc[c];
+            }
+            if (n_rec == 1)
+              for (int c = 0; c < 3; ++c) d0p[c] = cc[c];
+            if (kMode == kFill) {
+              const int64_t row = rec_offset + n_rec - 1;
+              put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
+              for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
+            }
+          }
+        }
+        break;
+      }
+      if (mat == 1) break;  // black absorber
+      if (!allow_record || n_rec >= max_depth) break;
+      V3 gn = surface_normal_at(sc, sid, v);
+      if (gn.x * d.x + gn.y * d.y + gn.z * d.z > 0.0) gn = V3{-gn.x, -gn.y, -gn.z};
+      nrm = gn;
+      k[0] = sc.albedo[sid][0];
+      k[1] = sc.albedo[sid][1];
+      k[2] = sc.albedo[sid][2];
+      class_id = sid;
+    }
+
+    // ---- record n_rec at v
+    double wc[3];
+    for (int c = 0; c < 3; ++c) wc[c] = mf.w[c] * rr_inv;
+    if (from_camera) {
+      for (int c = 0; c < 3; ++c) {
+        camw[c] = wc[c];
+        beta[c] = wc[c];
+      }
+    } else {
+      for (int c = 0; c < 3; ++c) beta[c] *= (ext_fs[c] / ext_pdf) * wc[c];
+    }
+    const V3 ax = d;  // arrival direction = phase anchor
+
+    const EmitterSample es = sample_emitter(sc, v, rng);
+    double rho_e;
+    if (volume) {
+      rho_e = hg_pdf(ax.x * es.w.x + ax.y * es.w.y + ax.z * es.w.z, gpar);
+    } else {
+      rho_e = pymax(0.0, nrm.x * es.w.x + nrm.y * es.w.y + nrm.z * es.w.z) * kInvPi;
+    }
+    const double p_p_at_e = rho_e;
+    double cn[3];
+    for (int c = 0; c < 3; ++c) {
+      const double fe = k[c] * rho_e;
+      cn[c] = es.delta ? fe * es.rad[c] : fe * es.rad[c] / (es.pdf + p_p_at_e);
+      est[c] += beta[c] * cn[c];
+    }
+    if (n_rec == 0)
+      for (int c = 0; c < 3; ++c) d0n[c] = cn[c];
+
+    const double u1 = rng.next();
+    const double u2 = rng.next();
+    V3 wp;
+    double pdf_p;
+    if (volume) {
+      wp = hg_sample_dir(gpar, ax, u1, u2);
+      pdf_p = hg_pdf(ax.x * wp.x + ax.y * wp.y + ax.z * wp.z, gpar);
+    } else {
+      wp = cosine_sample_dir(nrm, u1, u2);
+      pdf_p = pymax(0.0, nrm.x * wp.x + nrm.y * wp.y + nrm.z * wp.z) * kInvPi;
+    }
+    double fp[3];
+    for (int c = 0; c < 3; ++c) fp[c] = k[c] * pdf_p;
+
+    if (kMode == kFill) {
+      const int64_t row = rec_offset + n_rec;
+      put3(rec.pos, row, v.x, v.y, v.z);
+      put3(rec.omega_out, row, -ax.x, -ax.y, -ax.z);
+      put3(rec.normal, row, nrm.x, nrm.y, nrm.z);
+      put3(rec.coeff, row, k[0], k[1], k[2]);
+      rec.g[row] = gpar;
+      put3(rec.phase_dir, row, wp.x, wp.y, wp.z);
+      rec.pdf_phase[row] = pdf_p;
+      rec.pdf_emit_at_phase[row] = 0.0;
+      put3(rec.emit_dir, row, es.w.x, es.w.y, es.w.z);
+      rec.pdf_emit[row] = es.pdf;
+      put3(rec.d_emit, row, es.rad[0], es.rad[1], es.rad[2]);
+      put3(rec.d_phase, row, 0.0, 0.0, 0.0);
+      put3(rec.i_pt, row, cn[0], cn[1], cn[2]);  // staged D-bar, replaced by the sweep
+      put3(rec.w_cont, row, wc[0], wc[1], wc[2]);
+      rec.kind[row] = volume ? 0 : 1;
+      rec.emit_delta[row] = es.delta ? 1 : 0;
+      rec.class_id[row] = class_id;
+      rec.path_idx[row] = path_id;
+      rec.depth[row] = n_rec;
+    }
+    ++n_rec;
+    if (pdf_p <= 0.0) break;  // degenerate sample, no continuation
+
+    rr_inv = 1.0;
+    allow_record = true;
+    if (n_rec >= cfg.rr_start) {
+      double q = (beta[0] * fp[0] / pdf_p + beta[1] * fp[1] / pdf_p + beta[2] * fp[2] / pdf_p) / 3.0;
+      if (q > 1.0) q = 1.0;
+      if (q < cfg.rr_floor) q = cfg.rr_floor;
+      const double u = rng.next();
+      if (u >= q) allow_record = false;
+      else rr_inv = 1.0 / q;
+    }
+    for (int c = 0; c < 3; ++c) ext_fs[c] = fp[c];
+    ext_pdf = pdf_p;
+    from_camera = false;
+    if (volume) {
+      o = v;
+    } else {
+      o = V3{v.x + wp.x * kSurfOffset, v.y + wp.y * kSurfOffset, v.z + wp.z * kSurfOffset};
+    }
+    d = wp;
+  }
+
+  if (kMode == kFill && n_rec > 0) {  // backward sweep (kernels.py:393-408)
+    double in[3] = {0.0, 0.0, 0.0};
+    for (int kk = n_rec - 1; kk >= 0; --kk) {
+      const int64_t row = rec_offset + kk;
+      const double pp = rec.pdf_phase[row];
+      for (int c = 0; c < 3; ++c) {
+        const double dbar = rec.i_pt[row * 3 + c];
+        rec.i_pt[row * 3 + c] = in[c];
+        const double kc = rec.coeff[row * 3 + c];
+        const double fpp = pp > 0.0 ? kc * pp / pp : 0.0;
+        in[c] = rec.w_cont[row * 3 + c] * (dbar + fpp * in[c]);
+      }
+    }
+  }
+  if (kMode != kOff) {
+    put3(pth.cam_weight, slot, camw[0], camw[1], camw[2]);
+    put3(pth.d_cam, slot, dcam[0], dcam[1], dcam[2]);
+    put3(pth.direct0, slot, d0n[0] + d0p[0], d0n[1] + d0p[1], d0n[2] + d0p[2]);
+    put3(pth.direct0_nee, slot, d0n[0], d0n[1], d0n[2]);
+    put3(pth.direct0_phase, slot, d0p[0], d0p[1], d0p[2]);
+    put3(pth.pt_estimate, slot, est[0], est[1], est[2]);
+    if (kMode == kFill) put3(pth.extra_direct, slot, d0n[0] + d0p[0], d0n[1] + d0p[1], d0n[2] + d0p[2]);
+  }
+  PathResult res{n_rec, {est[0], est[1], est[2]}};
+  return res;
+}
+
+// count / fill over paths [path_begin, path_begin + path_count)
+template <int kMode>
+__global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const vpg_trace_cfg cfg,
+                                                     int64_t* __restrict__ counts,
+                                                     const vpg_records rec, const vpg_paths pth) {
+  const int64_t spp = cfg.spp;
+  const int64_t width = sc.width;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cfg.path_count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t path_id = cfg.path_begin + i;
+    const int64_t pix = path_id / spp;
+    const int64_t off = kMode == kFill ? pth.rec_start[i] : 0;
+    const PathResult r = trace_one<kMode>(sc, cfg, pix % width, pix / width, path_id, off, rec,
+                                          pth, i);
+    if (kMode == kCount) counts[i] = r.n_rec;
+  }
+}
+
+// record-free image (render_image_kernel): thread per pixel, samples in order
+__global__ void __launch_bounds__(128) k_trace_image(const vpg_scene sc, const vpg_trace_cfg cfg,
+                                                     double* __restrict__ image) {
+  const int64_t npix = int64_t(sc.width) * sc.height;
+  const vpg_records rec{};
+  const vpg_paths pth{};
+  for (int64_t pix = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pix < npix;
+       pix += int64_t(gridDim.x) * blockDim.x) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int s = 0; s < cfg.spp; ++s) {
+      const PathResult r = trace_one<kOff>(sc, cfg, pix % sc.width, pix / sc.width,
+                                           pix * cfg.spp + s, 0, rec, pth, 0);
+      for (int c = 0; c < 3; ++c) acc[c] += r.est[c];
+    }
+    for (int c = 0; c < 3; ++c) image[pix * 3 + c] = acc[c] / cfg.spp;
+  }
+}
+
+// extra_direct_kernel (kernels.py:499-553)
+__global__ void __launch_bounds__(128) k_extra_direct(const vpg_scene sc, const vpg_records rec,
+                                                      const vpg_paths pth, int64_t seed,
+                                                      int n_extra) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pth.n;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    if (pth.rec_count[p] == 0) {
+      put3(pth.extra_direct, p, 0.0, 0.0, 0.0);
+      continue;
+    }
+    const int64_t r0 = pth.rec_start[p];
+    const V3 v{rec.pos[r0 * 3], rec.pos[r0 * 3 + 1], rec.pos[r0 * 3 + 2]};
+    const V3 a{-rec.omega_out[r0 * 3], -rec.omega_out[r0 * 3 + 1], -rec.omega_out[r0 * 3 + 2]};
+    const V3 n{rec.normal[r0 * 3], rec.normal[r0 * 3 + 1], rec.normal[r0 * 3 + 2]};
+    const double kc[3] = {rec.coeff[r0 * 3], rec.coeff[r0 * 3 + 1], rec.coeff[r0 * 3 + 2]};
+    const double g = rec.g[r0];
+    const bool volume = rec.kind[r0] == 0;
+    double acc[3] = {pth.direct0_nee[p * 3], pth.direct0_nee[p * 3 + 1], pth.direct0_nee[p * 3 + 2]};
+    Rng rng = make_stream(seed, p, kSaltExtra);
+    for (int i = 0; i < n_extra; ++i) {
+      const EmitterSample es = sample_emitter(sc, v, rng);
+      const double rho_e = volume ? hg_pdf(a.x * es.w.x + a.y * es.w.y + a.z * es.w.z, g)
+                                  : pymax(0.0, n.x * es.w.x + n.y * es.w.y + n.z * es.w.z) * kInvPi;
+      for (int c = 0; c < 3; ++c) {
+        if (es.delta) acc[c] += kc[c] * rho_e * es.rad[c];
+        else acc[c] += kc[c] * rho_e * es.rad[c] / (es.pdf + rho_e);
+      }
+    }
+    const double inv = 1.0 / (1.0 + n_extra);
+    put3(pth.extra_direct, p, acc[0] * inv + pth.direct0_phase[p * 3],
+         acc[1] * inv + pth.direct0_phase[p * 3 + 1], acc[2] * inv + pth.direct0_phase[p * 3 + 2]);
+  }
+}
+
+int trace_grid(int64_t work) {
+  const int64_t cap = int64_t(sm_count()) * 16;
+  int64_t g = (work + 127) / 128;
+  return int(g < cap ? g : cap);
+}
+
+void check_scene(const vpg_scene& sc) {
+  VPG_REQUIRE(sc.n_surf >= 0 && sc.n_surf <= VPG_MAX_SURF, VPG_ELIMIT, "too many surfaces");
+  VPG_REQUIRE(sc.n_emit >= 1 && sc.n_emit <= VPG_MAX_EMIT, VPG_ELIMIT, "emitter count out of range");
+  VPG_REQUIRE(sc.n_med >= 0 && sc.n_med <= VPG_MAX_MED, VPG_ELIMIT, "too many media");
+}
+
+}  // namespace
+
+void trace_image(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* image, cudaStream_t s) {
+  check_scene(sc);
+  VPG_LAUNCH(k_trace_image, trace_grid(int64_t(sc.width) * sc.height), 128, 0, s, sc, cfg, image);
+}
+
+void trace_count(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t* counts,
+                 const vpg_paths& pth, cudaStream_t s) {
+  check_scene(sc);
+  VPG_LAUNCH(k_trace_paths<kCount>, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts,
+             vpg_records{}, pth);
+}
+
+void trace_fill(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& rec,
+                const vpg_paths& pth, cudaStream_t s) {
+  check_scene(sc);
+  VPG_LAUNCH(k_trace_paths<kFill>, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, nullptr, rec,
+             pth);
+}
+
+void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
+                  int n_extra, cudaStream_t s) {
+  check_scene(sc);
+  VPG_REQUIRE(n_extra >= 0, VPG_EINVAL, "n_extra must be >= 0");
+  VPG_LAUNCH(k_extra_direct, trace_grid(pth.n), 128, 0, s, sc, rec, pth, seed, n_extra);
+}
+
+}  // namespace vpg

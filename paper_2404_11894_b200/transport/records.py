@@ -1,0 +1,335 @@
+"""Vertex records and the per-path table, structure-of-arrays, host or HBM.
+
+Same fields, dtypes and semantics as the reference (transport/records.py:27-
+188): one record per scatter/surface event, contiguous per path in depth
+order, paths in (pixel, sample) order.  A `RecordSoA` / `PathSoA` here can be
+backed by host numpy arrays (built by a caller or loaded from a VPGR dump) or
+by device tensors written by the CUDA tracer; each side is materialised on
+first use and cached, so a device-traced record set never visits the host
+unless a caller reads a field.
+
+The VPGR dump format (records.py:191-256) is byte-compatible with the
+reference: magic, "<IQQIII" header, packed 290-byte records, 188-byte paths.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from paper_2404_11894_b200 import _native as N
+
+VPGR_MAGIC = b"VPGR"
+VPGR_VERSION = 1
+KIND_VOLUME = 0
+KIND_SURFACE = 1
+
+
+def _packed_dtype(fields):
+    parts = []
+    for name, width, code in fields:
+        base = "<" + code
+        parts.append((name, base, (width,)) if width > 1 else (name, base))
+    return np.dtype(parts)
+
+
+RECORD_DTYPE = _packed_dtype(N.RECORD_FIELDS)
+PATH_DTYPE = _packed_dtype(N.PATH_FIELDS)
+assert RECORD_DTYPE.itemsize == 290 and PATH_DTYPE.itemsize == 188
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class _DualSoA:
+    """Fields live on the host (numpy), on the device (torch), or both."""
+
+    _FIELDS: list = []
+    _STRUCT = None
+
+    def __init__(self, host: dict, dev: Optional[dict] = None, n: Optional[int] = None):
+        object.__setattr__(self, "_host", host)
+        object.__setattr__(self, "_dev", dev)
+        if n is None:
+            first = self._FIELDS[0][0]
+            n = host[first].shape[0] if first in host else dev[first].shape[0]
+        object.__setattr__(self, "_n", int(n))
+        object.__setattr__(self, "_struct", None)
+        object.__setattr__(self, "_pinned", None)
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    def _get(self, name):
+        arr = self._host.get(name)
+        if arr is None:
+            if self._dev is None:
+                raise AttributeError(name)
+            arr = self._dev[name].cpu().numpy()
+            self._host[name] = arr
+        return arr
+
+    def _set(self, name, value, width, code):
+        arr = np.ascontiguousarray(value, dtype=np.dtype("<" + code))
+        if self._dev is not None:
+            dev = self._dev[name]
+            if tuple(dev.shape) == arr.shape:
+                dev.copy_(_torch().from_numpy(arr))  # keep both sides in step
+            else:
+                # new length: the device copy is dropped (graphs keep their own reference)
+                for other, _, _ in self._FIELDS:
+                    self._get(other)
+                object.__setattr__(self, "_dev", None)
+                object.__setattr__(self, "_struct", None)
+                object.__setattr__(self, "_n", int(arr.shape[0]))
+        self._host[name] = arr
+
+    def on_device(self) -> bool:
+        return self._dev is not None
+
+    def pin_memory(self):
+        """Re-home the host arrays in page-locked memory (fast, async H2D)."""
+        torch = _torch()
+        pinned = {}
+        for name, _, _ in self._FIELDS:
+            src = self._get(name)
+            t = torch.from_numpy(np.ascontiguousarray(src)).pin_memory()
+            pinned[name] = t
+            self._host[name] = t.numpy()
+        object.__setattr__(self, "_pinned", pinned)
+        return self
+
+    def device(self, stream=None):
+        """Device tensors of every field (uploaded on first use) and the ABI struct."""
+        if self._dev is None:
+            torch = N.require_cuda()
+            dev = {}
+            for name, width, code in self._FIELDS:
+                if self._pinned is not None:
+                    src = self._pinned[name]
+                else:
+                    src = torch.from_numpy(np.ascontiguousarray(self._get(name)))
+                dev[name] = src.to("cuda", non_blocking=self._pinned is not None)
+            object.__setattr__(self, "_dev", dev)
+            object.__setattr__(self, "_struct", None)
+        if self._struct is None:
+            st = self._STRUCT()
+            st.n = self._n
+            for name, _, _ in self._FIELDS:
+                t = self._dev[name]
+                setattr(st, name, t.data_ptr() if t.numel() else None)
+            object.__setattr__(self, "_struct", st)
+        return self._struct
+
+    def device_tensors(self) -> dict:
+        self.device()
+        return self._dev
+
+    def drop_host(self):
+        """Forget cached host copies of device-resident fields."""
+        if self._dev is not None:
+            self._host.clear()
+
+    def host_arrays(self) -> dict:
+        return {name: self._get(name) for name, _, _ in self._FIELDS}
+
+
+def _install_fields(cls):
+    for name, width, code in cls._FIELDS:
+        def getter(self, _n=name):
+            return self._get(_n)
+
+        def setter(self, value, _n=name, _w=width, _c=code):
+            self._set(_n, value, _w, _c)
+
+        setattr(cls, name, property(getter, setter))
+    return cls
+
+
+def _zeros(fields, n):
+    out = {}
+    for name, width, code in fields:
+        shape = (n, width) if width > 1 else (n,)
+        out[name] = np.zeros(shape, dtype=np.dtype("<" + code))
+    return out
+
+
+@_install_fields
+class RecordSoA(_DualSoA):
+    """Shading-point records (reference: records.py:75-140)."""
+
+    _FIELDS = N.RECORD_FIELDS
+    _STRUCT = N.Records
+
+    def __init__(self, *args, cluster_id=None, _dev=None, _n=None, **kwargs):
+        host = {}
+        names = [f[0] for f in self._FIELDS]
+        for name, value in zip(names, args):
+            kwargs[name] = value
+        for name, width, code in self._FIELDS:
+            if name in kwargs and kwargs[name] is not None:
+                host[name] = np.ascontiguousarray(kwargs[name], dtype=np.dtype("<" + code))
+        if _dev is None and len(host) != len(names):
+            missing = [nm for nm in names if nm not in host]
+            raise TypeError(f"RecordSoA missing fields: {missing}")
+        super().__init__(host, _dev, _n)
+        object.__setattr__(self, "_cluster_id", None)
+        object.__setattr__(self, "_cluster_id_fn", None)
+        if cluster_id is not None:
+            self.cluster_id = cluster_id
+
+    @property
+    def cluster_id(self) -> np.ndarray:
+        if self._cluster_id is None:
+            if self._cluster_id_fn is not None:
+                object.__setattr__(self, "_cluster_id", self._cluster_id_fn())
+            else:
+                object.__setattr__(self, "_cluster_id", np.full(self.n, -1, dtype=np.int64))
+        return self._cluster_id
+
+    @cluster_id.setter
+    def cluster_id(self, value):
+        object.__setattr__(self, "_cluster_id", np.asarray(value, dtype=np.int64))
+        object.__setattr__(self, "_cluster_id_fn", None)
+
+    def _set_cluster_provider(self, fn: Callable[[], np.ndarray]):
+        object.__setattr__(self, "_cluster_id", None)
+        object.__setattr__(self, "_cluster_id_fn", fn)
+
+    @classmethod
+    def empty(cls, n: int) -> "RecordSoA":
+        return cls(**_zeros(cls._FIELDS, n))
+
+    @classmethod
+    def from_device(cls, tensors: dict, n: int) -> "RecordSoA":
+        return cls(_dev=tensors, _n=n)
+
+    def kernel_arrays(self):
+        return tuple(self._get(name) for name, _, _ in self._FIELDS)
+
+    def next_index(self) -> np.ndarray:
+        """Continuation child per record: r + 1 when it is on the same path, else -1."""
+        pid = self.path_idx
+        nxt = np.full(self.n, -1, dtype=np.int64)
+        if self.n > 1:
+            rows = np.flatnonzero(pid[1:] == pid[:-1])
+            nxt[rows] = rows + 1
+        return nxt
+
+
+@_install_fields
+class PathSoA(_DualSoA):
+    """Per-path table (reference: records.py:143-176)."""
+
+    _FIELDS = N.PATH_FIELDS
+    _STRUCT = N.Paths
+
+    def __init__(self, *args, _dev=None, _n=None, **kwargs):
+        host = {}
+        names = [f[0] for f in self._FIELDS]
+        for name, value in zip(names, args):
+            kwargs[name] = value
+        for name, width, code in self._FIELDS:
+            if name in kwargs and kwargs[name] is not None:
+                host[name] = np.ascontiguousarray(kwargs[name], dtype=np.dtype("<" + code))
+        if _dev is None and len(host) != len(names):
+            missing = [nm for nm in names if nm not in host]
+            raise TypeError(f"PathSoA missing fields: {missing}")
+        super().__init__(host, _dev, _n)
+
+    @classmethod
+    def empty(cls, n: int) -> "PathSoA":
+        return cls(**_zeros(cls._FIELDS, n))
+
+    @classmethod
+    def from_device(cls, tensors: dict, n: int) -> "PathSoA":
+        return cls(_dev=tensors, _n=n)
+
+    def kernel_arrays(self):
+        return (self.cam_weight, self.d_cam, self.direct0, self.direct0_nee,
+                self.direct0_phase, self.pt_estimate)
+
+
+class TraceOutput:
+    """Everything one instrumented render produces (reference: records.py:179-188).
+
+    `image` (the PT image) may be given or computed on the device on first access.
+    """
+
+    def __init__(self, image, records: RecordSoA, paths: PathSoA, width: int, height: int,
+                 spp: int):
+        self._image = image
+        self.records = records
+        self.paths = paths
+        self.width = int(width)
+        self.height = int(height)
+        self.spp = int(spp)
+
+    @property
+    def image(self) -> np.ndarray:
+        if self._image is None:
+            self._image = splat_pt_image(self.paths, self.width, self.height, self.spp)
+        return self._image
+
+    @image.setter
+    def image(self, value):
+        self._image = value
+
+
+def splat_pt_image(paths: PathSoA, width: int, height: int, spp: int) -> np.ndarray:
+    """Per-pixel mean of the PT estimates in sample order, on the device."""
+    torch = N.require_cuda()
+    st = paths.device()
+    img = torch.empty((height, width, 3), dtype=torch.float64, device="cuda")
+    N.check(N.lib().vpg_splat_pt(ctypes.byref(st), width, height, spp, img.data_ptr(),
+                                 N.stream_handle()))
+    return img.cpu().numpy()
+
+
+def save_records(path, out: TraceOutput) -> None:
+    """Write the versioned VPGR dump (reference: records.py:191-217)."""
+    rec = np.zeros(out.records.n, dtype=RECORD_DTYPE)
+    for name, _, _ in N.RECORD_FIELDS:
+        rec[name] = out.records._get(name)
+    pth = np.zeros(out.paths.n, dtype=PATH_DTYPE)
+    for name, _, _ in N.PATH_FIELDS:
+        pth[name] = out.paths._get(name)
+    with open(path, "wb") as f:
+        f.write(VPGR_MAGIC)
+        f.write(struct.pack("<IQQIII", VPGR_VERSION, out.records.n, out.paths.n,
+                            out.width, out.height, out.spp))
+        f.write(rec.tobytes())
+        f.write(pth.tobytes())
+
+
+def load_records(path, pin: bool = False) -> TraceOutput:
+    """Read a VPGR dump (reference: records.py:220-256) into host SoA arrays.
+
+    pin=True places the arrays in page-locked memory for asynchronous upload.
+    """
+    with open(path, "rb") as f:
+        if f.read(4) != VPGR_MAGIC:
+            raise IOError(f"{path}: not a VPGR record dump")
+        version, n_rec, n_path, width, height, spp = struct.unpack("<IQQIII", f.read(32))
+        if version != VPGR_VERSION:
+            raise IOError(f"{path}: unsupported VPGR version {version}")
+        rec = np.frombuffer(f.read(RECORD_DTYPE.itemsize * n_rec), dtype=RECORD_DTYPE)
+        if rec.size != n_rec:
+            raise IOError(f"{path}: truncated record block")
+        pth = np.frombuffer(f.read(PATH_DTYPE.itemsize * n_path), dtype=PATH_DTYPE)
+        if pth.size != n_path:
+            raise IOError(f"{path}: truncated path block")
+    records = RecordSoA(**{name: np.ascontiguousarray(rec[name]) for name, _, _ in N.RECORD_FIELDS})
+    paths = PathSoA(**{name: np.ascontiguousarray(pth[name]) for name, _, _ in N.PATH_FIELDS})
+    if pin:
+        records.pin_memory()
+        paths.pin_memory()
+    return TraceOutput(None, records, paths, width, height, spp)
