@@ -39,7 +39,7 @@ struct Pcg64 {
     s->inc_hi = uint64_t(inc >> 64);
     s->inc_lo = uint64_t(inc);
     s->has_uint32 = has32 ? 1 : 0;
-    s->uinteger = has32 ? buf32 : 0;
+    s->uinteger = buf32;  // numpy leaves the consumed half in place
   }
 
   // PCG XSL-RR 128/64: advance, then permute the new state.

@@ -1,0 +1,144 @@
+"""GPU parity of the path-graph build, solve and splat (through the C ABI) on
+the reference's own record sets (tests/golden), plus oracle comparisons on
+record sets traced on the device.
+
+Bars (BASELINE.json north_star): cluster membership and CSR topology
+bit-exact; propagated radiance within 1e-4 relative per entry with zeros
+exact (fp32 iteration, fp64-built weights); marginals to 1e-12 (fp64).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import assert_rel, golden
+from oracle import pathgraph_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c1_16", 32), ("c1_16", 8), ("c1_16", 1), ("c1floor_16", 32), ("cloud_16", 32),
+         ("dense_12", 32)]
+
+
+def _trace_from_golden(z):
+    from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
+
+    rec, paths = O.load_golden_records(z)
+    return TraceOutput(None, RecordSoA(**rec), PathSoA(**paths), int(z["width"]),
+                       int(z["height"]), int(z["spp"]))
+
+
+@pytest.mark.parametrize("name,K", CASES)
+def test_graph_topology_and_marginals_match_reference(cuda, name, K):
+    from paper_2404_11894_b200.pathgraph import build_graph
+
+    z = golden(name)
+    trace = _trace_from_golden(z)
+    g = build_graph(trace, K, seed=int(z["seed"]))
+    p = f"K{K}_"
+    assert np.array_equal(trace.records.cluster_id, z[p + "cluster_id"])
+    assert np.array_equal([c.center for c in g.clusters], z[p + "centers"])
+    assert np.array_equal(np.concatenate([c.members for c in g.clusters]), z[p + "members"])
+    assert np.array_equal(g.next_idx, z[p + "next_idx"])
+    W = g.w_indirect
+    assert np.array_equal(W.indptr, z[p + "w_indptr"])
+    assert np.array_equal(W.indices, z[p + "w_indices"])
+    assert_rel(W.data, z[p + "w_data"], 1e-6, what="W")
+    for a in ("phat_ind", "phat_dir_phase", "phat_dir_emit"):
+        assert_rel(getattr(g, a), z[p + a], 1e-12, floor=1e-300, what=a)
+    for a in ("included_phase", "included_emit"):
+        assert np.array_equal(getattr(g, a), z[p + a]), a
+    assert_rel(g.d_bar, z[p + "d_bar"], 1e-6, what="d_bar")
+
+
+@pytest.mark.parametrize("name,K", CASES)
+def test_solve_and_splat_match_reference(cuda, name, K):
+    from paper_2404_11894_b200.pathgraph import build_graph, solve, splat_output
+
+    z = golden(name)
+    trace = _trace_from_golden(z)
+    g = build_graph(trace, K, seed=int(z["seed"]))
+    p = f"K{K}_"
+    for iters in (0, 1, 10):
+        res = solve(g, iterations=iters, tol=0.0)
+        q = f"{p}it{iters}_"
+        assert res.iterations == iters
+        assert_rel(res.incoming, z[q + "incoming"], 1e-4, what=f"incoming it{iters}")
+        assert_rel(res.i_bar, z[q + "i_bar"], 1e-4, what=f"i_bar it{iters}")
+        np.testing.assert_allclose(res.residuals, z[q + "residuals"], rtol=1e-4, atol=1e-6)
+        assert_rel(splat_output(g, res), z[q + "image"], 1e-4, what=f"image it{iters}")
+        assert_rel(splat_output(g, res, aggregate_direct_term=True), z[q + "image_aggdirect"],
+                   1e-4, what="image aggregated direct")
+        if q + "image_extra" in z.files:
+            trace.paths.extra_direct = z["extra_direct"]
+            assert_rel(splat_output(g, res, extra_direct=True), z[q + "image_extra"], 1e-4,
+                       what="image extra direct")
+    res = solve(g, iterations=10, tol=1e-3)
+    assert res.iterations == int(z[p + "tol_iterations"])
+    np.testing.assert_allclose(res.residuals, z[p + "tol_residuals"], rtol=1e-4, atol=1e-6)
+    assert_rel(res.incoming, z[p + "tol_incoming"], 1e-4, what="incoming tol")
+
+
+def test_cluster_points_matches_reference_tail_shuffle(cuda):
+    from paper_2404_11894_b200.pathgraph import cluster_points
+
+    z = golden("clustering")
+    for tag in ("c1_48", "c1floor_40"):
+        rng = np.random.default_rng(np.random.SeedSequence([int(z[tag + "_seed"]) & 0xFFFFFFFF,
+                                                            0xC1A5]))
+        cid, cl = cluster_points(z[tag + "_pos"], z[tag + "_keys"], 32, rng)
+        assert np.array_equal(cid, z[tag + "_cluster_id"])
+        assert np.array_equal([c.center for c in cl], z[tag + "_centers"])
+        after = np.array([int(x) for x in rng.integers(0, 2**62, size=4)])
+        assert np.array_equal(after, z[tag + "_rng_after"])
+
+
+def test_operator_api_matches_oracle(cuda):
+    from paper_2404_11894_b200.pathgraph import (aggregate_direct, aggregate_indirect, build_graph,
+                                                 propagate, propagate_linear)
+
+    z = golden("cloud_16")
+    trace = _trace_from_golden(z)
+    g = build_graph(trace, 32, seed=int(z["seed"]))
+    rec, paths = O.load_golden_records(z)
+    og = O.build_graph(rec, paths, int(z["width"]), int(z["height"]), int(z["spp"]), 32,
+                       int(z["seed"]))
+    v = np.random.default_rng(0).random((rec["pos"].shape[0], 3))
+    assert_rel(aggregate_indirect(g, v), O.aggregate_indirect(og, v), 1e-5, what="A+ v")
+    assert_rel(propagate(g, v), O.propagate(og, v), 1e-14, floor=1e-300, what="P v")
+    assert_rel(propagate_linear(g, v), O.propagate_linear(og, v), 1e-14, floor=1e-300)
+    assert_rel(aggregate_direct(g), og.d_bar, 1e-6)
+
+
+def test_empty_and_single_record_graphs(cuda):
+    from paper_2404_11894_b200.pathgraph import build_graph, solve, splat_output
+    from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
+
+    paths = PathSoA.empty(4)
+    t = TraceOutput(None, RecordSoA.empty(0), paths, 2, 2, 1)
+    g = build_graph(t, 32)
+    res = solve(g, iterations=3, tol=0.0)
+    assert res.iterations == 3 and res.residuals == [0.0, 0.0, 0.0]
+    assert splat_output(g, res).shape == (2, 2, 3)
+    assert solve(g, iterations=3, tol=1e-3).iterations == 1
+    with pytest.raises(ValueError):
+        build_graph(t, 0)
+
+
+def test_divergence_is_detected(cuda):
+    """Inflating w_cont makes P A+ expansive: residuals grow -> SolveDivergence."""
+    from paper_2404_11894_b200.pathgraph import SolveDivergence, build_graph, solve
+    from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
+
+    z = golden("dense_12")
+    rec, paths = O.load_golden_records(z)
+    rec = dict(rec)
+    rec["w_cont"] = rec["w_cont"] * 50.0
+    og = O.build_graph(rec, paths, int(z["width"]), int(z["height"]), int(z["spp"]), 32, 0)
+    with pytest.raises(O.Divergence) as ref_err:
+        O.solve(og, 30, 0.0)
+    t = TraceOutput(None, RecordSoA(**rec), PathSoA(**paths), int(z["width"]), int(z["height"]),
+                    int(z["spp"]))
+    g = build_graph(t, 32, seed=0)
+    with pytest.raises(SolveDivergence):
+        solve(g, iterations=30, tol=0.0)
+    assert g.native.performed == len(ref_err.value.args[0])
