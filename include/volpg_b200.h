@@ -48,6 +48,16 @@ int vpg_abi_version(void);
 const char* vpg_last_error(void);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t vpg_launch_count(void);
+/* Bytes this library copied host->device / device->host internally (the
+ * build's class statistics, center picks, split-loop staging, exports). */
+void vpg_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+/* Per-kernel device timing: when enabled, every launch is bracketed by CUDA
+ * events on its stream; vpg_profile_read aggregates (count, total ms) per
+ * kernel name ('\n'-separated in `names`).  Diagnostic, used by bench.py. */
+void vpg_profile_enable(int32_t on);
+int vpg_profile_reset(void);
+int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* total_ms,
+                     int64_t cap, int64_t* n_kernels);
 /* sizeof() of the ABI structs, for binding self-checks:
  * 0 vpg_pcg64, 1 vpg_records, 2 vpg_paths, 3 vpg_graph_info, 4 vpg_scene, 5 vpg_trace_cfg */
 size_t vpg_struct_size(int32_t which);

@@ -108,7 +108,11 @@ _SIGNATURES = {
     "vpg_abi_version": (C.c_int, []),
     "vpg_last_error": (C.c_char_p, []),
     "vpg_launch_count": (c_u64, []),
+    "vpg_transfer_bytes": (None, [C.POINTER(c_u64), C.POINTER(c_u64)]),
     "vpg_struct_size": (C.c_size_t, [c_i32]),
+    "vpg_profile_enable": (None, [c_i32]),
+    "vpg_profile_reset": (C.c_int, []),
+    "vpg_profile_read": (C.c_int, [C.c_char_p, c_i64, c_p, c_p, c_i64, C.POINTER(c_i64)]),
     "vpg_rng_choice": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,
@@ -186,6 +190,33 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(lib().vpg_launch_count())
+
+
+def transfer_bytes() -> tuple[int, int]:
+    h, d = c_u64(), c_u64()
+    lib().vpg_transfer_bytes(C.byref(h), C.byref(d))
+    return int(h.value), int(d.value)
+
+
+def profile(enable: bool) -> None:
+    lib().vpg_profile_enable(1 if enable else 0)
+
+
+def profile_reset() -> None:
+    check(lib().vpg_profile_reset())
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total device ms)} since the last reset."""
+    cap = 256
+    names = C.create_string_buffer(1 << 16)
+    counts = np.zeros(cap, dtype=np.int64)
+    ms = np.zeros(cap)
+    nk = c_i64()
+    check(lib().vpg_profile_read(names, len(names), counts.ctypes.data, ms.ctypes.data, cap,
+                                 C.byref(nk)))
+    keys = names.value.decode().split("\n")[: nk.value]
+    return {k: (int(counts[i]), float(ms[i])) for i, k in enumerate(keys)}
 
 
 def require_cuda():

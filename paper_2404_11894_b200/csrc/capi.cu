@@ -1,5 +1,6 @@
 // extern "C" entry points of libvolpg_b200.so (declared in include/volpg_b200.h).
 #include <atomic>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -17,7 +18,41 @@ int g_sm_count = 0;
 }  // namespace
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+struct ProfEntry {
+  std::string name;
+  cudaEvent_t start, stop;
+};
+std::atomic<bool> g_profiling{false};
+std::mutex g_prof_mu;
+std::vector<ProfEntry> g_prof;
+}  // namespace
+
+bool profiling() { return g_profiling.load(std::memory_order_relaxed); }
+
+int prof_begin(const char* name, cudaStream_t s) {
+  ProfEntry e{name, nullptr, nullptr};
+  if (cudaEventCreate(&e.start) != cudaSuccess || cudaEventCreate(&e.stop) != cudaSuccess) return -1;
+  cudaEventRecord(e.start, s);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back(e);
+  return int(g_prof.size()) - 1;
+}
+
+void prof_end(int token, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (token >= 0 && token < int(g_prof.size())) cudaEventRecord(g_prof[token].stop, s);
+}
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+}
+void count_transfer(uint64_t h2d, uint64_t d2h) {
+  g_h2d.fetch_add(h2d, std::memory_order_relaxed);
+  g_d2h.fetch_add(d2h, std::memory_order_relaxed);
+}
 
 int sm_count() {
   if (g_sm_count == 0) {
@@ -66,6 +101,10 @@ extern "C" {
 int vpg_abi_version(void) { return VPG_ABI_VERSION; }
 const char* vpg_last_error(void) { return vpg::g_last_error.c_str(); }
 uint64_t vpg_launch_count(void) { return vpg::g_launches.load(); }
+void vpg_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+  *h2d = vpg::g_h2d.load();
+  *d2h = vpg::g_d2h.load();
+}
 
 size_t vpg_struct_size(int32_t which) {
   switch (which) {
@@ -77,6 +116,53 @@ size_t vpg_struct_size(int32_t which) {
     case 5: return sizeof(vpg_trace_cfg);
     default: return 0;
   }
+}
+
+void vpg_profile_enable(int32_t on) { vpg::g_profiling.store(on != 0); }
+
+int vpg_profile_reset(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(vpg::g_prof_mu);
+    for (auto& e : vpg::g_prof) {
+      cudaEventDestroy(e.start);
+      cudaEventDestroy(e.stop);
+    }
+    vpg::g_prof.clear();
+  });
+}
+
+int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* total_ms,
+                     int64_t cap, int64_t* n_kernels) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(vpg::g_prof_mu);
+    std::vector<std::string> keys;
+    std::vector<int64_t> cnt;
+    std::vector<double> ms;
+    for (auto& e : vpg::g_prof) {
+      VPG_CUDA(cudaEventSynchronize(e.stop));
+      float t = 0.f;
+      VPG_CUDA(cudaEventElapsedTime(&t, e.start, e.stop));
+      size_t k = 0;
+      while (k < keys.size() && keys[k] != e.name) ++k;
+      if (k == keys.size()) {
+        keys.push_back(e.name);
+        cnt.push_back(0);
+        ms.push_back(0.0);
+      }
+      cnt[k] += 1;
+      ms[k] += t;
+    }
+    *n_kernels = int64_t(keys.size());
+    std::string joined;
+    for (size_t k = 0; k < keys.size() && int64_t(k) < cap; ++k) {
+      counts[k] = cnt[k];
+      total_ms[k] = ms[k];
+      joined += keys[k];
+      joined += '\n';
+    }
+    VPG_REQUIRE(int64_t(joined.size()) < names_cap, VPG_ELIMIT, "profile name buffer too small");
+    memcpy(names, joined.c_str(), joined.size() + 1);
+  });
 }
 
 int vpg_rng_choice(vpg_pcg64* rng, int64_t n, int64_t m, int64_t* out) {

@@ -436,11 +436,13 @@ template <class T>
 void to_host(std::vector<T>& h, const T* d, size_t n, cudaStream_t s) {
   h.resize(n);
   if (n) VPG_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  count_transfer(0, n * sizeof(T));
 }
 template <class T>
 void to_device(T* d, const std::vector<T>& h, cudaStream_t s) {
   if (!h.empty())
     VPG_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  count_transfer(h.size() * sizeof(T), 0);
 }
 
 int bits_for(uint64_t max_value) {

@@ -20,6 +20,13 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 void count_launch(uint64_t n = 1);
+void count_transfer(uint64_t h2d, uint64_t d2h);
+
+// Optional per-kernel device timing (vpg_profile_*): CUDA events recorded on
+// the launching stream around each launch, aggregated by kernel name.
+bool profiling();
+int prof_begin(const char* name, cudaStream_t s);
+void prof_end(int token, cudaStream_t s);
 
 #define VPG_CUDA(expr)                                                                   \
   do {                                                                                   \
@@ -35,13 +42,15 @@ void count_launch(uint64_t n = 1);
   } while (0)
 
 // Launch wrapper: counts the launch and surfaces configuration errors.
-#define VPG_LAUNCH(kernel, grid, block, smem, stream, ...)            \
-  do {                                                                \
-    if ((grid) > 0) {                                                 \
-      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
-      ::vpg::count_launch();                                          \
-      VPG_CUDA(cudaGetLastError());                                   \
-    }                                                                 \
+#define VPG_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
+  do {                                                                     \
+    if ((grid) > 0) {                                                      \
+      const int _tok = ::vpg::profiling() ? ::vpg::prof_begin(#kernel, stream) : -1; \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);          \
+      if (_tok >= 0) ::vpg::prof_end(_tok, stream);                        \
+      ::vpg::count_launch();                                               \
+      VPG_CUDA(cudaGetLastError());                                        \
+    }                                                                      \
   } while (0)
 
 // Run `body`, translating exceptions into the C ABI's error codes.

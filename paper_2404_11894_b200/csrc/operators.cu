@@ -207,6 +207,7 @@ k_iterate(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
   const int wid = threadIdx.x >> 5;
   const int64_t nwarps = int64_t(gridDim.x) * kItWarps;
   float dmax[3] = {0.f, 0.f, 0.f}, smax[3] = {0.f, 0.f, 0.f};
+  unsigned nan_bits = 0;  // numpy's max propagates NaN per channel: remember it
 
   for (int64_t k = int64_t(blockIdx.x) * kItWarps + wid; k < m; k += nwarps) {
     const int32_t q0 = cl_off[k];
@@ -255,16 +256,21 @@ k_iterate(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
           old = make_float4(fmaf(A.x, pa.x, B.x), fmaf(A.y, pa.y, B.y), fmaf(A.z, pa.z, B.z), 0.f);
         }
         i_out[p] = make_float4(nx, ny, nz, 0.f);
-        dmax[0] = fmaxf(dmax[0], fabsf(nx - old.x));
-        dmax[1] = fmaxf(dmax[1], fabsf(ny - old.y));
-        dmax[2] = fmaxf(dmax[2], fabsf(nz - old.z));
-        smax[0] = fmaxf(smax[0], fabsf(nx));
-        smax[1] = fmaxf(smax[1], fabsf(ny));
-        smax[2] = fmaxf(smax[2], fabsf(nz));
+        const float dv[3] = {fabsf(nx - old.x), fabsf(ny - old.y), fabsf(nz - old.z)};
+        const float sv[3] = {fabsf(nx), fabsf(ny), fabsf(nz)};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (dv[c] != dv[c]) nan_bits |= 1u << c;
+          if (sv[c] != sv[c]) nan_bits |= 8u << c;
+          dmax[c] = fmaxf(dmax[c], dv[c]);
+          smax[c] = fmaxf(smax[c], sv[c]);
+        }
       }
     }
   }
   if (kMode != 0) return;
+  for (int off = 16; off; off >>= 1) nan_bits |= __shfl_xor_sync(0xFFFFFFFFu, nan_bits, off);
+  if (lane == 0 && nan_bits) atomicOr(&red[t * 8 + 6], nan_bits);
   float v[6] = {dmax[0], dmax[1], dmax[2], smax[0], smax[1], smax[2]};
 #pragma unroll
   for (int i = 0; i < 6; ++i)
@@ -285,8 +291,11 @@ __global__ void k_control(int t, double tol, const uint32_t* __restrict__ red,
                           const float* __restrict__ term_max, double* __restrict__ resid,
                           int32_t* __restrict__ ctl) {
   if (threadIdx.x != 0 || ctl[1]) return;
+  const unsigned nan_bits = red[t * 8 + 6];
   double worst = 0.0;
   for (int c = 0; c < 3; ++c) {
+    // a NaN channel never wins Python's max(worst, q) in the reference
+    if (nan_bits & ((1u | 8u) << c)) continue;
     const double delta = double(__uint_as_float(red[t * 8 + c]));
     double scale = double(fmaxf(__uint_as_float(red[t * 8 + 3 + c]), term_max[c]));
     scale = scale > 1e-12 ? scale : 1e-12;
@@ -544,6 +553,7 @@ void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
     VPG_CUDA(cudaMemcpyAsync(ctl_h, g->ctl.get(), sizeof(ctl_h), cudaMemcpyDeviceToHost, s));
     VPG_CUDA(cudaMemcpyAsync(residuals, g->resid.get(), sizeof(double) * iterations,
                              cudaMemcpyDeviceToHost, s));
+    count_transfer(0, sizeof(ctl_h) + sizeof(double) * iterations);
   } else if (iterations > 0) {
     // an empty graph: every residual is 0/1e-12 = 0 and the tol test stops at once
     for (int t = 0; t < iterations; ++t) residuals[t] = 0.0;
