@@ -149,7 +149,12 @@ typedef struct vpg_graph_info {
   int64_t n_classes;
   int64_t n_splits;    /* split-loop iterations performed (clustering.py:58-85) */
   int64_t n_fallback;  /* points resolved by the exact global search (clustering.py:142-147) */
-  double build_ms[8];  /* per-stage device/host timings of the last build (diagnostic) */
+  /* per-stage wall times of the last build when VPG_BUILD_TIMINGS is set: 0 classes,
+   * 1 center draw (host RNG), 2 grid + nearest center, 3 grouping, 4 split loop,
+   * 5 cluster layout, 6 operators */
+  double build_ms[8];
+  int64_t n_staged;     /* members of oversize groups sent to the host split loop */
+  int64_t split_visits; /* sum of group sizes over all splits (split-loop work) */
 } vpg_graph_info;
 
 /* flags for vpg_graph_build */

@@ -72,7 +72,8 @@ class Paths(C.Structure):
 
 class GraphInfo(C.Structure):
     _fields_ = [("n_records", c_i64), ("n_clusters", c_i64), ("nnz", c_i64), ("n_classes", c_i64),
-                ("n_splits", c_i64), ("n_fallback", c_i64), ("build_ms", c_f64 * 8)]
+                ("n_splits", c_i64), ("n_fallback", c_i64), ("build_ms", c_f64 * 8),
+                ("n_staged", c_i64), ("split_visits", c_i64)]
 
 
 def _arr(t, *dims):

@@ -1,5 +1,7 @@
 // extern "C" entry points of libvolpg_b200.so (declared in include/volpg_b200.h).
 #include <atomic>
+#include <map>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -88,6 +90,46 @@ void* dalloc(size_t bytes, cudaStream_t s) {
 
 void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
+}
+
+namespace {
+std::map<void*, size_t>& g_host_cap() {
+  static std::map<void*, size_t> caps;
+  return caps;
+}
+std::mutex g_host_mu;
+std::vector<std::pair<size_t, void*>> g_host_free;  // (capacity, pointer)
+}  // namespace
+
+void* halloc(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    size_t best = g_host_free.size();
+    for (size_t i = 0; i < g_host_free.size(); ++i)
+      if (g_host_free[i].first >= bytes &&
+          (best == g_host_free.size() || g_host_free[i].first < g_host_free[best].first))
+        best = i;
+    if (best < g_host_free.size() && g_host_free[best].first <= 4 * bytes + (1 << 20)) {
+      void* p = g_host_free[best].second;
+      g_host_free.erase(g_host_free.begin() + best);
+      return p;
+    }
+  }
+  const size_t cap = bytes < (1 << 20) ? (1 << 20) : bytes + bytes / 4;
+  void* p = nullptr;
+  if (cudaMallocHost(&p, cap) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(VPG_ENOMEM, "pinned host allocation failed");
+  }
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  g_host_cap()[p] = cap;
+  return p;
+}
+
+void hfree(void* p, size_t) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  g_host_free.emplace_back(g_host_cap()[p], p);
 }
 
 }  // namespace vpg
@@ -191,17 +233,21 @@ int vpg_split_groups(vpg_pcg64* rng, const double* pos, int64_t n_groups, const 
   return guarded([&] {
     vpg::Pcg64 g(*rng);
     std::vector<int64_t> over;
-    std::vector<std::vector<int64_t>> groups;
-    std::vector<int64_t> centers;
+    std::vector<int32_t> ids;
+    std::vector<double> xyz, cxyz;
+    std::vector<vpg::SplitGroup> groups;
     for (int64_t c = 0; c < n_groups; ++c) {
-      if (grp_off[c + 1] - grp_off[c] > max_size) {
-        over.push_back(c);
-        groups.emplace_back(grp_members + grp_off[c], grp_members + grp_off[c + 1]);
-        centers.push_back(grp_center[c]);
+      const int64_t size = grp_off[c + 1] - grp_off[c];
+      if (size <= max_size) continue;
+      over.push_back(c);
+      groups.push_back(vpg::SplitGroup{int64_t(ids.size()), size, grp_center[c]});
+      for (int a = 0; a < 3; ++a) cxyz.push_back(pos[grp_center[c] * 3 + a]);
+      for (int64_t t = grp_off[c]; t < grp_off[c + 1]; ++t) {
+        ids.push_back(int32_t(grp_members[t]));
+        for (int a = 0; a < 3; ++a) xyz.push_back(pos[grp_members[t] * 3 + a]);
       }
     }
-    vpg::split_oversize(g, groups, centers, max_size,
-                        [&](int64_t id) { return pos + size_t(id) * 3; });
+    vpg::split_oversize(g, ids.data(), xyz.data(), ids.size(), groups, max_size, cxyz.data());
     const int64_t total = n_groups + int64_t(groups.size()) - int64_t(over.size());
     VPG_REQUIRE(total <= cap_groups, VPG_ELIMIT, "output group capacity exceeded");
     int64_t w = 0, o = 0;
@@ -211,16 +257,17 @@ int vpg_split_groups(vpg_pcg64* rng, const double* pos, int64_t n_groups, const 
       for (const int64_t* p = b; p != e; ++p) out_members[o++] = *p;
       out_center[w++] = center;
     };
+    auto emit_split = [&](const vpg::SplitGroup& sg) {
+      std::vector<int64_t> wide(ids.begin() + sg.begin, ids.begin() + sg.begin + sg.size);
+      emit(wide.data(), wide.data() + wide.size(), sg.center);
+    };
     for (int64_t c = 0; c < n_groups; ++c) {
-      if (next < over.size() && over[next] == c) {
-        emit(groups[next].data(), groups[next].data() + groups[next].size(), centers[next]);
-        ++next;
-      } else {
+      if (next < over.size() && over[next] == c)
+        emit_split(groups[next++]);
+      else
         emit(grp_members + grp_off[c], grp_members + grp_off[c + 1], grp_center[c]);
-      }
     }
-    for (size_t k = over.size(); k < groups.size(); ++k)
-      emit(groups[k].data(), groups[k].data() + groups[k].size(), centers[k]);
+    for (size_t k = over.size(); k < groups.size(); ++k) emit_split(groups[k]);
     out_off[w] = o;
     *out_n_groups = w;
     g.store(rng);
@@ -235,8 +282,13 @@ int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng
     g->stream = as_stream(stream);
     g->rec = *rec;
     vpg::build_clusters(g, *rec, cluster_size, rng, (flags & VPG_BUILD_TIMINGS) != 0, g->stream);
+    const auto t0 = std::chrono::steady_clock::now();
     if (!(flags & VPG_BUILD_CLUSTERS_ONLY)) vpg::build_operators(g, *rec, g->stream);
-    if (flags & VPG_BUILD_TIMINGS) VPG_CUDA(cudaStreamSynchronize(g->stream));
+    if (flags & VPG_BUILD_TIMINGS) {
+      VPG_CUDA(cudaStreamSynchronize(g->stream));
+      g->info.build_ms[6] =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
     g->info.n_records = g->n;
     g->info.n_clusters = g->m;
     g->info.nnz = g->nnz;

@@ -278,29 +278,120 @@ __device__ __forceinline__ void scan_cell(const GridParams& gp, const CellEntry*
   }
 }
 
-// One thread per point: the reference's 27-cell candidate argmin.
-__global__ void k_assign(const int32_t* rows, int64_t row_off, int64_t n,
-                         const double* __restrict__ pos, GridParams gp,
-                         const CellEntry* __restrict__ table, const double4* __restrict__ spos,
-                         int32_t* __restrict__ assign, int32_t* __restrict__ fb_list,
-                         int32_t* fb_count) {
+
+// ------------------------------------------------ cell-sorted assignment
+constexpr int kCandCap = 128;  // candidate centers staged per warp
+constexpr int kAssignWarps = 8;
+
+// Sort key of a point's cell: a dense linear index over the padded grid when
+// the grid is packed, else the hashed key (ties only cost extra candidates).
+__device__ __forceinline__ unsigned long long sort_key(const GridParams& gp, long long x,
+                                                       long long y, long long z) {
+  if (gp.packed)
+    return (unsigned long long)(((x + 1) * (gp.dims[1] + 2) + (y + 1)) * (gp.dims[2] + 2) + (z + 1));
+  return cell_key(gp, x, y, z);
+}
+
+__global__ void k_point_keys(const int32_t* rows, int64_t row_off, int64_t n,
+                             const double* __restrict__ pos, GridParams gp,
+                             unsigned long long* __restrict__ keys, int32_t* __restrict__ ids) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = class_row(rows, row_off, i);
-    const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
-    const long long cx = cell_coord(px, gp.lo[0], gp.cell);
-    const long long cy = cell_coord(py, gp.lo[1], gp.cell);
-    const long long cz = cell_coord(pz, gp.lo[2], gp.cell);
-    Best b{INFINITY, 0x7FFFFFFF};
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dz = -1; dz <= 1; ++dz)
-          scan_cell(gp, table, spos, cx + dx, cy + dy, cz + dz, px, py, pz, b);
-    if (b.j == 0x7FFFFFFF || !(__dsqrt_rn(b.d2) < gp.cell)) {
-      fb_list[atomicAdd(fb_count, 1)] = int32_t(i);
-      assign[i] = -1;
+    keys[i] = sort_key(gp, cell_coord(pos[r * 3], gp.lo[0], gp.cell),
+                       cell_coord(pos[r * 3 + 1], gp.lo[1], gp.cell),
+                       cell_coord(pos[r * 3 + 2], gp.lo[2], gp.cell));
+    ids[i] = int32_t(i);
+  }
+}
+
+// One warp per run of points sharing a cell (points sorted by cell): lanes
+// 0..26 look up the 27 neighbour cells once, the candidate centers are staged
+// in shared memory, and every point of the run scans the same candidate set
+// -- exactly the reference's per-cell candidate list (clustering.py:121-137).
+__global__ void __launch_bounds__(kAssignWarps * 32)
+k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ pos, GridParams gp,
+               const CellEntry* __restrict__ table, const double4* __restrict__ spos,
+               const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ run_start,
+               const int32_t* __restrict__ run_len, const int32_t* __restrict__ n_runs,
+               int32_t* __restrict__ assign, int32_t* __restrict__ fb_list,
+               int32_t* __restrict__ fb_count) {
+  __shared__ double4 cand[kAssignWarps][kCandCap];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int runs = *n_runs;
+  const int warps = gridDim.x * kAssignWarps;
+  for (int run = blockIdx.x * kAssignWarps + wid; run < runs; run += warps) {
+    const int32_t b = run_start[run], len = run_len[run];
+    const int64_t r0 = class_row(rows, row_off, sorted_ids[b]);
+    const long long cx = cell_coord(pos[r0 * 3], gp.lo[0], gp.cell);
+    const long long cy = cell_coord(pos[r0 * 3 + 1], gp.lo[1], gp.cell);
+    const long long cz = cell_coord(pos[r0 * 3 + 2], gp.lo[2], gp.cell);
+    long long nx = 0, ny = 0, nz = 0;
+    int c_start = 0, c_cnt = 0;
+    if (lane < 27) {
+      nx = cx + lane / 9 - 1;
+      ny = cy + (lane / 3) % 3 - 1;
+      nz = cz + lane % 3 - 1;
+      const CellEntry* e = table_find(table, cell_key(gp, nx, ny, nz), gp.table_mask);
+      if (e) {
+        c_start = e->start;
+        c_cnt = e->end - e->start;
+      }
+    }
+    int incl = c_cnt;  // inclusive warp scan of candidate counts
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (total <= kCandCap) {
+      for (int t = 0; t < c_cnt; ++t) {
+        const double4 c = spos[c_start + t];
+        // hashed keys: a colliding cell's centers are filtered out here
+        const bool keep = gp.packed || (cell_coord(c.x, gp.lo[0], gp.cell) == nx &&
+                                        cell_coord(c.y, gp.lo[1], gp.cell) == ny &&
+                                        cell_coord(c.z, gp.lo[2], gp.cell) == nz);
+        cand[wid][incl - c_cnt + t] = keep ? c : make_double4(INFINITY, INFINITY, INFINITY,
+                                                              __longlong_as_double(0x7FFFFFFFLL));
+      }
+      __syncwarp();
+      for (int t = lane; t < len; t += 32) {
+        const int32_t i = sorted_ids[b + t];
+        const int64_t r = class_row(rows, row_off, i);
+        const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
+        Best best{INFINITY, 0x7FFFFFFF};
+        for (int q = 0; q < total; ++q) {
+          const double4 c = cand[wid][q];
+          const int j = int(__double_as_longlong(c.w));
+          if (j == 0x7FFFFFFF) continue;
+          best_update(best, dist2_exact(px, py, pz, c.x, c.y, c.z), j);
+        }
+        if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
+          fb_list[atomicAdd(fb_count, 1)] = i;
+          assign[i] = -1;
+        } else {
+          assign[i] = best.j;
+        }
+      }
+      __syncwarp();
     } else {
-      assign[i] = b.j;
+      // crowded neighbourhood: every lane scans the 27 cells itself
+      for (int t = lane; t < len; t += 32) {
+        const int32_t i = sorted_ids[b + t];
+        const int64_t r = class_row(rows, row_off, i);
+        const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
+        Best best{INFINITY, 0x7FFFFFFF};
+        for (int dx = -1; dx <= 1; ++dx)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dz = -1; dz <= 1; ++dz)
+              scan_cell(gp, table, spos, cx + dx, cy + dy, cz + dz, px, py, pz, best);
+        if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
+          fb_list[atomicAdd(fb_count, 1)] = i;
+          assign[i] = -1;
+        } else {
+          assign[i] = best.j;
+        }
+      }
     }
   }
 }
@@ -387,6 +478,27 @@ __global__ void k_histogram(const int32_t* __restrict__ assign, int64_t n, int32
     atomicAdd(&counts[assign[i]], 1);
 }
 
+struct Oversize {
+  const int32_t* counts;
+  int32_t limit;
+  __device__ bool operator()(int32_t j) const { return counts[j] > limit; }
+};
+
+// (group, count, start, center record) of the oversize groups, for the host.
+__global__ void k_oversize_info(const int32_t* __restrict__ over, const int32_t* __restrict__ n_over,
+                                const int32_t* __restrict__ counts,
+                                const int32_t* __restrict__ gstart,
+                                const int32_t* __restrict__ crec, int64_t* __restrict__ out) {
+  const int n = *n_over;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int j = over[k];
+    out[k * 4] = j;
+    out[k * 4 + 1] = counts[j];
+    out[k * 4 + 2] = gstart[j];
+    out[k * 4 + 3] = crec[j];
+  }
+}
+
 // Gather members (record id + position) of the oversize groups for the host.
 __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
                                   const int64_t* __restrict__ seg, int n_seg,
@@ -405,11 +517,55 @@ __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
   }
 }
 
-__global__ void k_square_sizes(const int32_t* __restrict__ size, int64_t m,
-                               int64_t* __restrict__ sq) {
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k <= m;
-       k += int64_t(gridDim.x) * blockDim.x)
-    sq[k] = k < m ? int64_t(size[k]) * size[k] : 0;
+// Entries of the final group list (clustering.py:87-93): class c's original
+// groups j occupy entries base_c + j, its split-off groups follow.
+__global__ void k_init_entries(const int32_t* __restrict__ counts, const int32_t* __restrict__ gstart,
+                               const int32_t* __restrict__ crec, int m, int64_t row_off,
+                               int64_t base, int32_t* __restrict__ e_size,
+                               int64_t* __restrict__ e_src, int32_t* __restrict__ e_center) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    e_size[base + j] = counts[j];
+    e_src[base + j] = row_off + gstart[j];
+    e_center[base + j] = crec[j];
+  }
+}
+
+// Split results: entry, size, source (-(1+offset) into the split buffer), center.
+__global__ void k_apply_entries(const int64_t* __restrict__ mods, int64_t n_mods,
+                                int32_t* __restrict__ e_size, int64_t* __restrict__ e_src,
+                                int32_t* __restrict__ e_center) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n_mods;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = mods[k * 4];
+    e_size[e] = int32_t(mods[k * 4 + 1]);
+    e_src[e] = mods[k * 4 + 2];
+    e_center[e] = int32_t(mods[k * 4 + 3]);
+  }
+}
+
+__global__ void k_entry_flags(const int32_t* __restrict__ e_size, int64_t n, int32_t* __restrict__ f) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    f[e] = e_size[e] > 0 ? 1 : 0;
+}
+
+// Non-empty entries -> clusters in entry order; sizes, sources, centers, and
+// the scan inputs for the member and kernel-block offsets.
+__global__ void k_compact_entries(const int32_t* __restrict__ e_size, const int64_t* __restrict__ e_src,
+                                  const int32_t* __restrict__ e_center,
+                                  const int32_t* __restrict__ cid, int64_t n_entries,
+                                  int32_t* __restrict__ cl_size, int64_t* __restrict__ cl_src,
+                                  int32_t* __restrict__ cl_center, int64_t* __restrict__ sq) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_entries;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t s = e_size[e];
+    if (s <= 0) continue;
+    const int32_t k = cid[e];
+    cl_size[k] = s;
+    cl_src[k] = e_src[e];
+    cl_center[k] = e_center[e];
+    sq[k] = int64_t(s) * s;
+  }
 }
 
 // Cluster-major permutation: warp per cluster copies its member list.
@@ -480,6 +636,41 @@ void cub_call(F&& f, cudaStream_t s) {
   count_launch(2);
 }
 
+struct ClassPlan {
+  int64_t n, row_off, m, center_off;
+  double lo[3], hi[3];
+};
+
+// The reference's grid for one class: lo/cell as clustering.py:102-106 (host
+// fp64, glibc pow like Python's float pow), plus the device table geometry.
+GridParams make_grid(const ClassPlan& p) {
+  GridParams gp{};
+  gp.m = int(p.m);
+  double extent[3];
+  for (int a = 0; a < 3; ++a) {
+    extent[a] = p.hi[a] - p.lo[a];
+    gp.lo[a] = p.lo[a];
+  }
+  double volume = std::max(extent[0], 1e-12) * std::max(extent[1], 1e-12);
+  volume = volume * std::max(extent[2], 1e-12);
+  gp.cell = std::max(std::pow(volume / double(p.m), 1.0 / 3.0), 1e-9);
+  bool fits = true;
+  gp.max_dim = 0;
+  for (int a = 0; a < 3; ++a) {
+    const double d = std::floor(extent[a] / gp.cell) + 2.0;
+    fits = fits && (d + 2.0 < 2097152.0);
+    gp.dims[a] = d < 9.0e18 ? (long long)d : (long long)9.0e18;
+    gp.max_dim = std::max(gp.max_dim, gp.dims[a]);
+  }
+  gp.packed = fits ? 1 : 0;
+  // u = (p-lo)/cell carries a relative error of a few ulp; allow 2^-44 * |u|
+  gp.slack = 2.0 * (double(std::min<long long>(gp.max_dim, 1LL << 52)) + 4.0) * 5.7e-14;
+  uint64_t cap = 1024;
+  while (cap < uint64_t(p.m) * 2) cap <<= 1;
+  gp.table_mask = cap - 1;
+  return gp;
+}
+
 }  // namespace
 
 void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng_state,
@@ -508,7 +699,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
     return;
   }
 
-  // ---- classes (np.unique order of kind<<32 | class_id)
+  // ---- classes (np.unique order of kind<<32 | class_id, graph.py:59)
   const int nbits_words = 2 * kSlotsPerKind / 32;
   DBuf<uint32_t> bitmap(nbits_words + 1, s);
   VPG_CUDA(cudaMemsetAsync(bitmap.get(), 0, bitmap.bytes(), s));
@@ -566,10 +757,6 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   VPG_CUDA(cudaStreamSynchronize(s));
   clk.mark(0);
 
-  struct ClassPlan {
-    int64_t n, row_off, m, center_off;
-    double lo[3], hi[3];
-  };
   std::vector<ClassPlan> plan(n_cls);
   int64_t row_off = 0, center_total = 0;
   for (int c = 0; c < n_cls; ++c) {
@@ -586,40 +773,70 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
     }
   }
 
-  // group storage for all classes (records grouped by center, class by class)
+  // per-class working storage (records grouped by center, class by class)
   DBuf<int32_t> grp_rec(n, s), assign(n, s), values(n, s), fb_list(n, s);
-  DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s);
-  DBuf<int32_t> fb_count(1, s);
+  DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s), gstart_all(center_total, s);
+  DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
 
-  // host-side final group lists
-  struct SplitOut {
-    std::vector<int64_t> modified_idx;               // original group index (class-local)
-    std::vector<std::vector<int64_t>> groups;        // modified first, then appended
-    std::vector<int64_t> centers;                    // record ids, same order
-  };
-  std::vector<SplitOut> splits(n_cls);
-  std::vector<std::vector<int32_t>> counts_h(n_cls), crec_h(n_cls);
+  std::vector<int32_t> split_rec;  // members of every split group, back to back
+  std::vector<int64_t> mods;       // (entry offset within class, size, src, center) x4
+  std::vector<int64_t> class_mod_begin(n_cls + 1, 0), class_appended(n_cls, 0);
   int64_t n_splits = 0;
-  std::vector<int32_t> zero1(1, 0);
+  const int64_t max_size = 2 * int64_t(K);
 
   for (int c = 0; c < n_cls; ++c) {
     const ClassPlan& p = plan[c];
     const int m = int(p.m);
-    std::vector<int64_t> picks(m);
-    rng_choice(rng, p.n, p.m, picks.data());
-    std::vector<int32_t> picks32(picks.begin(), picks.end());
-    DBuf<int32_t> d_local(m, s);
-    to_device(d_local.get(), picks32, s);
-    int32_t* assign_c = assign.get() + p.row_off;
     const int32_t* rows_p = rows.get();
+    int32_t* assign_c = assign.get() + p.row_off;
+    GridParams gp = make_grid(p);
+
+    // device: cell keys of the points and their sort, independent of the
+    // center draw, overlap the host RNG
+    DBuf<unsigned long long> pkeys, pkeys_sorted;
+    DBuf<int32_t> pids, pids_sorted, run_start, run_len;
+    int end_bits = 64;
+    if (m > 1) {
+      pkeys.alloc(p.n, s);
+      pkeys_sorted.alloc(p.n, s);
+      pids.alloc(p.n, s);
+      pids_sorted.alloc(p.n, s);
+      run_start.alloc(p.n + 1, s);
+      run_len.alloc(p.n + 1, s);
+      VPG_LAUNCH(k_point_keys, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n, rec.pos,
+                 gp, pkeys.get(), pids.get());
+      if (gp.packed)
+        end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
+      const int64_t nn = p.n;
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, pkeys.get(), pkeys_sorted.get(), pids.get(),
+                                               pids_sorted.get(), int(nn), 0, end_bits, s);
+      }, s);
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted.get(), pkeys.get(),
+                                                  run_len.get(), scalars.get() + 1, int(nn), s);
+      }, s);
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, run_len.get(), run_start.get(), int(nn), s);
+      }, s);
+    }
+
+    // host: m centers = Generator.choice(n, m) (clustering.py:51)
+    HostBuf<int64_t> picks(m);
+    HostBuf<int32_t> picks32(m);
+    rng_choice(rng, p.n, p.m, picks.get());
+    for (int j = 0; j < m; ++j) picks32[j] = int32_t(picks[j]);
+    DBuf<int32_t> d_local(m, s);
+    VPG_CUDA(cudaMemcpyAsync(d_local.get(), picks32.get(), sizeof(int32_t) * m,
+                             cudaMemcpyHostToDevice, s));
+    count_transfer(sizeof(int32_t) * m, 0);
+    clk.mark(1);
 
     DBuf<double> cpos(size_t(m) * 3, s);
     DBuf<unsigned long long> keys(m, s), skeys(m, s);
     DBuf<int32_t> ids(m, s), sids(m, s);
     DBuf<double4> spos(m, s);
-    GridParams gp{};
-    gp.m = m;
     if (m == 1) {
       // a single center takes every point (clustering.py:100-101)
       gp.cell = 1.0;
@@ -628,30 +845,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                  cpos.get(), crec_all.get() + p.center_off, keys.get(), ids.get());
       VPG_CUDA(cudaMemsetAsync(assign_c, 0, sizeof(int32_t) * p.n, s));
     } else {
-      double volume = 1.0;
-      double extent[3];
-      for (int a = 0; a < 3; ++a) {
-        extent[a] = p.hi[a] - p.lo[a];
-        gp.lo[a] = p.lo[a];
-      }
-      volume = std::max(extent[0], 1e-12) * std::max(extent[1], 1e-12);
-      volume = volume * std::max(extent[2], 1e-12);
-      gp.cell = std::max(std::pow(volume / double(m), 1.0 / 3.0), 1e-9);
-      bool fits = true;
-      gp.max_dim = 0;
-      for (int a = 0; a < 3; ++a) {
-        const double d = std::floor(extent[a] / gp.cell) + 2.0;
-        fits = fits && (d + 2.0 < 2097152.0);
-        gp.dims[a] = d < 9.0e18 ? (long long)d : (long long)9.0e18;
-        gp.max_dim = std::max(gp.max_dim, gp.dims[a]);
-      }
-      gp.packed = fits ? 1 : 0;
-      // u = (p-lo)/cell carries a relative error of a few ulp; allow 2^-44 * |u|
-      gp.slack = 2.0 * (double(std::min<long long>(gp.max_dim, 1LL << 52)) + 4.0) * 5.7e-14;
-      uint64_t cap = 1024;
-      while (cap < uint64_t(m) * 2) cap <<= 1;
-      gp.table_mask = cap - 1;
-      DBuf<CellEntry> table(cap, s);
+      DBuf<CellEntry> table(gp.table_mask + 1, s);
       VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
       VPG_LAUNCH(k_center_setup, grid_for(m, block), block, 0, s, d_local.get(), m, rows_p,
                  p.row_off, rec.pos, gp, cpos.get(), crec_all.get() + p.center_off, keys.get(),
@@ -664,22 +858,20 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                  cpos.get(), m, gp, spos.get(), table.get());
       VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
                  table.get());
-      to_device(fb_count.get(), zero1, s);
-      VPG_LAUNCH(k_assign, grid_for(p.n, block, sm_count() * 16), block, 0, s, rows_p, p.row_off,
-                 p.n, rec.pos, gp, table.get(), spos.get(), assign_c, fb_list.get(),
-                 fb_count.get());
+      VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
+      VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
+                 rec.pos, gp, table.get(), spos.get(), pids_sorted.get(), run_start.get(),
+                 run_len.get(), scalars.get() + 1, assign_c, fb_list.get(), scalars.get());
       VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
-                 table.get(), spos.get(), fb_list.get(), fb_count.get(), assign_c);
-      std::vector<int32_t> h_fb;
-      to_host(h_fb, fb_count.get(), 1, s);
-      VPG_CUDA(cudaStreamSynchronize(s));
-      g->info.n_fallback += h_fb[0];
+                 table.get(), spos.get(), fb_list.get(), scalars.get(), assign_c);
     }
-    clk.mark(1);
+    clk.mark(2);
 
-    // groups: stable sort of this class's records by center
+    // groups: stable sort of this class's records by center (clustering.py:55)
     VPG_LAUNCH(k_group_values, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
                values.get() + p.row_off);
+    int32_t* counts_c = counts_all.get() + p.center_off;
+    int32_t* gstart_c = gstart_all.get() + p.center_off;
     {
       DBuf<int32_t> sorted_keys(p.n, s);
       const int end_bit = bits_for(uint64_t(m > 1 ? m - 1 : 1));
@@ -691,146 +883,170 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                                                int(nn), 0, end_bit, s);
       }, s);
     }
-    int32_t* counts_c = counts_all.get() + p.center_off;
     VPG_LAUNCH(k_histogram, grid_for(p.n, block), block, 0, s, assign_c, p.n, counts_c);
-    to_host(counts_h[c], counts_c, m, s);
-    to_host(crec_h[c], crec_all.get() + p.center_off, m, s);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, counts_c, gstart_c, m, s);
+    }, s);
+    // oversize groups (> 2K members), in ascending group order
+    DBuf<int32_t> over(m, s);
+    DBuf<int64_t> over_info(size_t(m) * 4, s);
+    {
+      cub::CountingInputIterator<int32_t> it(0);
+      Oversize pred{counts_c, int32_t(max_size)};
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceSelect::If(t, b, it, over.get(), scalars.get() + 2, m, pred, s);
+      }, s);
+    }
+    VPG_LAUNCH(k_oversize_info, grid_for(m, block), block, 0, s, over.get(), scalars.get() + 2,
+               counts_c, gstart_c, crec_all.get() + p.center_off, over_info.get());
+    std::vector<int32_t> h_scalars;
+    to_host(h_scalars, scalars.get(), 4, s);
     VPG_CUDA(cudaStreamSynchronize(s));
-    clk.mark(2);
+    g->info.n_fallback += h_scalars[0];
+    const int n_over = h_scalars[2];
+    clk.mark(3);
 
     // ---- split loop on the oversize groups (host, exact RNG order)
-    const int64_t max_size = 2 * int64_t(K);
-    std::vector<int64_t> seg;  // (src, count, dst)
-    std::vector<int64_t> over_idx;
-    int64_t off = 0, staged = 0;
-    for (int j = 0; j < m; ++j) {
-      const int64_t cnt = counts_h[c][j];
-      if (cnt > max_size) {
-        over_idx.push_back(j);
-        seg.push_back(p.row_off + off);
-        seg.push_back(cnt);
-        seg.push_back(staged);
-        staged += cnt;
+    class_mod_begin[c] = int64_t(mods.size()) / 4;
+    if (n_over > 0) {
+      std::vector<int64_t> info;
+      to_host(info, over_info.get(), size_t(n_over) * 4, s);
+      VPG_CUDA(cudaStreamSynchronize(s));
+      std::vector<int64_t> seg(size_t(n_over) * 3);
+      std::vector<int32_t> h_crec_over(n_over);
+      int64_t staged = 0;
+      for (int k = 0; k < n_over; ++k) {
+        seg[k * 3] = p.row_off + info[k * 4 + 2];
+        seg[k * 3 + 1] = info[k * 4 + 1];
+        seg[k * 3 + 2] = staged;
+        h_crec_over[k] = int32_t(info[k * 4 + 3]);
+        staged += info[k * 4 + 1];
       }
-      off += cnt;
-    }
-    SplitOut& so = splits[c];
-    if (!over_idx.empty()) {
       DBuf<int64_t> d_seg(seg.size(), s);
       to_device(d_seg.get(), seg, s);
       DBuf<int32_t> d_srec(staged, s);
       DBuf<double> d_spos(staged * 3, s);
-      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(int64_t(over_idx.size()), 65535), 128, 0, s,
-                 grp_rec.get(), d_seg.get(), int(over_idx.size()), rec.pos, d_srec.get(),
-                 d_spos.get());
-      std::vector<int32_t> h_srec;
-      std::vector<double> h_spos, h_cpos;
-      to_host(h_srec, d_srec.get(), staged, s);
-      to_host(h_spos, d_spos.get(), staged * 3, s);
-      to_host(h_cpos, cpos.get(), size_t(m) * 3, s);
+      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec.get(),
+                 d_seg.get(), n_over, rec.pos, d_srec.get(), d_spos.get());
+      HostBuf<int32_t> h_srec(staged);
+      HostBuf<double> xyz(staged * 3);
+      VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec.get(), sizeof(int32_t) * staged,
+                               cudaMemcpyDeviceToHost, s));
+      VPG_CUDA(cudaMemcpyAsync(xyz.get(), d_spos.get(), sizeof(double) * 3 * staged,
+                               cudaMemcpyDeviceToHost, s));
+      count_transfer(0, 28 * staged);
       VPG_CUDA(cudaStreamSynchronize(s));
-      // ids in the split loop: staged member index (>= 0) or -(1+j) for an
-      // original center that is not among the staged members.
-      std::vector<std::vector<int64_t>> groups(over_idx.size());
-      std::vector<int64_t> centers(over_idx.size());
-      std::vector<int64_t> id_rec;  // staged index -> record id
-      id_rec.assign(h_srec.begin(), h_srec.end());
-      for (size_t k = 0; k < over_idx.size(); ++k) {
-        const int64_t base = seg[k * 3 + 2], cnt = seg[k * 3 + 1];
-        groups[k].resize(cnt);
-        for (int64_t t = 0; t < cnt; ++t) groups[k][t] = base + t;
-        // the center compares by record id: find it among the members
-        const int32_t crec = crec_h[c][over_idx[k]];
-        int64_t cid = -(1 + over_idx[k]);
-        for (int64_t t = 0; t < cnt; ++t)
-          if (h_srec[base + t] == crec) {
-            cid = base + t;
-            break;
-          }
-        centers[k] = cid;
+      // initial center positions: the center is one of its group's members
+      // except with coincident centers (then it is fetched by record id)
+      std::vector<SplitGroup> groups(n_over);
+      std::vector<double> c0(size_t(n_over) * 3);
+      for (int k = 0; k < n_over; ++k) {
+        const int64_t b = seg[k * 3 + 2], cnt = seg[k * 3 + 1];
+        groups[k] = SplitGroup{b, cnt, h_crec_over[k]};
+        int64_t t = b;
+        while (t < b + cnt && h_srec[t] != h_crec_over[k]) ++t;
+        if (t < b + cnt) {
+          for (int a = 0; a < 3; ++a) c0[k * 3 + a] = xyz[t * 3 + a];
+        } else {
+          VPG_CUDA(cudaMemcpy(&c0[k * 3], rec.pos + int64_t(h_crec_over[k]) * 3,
+                              3 * sizeof(double), cudaMemcpyDeviceToHost));
+          count_transfer(0, 24);
+        }
       }
-      auto pos_of = [&](int64_t id) -> const double* {
-        return id >= 0 ? &h_spos[size_t(id) * 3] : &h_cpos[size_t(-1 - id) * 3];
-      };
-      n_splits += split_oversize(rng, groups, centers, max_size, pos_of);
-      so.modified_idx = over_idx;
-      so.groups.resize(groups.size());
-      so.centers.resize(groups.size());
+      g->info.n_staged += staged;
+      n_splits += split_oversize(rng, h_srec.get(), xyz.get(), size_t(staged), groups, max_size,
+                                 c0.data(), &g->info.split_visits);
+      const int64_t base_split = int64_t(split_rec.size());
+      split_rec.insert(split_rec.end(), h_srec.get(), h_srec.get() + staged);
       for (size_t k = 0; k < groups.size(); ++k) {
-        so.groups[k].resize(groups[k].size());
-        for (size_t t = 0; t < groups[k].size(); ++t) so.groups[k][t] = id_rec[groups[k][t]];
-        const int64_t cid = centers[k];
-        so.centers[k] = cid >= 0 ? id_rec[cid] : crec_h[c][-1 - cid];
+        const int64_t entry = k < size_t(n_over) ? info[k * 4] : p.m + int64_t(k) - n_over;
+        mods.push_back(entry);
+        mods.push_back(groups[k].size);
+        mods.push_back(-1 - (base_split + groups[k].begin));
+        mods.push_back(groups[k].center);
       }
+      class_appended[c] = int64_t(groups.size()) - n_over;
     }
-    clk.mark(3);
+    class_mod_begin[c + 1] = int64_t(mods.size()) / 4;
+    clk.mark(4);
   }
   g->info.n_splits = n_splits;
   rng.store(rng_state);
 
-  // ---- final cluster table (clustering.py:87-93)
-  std::vector<int32_t> cl_size;
-  std::vector<int64_t> cl_src;
-  std::vector<int32_t> cl_center;
-  std::vector<int32_t> split_rec;
-  cl_size.reserve(center_total + n_splits);
-  cl_src.reserve(center_total + n_splits);
-  cl_center.reserve(center_total + n_splits);
+  // ---- final group list -> clusters (clustering.py:87-93), on the device
+  std::vector<int64_t> entry_base(n_cls + 1, 0);
+  for (int c = 0; c < n_cls; ++c) entry_base[c + 1] = entry_base[c] + plan[c].m + class_appended[c];
+  const int64_t F = entry_base[n_cls];
+  DBuf<int32_t> e_size(F + 1, s), e_center(F + 1, s), e_flag(F + 1, s), e_cid(F + 1, s);
+  DBuf<int64_t> e_src(F + 1, s);
   for (int c = 0; c < n_cls; ++c) {
     const ClassPlan& p = plan[c];
-    const SplitOut& so = splits[c];
-    size_t next_mod = 0;
-    int64_t off = 0;
-    auto emit_split = [&](size_t k) {
-      const std::vector<int64_t>& mem = so.groups[k];
-      cl_size.push_back(int32_t(mem.size()));
-      cl_src.push_back(-1 - int64_t(split_rec.size()));
-      cl_center.push_back(int32_t(so.centers[k]));
-      for (int64_t r : mem) split_rec.push_back(int32_t(r));
-    };
-    for (int64_t j = 0; j < p.m; ++j) {
-      const int64_t cnt = counts_h[c][j];
-      if (next_mod < so.modified_idx.size() && so.modified_idx[next_mod] == j) {
-        emit_split(next_mod);  // modified original keeps its slot
-        ++next_mod;
-      } else if (cnt > 0) {
-        cl_size.push_back(int32_t(cnt));
-        cl_src.push_back(p.row_off + off);
-        cl_center.push_back(crec_h[c][j]);
-      }
-      off += cnt;
-    }
-    for (size_t k = so.modified_idx.size(); k < so.groups.size(); ++k) emit_split(k);
+    VPG_LAUNCH(k_init_entries, grid_for(p.m, block), block, 0, s, counts_all.get() + p.center_off,
+               gstart_all.get() + p.center_off, crec_all.get() + p.center_off, int(p.m),
+               p.row_off, entry_base[c], e_size.get(), e_src.get(), e_center.get());
+    for (int64_t k = class_mod_begin[c]; k < class_mod_begin[c + 1]; ++k) mods[k * 4] += entry_base[c];
   }
-  const int64_t M = int64_t(cl_size.size());
-  g->m = M;
-  g->max_cluster = cl_size.empty() ? 0 : *std::max_element(cl_size.begin(), cl_size.end());
-
-  DBuf<int32_t> d_size(M + 1, s);
-  DBuf<int64_t> d_src(M, s), d_sq(M + 1, s);
+  const int64_t n_mods = int64_t(mods.size()) / 4;
+  DBuf<int64_t> d_mods(mods.size() + 1, s);
   DBuf<int32_t> d_split(split_rec.size() + 1, s);
-  to_device(d_size.get(), cl_size, s);
-  VPG_CUDA(cudaMemsetAsync(d_size.get() + M, 0, sizeof(int32_t), s));
-  to_device(d_src.get(), cl_src, s);
-  to_device(d_split.get(), split_rec, s);
-  g->cl_center.alloc(M, s);
-  to_device(g->cl_center.get(), cl_center, s);
-  g->cl_off.alloc(M + 1, s);
-  g->w_off.alloc(M + 1, s);
+  HostBuf<int64_t> hm;  // staging stays alive until the final synchronisation below
+  HostBuf<int32_t> hs;
+  if (n_mods) {
+    hm.alloc(mods.size());
+    hs.alloc(split_rec.size());
+    std::copy(mods.begin(), mods.end(), hm.get());
+    std::copy(split_rec.begin(), split_rec.end(), hs.get());
+    VPG_CUDA(cudaMemcpyAsync(d_mods.get(), hm.get(), sizeof(int64_t) * mods.size(),
+                             cudaMemcpyHostToDevice, s));
+    VPG_CUDA(cudaMemcpyAsync(d_split.get(), hs.get(), sizeof(int32_t) * split_rec.size(),
+                             cudaMemcpyHostToDevice, s));
+    count_transfer(8 * mods.size() + 4 * split_rec.size(), 0);
+    VPG_LAUNCH(k_apply_entries, grid_for(n_mods, block), block, 0, s, d_mods.get(), n_mods,
+               e_size.get(), e_src.get(), e_center.get());
+  }
+  VPG_CUDA(cudaMemsetAsync(e_size.get() + F, 0, sizeof(int32_t), s));
+  VPG_LAUNCH(k_entry_flags, grid_for(F + 1, block), block, 0, s, e_size.get(), F + 1, e_flag.get());
   cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, d_size.get(), g->cl_off.get(), int(M + 1), s);
+    return cub::DeviceScan::ExclusiveSum(t, b, e_flag.get(), e_cid.get(), int(F + 1), s);
   }, s);
-  VPG_LAUNCH(k_square_sizes, grid_for(M + 1, block), block, 0, s, d_size.get(), M, d_sq.get());
+  // M = e_cid[F]; clusters <= F
+  DBuf<int32_t> cl_size(F + 1, s);
+  DBuf<int64_t> cl_src(F + 1, s), d_sq(F + 1, s);
+  g->cl_center.alloc(F + 1, s);
+  VPG_CUDA(cudaMemsetAsync(d_sq.get(), 0, d_sq.bytes(), s));
+  VPG_CUDA(cudaMemsetAsync(cl_size.get(), 0, cl_size.bytes(), s));
+  VPG_LAUNCH(k_compact_entries, grid_for(F, block), block, 0, s, e_size.get(), e_src.get(),
+             e_center.get(), e_cid.get(), F, cl_size.get(), cl_src.get(), g->cl_center.get(),
+             d_sq.get());
+  g->cl_off.alloc(F + 1, s);
+  g->w_off.alloc(F + 1, s);
   cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, d_sq.get(), g->w_off.get(), int(M + 1), s);
+    return cub::DeviceScan::ExclusiveSum(t, b, cl_size.get(), g->cl_off.get(), int(F + 1), s);
   }, s);
-  VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), d_src.get(), M,
-             grp_rec.get(), d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
-  std::vector<int64_t> nnz_h;
-  to_host(nnz_h, g->w_off.get() + M, 1, s);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, d_sq.get(), g->w_off.get(), int(F + 1), s);
+  }, s);
+  DBuf<int32_t> d_max(1, s);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceReduce::Max(t, b, cl_size.get(), d_max.get(), int(F + 1), s);
+  }, s);
+  int32_t h_m = 0, h_max = 0;
+  VPG_CUDA(cudaMemcpyAsync(&h_m, e_cid.get() + F, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   VPG_CUDA(cudaStreamSynchronize(s));
-  g->nnz = nnz_h[0];
-  clk.mark(4);
+  count_transfer(0, 8);
+  const int64_t M = h_m;
+  g->m = M;
+  g->max_cluster = h_max;
+  // w_off / cl_off beyond M repeat the totals (sizes there are 0)
+  VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), cl_src.get(), M,
+             grp_rec.get(), d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
+  int64_t h_nnz = 0;
+  VPG_CUDA(cudaMemcpyAsync(&h_nnz, g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaStreamSynchronize(s));
+  count_transfer(0, 8);
+  g->nnz = h_nnz;
+  clk.mark(5);
 }
 
 }  // namespace vpg

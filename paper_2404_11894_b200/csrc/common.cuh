@@ -108,6 +108,34 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// Page-locked host staging (cudaMallocHost), recycled through a process-wide
+// cache so repeated builds do not pay for pinning.
+void* halloc(size_t bytes);
+void hfree(void* p, size_t bytes);
+
+template <class T>
+struct HostBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  HostBuf() = default;
+  explicit HostBuf(size_t count) { alloc(count); }
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    ptr = static_cast<T*>(halloc(count * sizeof(T) + 16));
+  }
+  void release() {
+    if (ptr) hfree(ptr, n * sizeof(T) + 16);
+    ptr = nullptr;
+    n = 0;
+  }
+  T* get() const { return ptr; }
+  T& operator[](size_t i) const { return ptr[i]; }
+};
+
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;
   if (g > max_blocks) g = max_blocks;

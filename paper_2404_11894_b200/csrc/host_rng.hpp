@@ -13,7 +13,10 @@
 // tests/test_rng.py.
 #pragma once
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
+#include <memory>
+#include <stdexcept>
 #include <vector>
 
 #include "../../include/volpg_b200.h"
@@ -96,65 +99,68 @@ struct Pcg64 {
   }
 };
 
-// Open-addressing map int64 -> int64 for the sparse Fisher-Yates tail.
-class SparseSwap {
+// Open-addressing map of the positions a partial Fisher-Yates has written
+// (int32 position -> int32 value, packed in one int64; -1 = empty slot).
+class SwapTable {
  public:
-  explicit SparseSwap(size_t expected) {
-    size_t cap = 16;
+  explicit SwapTable(size_t expected) {
+    size_t cap = 1024;
     while (cap < expected * 2) cap <<= 1;
-    keys_.assign(cap, -1);
-    vals_.resize(cap);
+    slots_.assign(cap, -1);
     mask_ = cap - 1;
   }
-  int64_t get(int64_t k) const {
+  size_t slot(int64_t k) const { return size_t(uint32_t(k) * 0x9E3779B1u) & mask_; }
+  void prefetch(int64_t k) const { __builtin_prefetch(&slots_[slot(k)]); }
+  int64_t get(int64_t k) const {  // value at position k (k itself if never written)
     size_t h = slot(k);
-    while (keys_[h] != -1) {
-      if (keys_[h] == k) return vals_[h];
+    for (;;) {
+      const int64_t e = slots_[h];
+      if (e == -1) return k;
+      if ((e >> 32) == k) return int64_t(int32_t(uint32_t(e)));
       h = (h + 1) & mask_;
     }
-    return k;
   }
   void put(int64_t k, int64_t v) {
     size_t h = slot(k);
-    while (keys_[h] != -1 && keys_[h] != k) h = (h + 1) & mask_;
-    keys_[h] = k;
-    vals_[h] = v;
+    while (slots_[h] != -1 && (slots_[h] >> 32) != k) h = (h + 1) & mask_;
+    slots_[h] = (k << 32) | int64_t(uint32_t(v));
   }
 
  private:
-  size_t slot(int64_t k) const {
-    uint64_t z = uint64_t(k) * 0x9E3779B97F4A7C15ull;
-    return size_t(z ^ (z >> 29)) & mask_;
-  }
-  std::vector<int64_t> keys_, vals_;
+  std::vector<int64_t> slots_;
   size_t mask_;
 };
 
 // Generator.choice(n, m, replace=False): numpy uses a partial Fisher-Yates
 // over arange(n) when n > 10000 and m > n // 50, else Floyd's algorithm
-// followed by a shuffle of the m picks.
+// followed by a shuffle of the m picks.  The swap targets depend only on the
+// random stream, so they are drawn first and the swaps replayed over a
+// compact table of written positions (prefetched a few steps ahead).
 inline void rng_choice(Pcg64& g, int64_t n, int64_t m, int64_t* out) {
   if (m <= 0) return;
+  if (n >= (int64_t(1) << 31)) throw std::length_error("choice population exceeds 2^31");
   if (n > 10000 && m > n / 50) {
-    SparseSwap perm(size_t(m) * 2);
     const int64_t stop = (n - m) > 1 ? (n - m) : 1;
-    for (int64_t i = n - 1; i >= stop; --i) {
-      const int64_t j = int64_t(g.bounded(uint64_t(i)));
-      const int64_t at_i = perm.get(i);
-      const int64_t at_j = perm.get(j);
-      perm.put(j, at_i);
-      out[i - (n - m)] = at_j;
+    const int64_t steps = n - stop;
+    std::vector<int32_t> target(size_t(steps > 0 ? steps : 0));
+    for (int64_t k = 0; k < steps; ++k) target[k] = int32_t(g.bounded(uint64_t(n - 1 - k)));
+    SwapTable tab{size_t(m)};
+    for (int64_t k = 0; k < steps; ++k) {
+      if (k + 8 < steps) tab.prefetch(target[k + 8]);
+      const int64_t i = n - 1 - k, j = target[k];
+      const int64_t at_i = tab.get(i);
+      out[i - (n - m)] = tab.get(j);
+      tab.put(j, at_i);
     }
-    if (n - m == 0) out[0] = perm.get(0);  // position 0 is never a swap source
+    if (n - m == 0) out[0] = tab.get(0);  // position 0 is never a swap source
     return;
   }
-  // Floyd: pick an unseen value for each slot (j itself on a repeat), then
-  // shuffle the picks.  `seen` maps value -> -1 as a set marker.
-  SparseSwap seen(size_t(m) * 2);
+  // Floyd: an unseen value per slot (j itself on a repeat), then a shuffle.
+  SwapTable seen{size_t(m)};  // value -> marker -2 (as a set)
   for (int64_t j = n - m; j < n; ++j) {
     int64_t v = int64_t(g.bounded(uint64_t(j)));
-    if (seen.get(v) == -1) v = j;
-    seen.put(v, -1);
+    if (seen.get(v) == -2) v = j;
+    seen.put(v, -2);
     out[j - (n - m)] = v;
   }
   for (int64_t i = m - 1; i >= 1; --i) {
@@ -174,58 +180,106 @@ inline double dist2(const double* a, const double* b) {
   return (dx * dx + dy * dy) + dz * dz;
 }
 
+// A group of the split loop: a contiguous range of the flat member arrays.
+struct SplitGroup {
+  int64_t begin, size;
+  int64_t center;  // member id of the center
+};
+
 // The LIFO split loop of clustering.py:58-85 over the oversize groups of one
-// compatibility class.  `groups` holds the oversize groups in ascending
-// original group order, each with ascending member ids; `centers` their
-// center ids.  `pos(id)` returns a pointer to the id's xyz.  On return,
-// groups[0..q) are the (modified) originals and groups[q..) the split-off
-// groups in append order; centers is extended alongside.  Returns the number
-// of splits performed.
-template <class PosFn>
-int64_t split_oversize(Pcg64& g, std::vector<std::vector<int64_t>>& groups,
-                       std::vector<int64_t>& centers, int64_t max_size, PosFn pos) {
+// compatibility class, on flat arrays.  `ids` holds the members of the
+// oversize groups back to back (each group ascending, groups in ascending
+// original order); `xyz` their positions (3 doubles per slot, moved with the
+// ids).  `groups` describes them; `center_xyz[3k..3k+3)` is the position of
+// groups[k].center.
+// Each split partitions its range in place (stable: kept members first), so
+// every final group stays a contiguous ascending range.  The squared
+// distance of each member to its current center is cached: a split only
+// evaluates the distance to the new center, and moved members inherit it.
+// On return groups[0..q) are the originals (possibly shrunk) and groups[q..)
+// the split-off groups in append order.  Returns the number of splits.
+inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
+                              std::vector<SplitGroup>& groups, int64_t max_size,
+                              const double* center_xyz, int64_t* visits = nullptr) {
+  std::unique_ptr<double[]> d0(new double[total + 1]), d1(new double[total + 1]);
+  for (size_t k = 0; k < groups.size(); ++k) {
+    const SplitGroup& gr = groups[k];
+    for (int64_t t = gr.begin; t < gr.begin + gr.size; ++t)
+      d0[t] = dist2(&xyz[t * 3], center_xyz + k * 3);
+  }
   std::vector<int64_t> stack;
   for (int64_t c = 0; c < int64_t(groups.size()); ++c)
-    if (int64_t(groups[c].size()) > max_size) stack.push_back(c);
-  std::vector<int64_t> cand, keep, moved;
+    if (groups[c].size > max_size) stack.push_back(c);
+  std::vector<int32_t> tid;
+  std::vector<double> txyz, td;
   int64_t splits = 0;
   while (!stack.empty()) {
     const int64_t c = stack.back();
     stack.pop_back();
-    const std::vector<int64_t>& mem = groups[c];
-    if (int64_t(mem.size()) <= max_size) continue;
-    const int64_t old_center = centers[c];
-    cand.clear();
-    for (int64_t x : mem)
-      if (x != old_center) cand.push_back(x);
-    const std::vector<int64_t>& pool = cand.empty() ? mem : cand;
-    const int64_t pick = int64_t(g.bounded(uint64_t(pool.size()) - 1));
-    const int64_t new_center = pool[size_t(pick)];
-    const double* p0 = pos(old_center);
-    const double* p1 = pos(new_center);
-    keep.clear();
-    moved.clear();
-    for (int64_t x : mem) {
-      const double* px = pos(x);
-      // np.argmin over (old, new): ties stay with the old center
-      if (dist2(px, p1) < dist2(px, p0))
-        moved.push_back(x);
-      else
-        keep.push_back(x);
+    const SplitGroup gr = groups[c];
+    if (gr.size <= max_size) continue;
+    const int64_t b = gr.begin, e = gr.begin + gr.size;
+    if (visits) *visits += gr.size;
+    // candidates = members != old center, in member order (clustering.py:65-67)
+    int64_t at = -1;
+    for (int64_t t = b; t < e; ++t)
+      if (ids[t] == gr.center) {
+        at = t - b;
+        break;
+      }
+    const int64_t pool = at >= 0 ? gr.size - 1 : gr.size;
+    int64_t pick;
+    if (pool > 0) {
+      pick = int64_t(g.bounded(uint64_t(pool) - 1));
+      if (at >= 0 && pick >= at) ++pick;
+    } else {
+      pick = int64_t(g.bounded(uint64_t(gr.size) - 1));
     }
-    if (keep.empty() || moved.empty()) {
-      const size_t half = mem.size() / 2;
-      keep.assign(mem.begin(), mem.begin() + half);
-      moved.assign(mem.begin() + half, mem.end());
+    const int64_t new_center = ids[b + pick];
+    const double pn[3] = {xyz[(b + pick) * 3], xyz[(b + pick) * 3 + 1], xyz[(b + pick) * 3 + 2]};
+    double* __restrict__ dd0 = d0.get();
+    double* __restrict__ dd1 = d1.get();
+    int64_t moved = 0;
+    for (int64_t t = b; t < e; ++t) {
+      const double v = dist2(&xyz[t * 3], pn);
+      dd1[t] = v;
+      moved += v < dd0[t];  // np.argmin over (old, new): ties stay
+    }
+    const int64_t kept = gr.size - moved;
+    if (kept == 0 || moved == 0) {
+      // coincident points: halves (clustering.py:75-78); the second half
+      // takes the new center, so its cached distance becomes d1
+      const int64_t half = gr.size / 2;
+      for (int64_t t = b + half; t < e; ++t) dd0[t] = dd1[t];
+      groups[c].size = half;
+      groups.push_back(SplitGroup{b + half, gr.size - half, new_center});
+    } else {
+      if (int64_t(tid.size()) < gr.size) {
+        tid.resize(gr.size);
+        td.resize(gr.size);
+        txyz.resize(gr.size * 3);
+      }
+      int64_t wk = 0, wm = kept;
+      for (int64_t t = b; t < e; ++t) {
+        const bool go = dd1[t] < dd0[t];
+        const int64_t w = go ? wm : wk;
+        wm += go;
+        wk += !go;
+        tid[w] = ids[t];
+        td[w] = go ? dd1[t] : dd0[t];
+        txyz[w * 3] = xyz[t * 3];
+        txyz[w * 3 + 1] = xyz[t * 3 + 1];
+        txyz[w * 3 + 2] = xyz[t * 3 + 2];
+      }
+      std::memcpy(ids + b, tid.data(), sizeof(int32_t) * gr.size);
+      std::memcpy(dd0 + b, td.data(), sizeof(double) * gr.size);
+      std::memcpy(xyz + b * 3, txyz.data(), sizeof(double) * 3 * gr.size);
+      groups[c].size = kept;
+      groups.push_back(SplitGroup{b + kept, moved, new_center});
     }
     ++splits;
-    const bool keep_big = int64_t(keep.size()) > max_size;
-    const bool moved_big = int64_t(moved.size()) > max_size;
-    groups[c] = keep;
-    groups.push_back(moved);
-    centers.push_back(new_center);
-    if (keep_big) stack.push_back(c);
-    if (moved_big) stack.push_back(int64_t(groups.size()) - 1);
+    if (groups[c].size > max_size) stack.push_back(c);
+    if (groups.back().size > max_size) stack.push_back(int64_t(groups.size()) - 1);
   }
   return splits;
 }

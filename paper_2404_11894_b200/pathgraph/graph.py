@@ -165,7 +165,8 @@ class PathGraph:
         gi = self.native.info()
         return {"n_records": gi.n_records, "n_clusters": gi.n_clusters, "nnz": gi.nnz,
                 "n_classes": gi.n_classes, "n_splits": gi.n_splits,
-                "n_fallback": gi.n_fallback, "build_ms": list(gi.build_ms)}
+                "n_fallback": gi.n_fallback, "build_ms": list(gi.build_ms),
+                "n_staged": gi.n_staged, "split_visits": gi.split_visits}
 
 
 def build_graph(out: TraceOutput, cluster_size: int, seed: int = 0, timings: bool = False) -> PathGraph:

@@ -152,3 +152,30 @@ def test_divergence_is_detected(cuda):
     _, _, r_ref, _ = O.solve(og2, 6, 0.0)
     g2 = build_graph(TraceOutput(None, RecordSoA(**rec2), PathSoA(**paths), 16, 16, 4), 32)
     np.testing.assert_allclose(solve(g2, iterations=6, tol=0.0).residuals, r_ref, rtol=1e-4)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_cluster_points_edge_cases_match_oracle(cuda, seed):
+    """Coincident points (the halves branch), dense clumps (crowded cells and
+    deep split chains), a flat class (hashed grid), isolated far points (the
+    exact shell search / brute force), several classes, K in {2, 8, 32}."""
+    from paper_2404_11894_b200.pathgraph import cluster_points
+
+    rs = np.random.default_rng(seed)
+    blobs = [rs.normal(size=(4000, 3)),
+             rs.normal(size=(3000, 3)) * 1e-3 + 5.0,                       # dense clump
+             np.repeat(rs.normal(size=(1, 3)), 300, axis=0),                # coincident
+             np.c_[rs.random(2000), np.full(2000, 0.25), rs.random(2000)],  # flat
+             rs.normal(size=(40, 3)) * 50.0]                                # far outliers
+    pos = np.concatenate(blobs)
+    keys = np.concatenate([np.full(len(b), k % 3) for k, b in enumerate(blobs)]).astype(np.int64)
+    keys[3000:3100] = 7  # a small class
+    for K in (2, 8, 32):
+        r_ref = np.random.default_rng(10 + seed)
+        r_gpu = np.random.default_rng(10 + seed)
+        cid_ref, cl_ref = O.cluster_points(pos, keys, K, r_ref)
+        cid, cl = cluster_points(pos, keys, K, r_gpu)
+        assert np.array_equal(cid, cid_ref), K
+        assert [c.center for c in cl] == [c.center for c in cl_ref]
+        assert r_gpu.bit_generator.state == r_ref.bit_generator.state
+        assert max(len(c.members) for c in cl) <= 2 * K
