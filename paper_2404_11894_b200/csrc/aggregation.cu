@@ -1,0 +1,328 @@
+// Build of the aggregation operators (graph.py:94-168) on the device.
+//
+//   k_pack_members  one coalesced pass over the records (record order) that
+//                   transposes what the operators need into a 192-byte
+//                   member struct at the record's cluster-major position
+//                   (full-sector scattered writes instead of ~17 scattered
+//                   field reads per member), plus the continuation parent and
+//                   terminal flag of each row.
+//   k_aggregate     one CTA per cluster: member geometry staged in shared
+//                   memory, every pair's strategy densities evaluated once in
+//                   fp64 (HG at g >= 0.9 needs it) and cached as
+//                   fp32 for the second pass; p-hat column sums in fp64 with
+//                   a fixed reduction order; the s x s kernel block W written
+//                   transposed, D-bar and the per-row solve vectors.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace vpg {
+namespace {
+
+constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
+constexpr double kInvPi = 1.0 / 3.14159265358979323846;
+constexpr int kAggThreads = 128;
+
+struct __align__(32) Member {
+  double ax, ay, az;  // -omega_out (volume) or the oriented normal (surface)
+  double px, py, pz;  // phase_dir
+  double ex, ey, ez;  // emit_dir
+  double g, pdf_eap, pdf_e;
+  float de[3], dp[3];  // d_emit, d_phase
+  float coeff[3], wc[3];
+  float ipt[3];
+  int32_t par;     // cluster-major position of the continuation parent, -1 at depth 0
+  uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface
+  uint32_t pad[7];
+};
+static_assert(sizeof(Member) == 192, "Member must stay 6 sectors");
+
+__device__ __forceinline__ double dot3(double ax, double ay, double az, double bx, double by,
+                                       double bz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
+}
+
+__device__ __forceinline__ float4 f4(double x, double y, double z) {
+  return make_float4(float(x), float(y), float(z), 0.f);
+}
+
+__global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpos,
+                               Member* __restrict__ out, float* __restrict__ term_max) {
+  const int64_t n = rec.n;
+  const int lane = threadIdx.x & 31;
+  float tmax[3] = {0.f, 0.f, 0.f};
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    Member m;
+    const bool volume = rec.kind[r] == 0;
+    if (volume) {
+      m.ax = -rec.omega_out[r * 3];
+      m.ay = -rec.omega_out[r * 3 + 1];
+      m.az = -rec.omega_out[r * 3 + 2];
+    } else {
+      m.ax = rec.normal[r * 3];
+      m.ay = rec.normal[r * 3 + 1];
+      m.az = rec.normal[r * 3 + 2];
+    }
+    m.px = rec.phase_dir[r * 3];
+    m.py = rec.phase_dir[r * 3 + 1];
+    m.pz = rec.phase_dir[r * 3 + 2];
+    m.ex = rec.emit_dir[r * 3];
+    m.ey = rec.emit_dir[r * 3 + 1];
+    m.ez = rec.emit_dir[r * 3 + 2];
+    m.g = rec.g[r];
+    m.pdf_eap = rec.pdf_emit_at_phase[r];
+    m.pdf_e = rec.pdf_emit[r];
+    for (int c = 0; c < 3; ++c) {
+      m.de[c] = float(rec.d_emit[r * 3 + c]);
+      m.dp[c] = float(rec.d_phase[r * 3 + c]);
+      m.coeff[c] = float(rec.coeff[r * 3 + c]);
+      m.wc[c] = float(rec.w_cont[r * 3 + c]);
+      m.ipt[c] = float(rec.i_pt[r * 3 + c]);
+    }
+    const int64_t pid = rec.path_idx[r];
+    m.par = (r > 0 && rec.path_idx[r - 1] == pid) ? clpos[r - 1] : -1;
+    const bool terminal = !(r + 1 < n && rec.path_idx[r + 1] == pid);
+    m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u);
+    for (int i = 0; i < 7; ++i) m.pad[i] = 0;
+    out[clpos[r]] = m;
+    if (terminal)
+      for (int c = 0; c < 3; ++c) tmax[c] = fmaxf(tmax[c], fabsf(m.ipt[c]));
+  }
+  for (int c = 0; c < 3; ++c) {
+    float v = tmax[c];
+    for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
+    if (lane == 0 && v > 0.f) atomicMax(reinterpret_cast<unsigned int*>(&term_max[c]), __float_as_uint(v));
+  }
+}
+
+// Member l's strategy density toward direction d (graph.py:82-91), fp64 in
+// the reference's rounding order.
+__device__ __forceinline__ double strategy_pdf(const double* __restrict__ geo, int S, int l,
+                                               bool volume, double dx, double dy, double dz) {
+  const double cs = dot3(geo[l], geo[S + l], geo[2 * S + l], dx, dy, dz);
+  if (!volume) return cs > 0.0 ? __dmul_rn(cs, kInvPi) : 0.0;
+  const double den = __dsub_rn(geo[10 * S + l], __dmul_rn(geo[11 * S + l], cs));
+  // num / (den * sqrt(den)) as num * rsqrt(den)^3: within ~2 ulp of the
+  // reference's sqrt-and-divide, at a fraction of the fp64 issue cost
+  const double rs = rsqrt(den);
+  return geo[9 * S + l] * (rs * rs * rs);
+}
+
+// Dynamic shared memory for clusters of up to S members:
+//   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2
+//   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
+//   pd, pe  S*(S+1) floats each (pair densities, row-padded)
+__global__ void __launch_bounds__(kAggThreads)
+k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
+            const int64_t* __restrict__ w_off, int64_t m, int64_t n, int S,
+            float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
+            float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
+            float4* __restrict__ i0_o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* geo = reinterpret_cast<double*>(smem);
+  double* wts = geo + 12 * S;
+  float* pd = reinterpret_cast<float*>(wts + 7 * S);
+  float* pe = pd + S * (S + 1);
+  __shared__ int s_volume;
+  const int tid = threadIdx.x;
+
+  for (int64_t k = blockIdx.x; k < m; k += gridDim.x) {
+    const int32_t q0 = cl_off[k];
+    const int s = cl_off[k + 1] - q0;
+    const int64_t wb = w_off[k];
+    for (int l = tid; l < s; l += blockDim.x) {
+      const Member& mb = mem[q0 + l];
+      geo[l] = mb.ax;
+      geo[S + l] = mb.ay;
+      geo[2 * S + l] = mb.az;
+      geo[3 * S + l] = mb.px;
+      geo[4 * S + l] = mb.py;
+      geo[5 * S + l] = mb.pz;
+      geo[6 * S + l] = mb.ex;
+      geo[7 * S + l] = mb.ey;
+      geo[8 * S + l] = mb.ez;
+      const double g = mb.g;
+      const double g2 = __dmul_rn(g, g);
+      geo[9 * S + l] = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
+      geo[10 * S + l] = __dadd_rn(1.0, g2);
+      geo[11 * S + l] = __dmul_rn(2.0, g);
+      if (l == 0) s_volume = (mb.flags & 4u) ? 0 : 1;
+    }
+    __syncthreads();
+    const bool volume = s_volume != 0;
+    const double ks = double(s);
+
+    // pass 1: columns j, P threads per column (P = 4 for s <= 32, else 2) each
+    // summing a contiguous slice of l; the slices combine in a fixed order
+    // (((p0 + p1) + (p2 + p3))), so p-hat is deterministic.  The loop trip
+    // count is uniform so every lane reaches the shuffles.
+    const int P = s <= 32 ? 4 : 2;
+    const int slice = (s + P - 1) / P;
+    for (int base = 0; base < P * s; base += blockDim.x) {
+      const int t = base + tid;
+      const bool active = t < P * s;
+      const int j = t / P, h = t % P;
+      double sp = 0.0, se = 0.0;
+      if (active) {
+        const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
+        const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
+        const int l0 = h * slice, l1 = min(s, l0 + slice);
+        for (int l = l0; l < l1; ++l) {
+          const double a = strategy_pdf(geo, S, l, volume, dpx, dpy, dpz);
+          const double b = strategy_pdf(geo, S, l, volume, dex, dey, dez);
+          pd[l * (S + 1) + j] = float(a);
+          pe[l * (S + 1) + j] = float(b);
+          sp = __dadd_rn(sp, a);
+          se = __dadd_rn(se, b);
+        }
+      }
+      sp = __dadd_rn(sp, __shfl_xor_sync(0xFFFFFFFFu, sp, 1));
+      se = __dadd_rn(se, __shfl_xor_sync(0xFFFFFFFFu, se, 1));
+      if (P == 4) {
+        sp = __dadd_rn(sp, __shfl_xor_sync(0xFFFFFFFFu, sp, 2));
+        se = __dadd_rn(se, __shfl_xor_sync(0xFFFFFFFFu, se, 2));
+      }
+      if (active && h == 0) {
+        const Member& mb = mem[q0 + j];
+        const double p_ind = sp;
+        const double p_dp = __dadd_rn(p_ind, __dmul_rn(ks, mb.pdf_eap));
+        const double p_de = (mb.flags & 1u) ? ks : __dadd_rn(se, __dmul_rn(ks, mb.pdf_e));
+        const int64_t q = q0 + j;
+        phat[q] = p_ind;
+        phat[n + q] = p_dp;
+        phat[2 * n + q] = p_de;
+        const bool inc_p = isfinite(p_ind) && p_ind > 0.0;
+        const bool inc_e = isfinite(p_de) && p_de > 0.0;
+        const bool ok_dp = inc_p && isfinite(p_dp) && p_dp > 0.0;
+        const double ie = inc_e ? __ddiv_rn(1.0, p_de) : 0.0;
+        const double ip = ok_dp ? __ddiv_rn(1.0, p_dp) : 0.0;
+        wts[j] = inc_p ? __ddiv_rn(1.0, p_ind) : 0.0;
+        wts[S + j] = double(mb.de[0]) * ie;
+        wts[2 * S + j] = double(mb.de[1]) * ie;
+        wts[3 * S + j] = double(mb.de[2]) * ie;
+        wts[4 * S + j] = double(mb.dp[0]) * ip;
+        wts[5 * S + j] = double(mb.dp[1]) * ip;
+        wts[6 * S + j] = double(mb.dp[2]) * ip;
+      }
+    }
+    __syncthreads();
+
+    // pass 2a: the kernel block, transposed (wt[wb + j*s + r] = W[r, j])
+    for (int idx = tid; idx < s * s; idx += blockDim.x) {
+      const int j = idx / s, r = idx - j * s;
+      wt[wb + idx] = float(double(pd[r * (S + 1) + j]) * wts[j]);
+    }
+    // pass 2b: rows: D-bar and the solve vectors
+    for (int r = tid; r < s; r += blockDim.x) {
+      double dx = 0.0, dy = 0.0, dz = 0.0;
+      const float* prow = pd + r * (S + 1);
+      const float* erow = pe + r * (S + 1);
+      for (int j = 0; j < s; ++j) {
+        const double a = prow[j], b = erow[j];
+        dx += b * wts[S + j] + a * wts[4 * S + j];
+        dy += b * wts[2 * S + j] + a * wts[5 * S + j];
+        dz += b * wts[3 * S + j] + a * wts[6 * S + j];
+      }
+      const Member& mb = mem[q0 + r];
+      const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
+      const double bx = kx * dx, by = ky * dy, bz = kz * dz;
+      const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
+      const int64_t q = q0 + r;
+      dbar_o[q] = f4(bx, by, bz);
+      coeff_o[q] = f4(kx, ky, kz);
+      rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
+                                  __int_as_float(mb.par));
+      rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
+      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
+    }
+    __syncthreads();
+  }
+}
+
+// Solve chunks (see graph.cuh): cost prefix and the first cluster of each chunk.
+__global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, int64_t m,
+                             int64_t* __restrict__ cost) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k <= m;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    if (k == m) { cost[k] = 0; continue; }
+    const int64_t s = cl_off[k + 1] - cl_off[k];
+    cost[k] = ((s * s + 3) & ~int64_t(3)) + 16 * s;
+  }
+}
+
+__global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_t n_chunks,
+                              int64_t chunk_floats, int32_t* __restrict__ first) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c <= n_chunks;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    if (c == n_chunks) { first[c] = int32_t(m); continue; }
+    const int64_t target = c * chunk_floats;
+    int64_t lo = 0, hi = m;  // first k with cst[k] >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cst[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    first[c] = int32_t(lo);
+  }
+}
+
+}  // namespace
+
+void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool timings) {
+  auto t_start = std::chrono::steady_clock::now();
+  const int64_t n = g->n, m = g->m;
+  const int S = std::max(1, g->max_cluster);
+  const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
+  VPG_REQUIRE(smem <= 200 * 1024, VPG_ELIMIT,
+              "clusters larger than 160 members (cluster_size > 80) are not supported");
+  g->wt.alloc(size_t(g->wt_len > 0 ? g->wt_len : 1), s);
+  g->phat.alloc(size_t(3 * n + 1), s);
+  for (auto* v : {&g->i0, &g->dbar, &g->coeff, &g->ibuf[0], &g->ibuf[1], &g->acc[0], &g->acc[1]})
+    v->alloc(size_t(n + 1), s);
+  g->rows.alloc(size_t(2 * n + 2), s);
+  g->term_max.alloc(4, s);
+  VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
+  if (n == 0) return;
+  DBuf<Member> members(size_t(n), s);
+  VPG_LAUNCH(k_pack_members, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), members.get(),
+             g->term_max.get());
+  static bool attr_set = false;
+  if (!attr_set) {
+    VPG_CUDA(cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr_set = true;
+  }
+  const int64_t blocks = std::min<int64_t>(m, int64_t(sm_count()) * 16);
+  VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, members.get(), g->cl_off.get(),
+             g->w_off.get(), m, n, S, g->wt.get(), g->phat.get(), g->dbar.get(), g->coeff.get(),
+             g->rows.get(), g->i0.get());
+  if (timings) {
+    VPG_CUDA(cudaStreamSynchronize(s));
+    g->info.build_ms[7] =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  }
+  // solve chunks
+  DBuf<int64_t> cost(m + 1, s), cst(m + 1, s);
+  VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), m, cost.get());
+  {
+    size_t bytes = 0;
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cost.get(), cst.get(), int(m + 1), s));
+    DBuf<char> tmp(bytes, s);
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, cost.get(), cst.get(), int(m + 1), s));
+    count_launch(1);
+  }
+  int64_t total = 0;
+  VPG_CUDA(cudaMemcpyAsync(&total, cst.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaStreamSynchronize(s));
+  count_transfer(0, 8);
+  g->n_chunks = (total + kChunkFloats - 1) / kChunkFloats;
+  g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
+  VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst.get(), m, g->n_chunks,
+             int64_t(kChunkFloats), g->chunk_first.get());
+}
+
+}  // namespace vpg

@@ -478,6 +478,10 @@ __global__ void k_histogram(const int32_t* __restrict__ assign, int64_t n, int32
     atomicAdd(&counts[assign[i]], 1);
 }
 
+struct SquareOp {
+  __host__ __device__ int64_t operator()(int32_t s) const { return int64_t(s) * s; }
+};
+
 struct Oversize {
   const int32_t* counts;
   int32_t limit;
@@ -564,7 +568,7 @@ __global__ void k_compact_entries(const int32_t* __restrict__ e_size, const int6
     cl_size[k] = s;
     cl_src[k] = e_src[e];
     cl_center[k] = e_center[e];
-    sq[k] = int64_t(s) * s;
+    sq[k] = (int64_t(s) * s + 3) & ~int64_t(3);  // blocks start 16-byte aligned
   }
 }
 
@@ -1041,11 +1045,21 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   // w_off / cl_off beyond M repeat the totals (sizes there are 0)
   VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), cl_src.get(), M,
              grp_rec.get(), d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
+  int64_t h_len = 0;
+  VPG_CUDA(cudaMemcpyAsync(&h_len, g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  DBuf<int64_t> d_nnz(1, s);
+  {
+    cub::TransformInputIterator<int64_t, SquareOp, const int32_t*> sq_it(cl_size.get(), SquareOp());
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceReduce::Sum(t, b, sq_it, d_nnz.get(), int(M > 0 ? M : 1), s);
+    }, s);
+  }
   int64_t h_nnz = 0;
-  VPG_CUDA(cudaMemcpyAsync(&h_nnz, g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_nnz, d_nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VPG_CUDA(cudaStreamSynchronize(s));
-  count_transfer(0, 8);
-  g->nnz = h_nnz;
+  count_transfer(0, 16);
+  g->nnz = M > 0 ? h_nnz : 0;
+  g->wt_len = h_len;
   clk.mark(5);
 }
 

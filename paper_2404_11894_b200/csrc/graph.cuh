@@ -6,29 +6,37 @@
 //   clpos[r]     int32   record -> cluster-major position (inverse of perm)
 //   cluster_id[r]int32   record -> cluster number (reference numbering)
 //   cl_off[k]    int32   (M+1) start of cluster k in cluster-major order
-//   w_off[k]     int64   (M+1) start of cluster k's dense kernel block
+//   w_off[k]     int64   (M+1) start of cluster k's dense kernel block (blocks
+//                        padded to 4 floats so every block is 16-byte aligned)
 //   wt[]         float   nnz   per cluster an s x s block stored transposed:
 //                        wt[w_off + j*s + r] = W[r, j] = rho_r(w_j)/phat_ind[j]
 //                        (graph.py:143-148), columns implicit
 //   phat[3][N]   double  phat_ind / phat_dir_phase / phat_dir_emit, cluster-major
-//   Solve vectors, cluster-major float4 (xyz = RGB):
-//     i0   = i_pt, a = w_cont*coeff, b = w_cont*D-bar, dbar = D-bar, coeff
-//     par[q] int32: position of the continuation parent (record r-1 on the same
-//     path), -1 for a path's first record.  Row q propagates into par[q]:
-//       I[par] = w_cont[q] * (coeff[q] * (W I)[q] + D-bar[q]) = a*acc + b
+//   Solve vectors, cluster-major (xyz = RGB):
+//     rows[q]  RowStatic {a = w_cont*coeff, b = w_cont*D-bar, par}: 32 bytes,
+//              par = position of the continuation parent (record r-1 on the
+//              same path), -1 for a path's first record.  Row q propagates
+//              into par:  I[par] = w_cont*(coeff*(W I)[q] + D-bar[q]) = a*acc + b
+//     i0 = i_pt, dbar = D-bar, coeff (float4)
 //   ibuf[2], acc[2]: double-buffered I and W*I (acc = i_bar / coeff).
+//   chunk_first[c]: first cluster of solve chunk c; chunks cut the cost prefix
+//     sum(pad4(s^2) + 16 s) floats at multiples of kChunkFloats, so one chunk's
+//     kernel blocks + row data fit a shared-memory stage (TMA bulk copies).
 #pragma once
 #include "common.cuh"
 
 struct vpg_graph {
   cudaStream_t stream = nullptr;
-  int64_t n = 0, m = 0, nnz = 0;
+  int64_t n = 0, m = 0, nnz = 0, wt_len = 0;
   int32_t K = 0;
-  vpg::DBuf<int32_t> perm, clpos, cluster_id, cl_off, cl_center, par;
+  vpg::DBuf<int32_t> perm, clpos, cluster_id, cl_off, cl_center;
   vpg::DBuf<int64_t> w_off;
   vpg::DBuf<float> wt;
   vpg::DBuf<double> phat;
-  vpg::DBuf<float4> i0, a, b, dbar, coeff, ibuf[2], acc[2];
+  vpg::DBuf<float4> i0, dbar, coeff, ibuf[2], acc[2];
+  vpg::DBuf<float4> rows;  // 2 float4 per row: (a.xyz, par bits), (b.xyz, 0)
+  vpg::DBuf<int32_t> chunk_first;
+  int64_t n_chunks = 0;
   vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows
   // solve state (device): red[t*8 + 0..5] float bits, ctl = {performed, stop, grow, diverged}
   vpg::DBuf<uint32_t> red;
@@ -43,9 +51,11 @@ struct vpg_graph {
 };
 
 namespace vpg {
+// floats of kernel blocks + row data per solve chunk (one shared-memory stage)
+constexpr int kChunkFloats = 8192;
 // cluster.cu: fills perm/clpos/cluster_id/cl_off/w_off/cl_center.
 void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng,
                     bool timings, cudaStream_t s);
 // operators.cu: marginals, kernel blocks, D-bar and solve vectors.
-void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s);
+void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool timings = false);
 }  // namespace vpg

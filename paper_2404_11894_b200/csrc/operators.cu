@@ -1,11 +1,6 @@
-// Aggregation operators, the device-resident fixed-point solve, and the splat.
+// The device-resident fixed-point solve, operator application, exports and the splat.
 //
-//   k_operators   compute_marginals (graph.py:94-120) + _build_operators
-//                 (graph.py:123-168): per cluster, p-hat for every member
-//                 sample, the s x s kernel block W (stored transposed, fp32),
-//                 D-bar, and the per-row solve vectors.  fp64 arithmetic
-//                 (HG at g >= 0.9 needs it), numpy's rounding
-//                 order for dot products.
+//   (the operators themselves are built in aggregation.cu)
 //   k_iterate     one fixed-point iteration (solve.py:78-83): block-dense
 //                 W*I per cluster, propagation along the continuation edge
 //                 (operators.py:41-47) fused as a scatter into the parent
@@ -27,33 +22,11 @@ namespace {
 constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 constexpr double kInvPi = 1.0 / 3.14159265358979323846;
 constexpr int kWarpCap = 64;  // members staged per warp in shared memory
-constexpr int kOpWarps = 4;   // warps per block in k_operators
-constexpr int kItWarps = 8;   // warps per block in k_iterate
 
 // numpy's einsum order for a length-3 contraction, no FMA.
 __device__ __forceinline__ double dot3(double ax, double ay, double az, double bx, double by,
                                        double bz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
-}
-
-// Member cache in shared memory (structure of arrays, one warp's cluster).
-struct MemberCache {
-  double ax[kWarpCap], ay[kWarpCap], az[kWarpCap];  // -omega_out (volume) or normal
-  double px[kWarpCap], py[kWarpCap], pz[kWarpCap];  // phase_dir
-  double ex[kWarpCap], ey[kWarpCap], ez[kWarpCap];  // emit_dir
-  double num[kWarpCap], c1[kWarpCap], c2[kWarpCap]; // HG: INV4PI(1-g^2), 1+g^2, 2g
-  double inv_p[kWarpCap];                            // 1/phat_ind or 0 (excluded)
-  double wex[kWarpCap], wey[kWarpCap], wez[kWarpCap];  // d_emit / phat_dir_emit
-  double wpx[kWarpCap], wpy[kWarpCap], wpz[kWarpCap];  // d_phase / phat_dir_phase
-};
-
-// Member l's strategy density toward direction d (graph.py:82-91).
-__device__ __forceinline__ double strategy_pdf(const MemberCache& c, int l, bool volume,
-                                               double dx, double dy, double dz) {
-  const double cs = dot3(c.ax[l], c.ay[l], c.az[l], dx, dy, dz);
-  if (!volume) return cs > 0.0 ? __dmul_rn(cs, kInvPi) : 0.0;
-  const double den = __dsub_rn(c.c1[l], __dmul_rn(c.c2[l], cs));
-  return __ddiv_rn(c.num[l], __dmul_rn(den, __dsqrt_rn(den)));
 }
 
 __device__ __forceinline__ double hg_pdf(double cs, double g) {
@@ -71,217 +44,279 @@ __device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
   atomicMax(reinterpret_cast<unsigned int*>(addr), __float_as_uint(v));
 }
 
-// One warp per cluster (s <= kWarpCap).
-__global__ void __launch_bounds__(kOpWarps * 32)
-k_operators(vpg_records rec, const int32_t* __restrict__ perm, const int32_t* __restrict__ clpos,
-            const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off, int64_t m,
-            int64_t n, float* __restrict__ wt, double* __restrict__ phat,
-            float4* __restrict__ dbar_o, float4* __restrict__ coeff_o, float4* __restrict__ a_o,
-            float4* __restrict__ b_o, float4* __restrict__ i0_o, int32_t* __restrict__ par_o,
-            float* __restrict__ term_max) {
-  __shared__ MemberCache cache[kOpWarps];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  MemberCache& c = cache[wid];
-  const int64_t nwarps = int64_t(gridDim.x) * kOpWarps;
-  float tmax[3] = {0.f, 0.f, 0.f};
-
-  for (int64_t k = int64_t(blockIdx.x) * kOpWarps + wid; k < m; k += nwarps) {
-    const int32_t q0 = cl_off[k];
-    const int s = cl_off[k + 1] - q0;
-    const int64_t wb = w_off[k];
-    const bool volume = rec.kind[perm[q0]] == 0;
-    const double ks = double(s);
-
-    // stage member geometry
-    for (int l = lane; l < s; l += 32) {
-      const int64_t r = perm[q0 + l];
-      if (volume) {
-        c.ax[l] = -rec.omega_out[r * 3];
-        c.ay[l] = -rec.omega_out[r * 3 + 1];
-        c.az[l] = -rec.omega_out[r * 3 + 2];
-        const double g = rec.g[r];
-        const double g2 = __dmul_rn(g, g);
-        c.num[l] = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
-        c.c1[l] = __dadd_rn(1.0, g2);
-        c.c2[l] = __dmul_rn(2.0, g);
-      } else {
-        c.ax[l] = rec.normal[r * 3];
-        c.ay[l] = rec.normal[r * 3 + 1];
-        c.az[l] = rec.normal[r * 3 + 2];
-      }
-      c.px[l] = rec.phase_dir[r * 3];
-      c.py[l] = rec.phase_dir[r * 3 + 1];
-      c.pz[l] = rec.phase_dir[r * 3 + 2];
-      c.ex[l] = rec.emit_dir[r * 3];
-      c.ey[l] = rec.emit_dir[r * 3 + 1];
-      c.ez[l] = rec.emit_dir[r * 3 + 2];
-    }
-    __syncwarp();
-
-    // pass 1: marginals of every member sample (column j)
-    for (int j = lane; j < s; j += 32) {
-      const int64_t r = perm[q0 + j];
-      double sp = 0.0, se = 0.0;
-      for (int l = 0; l < s; ++l) {
-        sp = __dadd_rn(sp, strategy_pdf(c, l, volume, c.px[j], c.py[j], c.pz[j]));
-        se = __dadd_rn(se, strategy_pdf(c, l, volume, c.ex[j], c.ey[j], c.ez[j]));
-      }
-      const double p_ind = sp;
-      const double p_dp = __dadd_rn(sp, __dmul_rn(ks, rec.pdf_emit_at_phase[r]));
-      const double p_de = rec.emit_delta[r] ? ks : __dadd_rn(se, __dmul_rn(ks, rec.pdf_emit[r]));
-      const int64_t q = q0 + j;
-      phat[q] = p_ind;
-      phat[n + q] = p_dp;
-      phat[2 * n + q] = p_de;
-      const bool inc_p = isfinite(p_ind) && p_ind > 0.0;
-      const bool inc_e = isfinite(p_de) && p_de > 0.0;
-      const bool ok_dp = inc_p && isfinite(p_dp) && p_dp > 0.0;
-      c.inv_p[j] = inc_p ? __ddiv_rn(1.0, p_ind) : 0.0;
-      const double ie = inc_e ? __ddiv_rn(1.0, p_de) : 0.0;
-      const double ip = ok_dp ? __ddiv_rn(1.0, p_dp) : 0.0;
-      c.wex[j] = rec.d_emit[r * 3] * ie;
-      c.wey[j] = rec.d_emit[r * 3 + 1] * ie;
-      c.wez[j] = rec.d_emit[r * 3 + 2] * ie;
-      c.wpx[j] = rec.d_phase[r * 3] * ip;
-      c.wpy[j] = rec.d_phase[r * 3 + 1] * ip;
-      c.wpz[j] = rec.d_phase[r * 3 + 2] * ip;
-    }
-    __syncwarp();
-
-    // pass 2: kernel rows, D-bar and solve vectors (row rr)
-    for (int rr = lane; rr < s; rr += 32) {
-      const int64_t r = perm[q0 + rr];
-      double dx = 0.0, dy = 0.0, dz = 0.0;
-      for (int j = 0; j < s; ++j) {
-        const double pd = strategy_pdf(c, rr, volume, c.px[j], c.py[j], c.pz[j]);
-        const double pe = strategy_pdf(c, rr, volume, c.ex[j], c.ey[j], c.ez[j]);
-        wt[wb + int64_t(j) * s + rr] = float(pd * c.inv_p[j]);
-        dx += pe * c.wex[j] + pd * c.wpx[j];
-        dy += pe * c.wey[j] + pd * c.wpy[j];
-        dz += pe * c.wez[j] + pd * c.wpz[j];
-      }
-      const double kx = rec.coeff[r * 3], ky = rec.coeff[r * 3 + 1], kz = rec.coeff[r * 3 + 2];
-      const double wx = rec.w_cont[r * 3], wy = rec.w_cont[r * 3 + 1], wz = rec.w_cont[r * 3 + 2];
-      const double bx = kx * dx, by = ky * dy, bz = kz * dz;
-      const int64_t q = q0 + rr;
-      dbar_o[q] = f4(bx, by, bz);
-      coeff_o[q] = f4(kx, ky, kz);
-      a_o[q] = f4(wx * kx, wy * ky, wz * kz);
-      b_o[q] = f4(wx * bx, wy * by, wz * bz);
-      const double ix = rec.i_pt[r * 3], iy = rec.i_pt[r * 3 + 1], iz = rec.i_pt[r * 3 + 2];
-      i0_o[q] = f4(ix, iy, iz);
-      const int64_t pid = rec.path_idx[r];
-      par_o[q] = (r > 0 && rec.path_idx[r - 1] == pid) ? clpos[r - 1] : -1;
-      const bool terminal = !(r + 1 < n && rec.path_idx[r + 1] == pid);
-      if (terminal) {
-        tmax[0] = fmaxf(tmax[0], fabsf(float(ix)));
-        tmax[1] = fmaxf(tmax[1], fabsf(float(iy)));
-        tmax[2] = fmaxf(tmax[2], fabsf(float(iz)));
-      }
-    }
-    __syncwarp();
+// ----------------------------------------------------- TMA / mbarrier PTX
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
   }
-  for (int ch = 0; ch < 3; ++ch) {
-    float v = tmax[ch];
-    for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
-    if (lane == 0 && v > 0.f) atomic_max_pos(&term_max[ch], v);
+}
+// 1-D TMA bulk copy global -> shared, completing on `bar` (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One fixed-point iteration t (solve.py:78-83) over TMA-staged chunks.
+//
+// A persistent CTA per SM walks its chunks (see graph.cuh) with a producer
+// warp and kConsumers consumer warps:
+//  - the producer streams each chunk's kernel blocks, static row data
+//    {a, b, par}, its slice of I and (t > 0) of the previous W*I into a
+//    shared-memory stage with cp.async.bulk, kStages chunks ahead; a stage
+//    is refilled once every cluster of its chunk has been consumed;
+//  - consumer warps pull clusters one at a time from a CTA-wide counter (in
+//    chunk order, so a warp never waits on a slower warp), wait on the
+//    chunk's mbarrier the first time they touch it, and for cluster k
+//    accumulate (W I)[r] from shared memory (lane = row), then propagate the
+//    row into its continuation parent, I_out[par] = a * acc + b, scattered
+//    to HBM, with the residual maxima of solve.py:54-61.  The old I[par] is
+//    recomputed from the previous W*I (same arithmetic as when it was stored)
+//    instead of gathered.
+constexpr int kConsumers = 12;
+constexpr int kStages = 3;
+
+__global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
+k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
+             const int32_t* __restrict__ chunk_first, int64_t n_chunks, int stage_floats,
+             const float* __restrict__ wt, const float4* __restrict__ rows,
+             const float4* __restrict__ i_in, float4* __restrict__ i_out,
+             const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
+             const float4* __restrict__ i0, int t, uint32_t* __restrict__ red,
+             const int32_t* __restrict__ ctl) {
+  if (ctl[1]) return;  // converged or diverged earlier
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // kStages barriers
+  int* done = reinterpret_cast<int*>(smem + 64);                  // kStages counters
+  int* next_item = reinterpret_cast<int*>(smem + 96);
+  int* issued = reinterpret_cast<int*>(smem + 104);               // kStages chunk ids
+  float* stage0 = reinterpret_cast<float*>(smem + 128);
+  __shared__ float blk[kConsumers][6];
+  __shared__ unsigned blk_nan[kConsumers];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      done[st] = 0;
+      issued[st] = -1;
+    }
+    *next_item = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t G = gridDim.x;
+
+  if (wid == kConsumers) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int64_t i = 0;; ++i) {
+        const int64_t c = blockIdx.x + i * G;
+        if (c >= n_chunks) break;
+        const int st = int(i % kStages);
+        if (i >= kStages) {
+          const int64_t cp = c - kStages * G;  // the chunk that last used this stage
+          const int need = chunk_first[cp + 1] - chunk_first[cp];
+          while (*reinterpret_cast<volatile int*>(&done[st]) < need) __nanosleep(64);
+          done[st] = 0;
+          fence_proxy_async();  // consumers' generic reads before the async refill
+        }
+        uint64_t* bar = &full[st];
+        float* buf = stage0 + st * int64_t(stage_floats);
+        const int32_t k0 = chunk_first[c], k1 = chunk_first[c + 1];
+        // the stage's previous phase has completed (its chunk was consumed), so
+        // a consumer that sees issued == i waits on this chunk's phase
+        *reinterpret_cast<volatile int*>(&issued[st]) = int(i);
+        if (k0 == k1) {
+          mbar_arrive(bar);
+          continue;
+        }
+        const int64_t w0 = w_off[k0], wc = w_off[k1] - w0;
+        const int32_t q0 = cl_off[k0], R = cl_off[k1] - q0;
+        const uint32_t wb = uint32_t(wc * 4), rb = uint32_t(R) * 32u, ib = uint32_t(R) * 16u;
+        mbar_expect_tx(bar, wb + rb + ib + (t > 0 ? ib : 0u));
+        if (wb) bulk_g2s(buf, wt + w0, wb, bar);
+        bulk_g2s(buf + wc, rows + 2 * int64_t(q0), rb, bar);
+        bulk_g2s(buf + wc + 8 * int64_t(R), i_in + q0, ib, bar);
+        if (t > 0) bulk_g2s(buf + wc + 12 * int64_t(R), acc_prev + q0, ib, bar);
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- consumers
+    float dmax[3] = {0.f, 0.f, 0.f}, smax[3] = {0.f, 0.f, 0.f};
+    unsigned nan_bits = 0;  // numpy's max propagates NaN per channel: remember it
+    int64_t ci = 0, cbase = 0, waited = -1;  // current chunk (local index), its first item
+    int32_t ck0 = 0, ck1 = 0;
+    {
+      const int64_t c = blockIdx.x;
+      if (c < n_chunks) {
+        ck0 = chunk_first[c];
+        ck1 = chunk_first[c + 1];
+      }
+    }
+    for (;;) {
+      int x = 0;
+      if (lane == 0) x = atomicAdd(next_item, 1);
+      x = __shfl_sync(0xFFFFFFFFu, x, 0);
+      // advance to the chunk holding item x
+      bool finished = false;
+      while (true) {
+        const int64_t c = blockIdx.x + ci * G;
+        if (c >= n_chunks) {
+          finished = true;
+          break;
+        }
+        if (x < cbase + (ck1 - ck0)) break;
+        cbase += ck1 - ck0;
+        ++ci;
+        const int64_t c2 = blockIdx.x + ci * G;
+        if (c2 < n_chunks) {
+          ck0 = chunk_first[c2];
+          ck1 = chunk_first[c2 + 1];
+        }
+      }
+      if (finished) break;
+      const int st = int(ci % kStages);
+      if (waited != ci) {
+        // never wait on a phase parity two uses ahead: first see the chunk issued
+        while (*reinterpret_cast<volatile int*>(&issued[st]) != int(ci)) __nanosleep(32);
+        mbar_wait(&full[st], uint32_t((ci / kStages) & 1));
+        waited = ci;
+      }
+      const float* buf = stage0 + st * int64_t(stage_floats);
+      const int64_t w0 = w_off[ck0], wc = w_off[ck1] - w0;
+      const int32_t cq0 = cl_off[ck0], R = cl_off[ck1] - cq0;
+      const float4* srow = reinterpret_cast<const float4*>(buf + wc);
+      const float4* sin = reinterpret_cast<const float4*>(buf + wc + 8 * int64_t(R));
+      const float4* sprev = reinterpret_cast<const float4*>(buf + wc + 12 * int64_t(R));
+      const int32_t k = ck0 + int32_t(x - cbase);
+      const int32_t q0 = cl_off[k];
+      const int s = cl_off[k + 1] - q0;
+      const float* w = buf + (w_off[k] - w0);
+      const int rl = q0 - cq0;
+      for (int rc = 0; rc < s; rc += 64) {
+        const int r0 = rc + lane, r1 = rc + lane + 32;
+        float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
+#pragma unroll 4
+        for (int j = 0; j < s; ++j) {
+          const float4 ij = sin[rl + j];
+          const float* col = w + j * s;
+          const float w0v = r0 < s ? col[r0] : 0.f;
+          const float w1v = r1 < s ? col[r1] : 0.f;
+          acc0.x = fmaf(w0v, ij.x, acc0.x);
+          acc0.y = fmaf(w0v, ij.y, acc0.y);
+          acc0.z = fmaf(w0v, ij.z, acc0.z);
+          acc1.x = fmaf(w1v, ij.x, acc1.x);
+          acc1.y = fmaf(w1v, ij.y, acc1.y);
+          acc1.z = fmaf(w1v, ij.z, acc1.z);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = h ? r1 : r0;
+          if (rr >= s) continue;
+          const float3 ac = h ? acc1 : acc0;
+          const int64_t q = q0 + rr;
+          acc_out[q] = make_float4(ac.x, ac.y, ac.z, 0.f);
+          const float4 A = srow[2 * (rl + rr)], B = srow[2 * (rl + rr) + 1];
+          const int32_t p = __float_as_int(A.w);
+          if (p < 0) continue;
+          const float nx = fmaf(A.x, ac.x, B.x), ny = fmaf(A.y, ac.y, B.y),
+                      nz = fmaf(A.z, ac.z, B.z);
+          float4 old;
+          if (t == 0) {
+            old = i0[p];
+          } else {
+            const float4 pa = sprev[rl + rr];
+            old = make_float4(fmaf(A.x, pa.x, B.x), fmaf(A.y, pa.y, B.y), fmaf(A.z, pa.z, B.z), 0.f);
+          }
+          i_out[p] = make_float4(nx, ny, nz, 0.f);
+          const float dv[3] = {fabsf(nx - old.x), fabsf(ny - old.y), fabsf(nz - old.z)};
+          const float sv[3] = {fabsf(nx), fabsf(ny), fabsf(nz)};
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            if (dv[ch] != dv[ch]) nan_bits |= 1u << ch;
+            if (sv[ch] != sv[ch]) nan_bits |= 8u << ch;
+            dmax[ch] = fmaxf(dmax[ch], dv[ch]);
+            smax[ch] = fmaxf(smax[ch], sv[ch]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) atomicAdd(&done[st], 1);
+    }
+    for (int off = 16; off; off >>= 1) nan_bits |= __shfl_xor_sync(0xFFFFFFFFu, nan_bits, off);
+    float v[6] = {dmax[0], dmax[1], dmax[2], smax[0], smax[1], smax[2]};
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      for (int off = 16; off; off >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xFFFFFFFFu, v[q], off));
+    if (lane == 0) {
+      for (int q = 0; q < 6; ++q) blk[wid][q] = v[q];
+      blk_nan[wid] = nan_bits;
+    }
+  }
+  __syncthreads();
+  if (tid < 6) {
+    float x = 0.f;
+    for (int w2 = 0; w2 < kConsumers; ++w2) x = fmaxf(x, blk[w2][tid]);
+    if (x > 0.f) atomicMax(&red[t * 8 + tid], __float_as_uint(x));
+  }
+  if (tid == 6) {
+    unsigned nb = 0;
+    for (int w2 = 0; w2 < kConsumers; ++w2) nb |= blk_nan[w2];
+    if (nb) atomicOr(&red[t * 8 + 6], nb);
   }
 }
 
-// One fixed-point iteration t; mode 0 = solve step, 1 = aggregate only.
-// Warp per cluster; rows and columns processed in chunks of 64.
-template <int kMode>
+// W * v per cluster from global memory (aggregate_indirect on an arbitrary
+// vector; not on the solve path).  Warp per cluster.
+constexpr int kItWarps = 8;
 __global__ void __launch_bounds__(kItWarps * 32)
-k_iterate(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off, int64_t m,
-          const float* __restrict__ wt, const float4* __restrict__ i_in,
-          float4* __restrict__ i_out, const float4* __restrict__ acc_prev,
-          float4* __restrict__ acc_out, const float4* __restrict__ av,
-          const float4* __restrict__ bv, const float4* __restrict__ i0,
-          const int32_t* __restrict__ par, int t, uint32_t* __restrict__ red,
-          const int32_t* __restrict__ ctl) {
-  if (kMode == 0 && ctl[1]) return;  // converged or diverged earlier
-  __shared__ float4 stage[kItWarps][kWarpCap];
-  __shared__ float blk[kItWarps][6];
+k_apply_w(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off, int64_t m,
+          const float* __restrict__ wt, const float4* __restrict__ v_in, float4* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
   const int64_t nwarps = int64_t(gridDim.x) * kItWarps;
-  float dmax[3] = {0.f, 0.f, 0.f}, smax[3] = {0.f, 0.f, 0.f};
-  unsigned nan_bits = 0;  // numpy's max propagates NaN per channel: remember it
-
-  for (int64_t k = int64_t(blockIdx.x) * kItWarps + wid; k < m; k += nwarps) {
+  for (int64_t k = int64_t(blockIdx.x) * kItWarps + (threadIdx.x >> 5); k < m; k += nwarps) {
     const int32_t q0 = cl_off[k];
     const int s = cl_off[k + 1] - q0;
     const float* w = wt + w_off[k];
-    for (int rc = 0; rc < s; rc += 64) {
-      const int r0 = rc + lane, r1 = rc + lane + 32;
-      float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
-      for (int cc = 0; cc < s; cc += kWarpCap) {
-        const int cn = min(kWarpCap, s - cc);
-        if (lane < cn) stage[wid][lane] = i_in[q0 + cc + lane];
-        if (lane + 32 < cn) stage[wid][lane + 32] = i_in[q0 + cc + lane + 32];
-        __syncwarp();
-#pragma unroll 4
-        for (int j = 0; j < cn; ++j) {
-          const float4 ij = stage[wid][j];
-          const float* col = w + int64_t(cc + j) * s;
-          const float w0 = r0 < s ? __ldg(col + r0) : 0.f;
-          const float w1 = r1 < s ? __ldg(col + r1) : 0.f;
-          acc0.x = fmaf(w0, ij.x, acc0.x);
-          acc0.y = fmaf(w0, ij.y, acc0.y);
-          acc0.z = fmaf(w0, ij.z, acc0.z);
-          acc1.x = fmaf(w1, ij.x, acc1.x);
-          acc1.y = fmaf(w1, ij.y, acc1.y);
-          acc1.z = fmaf(w1, ij.z, acc1.z);
-        }
-        __syncwarp();
+    for (int r = lane; r < s; r += 32) {
+      float3 acc = make_float3(0.f, 0.f, 0.f);
+      for (int j = 0; j < s; ++j) {
+        const float4 vj = v_in[q0 + j];
+        const float wv = w[int64_t(j) * s + r];
+        acc.x = fmaf(wv, vj.x, acc.x);
+        acc.y = fmaf(wv, vj.y, acc.y);
+        acc.z = fmaf(wv, vj.z, acc.z);
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rr = h ? r1 : r0;
-        if (rr >= s) continue;
-        const float3 ac = h ? acc1 : acc0;
-        const int64_t q = q0 + rr;
-        acc_out[q] = make_float4(ac.x, ac.y, ac.z, 0.f);
-        if (kMode != 0) continue;
-        const int32_t p = par[q];
-        if (p < 0) continue;
-        const float4 A = av[q], B = bv[q];
-        const float nx = fmaf(A.x, ac.x, B.x), ny = fmaf(A.y, ac.y, B.y), nz = fmaf(A.z, ac.z, B.z);
-        float4 old;
-        if (t == 0) {
-          old = i0[p];
-        } else {
-          const float4 pa = acc_prev[q];
-          old = make_float4(fmaf(A.x, pa.x, B.x), fmaf(A.y, pa.y, B.y), fmaf(A.z, pa.z, B.z), 0.f);
-        }
-        i_out[p] = make_float4(nx, ny, nz, 0.f);
-        const float dv[3] = {fabsf(nx - old.x), fabsf(ny - old.y), fabsf(nz - old.z)};
-        const float sv[3] = {fabsf(nx), fabsf(ny), fabsf(nz)};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (dv[c] != dv[c]) nan_bits |= 1u << c;
-          if (sv[c] != sv[c]) nan_bits |= 8u << c;
-          dmax[c] = fmaxf(dmax[c], dv[c]);
-          smax[c] = fmaxf(smax[c], sv[c]);
-        }
-      }
+      out[q0 + r] = make_float4(acc.x, acc.y, acc.z, 0.f);
     }
-  }
-  if (kMode != 0) return;
-  for (int off = 16; off; off >>= 1) nan_bits |= __shfl_xor_sync(0xFFFFFFFFu, nan_bits, off);
-  if (lane == 0 && nan_bits) atomicOr(&red[t * 8 + 6], nan_bits);
-  float v[6] = {dmax[0], dmax[1], dmax[2], smax[0], smax[1], smax[2]};
-#pragma unroll
-  for (int i = 0; i < 6; ++i)
-    for (int off = 16; off; off >>= 1) v[i] = fmaxf(v[i], __shfl_xor_sync(0xFFFFFFFFu, v[i], off));
-  if (lane == 0)
-    for (int i = 0; i < 6; ++i) blk[wid][i] = v[i];
-  __syncthreads();
-  if (threadIdx.x < 6) {
-    float x = 0.f;
-    for (int w2 = 0; w2 < kItWarps; ++w2) x = fmaxf(x, blk[w2][threadIdx.x]);
-    if (x > 0.f) atomicMax(&red[t * 8 + threadIdx.x], __float_as_uint(x));
   }
 }
 
@@ -497,27 +532,6 @@ int iterate_grid(int64_t m) {
 
 }  // namespace
 
-void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s) {
-  const int64_t n = g->n, m = g->m;
-  VPG_REQUIRE(g->max_cluster <= kWarpCap, VPG_ELIMIT,
-              "clusters larger than 64 members (cluster_size > 32) are not supported yet");
-  g->wt.alloc(size_t(g->nnz > 0 ? g->nnz : 1), s);
-  g->phat.alloc(size_t(3 * n + 1), s);
-  for (auto* v : {&g->i0, &g->a, &g->b, &g->dbar, &g->coeff, &g->ibuf[0], &g->ibuf[1], &g->acc[0],
-                  &g->acc[1]})
-    v->alloc(size_t(n + 1), s);
-  g->par.alloc(size_t(n + 1), s);
-  g->term_max.alloc(4, s);
-  VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
-  if (n == 0) return;
-  int64_t blocks = (m + kOpWarps - 1) / kOpWarps;
-  const int64_t cap = int64_t(sm_count()) * 16;
-  VPG_LAUNCH(k_operators, int(blocks < cap ? blocks : cap), kOpWarps * 32, 0, s, rec,
-             g->perm.get(), g->clpos.get(), g->cl_off.get(), g->w_off.get(), m, n, g->wt.get(),
-             g->phat.get(), g->dbar.get(), g->coeff.get(), g->a.get(), g->b.get(), g->i0.get(),
-             g->par.get(), g->term_max.get());
-}
-
 // ------------------------------------------------------------------ solve
 void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
            double* residuals, int32_t* performed, cudaStream_t s) {
@@ -539,12 +553,23 @@ void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
       VPG_LAUNCH(k_own_indirect, grid_for(n, block), block, 0, s, rec, g->perm.get(), n,
                  g->acc[0].get());
   }
-  const int grid = iterate_grid(m);
+  // stage = one chunk: kChunkFloats plus the largest cluster's blocks + rows
+  const int smax = std::max(1, g->max_cluster);
+  const int stage_floats = kChunkFloats + ((smax * smax + 3) & ~3) + 16 * smax;
+  const size_t smem = 128 + size_t(kStages) * stage_floats * sizeof(float);
+  VPG_REQUIRE(smem <= 220 * 1024, VPG_ELIMIT, "clusters too large for the staged solve");
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    VPG_CUDA(cudaFuncSetAttribute(k_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    smem_set = smem;
+  }
+  const int grid = int(std::min<int64_t>(g->n_chunks, sm_count()));
   for (int t = 0; t < iterations && n > 0; ++t) {
-    VPG_LAUNCH(k_iterate<0>, grid, kItWarps * 32, 0, s, g->cl_off.get(), g->w_off.get(), m,
-               g->wt.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
-               g->acc[(t + 1) & 1].get(), g->a.get(), g->b.get(), g->i0.get(), g->par.get(), t,
-               g->red.get(), g->ctl.get());
+    VPG_LAUNCH(k_solve_iter, grid, (kConsumers + 1) * 32, smem, s, g->cl_off.get(), g->w_off.get(),
+               g->chunk_first.get(), g->n_chunks, stage_floats, g->wt.get(), g->rows.get(),
+               g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
+               g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
     VPG_LAUNCH(k_control, 1, 32, 0, s, t, tol, g->red.get(), g->term_max.get(), g->resid.get(),
                g->ctl.get());
   }
@@ -594,9 +619,8 @@ void aggregate_indirect(const vpg_graph* g, const vpg_records& rec, const double
   const int block = 256;
   DBuf<float4> vin(n, s), vout(n, s);
   VPG_LAUNCH(k_gather_rec3, grid_for(n, block), block, 0, s, incoming, g->perm.get(), n, vin.get());
-  VPG_LAUNCH(k_iterate<1>, iterate_grid(g->m), kItWarps * 32, 0, s, g->cl_off.get(),
-             g->w_off.get(), g->m, g->wt.get(), vin.get(), nullptr, nullptr, vout.get(), nullptr,
-             nullptr, nullptr, nullptr, 0, nullptr, nullptr);
+  VPG_LAUNCH(k_apply_w, iterate_grid(g->m), kItWarps * 32, 0, s, g->cl_off.get(),
+             g->w_off.get(), g->m, g->wt.get(), vin.get(), vout.get());
   VPG_LAUNCH(k_scatter_rec3, grid_for(n, block), block, 0, s, vout.get(), g->clpos.get(),
              rec.coeff, n, out);
 }
