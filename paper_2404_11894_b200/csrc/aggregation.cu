@@ -14,6 +14,8 @@
 //                   transposed, D-bar and the per-row solve vectors.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include <cub/cub.cuh>
@@ -274,6 +276,15 @@ __global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_
 
 void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool timings) {
   auto t_start = std::chrono::steady_clock::now();
+  const bool dbg = getenv("VPG_DEBUG_TIMING") != nullptr;
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[vpg] %-28s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t_start).count());
+  };
+  mark("ops: enter");
   const int64_t n = g->n, m = g->m;
   const int S = std::max(1, g->max_cluster);
   const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
@@ -287,8 +298,10 @@ void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool 
   g->term_max.alloc(4, s);
   VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
   if (n == 0) return;
-  DBuf<Member> members(size_t(n), s);
-  VPG_LAUNCH(k_pack_members, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), members.get(),
+  mark("ops: alloc graph buffers");
+  Member* members = scratch_of<Member>(s, "members", size_t(n));
+  mark("ops: alloc members");
+  VPG_LAUNCH(k_pack_members, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), members,
              g->term_max.get());
   static bool attr_set = false;
   if (!attr_set) {
@@ -296,8 +309,9 @@ void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool 
                                   200 * 1024));
     attr_set = true;
   }
+  mark("ops: pack");
   const int64_t blocks = std::min<int64_t>(m, int64_t(sm_count()) * 16);
-  VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, members.get(), g->cl_off.get(),
+  VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, members, g->cl_off.get(),
              g->w_off.get(), m, n, S, g->wt.get(), g->phat.get(), g->dbar.get(), g->coeff.get(),
              g->rows.get(), g->i0.get());
   if (timings) {
@@ -305,14 +319,15 @@ void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool 
     g->info.build_ms[7] =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   }
+  mark("ops: aggregate");
   // solve chunks
   DBuf<int64_t> cost(m + 1, s), cst(m + 1, s);
   VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), m, cost.get());
   {
     size_t bytes = 0;
     VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cost.get(), cst.get(), int(m + 1), s));
-    DBuf<char> tmp(bytes, s);
-    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, cost.get(), cst.get(), int(m + 1), s));
+    void* tmp = scratch(s, "cub_temp", bytes + 256);
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cost.get(), cst.get(), int(m + 1), s));
     count_launch(1);
   }
   int64_t total = 0;
@@ -323,6 +338,7 @@ void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool 
   g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
   VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst.get(), m, g->n_chunks,
              int64_t(kChunkFloats), g->chunk_first.get());
+  mark("ops: chunks");
 }
 
 }  // namespace vpg

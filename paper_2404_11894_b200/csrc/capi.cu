@@ -93,6 +93,37 @@ void dfree(void* p, cudaStream_t s) {
 }
 
 namespace {
+std::mutex g_scratch_mu;
+std::map<std::pair<cudaStream_t, std::string>, std::pair<void*, size_t>>& g_scratch() {
+  static std::map<std::pair<cudaStream_t, std::string>, std::pair<void*, size_t>> m;
+  return m;
+}
+}  // namespace
+
+void* scratch(cudaStream_t s, const char* tag, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  auto& e = g_scratch()[{s, std::string(tag)}];
+  if (e.second < bytes) {
+    if (e.first) {
+      VPG_CUDA(cudaStreamSynchronize(s));  // the old buffer may still be in use
+      VPG_CUDA(cudaFree(e.first));
+      e.first = nullptr;
+    }
+    const size_t cap = bytes + bytes / 8;
+    void* p = nullptr;
+    const cudaError_t err = cudaMalloc(&p, cap);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      e.second = 0;
+      throw Error(VPG_ENOMEM, std::string("scratch allocation failed: ") + cudaGetErrorString(err));
+    }
+    e.first = p;
+    e.second = cap;
+  }
+  return e.first;
+}
+
+namespace {
 std::map<void*, size_t>& g_host_cap() {
   static std::map<void*, size_t> caps;
   return caps;

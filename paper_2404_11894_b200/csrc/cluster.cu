@@ -18,6 +18,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <vector>
@@ -635,10 +637,28 @@ template <class F>
 void cub_call(F&& f, cudaStream_t s) {
   size_t bytes = 0;
   VPG_CUDA(f(nullptr, bytes));
-  DBuf<char> tmp(bytes, s);
-  VPG_CUDA(f(tmp.get(), bytes));
+  void* tmp = scratch(s, "cub_temp", bytes + 256);
+  VPG_CUDA(f(tmp, bytes));
   count_launch(2);
 }
+
+// VPG_DEBUG_TIMING=1 prints sub-stage wall times of the build to stderr.
+struct DebugClock {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0;
+  explicit DebugClock(cudaStream_t st) : on(getenv("VPG_DEBUG_TIMING") != nullptr), s(st) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, bool sync = true) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[vpg] %-28s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 
 struct ClassPlan {
   int64_t n, row_off, m, center_off;
@@ -778,7 +798,10 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   }
 
   // per-class working storage (records grouped by center, class by class)
-  DBuf<int32_t> grp_rec(n, s), assign(n, s), values(n, s), fb_list(n, s);
+  int32_t* grp_rec = scratch_of<int32_t>(s, "grp_rec", n);
+  int32_t* assign_all = scratch_of<int32_t>(s, "assign", n);
+  int32_t* values = scratch_of<int32_t>(s, "values", n);
+  int32_t* fb_list = scratch_of<int32_t>(s, "fb_list", n);
   DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s), gstart_all(center_total, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
@@ -793,36 +816,36 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
     const ClassPlan& p = plan[c];
     const int m = int(p.m);
     const int32_t* rows_p = rows.get();
-    int32_t* assign_c = assign.get() + p.row_off;
+    int32_t* assign_c = assign_all + p.row_off;
     GridParams gp = make_grid(p);
 
     // device: cell keys of the points and their sort, independent of the
     // center draw, overlap the host RNG
-    DBuf<unsigned long long> pkeys, pkeys_sorted;
-    DBuf<int32_t> pids, pids_sorted, run_start, run_len;
+    unsigned long long *pkeys = nullptr, *pkeys_sorted = nullptr;
+    int32_t *pids = nullptr, *pids_sorted = nullptr, *run_start = nullptr, *run_len = nullptr;
     int end_bits = 64;
     if (m > 1) {
-      pkeys.alloc(p.n, s);
-      pkeys_sorted.alloc(p.n, s);
-      pids.alloc(p.n, s);
-      pids_sorted.alloc(p.n, s);
-      run_start.alloc(p.n + 1, s);
-      run_len.alloc(p.n + 1, s);
+      pkeys = scratch_of<unsigned long long>(s, "pkeys", p.n);
+      pkeys_sorted = scratch_of<unsigned long long>(s, "pkeys_sorted", p.n);
+      pids = scratch_of<int32_t>(s, "pids", p.n);
+      pids_sorted = scratch_of<int32_t>(s, "pids_sorted", p.n);
+      run_start = scratch_of<int32_t>(s, "run_start", p.n + 1);
+      run_len = scratch_of<int32_t>(s, "run_len", p.n + 1);
       VPG_LAUNCH(k_point_keys, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n, rec.pos,
-                 gp, pkeys.get(), pids.get());
+                 gp, pkeys, pids);
       if (gp.packed)
         end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
       const int64_t nn = p.n;
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, pkeys.get(), pkeys_sorted.get(), pids.get(),
-                                               pids_sorted.get(), int(nn), 0, end_bits, s);
+        return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids,
+                                               pids_sorted, int(nn), 0, end_bits, s);
       }, s);
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted.get(), pkeys.get(),
-                                                  run_len.get(), scalars.get() + 1, int(nn), s);
+        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys,
+                                                  run_len, scalars.get() + 1, int(nn), s);
       }, s);
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, run_len.get(), run_start.get(), int(nn), s);
+        return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(nn), s);
       }, s);
     }
 
@@ -864,16 +887,16 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                  table.get());
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
-                 rec.pos, gp, table.get(), spos.get(), pids_sorted.get(), run_start.get(),
-                 run_len.get(), scalars.get() + 1, assign_c, fb_list.get(), scalars.get());
+                 rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start,
+                 run_len, scalars.get() + 1, assign_c, fb_list, scalars.get());
       VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
-                 table.get(), spos.get(), fb_list.get(), scalars.get(), assign_c);
+                 table.get(), spos.get(), fb_list, scalars.get(), assign_c);
     }
     clk.mark(2);
 
     // groups: stable sort of this class's records by center (clustering.py:55)
     VPG_LAUNCH(k_group_values, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
-               values.get() + p.row_off);
+               values + p.row_off);
     int32_t* counts_c = counts_all.get() + p.center_off;
     int32_t* gstart_c = gstart_all.get() + p.center_off;
     {
@@ -883,7 +906,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, reinterpret_cast<uint32_t*>(assign_c),
                                                reinterpret_cast<uint32_t*>(sorted_keys.get()),
-                                               values.get() + p.row_off, grp_rec.get() + p.row_off,
+                                               values + p.row_off, grp_rec + p.row_off,
                                                int(nn), 0, end_bit, s);
       }, s);
     }
@@ -912,6 +935,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
 
     // ---- split loop on the oversize groups (host, exact RNG order)
     class_mod_begin[c] = int64_t(mods.size()) / 4;
+    DebugClock dbg(s);
     if (n_over > 0) {
       std::vector<int64_t> info;
       to_host(info, over_info.get(), size_t(n_over) * 4, s);
@@ -930,7 +954,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
       to_device(d_seg.get(), seg, s);
       DBuf<int32_t> d_srec(staged, s);
       DBuf<double> d_spos(staged * 3, s);
-      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec.get(),
+      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec,
                  d_seg.get(), n_over, rec.pos, d_srec.get(), d_spos.get());
       HostBuf<int32_t> h_srec(staged);
       HostBuf<double> xyz(staged * 3);
@@ -940,6 +964,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                                cudaMemcpyDeviceToHost, s));
       count_transfer(0, 28 * staged);
       VPG_CUDA(cudaStreamSynchronize(s));
+      dbg.mark("split: info+gather+D2H", false);
       // initial center positions: the center is one of its group's members
       // except with coincident centers (then it is fetched by record id)
       std::vector<SplitGroup> groups(n_over);
@@ -958,8 +983,10 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
         }
       }
       g->info.n_staged += staged;
+      dbg.mark("split: center lookup", false);
       n_splits += split_oversize(rng, h_srec.get(), xyz.get(), size_t(staged), groups, max_size,
                                  c0.data(), &g->info.split_visits);
+      dbg.mark("split: loop", false);
       const int64_t base_split = int64_t(split_rec.size());
       split_rec.insert(split_rec.end(), h_srec.get(), h_srec.get() + staged);
       for (size_t k = 0; k < groups.size(); ++k) {
@@ -970,6 +997,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
         mods.push_back(groups[k].center);
       }
       class_appended[c] = int64_t(groups.size()) - n_over;
+      dbg.mark("split: mods", false);
     }
     class_mod_begin[c + 1] = int64_t(mods.size()) / 4;
     clk.mark(4);
@@ -1044,7 +1072,7 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   g->max_cluster = h_max;
   // w_off / cl_off beyond M repeat the totals (sizes there are 0)
   VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), cl_src.get(), M,
-             grp_rec.get(), d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
+             grp_rec, d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
   int64_t h_len = 0;
   VPG_CUDA(cudaMemcpyAsync(&h_len, g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   DBuf<int64_t> d_nnz(1, s);

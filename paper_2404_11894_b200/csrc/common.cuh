@@ -108,6 +108,17 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// Persistent device scratch for large build temporaries, keyed by (stream,
+// tag): grown with cudaMalloc when a larger size is requested, never returned
+// to the pool, so steady-state builds allocate nothing.  Calls on one stream
+// are ordered, so reuse across successive builds on that stream is safe.
+void* scratch(cudaStream_t s, const char* tag, size_t bytes);
+
+template <class T>
+T* scratch_of(cudaStream_t s, const char* tag, size_t count) {
+  return static_cast<T*>(scratch(s, tag, count * sizeof(T) + 16));
+}
+
 // Page-locked host staging (cudaMallocHost), recycled through a process-wide
 // cache so repeated builds do not pay for pinning.
 void* halloc(size_t bytes);
