@@ -269,6 +269,18 @@ int vpg_trace_count(const vpg_scene* scene, const vpg_trace_cfg* cfg, int64_t* c
  * paths->rec_start offsets (relative to `rec`), and the path table. */
 int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* rec,
                    const vpg_paths* paths, void* stream);
+/* Single-pass capture (replaces pass 1 + pass 2): every path is traced once
+ * and its records go to scratch slots (capacity `capacity`) claimed through
+ * the device `counter`; counts (path_count) and the path table are written as
+ * in pass 1.  If *counter > capacity afterwards, records were dropped: retry
+ * with capacity >= *counter (deterministic).  Then vpg_scatter_records moves
+ * the n = *counter scratch records into path order, row = rec_start[path -
+ * path_begin] + depth.  max_depth <= 128. */
+int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* scratch,
+                      int64_t capacity, uint64_t* counter, int64_t* counts, const vpg_paths* paths,
+                      void* stream);
+int vpg_scatter_records(const vpg_records* scratch, int64_t n, const int64_t* rec_start,
+                        int64_t path_begin, const vpg_records* out, void* stream);
 /* extra_direct_kernel (kernels.py:499-553). */
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream);

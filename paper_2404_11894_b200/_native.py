@@ -138,6 +138,10 @@ _SIGNATURES = {
                                  C.POINTER(Paths), c_p]),
     "vpg_extra_direct": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(Records), C.POINTER(Paths),
                                    c_i64, c_i32, c_p]),
+    "vpg_trace_capture": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(TraceCfg), C.POINTER(Records),
+                                    c_i64, c_p, c_p, C.POINTER(Paths), c_p]),
+    "vpg_scatter_records": (C.c_int, [C.POINTER(Records), c_i64, c_p, c_i64, C.POINTER(Records),
+                                      c_p]),
 }
 
 _lock = threading.Lock()

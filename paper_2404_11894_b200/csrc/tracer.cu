@@ -29,7 +29,8 @@ constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t kSaltTrace = 0x7E;
 constexpr uint64_t kSaltExtra = 0xED;
 
-enum Mode { kOff = 0, kCount = 1, kFill = 2 };
+enum Mode { kOff = 0, kCount = 1, kFill = 2, kCapture = 3 };
+constexpr int kMaxCaptureDepth = 128;  // slot list per path in capture mode
 
 // ---------------------------------------------------------- rng (rng.py)
 struct Rng {
@@ -459,10 +460,33 @@ struct PathResult {
 };
 
 // ------------------------------------------------------- kernels.py
+// Capture mode: records go to scratch slots handed out by a warp-aggregated
+// counter (paths interleave); the path keeps its slot list for the backward
+// sweep and a scatter pass later moves records into path order.
+struct Capture {
+  unsigned long long* counter;
+  int64_t capacity;
+};
+
+__device__ __forceinline__ int64_t claim_slot(const Capture& cap) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(act) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cap.counter, (unsigned long long)__popc(act));
+  base = __shfl_sync(act, base, leader);
+  return int64_t(base) + __popc(act & ((1u << lane) - 1u));
+}
+
 template <int kMode>
 __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
                                 int64_t py, int64_t path_id, int64_t rec_offset,
-                                const vpg_records& rec, const vpg_paths& pth, int64_t slot) {
+                                const vpg_records& rec, const vpg_paths& pth, int64_t slot,
+                                const Capture& cap = Capture{nullptr, 0}) {
+  constexpr bool kStore = kMode == kFill || kMode == kCapture;
+  int64_t rows[kMode == kCapture ? kMaxCaptureDepth : 1];
+  // row of record k of this path; -1 when a capture slot overflowed
+  auto row_of = [&](int k) -> int64_t { return kMode == kCapture ? rows[k] : rec_offset + k; };
   Rng rng = make_stream(cfg.seed, path_id, kSaltTrace);
   const double jx = rng.next();
   const double jy = rng.next();
@@ -490,7 +514,10 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
     int sid;
     const double t_hit = intersect(sc, o, d, kTEps, kNoHit, sid);
     const double pe_at_dir = emitter_dir_pdf_from_hit(sc, sid, t_hit, d);
-    if (kMode == kFill && !from_camera) rec.pdf_emit_at_phase[rec_offset + n_rec - 1] = pe_at_dir;
+    if (kStore && !from_camera) {
+      const int64_t prow = row_of(n_rec - 1);
+      if (prow >= 0) rec.pdf_emit_at_phase[prow] = pe_at_dir;
+    }
     const MediaFlight mf = media_flight(sc, o, d, 0.0, t_hit, rng);
     V3 v{o.x + mf.t * d.x, o.y + mf.t * d.y, o.z + mf.t * d.z};
     bool volume = false;
@@ -539,10 +566,12 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
             }
             if (n_rec == 1)
               for (int c = 0; c < 3; ++c) d0p[c] = cc[c];
-            if (kMode == kFill) {
-              const int64_t row = rec_offset + n_rec - 1;
-              put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
-              for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
+            if (kStore) {
+              const int64_t row = row_of(n_rec - 1);
+              if (row >= 0) {
+                put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
+                for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
+              }
             }
           }
         }
@@ -603,8 +632,14 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
     double fp[3];
     for (int c = 0; c < 3; ++c) fp[c] = k[c] * pdf_p;
 
-    if (kMode == kFill) {
-      const int64_t row = rec_offset + n_rec;
+    int64_t row = -1;
+    if (kMode == kFill) row = rec_offset + n_rec;
+    if (kMode == kCapture) {
+      const int64_t got = claim_slot(cap);
+      row = got < cap.capacity ? got : -1;
+      rows[n_rec] = row;
+    }
+    if (kStore && row >= 0) {
       put3(rec.pos, row, v.x, v.y, v.z);
       put3(rec.omega_out, row, -ax.x, -ax.y, -ax.z);
       put3(rec.normal, row, nrm.x, nrm.y, nrm.z);
@@ -649,10 +684,11 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
     d = wp;
   }
 
-  if (kMode == kFill && n_rec > 0) {  // backward sweep (kernels.py:393-408)
+  if (kStore && n_rec > 0) {  // backward sweep (kernels.py:393-408)
     double in[3] = {0.0, 0.0, 0.0};
     for (int kk = n_rec - 1; kk >= 0; --kk) {
-      const int64_t row = rec_offset + kk;
+      const int64_t row = row_of(kk);
+      if (row < 0) break;  // overflowed capture: the host retries with room
       const double pp = rec.pdf_phase[row];
       for (int c = 0; c < 3; ++c) {
         const double dbar = rec.i_pt[row * 3 + c];
@@ -670,7 +706,7 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
     put3(pth.direct0_nee, slot, d0n[0], d0n[1], d0n[2]);
     put3(pth.direct0_phase, slot, d0p[0], d0p[1], d0p[2]);
     put3(pth.pt_estimate, slot, est[0], est[1], est[2]);
-    if (kMode == kFill) put3(pth.extra_direct, slot, d0n[0] + d0p[0], d0n[1] + d0p[1], d0n[2] + d0p[2]);
+    if (kStore) put3(pth.extra_direct, slot, d0n[0] + d0p[0], d0n[1] + d0p[1], d0n[2] + d0p[2]);
   }
   PathResult res{n_rec, {est[0], est[1], est[2]}};
   return res;
@@ -691,6 +727,49 @@ __global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const v
     const PathResult r = trace_one<kMode>(sc, cfg, pix % width, pix / width, path_id, off, rec,
                                           pth, i);
     if (kMode == kCount) counts[i] = r.n_rec;
+  }
+}
+
+// Single-pass capture: trace every path once, records into scratch slots.
+__global__ void __launch_bounds__(128) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
+                                                       int64_t* __restrict__ counts,
+                                                       const vpg_records scratch,
+                                                       const vpg_paths pth, Capture cap) {
+  const int64_t spp = cfg.spp;
+  const int64_t width = sc.width;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cfg.path_count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t path_id = cfg.path_begin + i;
+    const int64_t pix = path_id / spp;
+    const PathResult r = trace_one<kCapture>(sc, cfg, pix % width, pix / width, path_id, 0,
+                                             scratch, pth, i, cap);
+    counts[i] = r.n_rec;
+  }
+}
+
+// Scratch slot -> its row in path order: rec_start[path] + depth.
+__global__ void k_scatter_records(const vpg_records src, int64_t n, const int64_t* __restrict__ rec_start,
+                                  int64_t path_begin, const vpg_records dst) {
+  for (int64_t sidx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; sidx < n;
+       sidx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pid = src.path_idx[sidx];
+    const int64_t r = rec_start[pid - path_begin] + src.depth[sidx];
+    double* const v3d[10] = {dst.pos, dst.omega_out, dst.normal, dst.coeff, dst.phase_dir,
+                             dst.emit_dir, dst.d_emit, dst.d_phase, dst.i_pt, dst.w_cont};
+    const double* const v3s[10] = {src.pos, src.omega_out, src.normal, src.coeff, src.phase_dir,
+                                   src.emit_dir, src.d_emit, src.d_phase, src.i_pt, src.w_cont};
+#pragma unroll
+    for (int f = 0; f < 10; ++f)
+      for (int c = 0; c < 3; ++c) v3d[f][r * 3 + c] = v3s[f][sidx * 3 + c];
+    dst.g[r] = src.g[sidx];
+    dst.pdf_phase[r] = src.pdf_phase[sidx];
+    dst.pdf_emit_at_phase[r] = src.pdf_emit_at_phase[sidx];
+    dst.pdf_emit[r] = src.pdf_emit[sidx];
+    dst.kind[r] = src.kind[sidx];
+    dst.emit_delta[r] = src.emit_delta[sidx];
+    dst.class_id[r] = src.class_id[sidx];
+    dst.path_idx[r] = pid;
+    dst.depth[r] = src.depth[sidx];
   }
 }
 
@@ -777,6 +856,23 @@ void trace_fill(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records
   check_scene(sc);
   VPG_LAUNCH(k_trace_paths<kFill>, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, nullptr, rec,
              pth);
+}
+
+void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& scratch,
+                   int64_t capacity, unsigned long long* counter, int64_t* counts,
+                   const vpg_paths& pth, cudaStream_t s) {
+  check_scene(sc);
+  VPG_REQUIRE(cfg.max_depth <= kMaxCaptureDepth, VPG_ELIMIT,
+              "single-pass capture supports max_depth <= 128 (use the count/fill passes)");
+  VPG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+  VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts, scratch, pth,
+             Capture{counter, capacity});
+}
+
+void scatter_records(const vpg_records& scratch, int64_t n, const int64_t* rec_start,
+                     int64_t path_begin, const vpg_records& out, cudaStream_t s) {
+  VPG_LAUNCH(k_scatter_records, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin,
+             out);
 }
 
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,

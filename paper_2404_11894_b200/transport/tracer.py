@@ -1,8 +1,8 @@
 """Tracing API over the CUDA tracer (reference: transport/tracer.py:37-127).
 
-render_pt runs the same two passes as the reference (count, exclusive scan of
-the counts into rec_start, fill) but on the device; the record set stays in
-HBM and host copies are made only for fields a caller reads.  Path ids are
+render_pt captures records in one device pass (the reference traces twice:
+count, exclusive scan of the counts into rec_start, fill); the record set
+stays in HBM and host copies are made only for fields a caller reads.  Path ids are
 (y*W + x)*spp + s and every path owns its splitmix64 stream, so a record set
 is identical however the paths are partitioned (multi-GPU row partition:
 `path_range`).
@@ -29,12 +29,13 @@ def _cfg(config: RenderConfig, begin: int, count: int) -> N.TraceCfg:
     return c
 
 
-def _alloc(fields, n, torch):
+def _alloc(fields, n, torch, zero=True):
     out = {}
     dt = {"f8": torch.float64, "i8": torch.int64, "i4": torch.int32, "u1": torch.uint8}
+    make = torch.zeros if zero else torch.empty
     for name, width, code in fields:
         shape = (n, width) if width > 1 else (n,)
-        out[name] = torch.zeros(shape, dtype=dt[code], device="cuda")
+        out[name] = make(shape, dtype=dt[code], device="cuda")
     return out
 
 
@@ -46,8 +47,18 @@ def _struct(cls, tensors, n):
     return st
 
 
+_CAPACITY_HINT: dict = {}  # (scene id, spp, depth, seed, range) -> record count of the last trace
+MAX_CAPTURE_DEPTH = 128
+
+
 def trace_records_device(scene, config: RenderConfig, path_range=None):
-    """Record-capturing trace; returns (records dict, paths dict, n_records) on the device."""
+    """Record-capturing trace; returns (records dict, paths dict, n_records) on the device.
+
+    Single pass: records land in scratch slots, then are scattered into path
+    order (rec_start = exclusive scan of the per-path counts).  Deeper paths
+    than the capture slot list (max_depth > 128) use the reference's two
+    passes (count, then re-trace and fill at the prefix-sum offsets).
+    """
     torch = N.require_cuda()
     packed = pack_scene(scene)
     sc = packed.device()
@@ -59,20 +70,40 @@ def trace_records_device(scene, config: RenderConfig, path_range=None):
     stream = N.stream_handle()
     lib = N.lib()
     counts = torch.empty(count, dtype=torch.int64, device="cuda")
-    N.check(lib.vpg_trace_count(ctypes.byref(sc), ctypes.byref(cfg), counts.data_ptr(),
-                                ctypes.byref(pst), stream))
+    if int(config.max_depth) <= MAX_CAPTURE_DEPTH:
+        key = (id(scene), int(config.spp), int(config.max_depth), int(config.seed), begin, count)
+        capacity = _CAPACITY_HINT.get(key, max(64, 6 * count))
+        counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+        while True:
+            scratch = _alloc(N.RECORD_FIELDS, capacity, torch, zero=False)
+            sst = _struct(N.Records, scratch, capacity)
+            N.check(lib.vpg_trace_capture(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(sst),
+                                          capacity, counter.data_ptr(), counts.data_ptr(),
+                                          ctypes.byref(pst), stream))
+            n_rec = int(counter.item())
+            if n_rec <= capacity:
+                break
+            capacity = n_rec  # dropped records: retrace with exactly enough room
+        _CAPACITY_HINT[key] = n_rec
+    else:
+        N.check(lib.vpg_trace_count(ctypes.byref(sc), ctypes.byref(cfg), counts.data_ptr(),
+                                    ctypes.byref(pst), stream))
+        n_rec = int(counts.sum().item()) if count else 0
     if count:
         torch.cumsum(counts, 0, out=paths["rec_start"])
         paths["rec_start"] -= counts
-        n_rec = int((paths["rec_start"][-1] + counts[-1]).item())
-    else:
-        n_rec = 0
     paths["rec_count"].copy_(counts)
     paths["pixel_idx"].copy_(torch.arange(begin, begin + count, device="cuda") // int(config.spp))
-    recs = _alloc(N.RECORD_FIELDS, n_rec, torch)
+    recs = _alloc(N.RECORD_FIELDS, n_rec, torch, zero=False)
     rst = _struct(N.Records, recs, n_rec)
-    N.check(lib.vpg_trace_fill(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(rst),
-                               ctypes.byref(pst), stream))
+    if int(config.max_depth) <= MAX_CAPTURE_DEPTH:
+        if n_rec:
+            N.check(lib.vpg_scatter_records(ctypes.byref(sst), n_rec, paths["rec_start"].data_ptr(),
+                                            begin, ctypes.byref(rst), stream))
+        del scratch
+    else:
+        N.check(lib.vpg_trace_fill(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(rst),
+                                   ctypes.byref(pst), stream))
     return recs, paths, n_rec
 
 
