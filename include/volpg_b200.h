@@ -150,8 +150,9 @@ typedef struct vpg_graph_info {
   int64_t n_splits;    /* split-loop iterations performed (clustering.py:58-85) */
   int64_t n_fallback;  /* points resolved by the exact global search (clustering.py:142-147) */
   /* per-stage wall times of the last build when VPG_BUILD_TIMINGS is set: 0 classes,
-   * 1 center draw (host RNG), 2 grid + nearest center, 3 grouping, 4 split loop,
-   * 5 cluster layout, 6 operators (all), 7 of which pack + aggregate kernels */
+   * 1 center draw, 2 grid + nearest center, 3 grouping + launch of the part
+   * needing no split, 4 host split loop (overlapping the device), 5 split
+   * results + wait for the operator kernels, 6 solve chunk table */
   double build_ms[8];
   int64_t n_staged;     /* members of oversize groups sent to the host split loop */
   int64_t split_visits; /* sum of group sizes over all splits (split-loop work) */

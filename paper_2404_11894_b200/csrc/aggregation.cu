@@ -37,9 +37,8 @@ struct __align__(32) Member {
   float de[3], dp[3];  // d_emit, d_phase
   float coeff[3], wc[3];
   float ipt[3];
-  int32_t par;     // cluster-major position of the continuation parent, -1 at depth 0
   uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface
-  uint32_t pad[7];
+  uint32_t pad[8];
 };
 static_assert(sizeof(Member) == 192, "Member must stay 6 sectors");
 
@@ -52,13 +51,19 @@ __device__ __forceinline__ float4 f4(double x, double y, double z) {
   return make_float4(float(x), float(y), float(z), 0.f);
 }
 
+// Pack the records list[i] (or off + i when list is null) whose cluster-major
+// position is already known (clpos >= 0).
 __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpos,
+                               const int32_t* __restrict__ list, int64_t list_n, int64_t off,
                                Member* __restrict__ out, float* __restrict__ term_max) {
   const int64_t n = rec.n;
   const int lane = threadIdx.x & 31;
   float tmax[3] = {0.f, 0.f, 0.f};
-  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
-       r += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < list_n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = list ? int64_t(list[i]) : off + i;
+    const int32_t q = clpos[r];
+    if (q < 0) continue;
     Member m;
     const bool volume = rec.kind[r] == 0;
     if (volume) {
@@ -87,18 +92,29 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
       m.ipt[c] = float(rec.i_pt[r * 3 + c]);
     }
     const int64_t pid = rec.path_idx[r];
-    m.par = (r > 0 && rec.path_idx[r - 1] == pid) ? clpos[r - 1] : -1;
     const bool terminal = !(r + 1 < n && rec.path_idx[r + 1] == pid);
     m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u);
-    for (int i = 0; i < 7; ++i) m.pad[i] = 0;
-    out[clpos[r]] = m;
+    for (int k = 0; k < 8; ++k) m.pad[k] = 0;
+    out[q] = m;
     if (terminal)
       for (int c = 0; c < 3; ++c) tmax[c] = fmaxf(tmax[c], fabsf(m.ipt[c]));
   }
   for (int c = 0; c < 3; ++c) {
     float v = tmax[c];
-    for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
     if (lane == 0 && v > 0.f) atomicMax(reinterpret_cast<unsigned int*>(&term_max[c]), __float_as_uint(v));
+  }
+}
+
+// Continuation parents, record order: row clpos[r] propagates into clpos[r-1]
+// when r-1 is on the same path (records.py:128-140), else nowhere (-1).
+__global__ void k_parent_links(vpg_records rec, const int32_t* __restrict__ clpos,
+                               float4* __restrict__ rows) {
+  const int64_t n = rec.n;
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t par = (r > 0 && rec.path_idx[r - 1] == rec.path_idx[r]) ? clpos[r - 1] : -1;
+    reinterpret_cast<int32_t*>(rows)[8 * int64_t(clpos[r]) + 3] = par;
   }
 }
 
@@ -121,7 +137,8 @@ __device__ __forceinline__ double strategy_pdf(const double* __restrict__ geo, i
 //   pd, pe  S*(S+1) floats each (pair densities, row-padded)
 __global__ void __launch_bounds__(kAggThreads)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
-            const int64_t* __restrict__ w_off, int64_t m, int64_t n, int S,
+            const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
+            const int64_t* __restrict__ range, int64_t n, int S,
             float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
             float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
             float4* __restrict__ i0_o) {
@@ -133,9 +150,10 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   __shared__ int s_volume;
   const int tid = threadIdx.x;
 
-  for (int64_t k = blockIdx.x; k < m; k += gridDim.x) {
+  const int64_t k_end = range[1];
+  for (int64_t k = range[0] + blockIdx.x; k < k_end; k += gridDim.x) {
     const int32_t q0 = cl_off[k];
-    const int s = cl_off[k + 1] - q0;
+    const int s = cl_size[k];
     const int64_t wb = w_off[k];
     for (int l = tid; l < s; l += blockDim.x) {
       const Member& mb = mem[q0 + l];
@@ -238,7 +256,7 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
       dbar_o[q] = f4(bx, by, bz);
       coeff_o[q] = f4(kx, ky, kz);
       rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
-                                  __int_as_float(mb.par));
+                                  __int_as_float(-1));  // parent set by k_parent_links
       rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
       i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
@@ -274,71 +292,73 @@ __global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_
 
 }  // namespace
 
-void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool timings) {
-  auto t_start = std::chrono::steady_clock::now();
-  const bool dbg = getenv("VPG_DEBUG_TIMING") != nullptr;
-  auto mark = [&](const char* what) {
-    if (!dbg) return;
-    cudaStreamSynchronize(s);
-    const auto t1 = std::chrono::steady_clock::now();
-    fprintf(stderr, "[vpg] %-28s %8.3f ms\n", what,
-            std::chrono::duration<double, std::milli>(t1 - t_start).count());
-  };
-  mark("ops: enter");
-  const int64_t n = g->n, m = g->m;
-  const int S = std::max(1, g->max_cluster);
-  const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
-  VPG_REQUIRE(smem <= 200 * 1024, VPG_ELIMIT,
-              "clusters larger than 160 members (cluster_size > 80) are not supported");
-  g->wt.alloc(size_t(g->wt_len > 0 ? g->wt_len : 1), s);
+size_t member_bytes() { return sizeof(Member); }
+
+void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s) {
+  const int64_t n = g->n;
+  g->wt.alloc(size_t(wt_capacity > 0 ? wt_capacity : 1), s);
   g->phat.alloc(size_t(3 * n + 1), s);
   for (auto* v : {&g->i0, &g->dbar, &g->coeff, &g->ibuf[0], &g->ibuf[1], &g->acc[0], &g->acc[1]})
     v->alloc(size_t(n + 1), s);
   g->rows.alloc(size_t(2 * n + 2), s);
   g->term_max.alloc(4, s);
   VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
-  if (n == 0) return;
-  mark("ops: alloc graph buffers");
-  Member* members = scratch_of<Member>(s, "members", size_t(n));
-  mark("ops: alloc members");
-  VPG_LAUNCH(k_pack_members, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), members,
-             g->term_max.get());
+}
+
+void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
+                  int64_t off, void* members, cudaStream_t s) {
+  if (list_n <= 0) return;
+  VPG_LAUNCH(k_pack_members, grid_for(list_n, 256), 256, 0, s, rec, g->clpos.get(), list, list_n,
+             off, static_cast<Member*>(members), g->term_max.get());
+}
+
+void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
+                     int S, cudaStream_t s) {
+  if (max_count <= 0) return;
+  const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
+  VPG_REQUIRE(smem <= 200 * 1024, VPG_ELIMIT,
+              "clusters larger than 160 members (cluster_size > 80) are not supported");
   static bool attr_set = false;
   if (!attr_set) {
     VPG_CUDA(cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_set = true;
   }
-  mark("ops: pack");
-  const int64_t blocks = std::min<int64_t>(m, int64_t(sm_count()) * 16);
-  VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, members, g->cl_off.get(),
-             g->w_off.get(), m, n, S, g->wt.get(), g->phat.get(), g->dbar.get(), g->coeff.get(),
-             g->rows.get(), g->i0.get());
-  if (timings) {
-    VPG_CUDA(cudaStreamSynchronize(s));
-    g->info.build_ms[7] =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
-  }
-  mark("ops: aggregate");
-  // solve chunks
-  DBuf<int64_t> cost(m + 1, s), cst(m + 1, s);
-  VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), m, cost.get());
-  {
-    size_t bytes = 0;
-    VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cost.get(), cst.get(), int(m + 1), s));
-    void* tmp = scratch(s, "cub_temp", bytes + 256);
-    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cost.get(), cst.get(), int(m + 1), s));
-    count_launch(1);
-  }
-  int64_t total = 0;
-  VPG_CUDA(cudaMemcpyAsync(&total, cst.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  VPG_CUDA(cudaStreamSynchronize(s));
+  const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
+  VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, static_cast<const Member*>(members),
+             g->cl_off.get(), g->cl_size.get(), g->w_off.get(), range, g->n, S, g->wt.get(),
+             g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get());
+}
+
+void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s) {
+  const int64_t n = g->n, m = g->m;
+  g->chunk_total = 0;
+  if (n == 0) return;
+  VPG_LAUNCH(k_parent_links, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), g->rows.get());
+  // solve chunks: cost prefix over the clusters (internal order)
+  int64_t* cost = scratch_of<int64_t>(s, "chunk_cost", size_t(m) + 1);
+  int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
+  VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), m, cost);
+  size_t bytes = 0;
+  VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cost, cst, int(m + 1), s));
+  void* tmp = scratch(s, "cub_temp", bytes + 256);
+  VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cost, cst, int(m + 1), s));
+  count_launch(1);
+  VPG_CUDA(cudaMemcpyAsync(&g->chunk_total, cst + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   count_transfer(0, 8);
-  g->n_chunks = (total + kChunkFloats - 1) / kChunkFloats;
+}
+
+void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchronised
+  const int64_t m = g->m;
+  g->n_chunks = (g->chunk_total + kChunkFloats - 1) / kChunkFloats;
   g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
-  VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst.get(), m, g->n_chunks,
+  if (g->n == 0) {
+    VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
+    return;
+  }
+  const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
+  VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst, m, g->n_chunks,
              int64_t(kChunkFloats), g->chunk_first.get());
-  mark("ops: chunks");
 }
 
 }  // namespace vpg

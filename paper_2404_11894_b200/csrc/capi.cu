@@ -312,15 +312,8 @@ int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng
   const int rc = guarded([&] {
     g->stream = as_stream(stream);
     g->rec = *rec;
-    vpg::build_clusters(g, *rec, cluster_size, rng, (flags & VPG_BUILD_TIMINGS) != 0, g->stream);
-    const auto t0 = std::chrono::steady_clock::now();
-    if (!(flags & VPG_BUILD_CLUSTERS_ONLY))
-      vpg::build_operators(g, *rec, g->stream, (flags & VPG_BUILD_TIMINGS) != 0);
-    if (flags & VPG_BUILD_TIMINGS) {
-      VPG_CUDA(cudaStreamSynchronize(g->stream));
-      g->info.build_ms[6] =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    }
+    vpg::build_graph(g, *rec, cluster_size, rng, (flags & VPG_BUILD_TIMINGS) != 0,
+                     !(flags & VPG_BUILD_CLUSTERS_ONLY), g->stream);
     g->info.n_records = g->n;
     g->info.n_clusters = g->m;
     g->info.nnz = g->nnz;

@@ -281,6 +281,66 @@ __device__ __forceinline__ void scan_cell(const GridParams& gp, const CellEntry*
 }
 
 
+// ------------------------------------ Generator.choice tail shuffle on device
+// numpy's partial Fisher-Yates (n > 10000, m > n // 50): step k swaps
+// positions i_k = n-1-k and j_k (drawn on the host).  Position i_k is final
+// after step k, so out[m-1-k] = value at j_k before step k, and step k writes
+// the value of position i_k into j_k.  With the (j, k) pairs sorted, the
+// previous writer of any position is found by search, and values follow short
+// chains of earlier writers back to an untouched position.
+__global__ void k_swap_keys(const int32_t* __restrict__ target, int64_t steps,
+                            unsigned long long* __restrict__ keys) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < steps;
+       k += int64_t(gridDim.x) * blockDim.x)
+    keys[k] = (unsigned long long)(uint32_t(target[k])) << 32 | uint32_t(k);
+}
+
+// Largest step k' < k that wrote position p, or -1.
+__device__ __forceinline__ int64_t last_writer(const unsigned long long* __restrict__ sk,
+                                               int64_t steps, uint32_t p, int64_t k) {
+  const unsigned long long key = (unsigned long long)p << 32 | uint32_t(k);
+  int64_t lo = 0, hi = steps;  // first index with sk >= key
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sk[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  if (lo == 0) return -1;
+  const unsigned long long prev = sk[lo - 1];
+  return uint32_t(prev >> 32) == p ? int64_t(uint32_t(prev)) : -1;
+}
+
+// prev_i[k]: last writer of position i_k before step k.
+__global__ void k_swap_links(const unsigned long long* __restrict__ sk, int64_t steps, int64_t n,
+                             int32_t* __restrict__ prev_i) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < steps;
+       k += int64_t(gridDim.x) * blockDim.x)
+    prev_i[k] = int32_t(last_writer(sk, steps, uint32_t(n - 1 - k), k));
+}
+
+// value written by step k = the untouched position at the end of its chain
+__device__ __forceinline__ int32_t written_value(const int32_t* __restrict__ prev_i, int64_t n,
+                                                 int64_t k) {
+  while (prev_i[k] >= 0) k = prev_i[k];
+  return int32_t(n - 1 - k);
+}
+
+__global__ void k_swap_resolve(const int32_t* __restrict__ target,
+                               const unsigned long long* __restrict__ sk,
+                               const int32_t* __restrict__ prev_i, int64_t steps, int64_t n,
+                               int64_t m, int32_t* __restrict__ out) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < steps;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t j = target[k];
+    const int64_t w = last_writer(sk, steps, uint32_t(j), k);
+    out[m - 1 - k] = w < 0 ? j : written_value(prev_i, n, w);
+  }
+  // m == n: position 0 is never a swap source; its final value
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n == m) {
+    const int64_t w = last_writer(sk, steps, 0u, steps);
+    out[0] = w < 0 ? 0 : written_value(prev_i, n, w);
+  }
+}
+
 // ------------------------------------------------ cell-sorted assignment
 constexpr int kCandCap = 128;  // candidate centers staged per warp
 constexpr int kAssignWarps = 8;
@@ -483,6 +543,9 @@ __global__ void k_histogram(const int32_t* __restrict__ assign, int64_t n, int32
 struct SquareOp {
   __host__ __device__ int64_t operator()(int32_t s) const { return int64_t(s) * s; }
 };
+struct MaxOp {
+  __host__ __device__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
 
 struct Oversize {
   const int32_t* counts;
@@ -505,13 +568,33 @@ __global__ void k_oversize_info(const int32_t* __restrict__ over, const int32_t*
   }
 }
 
+// Staging layout of the oversize groups: dst = exclusive scan of their sizes.
+__global__ void k_oversize_seg(const int64_t* __restrict__ info, const int32_t* __restrict__ n_over,
+                               const int64_t* __restrict__ dst, int64_t row_off,
+                               int64_t* __restrict__ seg, int32_t* __restrict__ scalars) {
+  const int n = *n_over;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    seg[k * 3] = row_off + info[k * 4 + 2];
+    seg[k * 3 + 1] = info[k * 4 + 1];
+    seg[k * 3 + 2] = dst[k];
+    if (k == n - 1) scalars[3] = int32_t(dst[k] + info[k * 4 + 1]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n == 0) scalars[3] = 0;
+}
+
+struct OverCount {
+  const int64_t* info;
+  __host__ __device__ int64_t operator()(int32_t k) const { return info[k * 4 + 1]; }
+};
+
 // Gather members (record id + position) of the oversize groups for the host.
 __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
-                                  const int64_t* __restrict__ seg, int n_seg,
+                                  const int64_t* __restrict__ seg, const int32_t* __restrict__ n_seg,
                                   const double* __restrict__ pos, int32_t* __restrict__ out_rec,
                                   double* __restrict__ out_pos) {
   // seg[k*3+0] = source offset, seg[k*3+1] = count, seg[k*3+2] = destination offset
-  for (int k = blockIdx.x; k < n_seg; k += gridDim.x) {
+  const int nk = *n_seg;
+  for (int k = blockIdx.x; k < nk; k += gridDim.x) {
     const int64_t src = seg[k * 3], cnt = seg[k * 3 + 1], dst = seg[k * 3 + 2];
     for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) {
       const int32_t r = grp_rec[src + t];
@@ -523,75 +606,136 @@ __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
   }
 }
 
-// Entries of the final group list (clustering.py:87-93): class c's original
-// groups j occupy entries base_c + j, its split-off groups follow.
-__global__ void k_init_entries(const int32_t* __restrict__ counts, const int32_t* __restrict__ gstart,
-                               const int32_t* __restrict__ crec, int m, int64_t row_off,
-                               int64_t base, int32_t* __restrict__ e_size,
-                               int64_t* __restrict__ e_src, int32_t* __restrict__ e_center) {
+// ------------------------------------------------------------ layout
+// Internal cluster order: part A = every group that needed no split, class by
+// class in group order; part B = the split loop's results (modified groups and
+// split-off groups).  Part A is laid out, packed and aggregated on the device
+// while the host runs the split loop; the reference's numbering (groups in
+// order, skipping empty ones, split-off groups appended per class,
+// clustering.py:87-93) is kept in ref_of.
+struct LayoutAcc {  // exclusive-scan element over a class's groups
+  int32_t a, ne, rows;
+  int64_t w;
+};
+struct LayoutSum {
+  __host__ __device__ LayoutAcc operator()(const LayoutAcc& x, const LayoutAcc& y) const {
+    return LayoutAcc{x.a + y.a, x.ne + y.ne, x.rows + y.rows, x.w + y.w};
+  }
+};
+struct LayoutOf {
+  int32_t max_size;
+  __host__ __device__ LayoutAcc operator()(int32_t size) const {
+    const bool in_a = size > 0 && size <= max_size;
+    return LayoutAcc{in_a ? 1 : 0, size > 0 ? 1 : 0, in_a ? size : 0,
+                     in_a ? ((int64_t(size) * size + 3) & ~int64_t(3)) : 0};
+  }
+};
+
+// Device totals: acc = {A clusters, A rows, A kernel floats, non-empty groups}.
+// cls = per class {A begin, A end, reference base, non-empty groups}.
+__global__ void k_layout_a(const int32_t* __restrict__ counts, const int32_t* __restrict__ gstart,
+                           const int32_t* __restrict__ crec, const LayoutAcc* __restrict__ pre,
+                           int m, int32_t max_size, int64_t row_off, int64_t appended_before,
+                           const int64_t* __restrict__ acc, int32_t* __restrict__ cl_off,
+                           int32_t* __restrict__ cl_size, int64_t* __restrict__ w_off,
+                           int64_t* __restrict__ cl_src, int32_t* __restrict__ cl_center,
+                           int32_t* __restrict__ ref_of, int32_t* __restrict__ ne_prefix) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
-    e_size[base + j] = counts[j];
-    e_src[base + j] = row_off + gstart[j];
-    e_center[base + j] = crec[j];
+    const int32_t size = counts[j];
+    const LayoutAcc e = pre[j];
+    ne_prefix[j] = e.ne;
+    if (size <= 0 || size > max_size) continue;
+    const int64_t k = acc[0] + e.a;
+    cl_off[k] = int32_t(acc[1] + e.rows);
+    cl_size[k] = size;
+    w_off[k] = acc[2] + e.w;
+    cl_src[k] = row_off + gstart[j];
+    cl_center[k] = crec[j];
+    ref_of[k] = int32_t(acc[3] + appended_before + e.ne);
   }
 }
 
-// Split results: entry, size, source (-(1+offset) into the split buffer), center.
-__global__ void k_apply_entries(const int64_t* __restrict__ mods, int64_t n_mods,
-                                int32_t* __restrict__ e_size, int64_t* __restrict__ e_src,
-                                int32_t* __restrict__ e_center) {
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n_mods;
-       k += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e = mods[k * 4];
-    e_size[e] = int32_t(mods[k * 4 + 1]);
-    e_src[e] = mods[k * 4 + 2];
-    e_center[e] = int32_t(mods[k * 4 + 3]);
+__global__ void k_layout_a_totals(const int32_t* __restrict__ counts,
+                                  const LayoutAcc* __restrict__ pre, int m, int32_t max_size,
+                                  int64_t appended_before, int64_t* __restrict__ acc,
+                                  int64_t* __restrict__ cls) {
+  const LayoutAcc last = LayoutSum()(pre[m - 1], LayoutOf{max_size}(counts[m - 1]));
+  cls[0] = acc[0];
+  cls[1] = acc[0] + last.a;
+  cls[2] = acc[3] + appended_before;
+  cls[3] = last.ne;
+  acc[0] += last.a;
+  acc[1] += last.rows;
+  acc[2] += last.w;
+  acc[3] += last.ne;
+}
+
+// Part B: b[t*8..] = {class, group j (>= 0) or -(1+appended index), size, row
+// offset in part B, kernel offset in part B, split-buffer offset, center, 0}.
+__global__ void k_layout_b(const int64_t* __restrict__ b, int64_t nb, const int64_t* __restrict__ acc,
+                           const int64_t* __restrict__ cls, const int32_t* __restrict__ ne_prefix_all,
+                           const int64_t* __restrict__ class_center_off, int32_t* __restrict__ cl_off,
+                           int32_t* __restrict__ cl_size, int64_t* __restrict__ w_off,
+                           int64_t* __restrict__ cl_src, int32_t* __restrict__ cl_center,
+                           int32_t* __restrict__ ref_of) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nb;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t* e = b + t * 8;
+    const int c = int(e[0]);
+    const int64_t k = acc[0] + t;
+    cl_off[k] = int32_t(acc[1] + e[3]);
+    cl_size[k] = int32_t(e[2]);
+    w_off[k] = acc[2] + e[4];
+    cl_src[k] = -1 - e[5];
+    cl_center[k] = int32_t(e[6]);
+    const int64_t* ci = cls + 4 * c;
+    ref_of[k] = int32_t(e[1] >= 0 ? ci[2] + ne_prefix_all[class_center_off[c] + e[1]]
+                                  : ci[2] + ci[3] + (-1 - e[1]));
   }
 }
 
-__global__ void k_entry_flags(const int32_t* __restrict__ e_size, int64_t n, int32_t* __restrict__ f) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-       e += int64_t(gridDim.x) * blockDim.x)
-    f[e] = e_size[e] > 0 ? 1 : 0;
+// Closing offsets cl_off[M], w_off[M] and the internal range of part B.
+__global__ void k_layout_close(int64_t nb, int64_t rows_b, int64_t w_b, const int64_t* __restrict__ acc,
+                               int32_t* __restrict__ cl_off, int64_t* __restrict__ w_off,
+                               int64_t* __restrict__ range_b) {
+  const int64_t M = acc[0] + nb;
+  cl_off[M] = int32_t(acc[1] + rows_b);
+  w_off[M] = acc[2] + w_b;
+  range_b[0] = acc[0];
+  range_b[1] = M;
 }
 
-// Non-empty entries -> clusters in entry order; sizes, sources, centers, and
-// the scan inputs for the member and kernel-block offsets.
-__global__ void k_compact_entries(const int32_t* __restrict__ e_size, const int64_t* __restrict__ e_src,
-                                  const int32_t* __restrict__ e_center,
-                                  const int32_t* __restrict__ cid, int64_t n_entries,
-                                  int32_t* __restrict__ cl_size, int64_t* __restrict__ cl_src,
-                                  int32_t* __restrict__ cl_center, int64_t* __restrict__ sq) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_entries;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int32_t s = e_size[e];
-    if (s <= 0) continue;
-    const int32_t k = cid[e];
-    cl_size[k] = s;
-    cl_src[k] = e_src[e];
-    cl_center[k] = e_center[e];
-    sq[k] = (int64_t(s) * s + 3) & ~int64_t(3);  // blocks start 16-byte aligned
-  }
-}
-
-// Cluster-major permutation: warp per cluster copies its member list.
-__global__ void k_fill_perm(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ cl_src,
-                            int64_t m, const int32_t* __restrict__ grp_rec,
+// Cluster-major permutation for the clusters in [range[0], range[1]): warp
+// per cluster copies its member list; records get their position and the
+// reference cluster number.
+__global__ void k_fill_perm(const int64_t* __restrict__ range, const int32_t* __restrict__ cl_off,
+                            const int32_t* __restrict__ cl_size, const int64_t* __restrict__ cl_src,
+                            const int32_t* __restrict__ ref_of, const int32_t* __restrict__ grp_rec,
                             const int32_t* __restrict__ split_rec, int32_t* __restrict__ perm,
                             int32_t* __restrict__ clpos, int32_t* __restrict__ cluster_id) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < m; k += warps) {
-    const int32_t q0 = cl_off[k], q1 = cl_off[k + 1];
+  const int64_t k1 = range[1];
+  for (int64_t k = range[0] + ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5); k < k1;
+       k += warps) {
+    const int32_t q0 = cl_off[k], sz = cl_size[k];
     const int64_t src = cl_src[k];
     const int32_t* from = src >= 0 ? grp_rec + src : split_rec + (-1 - src);
-    for (int32_t t = lane; t < q1 - q0; t += 32) {
+    const int32_t ref = ref_of[k];
+    for (int32_t t = lane; t < sz; t += 32) {
       const int32_t r = from[t];
       perm[q0 + t] = r;
       clpos[r] = q0 + t;
-      cluster_id[r] = int32_t(k);
+      cluster_id[r] = ref;
     }
   }
+}
+
+__global__ void k_invert_ref(const int32_t* __restrict__ ref_of, int64_t m,
+                             int32_t* __restrict__ internal_of) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < m;
+       k += int64_t(gridDim.x) * blockDim.x)
+    internal_of[ref_of[k]] = int32_t(k);
 }
 
 template <class T>
@@ -697,8 +841,8 @@ GridParams make_grid(const ClassPlan& p) {
 
 }  // namespace
 
-void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng_state,
-                    bool timings, cudaStream_t s) {
+void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng_state,
+                 bool timings, bool with_ops, cudaStream_t s) {
   const int64_t n = rec.n;
   VPG_REQUIRE(K >= 1, VPG_EINVAL, "cluster size K must be >= 1");
   VPG_REQUIRE(n < (int64_t(1) << 31) - 1, VPG_ELIMIT, "more than 2^31-2 records per device");
@@ -714,14 +858,20 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   g->cluster_id.alloc(n, s);
   if (n == 0) {
     g->m = 0;
-    g->cl_off.alloc(1, s);
+    for (auto* v : {&g->cl_off, &g->cl_size, &g->cl_center, &g->ref_of, &g->internal_of}) {
+      v->alloc(1, s);
+      VPG_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(int32_t), s));
+    }
     g->w_off.alloc(1, s);
-    g->cl_center.alloc(1, s);
-    VPG_CUDA(cudaMemsetAsync(g->cl_off.get(), 0, sizeof(int32_t), s));
     VPG_CUDA(cudaMemsetAsync(g->w_off.get(), 0, sizeof(int64_t), s));
+    if (with_ops) alloc_operator_buffers(g, 1, s);
+    g->chunk_first.alloc(1, s);
+    VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
+    g->n_chunks = 0;
     rng.store(rng_state);
     return;
   }
+  VPG_CUDA(cudaMemsetAsync(g->clpos.get(), 0xFF, sizeof(int32_t) * n, s));  // -1: not placed
 
   // ---- classes (np.unique order of kind<<32 | class_id, graph.py:59)
   const int nbits_words = 2 * kSlotsPerKind / 32;
@@ -803,14 +953,45 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
   int32_t* values = scratch_of<int32_t>(s, "values", n);
   int32_t* fb_list = scratch_of<int32_t>(s, "fb_list", n);
   DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s), gstart_all(center_total, s);
+  DBuf<int32_t> ne_prefix_all(center_total + 1, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
+  DBuf<int64_t> acc(8, s), cls_info(size_t(4) * n_cls + 4, s), ranges(size_t(2) * n_cls + 2, s);
+  DBuf<int64_t> class_center_off(n_cls + 1, s);
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
-
-  std::vector<int32_t> split_rec;  // members of every split group, back to back
-  std::vector<int64_t> mods;       // (entry offset within class, size, src, center) x4
-  std::vector<int64_t> class_mod_begin(n_cls + 1, 0), class_appended(n_cls, 0);
-  int64_t n_splits = 0;
+  VPG_CUDA(cudaMemsetAsync(acc.get(), 0, acc.bytes(), s));
+  {
+    std::vector<int64_t> cco(n_cls + 1, 0);
+    for (int c = 0; c < n_cls; ++c) cco[c] = plan[c].center_off;
+    to_device(class_center_off.get(), cco, s);
+  }
   const int64_t max_size = 2 * int64_t(K);
+  const int S = int(std::max<int64_t>(1, std::min<int64_t>(max_size, n)));
+
+  // part A cluster arrays (at most one cluster per center)
+  const int64_t cap_a = center_total + 1;
+  DBuf<int32_t> a_off(cap_a, s), a_size(cap_a, s), a_center(cap_a, s), a_ref(cap_a, s);
+  DBuf<int64_t> a_w(cap_a, s), a_src(cap_a, s);
+  // the operator passes run against g's arrays: point them at part A for now
+  g->cl_off = std::move(a_off);
+  g->cl_size = std::move(a_size);
+  g->cl_center = std::move(a_center);
+  g->ref_of = std::move(a_ref);
+  g->w_off = std::move(a_w);
+  void* members = nullptr;
+  if (with_ops) {
+    // kernel blocks: sum of pad4(s^2) <= 2K * N + 3 per cluster
+    const int64_t wt_cap = std::min<int64_t>(max_size, n) * n + 4 * (center_total + n) + 16;
+    alloc_operator_buffers(g, wt_cap, s);
+    members = scratch(s, "members", member_bytes() * size_t(n) + 256);
+  }
+
+  std::vector<int32_t> split_rec;    // members of every split group, back to back
+  std::vector<int64_t> part_b;       // 8 int64 per split group, see k_layout_b
+  int64_t rows_b = 0, w_b = 0, appended_before = 0;
+  int64_t n_splits = 0;
+  HostBuf<int64_t> h_acc(8);
+  cudaEvent_t acc_ready;
+  VPG_CUDA(cudaEventCreateWithFlags(&acc_ready, cudaEventDisableTiming));
 
   for (int c = 0; c < n_cls; ++c) {
     const ClassPlan& p = plan[c];
@@ -837,27 +1018,52 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
         end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
       const int64_t nn = p.n;
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids,
-                                               pids_sorted, int(nn), 0, end_bits, s);
+        return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted, int(nn),
+                                               0, end_bits, s);
       }, s);
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys,
-                                                  run_len, scalars.get() + 1, int(nn), s);
+        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
+                                                  scalars.get() + 1, int(nn), s);
       }, s);
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(nn), s);
       }, s);
     }
 
-    // host: m centers = Generator.choice(n, m) (clustering.py:51)
-    HostBuf<int64_t> picks(m);
-    HostBuf<int32_t> picks32(m);
-    rng_choice(rng, p.n, p.m, picks.get());
-    for (int j = 0; j < m; ++j) picks32[j] = int32_t(picks[j]);
+    // m centers = Generator.choice(n, m) (clustering.py:51)
     DBuf<int32_t> d_local(m, s);
-    VPG_CUDA(cudaMemcpyAsync(d_local.get(), picks32.get(), sizeof(int32_t) * m,
-                             cudaMemcpyHostToDevice, s));
-    count_transfer(sizeof(int32_t) * m, 0);
+    if (p.n > 10000 && p.m > p.n / 50) {
+      // tail shuffle: the host draws the swap targets (sequential stream),
+      // the device resolves the swaps
+      const int64_t stop = (p.n - p.m) > 1 ? (p.n - p.m) : 1;
+      const int64_t steps = p.n - stop;
+      HostBuf<int32_t> targets(size_t(steps) + 1);
+      for (int64_t k = 0; k < steps; ++k) targets[k] = int32_t(rng.bounded(uint64_t(p.n - 1 - k)));
+      int32_t* d_target = scratch_of<int32_t>(s, "swap_target", steps + 1);
+      unsigned long long* d_keys = scratch_of<unsigned long long>(s, "swap_keys", steps + 1);
+      unsigned long long* d_sk = scratch_of<unsigned long long>(s, "swap_sorted", steps + 1);
+      int32_t* d_prev = scratch_of<int32_t>(s, "swap_prev", steps + 1);
+      VPG_CUDA(cudaMemcpyAsync(d_target, targets.get(), sizeof(int32_t) * steps,
+                               cudaMemcpyHostToDevice, s));
+      count_transfer(sizeof(int32_t) * steps, 0);
+      VPG_LAUNCH(k_swap_keys, grid_for(steps, block), block, 0, s, d_target, steps, d_keys);
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, d_keys, d_sk, int(steps), 0, 64, s);
+      }, s);
+      VPG_LAUNCH(k_swap_links, grid_for(steps, block), block, 0, s, d_sk, steps, p.n, d_prev);
+      VPG_LAUNCH(k_swap_resolve, grid_for(steps, block), block, 0, s, d_target, d_sk, d_prev, steps,
+                 p.n, p.m, d_local.get());
+      VPG_CUDA(cudaStreamSynchronize(s));  // `targets` (pinned) must outlive the copy
+    } else {
+      HostBuf<int64_t> picks(m);
+      HostBuf<int32_t> picks32(m);
+      rng_choice(rng, p.n, p.m, picks.get());
+      for (int j = 0; j < m; ++j) picks32[j] = int32_t(picks[j]);
+      VPG_CUDA(cudaMemcpyAsync(d_local.get(), picks32.get(), sizeof(int32_t) * m,
+                               cudaMemcpyHostToDevice, s));
+      count_transfer(sizeof(int32_t) * m, 0);
+      VPG_CUDA(cudaStreamSynchronize(s));
+    }
     clk.mark(1);
 
     DBuf<double> cpos(size_t(m) * 3, s);
@@ -887,8 +1093,8 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
                  table.get());
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
-                 rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start,
-                 run_len, scalars.get() + 1, assign_c, fb_list, scalars.get());
+                 rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start, run_len,
+                 scalars.get() + 1, assign_c, fb_list, scalars.get());
       VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
                  table.get(), spos.get(), fb_list, scalars.get(), assign_c);
     }
@@ -900,14 +1106,14 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
     int32_t* counts_c = counts_all.get() + p.center_off;
     int32_t* gstart_c = gstart_all.get() + p.center_off;
     {
-      DBuf<int32_t> sorted_keys(p.n, s);
+      int32_t* sorted_keys = scratch_of<int32_t>(s, "sorted_keys", p.n);
       const int end_bit = bits_for(uint64_t(m > 1 ? m - 1 : 1));
       const int64_t nn = p.n;
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, reinterpret_cast<uint32_t*>(assign_c),
-                                               reinterpret_cast<uint32_t*>(sorted_keys.get()),
-                                               values + p.row_off, grp_rec + p.row_off,
-                                               int(nn), 0, end_bit, s);
+                                               reinterpret_cast<uint32_t*>(sorted_keys),
+                                               values + p.row_off, grp_rec + p.row_off, int(nn), 0,
+                                               end_bit, s);
       }, s);
     }
     VPG_LAUNCH(k_histogram, grid_for(p.n, block), block, 0, s, assign_c, p.n, counts_c);
@@ -926,61 +1132,110 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
     }
     VPG_LAUNCH(k_oversize_info, grid_for(m, block), block, 0, s, over.get(), scalars.get() + 2,
                counts_c, gstart_c, crec_all.get() + p.center_off, over_info.get());
-    std::vector<int32_t> h_scalars;
-    to_host(h_scalars, scalars.get(), 4, s);
+    int64_t* over_dst = scratch_of<int64_t>(s, "over_dst", size_t(m) + 1);
+    int64_t* over_seg = scratch_of<int64_t>(s, "over_seg", size_t(m) * 3 + 3);
+    {
+      cub::CountingInputIterator<int32_t> it0(0);
+      cub::TransformInputIterator<int64_t, OverCount, cub::CountingInputIterator<int32_t>> cnt_it(
+          it0, OverCount{over_info.get()});
+      // scanning all m entries is cheap; entries past n_over are unused
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, cnt_it, over_dst, m, s);
+      }, s);
+    }
+    VPG_LAUNCH(k_oversize_seg, grid_for(m, block), block, 0, s, over_info.get(), scalars.get() + 2,
+               over_dst, p.row_off, over_seg, scalars.get());
+
+    // ---- part A of this class: layout (device)
+    {
+      LayoutAcc* pre = scratch_of<LayoutAcc>(s, "layout_pre", size_t(m) + 1);
+      cub::TransformInputIterator<LayoutAcc, LayoutOf, const int32_t*> it(
+          counts_c, LayoutOf{int32_t(max_size)});
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveScan(t, b, it, pre, LayoutSum(), LayoutAcc{0, 0, 0, 0}, m, s);
+      }, s);
+      VPG_LAUNCH(k_layout_a, grid_for(m, block), block, 0, s, counts_c, gstart_c,
+                 crec_all.get() + p.center_off, pre, m, int32_t(max_size), p.row_off,
+                 appended_before, acc.get(), g->cl_off.get(), g->cl_size.get(), g->w_off.get(),
+                 a_src.get(), g->cl_center.get(), g->ref_of.get(),
+                 ne_prefix_all.get() + p.center_off);
+      VPG_LAUNCH(k_layout_a_totals, 1, 1, 0, s, counts_c, pre, m, int32_t(max_size),
+                 appended_before, acc.get(), cls_info.get() + 4 * c);
+      VPG_CUDA(cudaMemcpyAsync(ranges.get() + 2 * c, cls_info.get() + 4 * c, 2 * sizeof(int64_t),
+                               cudaMemcpyDeviceToDevice, s));
+      if (c == n_cls - 1) {
+        VPG_CUDA(cudaMemcpyAsync(h_acc.get(), acc.get(), 8 * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s));
+        count_transfer(0, 64);
+        VPG_CUDA(cudaEventRecord(acc_ready, s));
+      }
+    }
+    // sizes of the oversize staging (nothing heavy is queued before this sync)
+    HostBuf<int32_t> h_scalars(4);
+    VPG_CUDA(cudaMemcpyAsync(h_scalars.get(), scalars.get(), 4 * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+    count_transfer(0, 16);
     VPG_CUDA(cudaStreamSynchronize(s));
     g->info.n_fallback += h_scalars[0];
     const int n_over = h_scalars[2];
+    const int64_t staged = n_over > 0 ? h_scalars[3] : 0;
+    // oversize members and positions to the host, queued ahead of part A
+    HostBuf<int64_t> info(size_t(n_over) * 4 + 4);
+    HostBuf<int32_t> h_srec(size_t(staged) + 1);
+    HostBuf<double> xyz(size_t(staged) * 3 + 3);
+    cudaEvent_t staged_ready;
+    VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
+    if (n_over > 0) {
+      int32_t* d_srec = scratch_of<int32_t>(s, "staged_rec", size_t(staged) + 1);
+      double* d_spos = scratch_of<double>(s, "staged_pos", size_t(staged) * 3 + 3);
+      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec, over_seg,
+                 scalars.get() + 2, rec.pos, d_srec, d_spos);
+      VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
+                               cudaMemcpyDeviceToHost, s));
+      VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec, sizeof(int32_t) * staged,
+                               cudaMemcpyDeviceToHost, s));
+      VPG_CUDA(cudaMemcpyAsync(xyz.get(), d_spos, sizeof(double) * 3 * staged,
+                               cudaMemcpyDeviceToHost, s));
+      count_transfer(0, 32 * n_over + 28 * staged);
+    }
+    VPG_CUDA(cudaEventRecord(staged_ready, s));
+    // ---- part A of this class: permutation, pack, aggregate (device, async)
+    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
+               g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
+               g->clpos.get(), g->cluster_id.get());
+    if (with_ops) {
+      pack_members(g, rec, rows_p ? rows_p + p.row_off : nullptr, p.n, p.row_off, members, s);
+      aggregate_range(g, members, ranges.get() + 2 * c, m, S, s);
+    }
     clk.mark(3);
 
-    // ---- split loop on the oversize groups (host, exact RNG order)
-    class_mod_begin[c] = int64_t(mods.size()) / 4;
+    // ---- split loop on the oversize groups (host, exact RNG order), while
+    // the device aggregates part A
     DebugClock dbg(s);
+    VPG_CUDA(cudaEventSynchronize(staged_ready));
+    cudaEventDestroy(staged_ready);
+    int64_t appended_c = 0;
     if (n_over > 0) {
-      std::vector<int64_t> info;
-      to_host(info, over_info.get(), size_t(n_over) * 4, s);
-      VPG_CUDA(cudaStreamSynchronize(s));
-      std::vector<int64_t> seg(size_t(n_over) * 3);
-      std::vector<int32_t> h_crec_over(n_over);
-      int64_t staged = 0;
-      for (int k = 0; k < n_over; ++k) {
-        seg[k * 3] = p.row_off + info[k * 4 + 2];
-        seg[k * 3 + 1] = info[k * 4 + 1];
-        seg[k * 3 + 2] = staged;
-        h_crec_over[k] = int32_t(info[k * 4 + 3]);
-        staged += info[k * 4 + 1];
-      }
-      DBuf<int64_t> d_seg(seg.size(), s);
-      to_device(d_seg.get(), seg, s);
-      DBuf<int32_t> d_srec(staged, s);
-      DBuf<double> d_spos(staged * 3, s);
-      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec,
-                 d_seg.get(), n_over, rec.pos, d_srec.get(), d_spos.get());
-      HostBuf<int32_t> h_srec(staged);
-      HostBuf<double> xyz(staged * 3);
-      VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec.get(), sizeof(int32_t) * staged,
-                               cudaMemcpyDeviceToHost, s));
-      VPG_CUDA(cudaMemcpyAsync(xyz.get(), d_spos.get(), sizeof(double) * 3 * staged,
-                               cudaMemcpyDeviceToHost, s));
-      count_transfer(0, 28 * staged);
-      VPG_CUDA(cudaStreamSynchronize(s));
       dbg.mark("split: info+gather+D2H", false);
       // initial center positions: the center is one of its group's members
       // except with coincident centers (then it is fetched by record id)
       std::vector<SplitGroup> groups(n_over);
       std::vector<double> c0(size_t(n_over) * 3);
+      int64_t b = 0;
       for (int k = 0; k < n_over; ++k) {
-        const int64_t b = seg[k * 3 + 2], cnt = seg[k * 3 + 1];
-        groups[k] = SplitGroup{b, cnt, h_crec_over[k]};
+        const int64_t cnt = info[k * 4 + 1];
+        const int32_t crec = int32_t(info[k * 4 + 3]);
+        groups[k] = SplitGroup{b, cnt, crec};
         int64_t t = b;
-        while (t < b + cnt && h_srec[t] != h_crec_over[k]) ++t;
+        while (t < b + cnt && h_srec[t] != crec) ++t;
         if (t < b + cnt) {
           for (int a = 0; a < 3; ++a) c0[k * 3 + a] = xyz[t * 3 + a];
         } else {
-          VPG_CUDA(cudaMemcpy(&c0[k * 3], rec.pos + int64_t(h_crec_over[k]) * 3,
-                              3 * sizeof(double), cudaMemcpyDeviceToHost));
+          VPG_CUDA(cudaMemcpy(&c0[k * 3], rec.pos + int64_t(crec) * 3, 3 * sizeof(double),
+                              cudaMemcpyDeviceToHost));
           count_transfer(0, 24);
         }
+        b += cnt;
       }
       g->info.n_staged += staged;
       dbg.mark("split: center lookup", false);
@@ -990,105 +1245,109 @@ void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* 
       const int64_t base_split = int64_t(split_rec.size());
       split_rec.insert(split_rec.end(), h_srec.get(), h_srec.get() + staged);
       for (size_t k = 0; k < groups.size(); ++k) {
-        const int64_t entry = k < size_t(n_over) ? info[k * 4] : p.m + int64_t(k) - n_over;
-        mods.push_back(entry);
-        mods.push_back(groups[k].size);
-        mods.push_back(-1 - (base_split + groups[k].begin));
-        mods.push_back(groups[k].center);
+        const int64_t sz = groups[k].size;
+        const int64_t j = k < size_t(n_over) ? info[k * 4] : -1 - (int64_t(k) - n_over);
+        const int64_t e[8] = {c, j, sz, rows_b, w_b, base_split + groups[k].begin,
+                              groups[k].center, 0};
+        part_b.insert(part_b.end(), e, e + 8);
+        rows_b += sz;
+        w_b += (sz * sz + 3) & ~int64_t(3);
       }
-      class_appended[c] = int64_t(groups.size()) - n_over;
+      appended_c = int64_t(groups.size()) - n_over;
       dbg.mark("split: mods", false);
     }
-    class_mod_begin[c + 1] = int64_t(mods.size()) / 4;
+    appended_before += appended_c;
     clk.mark(4);
   }
   g->info.n_splits = n_splits;
   rng.store(rng_state);
 
-  // ---- final group list -> clusters (clustering.py:87-93), on the device
-  std::vector<int64_t> entry_base(n_cls + 1, 0);
-  for (int c = 0; c < n_cls; ++c) entry_base[c + 1] = entry_base[c] + plan[c].m + class_appended[c];
-  const int64_t F = entry_base[n_cls];
-  DBuf<int32_t> e_size(F + 1, s), e_center(F + 1, s), e_flag(F + 1, s), e_cid(F + 1, s);
-  DBuf<int64_t> e_src(F + 1, s);
-  for (int c = 0; c < n_cls; ++c) {
-    const ClassPlan& p = plan[c];
-    VPG_LAUNCH(k_init_entries, grid_for(p.m, block), block, 0, s, counts_all.get() + p.center_off,
-               gstart_all.get() + p.center_off, crec_all.get() + p.center_off, int(p.m),
-               p.row_off, entry_base[c], e_size.get(), e_src.get(), e_center.get());
-    for (int64_t k = class_mod_begin[c]; k < class_mod_begin[c + 1]; ++k) mods[k * 4] += entry_base[c];
+  // ---- part B: the split results, appended after part A
+  VPG_CUDA(cudaEventSynchronize(acc_ready));
+  cudaEventDestroy(acc_ready);
+  const int64_t m_a = h_acc[0];
+  const int64_t nb = int64_t(part_b.size()) / 8;
+  const int64_t M = m_a + nb;
+  g->m = M;
+  {
+    // final cluster arrays: part A copied over, part B written below
+    DBuf<int32_t> f_off(M + 1, s), f_size(M + 1, s), f_center(M + 1, s), f_ref(M + 1, s);
+    DBuf<int64_t> f_w(M + 1, s), f_src(M + 1, s);
+    auto copy_a = [&](void* dst, const void* src, size_t elem) {
+      if (m_a) VPG_CUDA(cudaMemcpyAsync(dst, src, elem * m_a, cudaMemcpyDeviceToDevice, s));
+    };
+    copy_a(f_off.get(), g->cl_off.get(), 4);
+    copy_a(f_size.get(), g->cl_size.get(), 4);
+    copy_a(f_center.get(), g->cl_center.get(), 4);
+    copy_a(f_ref.get(), g->ref_of.get(), 4);
+    copy_a(f_w.get(), g->w_off.get(), 8);
+    copy_a(f_src.get(), a_src.get(), 8);
+    g->cl_off = std::move(f_off);
+    g->cl_size = std::move(f_size);
+    g->cl_center = std::move(f_center);
+    g->ref_of = std::move(f_ref);
+    g->w_off = std::move(f_w);
+    a_src = std::move(f_src);
   }
-  const int64_t n_mods = int64_t(mods.size()) / 4;
-  DBuf<int64_t> d_mods(mods.size() + 1, s);
-  DBuf<int32_t> d_split(split_rec.size() + 1, s);
-  HostBuf<int64_t> hm;  // staging stays alive until the final synchronisation below
+  HostBuf<int64_t> hb;
   HostBuf<int32_t> hs;
-  if (n_mods) {
-    hm.alloc(mods.size());
+  DBuf<int64_t> d_b(part_b.size() + 8, s);
+  DBuf<int32_t> d_split(split_rec.size() + 1, s);
+  DBuf<int64_t> range_b(2, s);
+  if (nb) {
+    hb.alloc(part_b.size());
     hs.alloc(split_rec.size());
-    std::copy(mods.begin(), mods.end(), hm.get());
+    std::copy(part_b.begin(), part_b.end(), hb.get());
     std::copy(split_rec.begin(), split_rec.end(), hs.get());
-    VPG_CUDA(cudaMemcpyAsync(d_mods.get(), hm.get(), sizeof(int64_t) * mods.size(),
+    VPG_CUDA(cudaMemcpyAsync(d_b.get(), hb.get(), sizeof(int64_t) * part_b.size(),
                              cudaMemcpyHostToDevice, s));
     VPG_CUDA(cudaMemcpyAsync(d_split.get(), hs.get(), sizeof(int32_t) * split_rec.size(),
                              cudaMemcpyHostToDevice, s));
-    count_transfer(8 * mods.size() + 4 * split_rec.size(), 0);
-    VPG_LAUNCH(k_apply_entries, grid_for(n_mods, block), block, 0, s, d_mods.get(), n_mods,
-               e_size.get(), e_src.get(), e_center.get());
+    count_transfer(8 * part_b.size() + 4 * split_rec.size(), 0);
+    VPG_LAUNCH(k_layout_b, grid_for(nb, block), block, 0, s, d_b.get(), nb, acc.get(),
+               cls_info.get(), ne_prefix_all.get(), class_center_off.get(), g->cl_off.get(),
+               g->cl_size.get(), g->w_off.get(), a_src.get(), g->cl_center.get(), g->ref_of.get());
   }
-  VPG_CUDA(cudaMemsetAsync(e_size.get() + F, 0, sizeof(int32_t), s));
-  VPG_LAUNCH(k_entry_flags, grid_for(F + 1, block), block, 0, s, e_size.get(), F + 1, e_flag.get());
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, e_flag.get(), e_cid.get(), int(F + 1), s);
-  }, s);
-  // M = e_cid[F]; clusters <= F
-  DBuf<int32_t> cl_size(F + 1, s);
-  DBuf<int64_t> cl_src(F + 1, s), d_sq(F + 1, s);
-  g->cl_center.alloc(F + 1, s);
-  VPG_CUDA(cudaMemsetAsync(d_sq.get(), 0, d_sq.bytes(), s));
-  VPG_CUDA(cudaMemsetAsync(cl_size.get(), 0, cl_size.bytes(), s));
-  VPG_LAUNCH(k_compact_entries, grid_for(F, block), block, 0, s, e_size.get(), e_src.get(),
-             e_center.get(), e_cid.get(), F, cl_size.get(), cl_src.get(), g->cl_center.get(),
-             d_sq.get());
-  g->cl_off.alloc(F + 1, s);
-  g->w_off.alloc(F + 1, s);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, cl_size.get(), g->cl_off.get(), int(F + 1), s);
-  }, s);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, d_sq.get(), g->w_off.get(), int(F + 1), s);
-  }, s);
-  DBuf<int32_t> d_max(1, s);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceReduce::Max(t, b, cl_size.get(), d_max.get(), int(F + 1), s);
-  }, s);
-  int32_t h_m = 0, h_max = 0;
-  VPG_CUDA(cudaMemcpyAsync(&h_m, e_cid.get() + F, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  VPG_CUDA(cudaStreamSynchronize(s));
-  count_transfer(0, 8);
-  const int64_t M = h_m;
-  g->m = M;
-  g->max_cluster = h_max;
-  // w_off / cl_off beyond M repeat the totals (sizes there are 0)
-  VPG_LAUNCH(k_fill_perm, grid_for(M * 32, block), block, 0, s, g->cl_off.get(), cl_src.get(), M,
-             grp_rec, d_split.get(), g->perm.get(), g->clpos.get(), g->cluster_id.get());
-  int64_t h_len = 0;
-  VPG_CUDA(cudaMemcpyAsync(&h_len, g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_LAUNCH(k_layout_close, 1, 1, 0, s, nb, rows_b, w_b, acc.get(), g->cl_off.get(),
+             g->w_off.get(), range_b.get());
+  if (nb) {
+    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, range_b.get(), g->cl_off.get(),
+               g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, d_split.get(),
+               g->perm.get(), g->clpos.get(), g->cluster_id.get());
+    if (with_ops) {
+      pack_members(g, rec, d_split.get(), int64_t(split_rec.size()), 0, members, s);
+      aggregate_range(g, members, range_b.get(), nb, S, s);
+    }
+  }
+  g->internal_of.alloc(M + 1, s);
+  VPG_LAUNCH(k_invert_ref, grid_for(M, block), block, 0, s, g->ref_of.get(), M,
+             g->internal_of.get());
+  // totals: nnz (sum of s^2), padded kernel length, largest cluster
   DBuf<int64_t> d_nnz(1, s);
+  DBuf<int32_t> d_max(1, s);
   {
-    cub::TransformInputIterator<int64_t, SquareOp, const int32_t*> sq_it(cl_size.get(), SquareOp());
+    cub::TransformInputIterator<int64_t, SquareOp, const int32_t*> sq_it(g->cl_size.get(), SquareOp());
     cub_call([&](void* t, size_t& b) {
-      return cub::DeviceReduce::Sum(t, b, sq_it, d_nnz.get(), int(M > 0 ? M : 1), s);
+      return cub::DeviceReduce::Sum(t, b, sq_it, d_nnz.get(), int(M), s);
+    }, s);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceReduce::Reduce(t, b, g->cl_size.get(), d_max.get(), int(M), MaxOp(), 0, s);
     }, s);
   }
-  int64_t h_nnz = 0;
-  VPG_CUDA(cudaMemcpyAsync(&h_nnz, d_nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  int64_t h_tot[2] = {0, 0};
+  int32_t h_max = 0;
+  VPG_CUDA(cudaMemcpyAsync(&h_tot[0], d_nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_tot[1], g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (with_ops) finalize_operators_async(g, rec, s);
   VPG_CUDA(cudaStreamSynchronize(s));
-  count_transfer(0, 16);
-  g->nnz = M > 0 ? h_nnz : 0;
-  g->wt_len = h_len;
+  count_transfer(0, 20);
+  g->nnz = h_tot[0];
+  g->wt_len = h_tot[1];
+  g->max_cluster = h_max;
   clk.mark(5);
+  if (with_ops) finalize_chunks(g, s);
+  clk.mark(6);
 }
 
 }  // namespace vpg

@@ -5,7 +5,12 @@
 //                        contiguous, members ascending (clustering.py:87-93)
 //   clpos[r]     int32   record -> cluster-major position (inverse of perm)
 //   cluster_id[r]int32   record -> cluster number (reference numbering)
+//   Internally clusters are ordered [groups that needed no split, in group
+//   order | split results]: the first part is packed and aggregated on the
+//   device while the host runs the split loop.  ref_of[k] / internal_of[r]
+//   map internal order <-> the reference's cluster numbering.
 //   cl_off[k]    int32   (M+1) start of cluster k in cluster-major order
+//   cl_size[k]   int32   members of cluster k
 //   w_off[k]     int64   (M+1) start of cluster k's dense kernel block (blocks
 //                        padded to 4 floats so every block is 16-byte aligned)
 //   wt[]         float   nnz   per cluster an s x s block stored transposed:
@@ -29,14 +34,14 @@ struct vpg_graph {
   cudaStream_t stream = nullptr;
   int64_t n = 0, m = 0, nnz = 0, wt_len = 0;
   int32_t K = 0;
-  vpg::DBuf<int32_t> perm, clpos, cluster_id, cl_off, cl_center;
+  vpg::DBuf<int32_t> perm, clpos, cluster_id, cl_off, cl_size, cl_center, ref_of, internal_of;
   vpg::DBuf<int64_t> w_off;
   vpg::DBuf<float> wt;
   vpg::DBuf<double> phat;
   vpg::DBuf<float4> i0, dbar, coeff, ibuf[2], acc[2];
   vpg::DBuf<float4> rows;  // 2 float4 per row: (a.xyz, par bits), (b.xyz, 0)
   vpg::DBuf<int32_t> chunk_first;
-  int64_t n_chunks = 0;
+  int64_t n_chunks = 0, chunk_total = 0;
   vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows
   // solve state (device): red[t*8 + 0..5] float bits, ctl = {performed, stop, grow, diverged}
   vpg::DBuf<uint32_t> red;
@@ -53,9 +58,19 @@ struct vpg_graph {
 namespace vpg {
 // floats of kernel blocks + row data per solve chunk (one shared-memory stage)
 constexpr int kChunkFloats = 8192;
-// cluster.cu: fills perm/clpos/cluster_id/cl_off/w_off/cl_center.
-void build_clusters(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng,
-                    bool timings, cudaStream_t s);
-// operators.cu: marginals, kernel blocks, D-bar and solve vectors.
-void build_operators(vpg_graph* g, const vpg_records& rec, cudaStream_t s, bool timings = false);
+// cluster.cu: the whole build (clusters, layout, and the operator passes
+// below, overlapped with the host split loop); `with_operators` = false for
+// cluster_points.
+void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng, bool timings,
+                 bool with_operators, cudaStream_t s);
+// aggregation.cu
+size_t member_bytes();
+void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s);
+void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
+                  int64_t off, void* members, cudaStream_t s);
+void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
+                     int S, cudaStream_t s);
+// parent links + chunk cost scan (async); chunk table once the host has the total
+void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s);
+void finalize_chunks(vpg_graph* g, cudaStream_t s);
 }  // namespace vpg

@@ -419,28 +419,52 @@ __global__ void k_scatter_phat(const double* __restrict__ phat, const int32_t* _
   }
 }
 
-__global__ void k_row_sizes(const int32_t* __restrict__ cluster_id, const int32_t* __restrict__ cl_off,
-                            int64_t n, int64_t* __restrict__ sz) {
+__global__ void k_row_sizes(const int32_t* __restrict__ cluster_id,
+                            const int32_t* __restrict__ internal_of,
+                            const int32_t* __restrict__ cl_size, int64_t n, int64_t* __restrict__ sz) {
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r <= n;
        r += int64_t(gridDim.x) * blockDim.x) {
     if (r == n) { sz[r] = 0; continue; }
-    const int32_t k = cluster_id[r];
-    sz[r] = cl_off[k + 1] - cl_off[k];
+    sz[r] = cl_size[internal_of[cluster_id[r]]];
+  }
+}
+
+// Clusters in the reference's numbering: sizes, member lists, centers.
+__global__ void k_ref_sizes(const int32_t* __restrict__ internal_of,
+                            const int32_t* __restrict__ cl_size, int64_t m, int64_t* __restrict__ sz) {
+  for (int64_t rr = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; rr <= m;
+       rr += int64_t(gridDim.x) * blockDim.x)
+    sz[rr] = rr < m ? cl_size[internal_of[rr]] : 0;
+}
+
+__global__ void k_ref_members(const int32_t* __restrict__ internal_of,
+                              const int32_t* __restrict__ cl_off, const int32_t* __restrict__ cl_size,
+                              const int32_t* __restrict__ cl_center, const int32_t* __restrict__ perm,
+                              const int64_t* __restrict__ off, int64_t m, int64_t* __restrict__ members,
+                              int64_t* __restrict__ centers) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t rr = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; rr < m; rr += warps) {
+    const int32_t k = internal_of[rr];
+    const int32_t q0 = cl_off[k], sz = cl_size[k];
+    for (int32_t t = lane; t < sz; t += 32) members[off[rr] + t] = perm[q0 + t];
+    if (lane == 0) centers[rr] = cl_center[k];
   }
 }
 
 // CSR rows of W in record order (graph.py:167): warp per row.
-__global__ void k_export_csr(const int32_t* __restrict__ cluster_id, const int32_t* __restrict__ clpos,
-                             const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
-                             const int32_t* __restrict__ perm, const float* __restrict__ wt,
-                             const int64_t* __restrict__ indptr, int64_t n,
-                             int64_t* __restrict__ indices, double* __restrict__ data) {
+__global__ void k_export_csr(const int32_t* __restrict__ cluster_id,
+                             const int32_t* __restrict__ internal_of, const int32_t* __restrict__ clpos,
+                             const int32_t* __restrict__ cl_off, const int32_t* __restrict__ cl_size,
+                             const int64_t* __restrict__ w_off, const int32_t* __restrict__ perm,
+                             const float* __restrict__ wt, const int64_t* __restrict__ indptr,
+                             int64_t n, int64_t* __restrict__ indices, double* __restrict__ data) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < n; r += nwarps) {
-    const int32_t k = cluster_id[r];
+    const int32_t k = internal_of[cluster_id[r]];
     const int32_t q0 = cl_off[k];
-    const int s = cl_off[k + 1] - q0;
+    const int s = cl_size[k];
     const int rl = clpos[r] - q0;
     const int64_t base = indptr[r];
     for (int j = lane; j < s; j += 32) {
@@ -635,17 +659,30 @@ void export_clusters(const vpg_graph* g, int64_t* cluster_id, int64_t* cl_off, i
                      int64_t* centers, cudaStream_t s) {
   const int64_t n = g->n, m = g->m;
   const int block = 256;
-  DBuf<int64_t> tmp(size_t(std::max<int64_t>(n, m + 1)) + 1, s);
-  auto out = [&](const int32_t* src, int64_t cnt, int64_t* host) {
-    if (!host || cnt == 0) return;
-    VPG_LAUNCH(k_i32_to_i64, grid_for(cnt, block), block, 0, s, src, cnt, tmp.get());
-    VPG_CUDA(cudaMemcpyAsync(host, tmp.get(), cnt * 8, cudaMemcpyDeviceToHost, s));
+  if (cluster_id && n) {
+    DBuf<int64_t> tmp(n, s);
+    VPG_LAUNCH(k_i32_to_i64, grid_for(n, block), block, 0, s, g->cluster_id.get(), n, tmp.get());
+    VPG_CUDA(cudaMemcpyAsync(cluster_id, tmp.get(), n * 8, cudaMemcpyDeviceToHost, s));
     VPG_CUDA(cudaStreamSynchronize(s));
-  };
-  out(g->cluster_id.get(), n, cluster_id);
-  out(g->cl_off.get(), m + 1, cl_off);
-  out(g->perm.get(), n, members);
-  out(g->cl_center.get(), m, centers);
+  }
+  if (!(cl_off || members || centers)) return;
+  DBuf<int64_t> sz(m + 1, s), off(m + 1, s), mem(n + 1, s), cen(m + 1, s);
+  VPG_LAUNCH(k_ref_sizes, grid_for(m + 1, block), block, 0, s, g->internal_of.get(),
+             g->cl_size.get(), m, sz.get());
+  size_t bytes = 0;
+  VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), off.get(), int(m + 1), s));
+  {
+    DBuf<char> t(bytes, s);
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), bytes, sz.get(), off.get(), int(m + 1), s));
+    count_launch(1);
+  }
+  VPG_LAUNCH(k_ref_members, grid_for(m * 32, block), block, 0, s, g->internal_of.get(),
+             g->cl_off.get(), g->cl_size.get(), g->cl_center.get(), g->perm.get(), off.get(), m,
+             mem.get(), cen.get());
+  if (cl_off) VPG_CUDA(cudaMemcpyAsync(cl_off, off.get(), (m + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (members && n) VPG_CUDA(cudaMemcpyAsync(members, mem.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  if (centers && m) VPG_CUDA(cudaMemcpyAsync(centers, cen.get(), m * 8, cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaStreamSynchronize(s));
 }
 
 void export_marginals(const vpg_graph* g, double* p0, double* p1, double* p2, cudaStream_t s) {
@@ -671,7 +708,7 @@ void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, dou
   if (indptr || indices || data) {
     DBuf<int64_t> sz(n + 1, s), ip(n + 1, s);
     VPG_LAUNCH(k_row_sizes, grid_for(n + 1, block), block, 0, s, g->cluster_id.get(),
-               g->cl_off.get(), n, sz.get());
+               g->internal_of.get(), g->cl_size.get(), n, sz.get());
     size_t bytes = 0;
     VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), ip.get(), int(n + 1), s));
     {
@@ -684,8 +721,8 @@ void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, dou
       DBuf<int64_t> ind(size_t(g->nnz) + 1, s);
       DBuf<double> dat(size_t(g->nnz) + 1, s);
       VPG_LAUNCH(k_export_csr, grid_for(n * 32, block), block, 0, s, g->cluster_id.get(),
-                 g->clpos.get(), g->cl_off.get(), g->w_off.get(), g->perm.get(), g->wt.get(),
-                 ip.get(), n, ind.get(), dat.get());
+                 g->internal_of.get(), g->clpos.get(), g->cl_off.get(), g->cl_size.get(),
+                 g->w_off.get(), g->perm.get(), g->wt.get(), ip.get(), n, ind.get(), dat.get());
       if (indices) VPG_CUDA(cudaMemcpyAsync(indices, ind.get(), g->nnz * 8, cudaMemcpyDeviceToHost, s));
       if (data) VPG_CUDA(cudaMemcpyAsync(data, dat.get(), g->nnz * 8, cudaMemcpyDeviceToHost, s));
       VPG_CUDA(cudaStreamSynchronize(s));
