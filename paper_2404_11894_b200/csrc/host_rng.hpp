@@ -191,28 +191,33 @@ struct SplitGroup {
 // oversize groups back to back (each group ascending, groups in ascending
 // original order); `xyz` their positions (3 doubles per slot, moved with the
 // ids).  `groups` describes them; `center_xyz[3k..3k+3)` is the position of
-// groups[k].center.
-// Each split partitions its range in place (stable: kept members first), so
-// every final group stays a contiguous ascending range.  The squared
-// distance of each member to its current center is cached: a split only
-// evaluates the distance to the new center, and moved members inherit it.
-// On return groups[0..q) are the originals (possibly shrunk) and groups[q..)
-// the split-off groups in append order.  Returns the number of splits.
+// groups[k].center.  Each split partitions its range in place (stable: kept
+// members compacted forward, moved ones appended after them), so every final
+// group stays a contiguous ascending range.  The squared distance of each
+// member to its current center is cached (a split only evaluates the
+// distance to the new center; moved members inherit it) and each group knows
+// the slot of its center, so no pass searches for it.  On return
+// groups[0..q) are the originals (possibly shrunk) and groups[q..) the
+// split-off groups in append order.  Returns the number of splits.
 inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
                               std::vector<SplitGroup>& groups, int64_t max_size,
                               const double* center_xyz, int64_t* visits = nullptr) {
-  std::unique_ptr<double[]> d0(new double[total + 1]), d1(new double[total + 1]);
+  std::unique_ptr<double[]> d0(new double[total + 1]);
+  std::vector<int64_t> cslot(groups.size(), -1);  // slot of each group's center, -1 if absent
   for (size_t k = 0; k < groups.size(); ++k) {
     const SplitGroup& gr = groups[k];
-    for (int64_t t = gr.begin; t < gr.begin + gr.size; ++t)
+    for (int64_t t = gr.begin; t < gr.begin + gr.size; ++t) {
       d0[t] = dist2(&xyz[t * 3], center_xyz + k * 3);
+      if (ids[t] == gr.center && cslot[k] < 0) cslot[k] = t;
+    }
   }
   std::vector<int64_t> stack;
   for (int64_t c = 0; c < int64_t(groups.size()); ++c)
     if (groups[c].size > max_size) stack.push_back(c);
-  std::vector<int32_t> tid;
-  std::vector<double> txyz, td;
+  std::vector<int32_t> mid;
+  std::vector<double> mxyz, md;
   int64_t splits = 0;
+  double* __restrict__ dd0 = d0.get();
   while (!stack.empty()) {
     const int64_t c = stack.back();
     stack.pop_back();
@@ -221,12 +226,7 @@ inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
     const int64_t b = gr.begin, e = gr.begin + gr.size;
     if (visits) *visits += gr.size;
     // candidates = members != old center, in member order (clustering.py:65-67)
-    int64_t at = -1;
-    for (int64_t t = b; t < e; ++t)
-      if (ids[t] == gr.center) {
-        at = t - b;
-        break;
-      }
+    const int64_t at = cslot[c] >= 0 ? cslot[c] - b : -1;
     const int64_t pool = at >= 0 ? gr.size - 1 : gr.size;
     int64_t pick;
     if (pool > 0) {
@@ -237,45 +237,55 @@ inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
     }
     const int64_t new_center = ids[b + pick];
     const double pn[3] = {xyz[(b + pick) * 3], xyz[(b + pick) * 3 + 1], xyz[(b + pick) * 3 + 2]};
-    double* __restrict__ dd0 = d0.get();
-    double* __restrict__ dd1 = d1.get();
-    int64_t moved = 0;
+    // one pass: keep members compacted forward in place, moved ones to the side
+    if (int64_t(mid.size()) < gr.size) {
+      mid.resize(gr.size);
+      md.resize(gr.size);
+      mxyz.resize(gr.size * 3);
+    }
+    int64_t wk = b, wm = 0, keep_center = -1, moved_center = -1;
+    const int64_t old_slot = cslot[c], new_slot = b + pick;
     for (int64_t t = b; t < e; ++t) {
       const double v = dist2(&xyz[t * 3], pn);
-      dd1[t] = v;
-      moved += v < dd0[t];  // np.argmin over (old, new): ties stay
+      if (v < dd0[t]) {  // np.argmin over (old, new): ties stay
+        if (t == new_slot) moved_center = wm;
+        mid[wm] = ids[t];
+        md[wm] = v;
+        mxyz[wm * 3] = xyz[t * 3];
+        mxyz[wm * 3 + 1] = xyz[t * 3 + 1];
+        mxyz[wm * 3 + 2] = xyz[t * 3 + 2];
+        ++wm;
+      } else {
+        if (t == old_slot) keep_center = wk;
+        if (wk != t) {
+          ids[wk] = ids[t];
+          dd0[wk] = dd0[t];
+          xyz[wk * 3] = xyz[t * 3];
+          xyz[wk * 3 + 1] = xyz[t * 3 + 1];
+          xyz[wk * 3 + 2] = xyz[t * 3 + 2];
+        }
+        ++wk;
+      }
     }
-    const int64_t kept = gr.size - moved;
+    const int64_t kept = wk - b, moved = wm;
     if (kept == 0 || moved == 0) {
-      // coincident points: halves (clustering.py:75-78); the second half
-      // takes the new center, so its cached distance becomes d1
+      // coincident points: halves (clustering.py:75-78).  Nothing was written
+      // back, so the range still holds the group in member order.  The second
+      // half takes the new center: its cached distances become d(., new).
       const int64_t half = gr.size / 2;
-      for (int64_t t = b + half; t < e; ++t) dd0[t] = dd1[t];
+      for (int64_t t = b + half; t < e; ++t) dd0[t] = dist2(&xyz[t * 3], pn);
       groups[c].size = half;
+      cslot[c] = (old_slot >= 0 && old_slot < b + half) ? old_slot : -1;
       groups.push_back(SplitGroup{b + half, gr.size - half, new_center});
+      cslot.push_back(new_slot >= b + half ? new_slot : -1);
     } else {
-      if (int64_t(tid.size()) < gr.size) {
-        tid.resize(gr.size);
-        td.resize(gr.size);
-        txyz.resize(gr.size * 3);
-      }
-      int64_t wk = 0, wm = kept;
-      for (int64_t t = b; t < e; ++t) {
-        const bool go = dd1[t] < dd0[t];
-        const int64_t w = go ? wm : wk;
-        wm += go;
-        wk += !go;
-        tid[w] = ids[t];
-        td[w] = go ? dd1[t] : dd0[t];
-        txyz[w * 3] = xyz[t * 3];
-        txyz[w * 3 + 1] = xyz[t * 3 + 1];
-        txyz[w * 3 + 2] = xyz[t * 3 + 2];
-      }
-      std::memcpy(ids + b, tid.data(), sizeof(int32_t) * gr.size);
-      std::memcpy(dd0 + b, td.data(), sizeof(double) * gr.size);
-      std::memcpy(xyz + b * 3, txyz.data(), sizeof(double) * 3 * gr.size);
+      std::memcpy(ids + wk, mid.data(), sizeof(int32_t) * moved);
+      std::memcpy(dd0 + wk, md.data(), sizeof(double) * moved);
+      std::memcpy(xyz + wk * 3, mxyz.data(), sizeof(double) * 3 * moved);
       groups[c].size = kept;
-      groups.push_back(SplitGroup{b + kept, moved, new_center});
+      cslot[c] = keep_center;
+      groups.push_back(SplitGroup{wk, moved, new_center});
+      cslot.push_back(moved_center >= 0 ? wk + moved_center : -1);
     }
     ++splits;
     if (groups[c].size > max_size) stack.push_back(c);
