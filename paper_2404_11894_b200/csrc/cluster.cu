@@ -343,6 +343,7 @@ __global__ void k_swap_resolve(const int32_t* __restrict__ target,
 
 // ------------------------------------------------ cell-sorted assignment
 constexpr int kCandCap = 128;  // candidate centers staged per warp
+constexpr long long kShellBudget = 4096;  // cells one fallback point may enumerate
 constexpr int kAssignWarps = 8;
 
 // Sort key of a point's cell: a dense linear index over the padded grid when
@@ -480,7 +481,10 @@ __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
                                   const CellEntry* __restrict__ table,
                                   const double4* __restrict__ spos,
                                   const int32_t* __restrict__ fb_list, const int32_t* fb_count,
-                                  int32_t* __restrict__ assign) {
+                                  int32_t* __restrict__ assign, int32_t* __restrict__ far_list,
+                                  int32_t* __restrict__ far_count,
+                                  unsigned long long* __restrict__ far_d,
+                                  int32_t* __restrict__ far_j) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *fb_count;
@@ -496,20 +500,18 @@ __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
       scan_cell(gp, table, spos, cx + lane / 9 - 1, cy + (lane / 3) % 3 - 1, cz + lane % 3 - 1,
                 px, py, pz, b);
     warp_best(b);
+    bool resolved = false;
+    long long spent = 27;  // cells enumerated; beyond kShellBudget the tiled scan is cheaper
     for (int R = 1;; ++R) {
       const double lim = (double(R) - gp.slack) * gp.cell;
-      if (b.j != 0x7FFFFFFF && b.d2 < lim * lim * (1.0 - 1e-9)) break;
-      const long long side = 2LL * R + 3;
-      const long long cube = side * side * side;
-      const long long shell = cube - (side - 2) * (side - 2) * (side - 2);
-      if (shell > gp.m || R > gp.max_dim + 1) {
-        for (int t = lane; t < gp.m; t += 32) {
-          const double4 c = spos[t];
-          best_update(b, dist2_exact(px, py, pz, c.x, c.y, c.z), int(__double_as_longlong(c.w)));
-        }
-        warp_best(b);
+      if (b.j != 0x7FFFFFFF && b.d2 < lim * lim * (1.0 - 1e-9)) {
+        resolved = true;
         break;
       }
+      const long long side = 2LL * R + 3;
+      const long long cube = side * side * side;
+      if (spent + cube > kShellBudget || R > gp.max_dim + 1) break;
+      spent += cube;
       const int Rn = R + 1;
       for (long long t = lane; t < cube; t += 32) {
         const int dx = int(t / (side * side)) - Rn;
@@ -524,8 +526,81 @@ __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
       }
       warp_best(b);
     }
-    if (lane == 0) assign[i] = b.j;
+    if (lane == 0) {
+      if (resolved) assign[i] = b.j;
+      else {
+        const int slot = atomicAdd(far_count, 1);
+        far_list[slot] = int32_t(i);
+        far_d[slot] = ~0ULL;
+        far_j[slot] = 0x7FFFFFFF;
+      }
+    }
   }
+}
+
+// Exact global argmin for the few points far from every center: blocks take
+// (256 points) x (a slice of the centers), the slice is staged through shared
+// memory and shared by all the block's points.  The slices merge through two
+// atomics that keep the result lexicographic in (d2, center): pass 0 takes the
+// min of d2 (non-negative doubles order like their bit patterns), pass 1 the
+// lowest center attaining it.
+constexpr int kFarSlices = 32;
+__global__ void __launch_bounds__(256)
+k_far_tiles(const int32_t* rows, int64_t row_off, const double* __restrict__ pos,
+            const double4* __restrict__ spos, int m, const int32_t* __restrict__ far_list,
+            const int32_t* __restrict__ far_count, unsigned long long* __restrict__ far_d,
+            int32_t* __restrict__ far_j, int pass) {
+  __shared__ double4 tile[256];
+  const int nf = *far_count;
+  const int groups = (nf + 255) / 256;
+  const int64_t per = (int64_t(m) + kFarSlices - 1) / kFarSlices;
+  for (int blk = blockIdx.x; blk < groups * kFarSlices; blk += gridDim.x) {
+    const int grp = blk / kFarSlices, slice = blk % kFarSlices;
+    const int pi = grp * 256 + threadIdx.x;
+    const bool active = pi < nf;
+    double px = 0, py = 0, pz = 0, target = 0;
+    if (active) {
+      const int64_t r = class_row(rows, row_off, far_list[pi]);
+      px = pos[r * 3];
+      py = pos[r * 3 + 1];
+      pz = pos[r * 3 + 2];
+      if (pass) target = __longlong_as_double((long long)far_d[pi]);
+    }
+    Best b{INFINITY, 0x7FFFFFFF};
+    const int64_t c0 = slice * per;
+    const int64_t c1 = (c0 + per < int64_t(m)) ? c0 + per : int64_t(m);
+    for (int64_t base = c0; base < c1; base += 256) {
+      __syncthreads();
+      if (base + threadIdx.x < c1) tile[threadIdx.x] = spos[base + threadIdx.x];
+      __syncthreads();
+      const int cnt = (c1 - base < 256) ? int(c1 - base) : 256;
+      if (active) {
+        if (pass == 0) {
+          for (int q = 0; q < cnt; ++q) {
+            const double4 c = tile[q];
+            b.d2 = fmin(b.d2, dist2_exact(px, py, pz, c.x, c.y, c.z));
+          }
+        } else {
+          for (int q = 0; q < cnt; ++q) {
+            const double4 c = tile[q];
+            if (dist2_exact(px, py, pz, c.x, c.y, c.z) == target)
+              b.j = min(b.j, int(__double_as_longlong(c.w)));
+          }
+        }
+      }
+    }
+    if (active) {
+      if (pass == 0) atomicMin(&far_d[pi], (unsigned long long)__double_as_longlong(b.d2));
+      else if (b.j != 0x7FFFFFFF) atomicMin(&far_j[pi], b.j);
+    }
+  }
+}
+
+__global__ void k_far_store(const int32_t* __restrict__ far_list, const int32_t* __restrict__ far_count,
+                            const int32_t* __restrict__ far_j, int32_t* __restrict__ assign) {
+  const int nf = *far_count;
+  for (int pi = blockIdx.x * blockDim.x + threadIdx.x; pi < nf; pi += gridDim.x * blockDim.x)
+    assign[far_list[pi]] = far_j[pi];
 }
 
 __global__ void k_group_values(const int32_t* rows, int64_t row_off, int64_t n, int32_t* out) {
@@ -955,6 +1030,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s), gstart_all(center_total, s);
   DBuf<int32_t> ne_prefix_all(center_total + 1, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
+  DBuf<int32_t> far_count(1, s);
   DBuf<int64_t> acc(8, s), cls_info(size_t(4) * n_cls + 4, s), ranges(size_t(2) * n_cls + 2, s);
   DBuf<int64_t> class_center_off(n_cls + 1, s);
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
@@ -1095,8 +1171,20 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
                  rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start, run_len,
                  scalars.get() + 1, assign_c, fb_list, scalars.get());
+      int32_t* far_list = scratch_of<int32_t>(s, "far_list", p.n + 1);
+      auto* far_d = scratch_of<unsigned long long>(s, "far_d", p.n + 1);
+      int32_t* far_j = scratch_of<int32_t>(s, "far_j", p.n + 1);
+      VPG_CUDA(cudaMemsetAsync(far_count.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
-                 table.get(), spos.get(), fb_list, scalars.get(), assign_c);
+                 table.get(), spos.get(), fb_list, scalars.get(), assign_c, far_list,
+                 far_count.get(), far_d, far_j);
+      // points beyond the shell budget: tiled exact scan (grid sized for the
+      // worst case; blocks past the list's end exit at once)
+      for (int pass = 0; pass < 2; ++pass)
+        VPG_LAUNCH(k_far_tiles, sm_count() * 4, 256, 0, s, rows_p, p.row_off, rec.pos, spos.get(),
+                   m, far_list, far_count.get(), far_d, far_j, pass);
+      VPG_LAUNCH(k_far_store, sm_count() * 2, 256, 0, s, far_list, far_count.get(), far_j,
+                 assign_c);
     }
     clk.mark(2);
 
