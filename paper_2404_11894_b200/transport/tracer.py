@@ -49,6 +49,22 @@ def _struct(cls, tensors, n):
 
 _CAPACITY_HINT: dict = {}  # (scene id, spp, depth, seed, range) -> record count of the last trace
 MAX_CAPTURE_DEPTH = 128
+# Capture scratch, kept across calls (grow-only): re-allocating ~290 B x
+# capacity every frame costs more than the scatter itself.
+_SCRATCH: dict = {"capacity": 0, "tensors": None}
+
+
+def _scratch(capacity, torch):
+    if _SCRATCH["capacity"] < capacity or _SCRATCH["tensors"] is None:
+        _SCRATCH["tensors"] = None
+        _SCRATCH["tensors"] = _alloc(N.RECORD_FIELDS, capacity, torch, zero=False)
+        _SCRATCH["capacity"] = capacity
+    return _SCRATCH["tensors"], _SCRATCH["capacity"]
+
+
+def release_scratch():
+    """Free the capture scratch (it is otherwise kept for the next trace)."""
+    _SCRATCH["tensors"], _SCRATCH["capacity"] = None, 0
 
 
 def trace_records_device(scene, config: RenderConfig, path_range=None):
@@ -75,7 +91,7 @@ def trace_records_device(scene, config: RenderConfig, path_range=None):
         capacity = _CAPACITY_HINT.get(key, max(64, 6 * count))
         counter = torch.zeros(1, dtype=torch.int64, device="cuda")
         while True:
-            scratch = _alloc(N.RECORD_FIELDS, capacity, torch, zero=False)
+            scratch, capacity = _scratch(capacity, torch)
             sst = _struct(N.Records, scratch, capacity)
             N.check(lib.vpg_trace_capture(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(sst),
                                           capacity, counter.data_ptr(), counts.data_ptr(),
@@ -100,7 +116,6 @@ def trace_records_device(scene, config: RenderConfig, path_range=None):
         if n_rec:
             N.check(lib.vpg_scatter_records(ctypes.byref(sst), n_rec, paths["rec_start"].data_ptr(),
                                             begin, ctypes.byref(rst), stream))
-        del scratch
     else:
         N.check(lib.vpg_trace_fill(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(rst),
                                    ctypes.byref(pst), stream))
