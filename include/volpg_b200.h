@@ -59,7 +59,8 @@ int vpg_profile_reset(void);
 int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* total_ms,
                      int64_t cap, int64_t* n_kernels);
 /* sizeof() of the ABI structs, for binding self-checks:
- * 0 vpg_pcg64, 1 vpg_records, 2 vpg_paths, 3 vpg_graph_info, 4 vpg_scene, 5 vpg_trace_cfg */
+ * 0 vpg_pcg64, 1 vpg_records, 2 vpg_paths, 3 vpg_graph_info, 4 vpg_scene, 5 vpg_trace_cfg,
+ * 6 vpg_graph_views */
 size_t vpg_struct_size(int32_t which);
 
 /* ------------------------------------------------- numpy Generator replica
@@ -186,6 +187,49 @@ int vpg_graph_export_marginals(const vpg_graph* g, double* phat_ind, double* pha
 int vpg_graph_export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices,
                                double* data, double* d_bar, void* stream);
 
+/* ------------------------------------------------------ shard-local graph
+ * Multi-GPU row partition (pathgraph/sharded.py; SURVEY §8e option B): the
+ * clusters are partitioned over the shards, every record moves once to the
+ * shard owning its cluster, and each shard builds the operators of its own
+ * clusters with this call.  `rec` (device, n rows) is already cluster-major:
+ * the n_clusters clusters lie back to back with cl_size[k] (host) members in
+ * ascending global record order, so marginals, kernel blocks and D-bar are
+ * computed exactly as by vpg_graph_build (graph.py:94-168).  Continuation
+ * edges are explicit because a record's parent (record r-1 of the same path,
+ * records.py:128-140) may live on another shard:
+ *   parent[q]    (n, device) local row of q's parent, -1 for a path's first
+ *                record, or n + h: halo slot h (the parent is remote)
+ *   has_child[q] (n, device u8) 1 if q has a continuation child anywhere
+ *   halo_ipt     (n_halo x 3 fp64, device) i_pt of each halo slot's parent
+ *                (its I_0, solve.py:72)
+ * The solve then runs as vpg_solve_begin, per iteration vpg_solve_step ->
+ * (the caller sends halo slots n.. of the output I vector to their owners,
+ * writes the received values into its own rows, and max-reduces the 7
+ * residual words red[t*8 .. t*8+6] and, once, term_max[0..2] over all
+ * shards) -> vpg_solve_control, and finally vpg_solve_end.  On one shard
+ * (n_halo = 0, nothing to exchange) this is exactly vpg_solve. */
+int vpg_graph_build_local(const vpg_records* rec, int64_t n_clusters, const int32_t* cl_size,
+                          const int32_t* parent, const uint8_t* has_child, int64_t n_halo,
+                          const double* halo_ipt, void* stream, vpg_graph** out);
+
+/* Device pointers into a graph (read-only unless stated; valid until
+ * vpg_graph_free).  float* vectors are float4 per row (xyz = RGB).
+ * ibuf[t&1] is iteration t's input I, ibuf[(t+1)&1] its output (halo slots
+ * n .. n+n_halo-1 included); acc = W*I; red[t*8 + 0..5] = float bits of the
+ * residual maxima, red[t*8 + 6] = NaN channel bits (writable between step
+ * and control); term_max[0..2] writable after the build. */
+typedef struct vpg_graph_views {
+  int64_t n, m, n_halo;
+  int32_t *perm, *clpos, *cluster_id, *cl_off, *cl_size, *cl_center, *ref_of, *internal_of;
+  float *i0, *ibuf[2], *acc[2], *dbar;
+  float* term_max;
+  uint32_t* red;
+  int32_t* ctl;
+  int32_t performed;
+  int32_t _pad;
+} vpg_graph_views;
+int vpg_graph_views_get(const vpg_graph* g, vpg_graph_views* views);
+
 /* ----------------------------------------------------------------- solve
  * Replaces solve (solve.py:64-98): device-resident fixed point
  * I <- P A+ I + P Ao D with the residual, tol break and 3-growth divergence
@@ -193,6 +237,11 @@ int vpg_graph_export_operators(const vpg_graph* g, int64_t* indptr, int64_t* ind
  * Returns VPG_EDIVERGED (after filling residuals/performed) on divergence. */
 int vpg_solve(vpg_graph* g, int32_t iterations, double tol, double* residuals,
               int32_t* performed, void* stream);
+/* The pieces of vpg_solve, for shard-local graphs (see vpg_graph_build_local). */
+int vpg_solve_begin(vpg_graph* g, int32_t iterations, double tol, void* stream);
+int vpg_solve_step(vpg_graph* g, int32_t t, void* stream);
+int vpg_solve_control(vpg_graph* g, int32_t t, void* stream);
+int vpg_solve_end(vpg_graph* g, double* residuals, int32_t* performed, void* stream);
 /* incoming, i_bar: (n,3) float64 host, record order (SolveResult fields). */
 int vpg_solve_export(const vpg_graph* g, double* incoming, double* i_bar, void* stream);
 
@@ -213,6 +262,12 @@ int vpg_propagate(const vpg_records* rec, const double* l_bar, double* out, int3
 #define VPG_DIRECT_AGGREGATED 2
 int vpg_splat(const vpg_graph* g, const vpg_paths* paths, int32_t width, int32_t height,
               int32_t spp, int32_t direct_mode, double* image, void* stream);
+/* splat_output over explicit arrays (a shard's pixel range): path p's first
+ * record r0 = paths->rec_start[p] reads coeff[r0] (fp64 x3) and the float4
+ * acc / dbar at index clpos[r0].  n_pixels * spp == paths->n. */
+int vpg_splat_arrays(const vpg_paths* paths, const double* coeff, const int32_t* clpos,
+                     const float* acc4, const float* dbar4, int64_t n_pixels, int32_t spp,
+                     int32_t direct_mode, double* image, void* stream);
 /* splat_pt_image (records.py:259-265): per-pixel mean of pt_estimate. */
 int vpg_splat_pt(const vpg_paths* paths, int32_t width, int32_t height, int32_t spp,
                  double* image, void* stream);

@@ -76,6 +76,14 @@ class GraphInfo(C.Structure):
                 ("n_staged", c_i64), ("split_visits", c_i64)]
 
 
+class GraphViews(C.Structure):
+    _fields_ = ([("n", c_i64), ("m", c_i64), ("n_halo", c_i64)] +
+                [(f, c_p) for f in ("perm", "clpos", "cluster_id", "cl_off", "cl_size",
+                                    "cl_center", "ref_of", "internal_of", "i0")] +
+                [("ibuf", c_p * 2), ("acc", c_p * 2), ("dbar", c_p), ("term_max", c_p),
+                 ("red", c_p), ("ctl", c_p), ("performed", c_i32), ("_pad", c_i32)])
+
+
 def _arr(t, *dims):
     for d in reversed(dims):
         t = t * d
@@ -142,6 +150,15 @@ _SIGNATURES = {
                                     c_i64, c_p, c_p, C.POINTER(Paths), c_p]),
     "vpg_scatter_records": (C.c_int, [C.POINTER(Records), c_i64, c_p, c_i64, C.POINTER(Records),
                                       c_p]),
+    "vpg_graph_build_local": (C.c_int, [C.POINTER(Records), c_i64, c_p, c_p, c_p, c_i64, c_p, c_p,
+                                        C.POINTER(c_p)]),
+    "vpg_graph_views_get": (C.c_int, [c_p, C.POINTER(GraphViews)]),
+    "vpg_solve_begin": (C.c_int, [c_p, c_i32, c_f64, c_p]),
+    "vpg_solve_step": (C.c_int, [c_p, c_i32, c_p]),
+    "vpg_solve_control": (C.c_int, [c_p, c_i32, c_p]),
+    "vpg_solve_end": (C.c_int, [c_p, c_p, C.POINTER(c_i32), c_p]),
+    "vpg_splat_arrays": (C.c_int, [C.POINTER(Paths), c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p,
+                                   c_p]),
 }
 
 _lock = threading.Lock()
@@ -169,7 +186,8 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        for which, st in enumerate((Pcg64State, Records, Paths, GraphInfo, SceneStruct, TraceCfg)):
+        for which, st in enumerate((Pcg64State, Records, Paths, GraphInfo, SceneStruct, TraceCfg,
+                                    GraphViews)):
             if handle.vpg_struct_size(which) != C.sizeof(st):
                 raise NativeError(f"ABI mismatch for {st.__name__}: "
                                   f"{handle.vpg_struct_size(which)} != {C.sizeof(st)}")

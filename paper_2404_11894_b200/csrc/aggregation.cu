@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -55,7 +56,8 @@ __device__ __forceinline__ float4 f4(double x, double y, double z) {
 // position is already known (clpos >= 0).
 __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpos,
                                const int32_t* __restrict__ list, int64_t list_n, int64_t off,
-                               Member* __restrict__ out, float* __restrict__ term_max) {
+                               Member* __restrict__ out, float* __restrict__ term_max,
+                               const uint8_t* __restrict__ has_child) {
   const int64_t n = rec.n;
   const int lane = threadIdx.x & 31;
   float tmax[3] = {0.f, 0.f, 0.f};
@@ -91,8 +93,9 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
       m.wc[c] = float(rec.w_cont[r * 3 + c]);
       m.ipt[c] = float(rec.i_pt[r * 3 + c]);
     }
-    const int64_t pid = rec.path_idx[r];
-    const bool terminal = !(r + 1 < n && rec.path_idx[r + 1] == pid);
+    // no continuation child (records.py:128-140); shard-local records carry it
+    const bool terminal = has_child ? !has_child[r]
+                                    : !(r + 1 < n && rec.path_idx[r + 1] == rec.path_idx[r]);
     m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u);
     for (int k = 0; k < 8; ++k) m.pad[k] = 0;
     out[q] = m;
@@ -264,6 +267,35 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   }
 }
 
+// Shard-local parents: given directly (a halo slot n + h for a parent on
+// another shard, -1 for none).
+__global__ void k_set_parents(const int32_t* __restrict__ parent, int64_t n,
+                              float4* __restrict__ rows) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x)
+    reinterpret_cast<int32_t*>(rows)[8 * q + 3] = parent[q];
+}
+
+// I_0 of the halo slots: the remote parent's i_pt (solve.py:72, I_0 = i_pt).
+__global__ void k_halo_i0(const double* __restrict__ ipt, int64_t n_halo, float4* __restrict__ i0) {
+  for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < n_halo;
+       h += int64_t(gridDim.x) * blockDim.x)
+    i0[h] = make_float4(float(ipt[3 * h]), float(ipt[3 * h + 1]), float(ipt[3 * h + 2]), 0.f);
+}
+
+__global__ void k_iota32(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = int32_t(i);
+}
+
+__global__ void k_cluster_of_rows(const int32_t* __restrict__ cl_off, int64_t m,
+                                  int32_t* __restrict__ cluster_id) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < m;
+       k += int64_t(gridDim.x) * blockDim.x)
+    for (int32_t q = cl_off[k]; q < cl_off[k + 1]; ++q) cluster_id[q] = int32_t(k);
+}
+
 // Solve chunks (see graph.cuh): cost prefix and the first cluster of each chunk.
 __global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, int64_t m,
                              int64_t* __restrict__ cost) {
@@ -298,18 +330,19 @@ void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s) {
   const int64_t n = g->n;
   g->wt.alloc(size_t(wt_capacity > 0 ? wt_capacity : 1), s);
   g->phat.alloc(size_t(3 * n + 1), s);
-  for (auto* v : {&g->i0, &g->dbar, &g->coeff, &g->ibuf[0], &g->ibuf[1], &g->acc[0], &g->acc[1]})
-    v->alloc(size_t(n + 1), s);
+  for (auto* v : {&g->dbar, &g->coeff, &g->acc[0], &g->acc[1]}) v->alloc(size_t(n + 1), s);
+  // I vectors carry the halo slots after the n rows
+  for (auto* v : {&g->i0, &g->ibuf[0], &g->ibuf[1]}) v->alloc(size_t(n + g->n_halo + 1), s);
   g->rows.alloc(size_t(2 * n + 2), s);
   g->term_max.alloc(4, s);
   VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
 }
 
 void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
-                  int64_t off, void* members, cudaStream_t s) {
+                  int64_t off, void* members, cudaStream_t s, const uint8_t* has_child) {
   if (list_n <= 0) return;
   VPG_LAUNCH(k_pack_members, grid_for(list_n, 256), 256, 0, s, rec, g->clpos.get(), list, list_n,
-             off, static_cast<Member*>(members), g->term_max.get());
+             off, static_cast<Member*>(members), g->term_max.get(), has_child);
 }
 
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
@@ -330,11 +363,15 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
              g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get());
 }
 
-void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s) {
+void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s,
+                              const int32_t* parent) {
   const int64_t n = g->n, m = g->m;
   g->chunk_total = 0;
   if (n == 0) return;
-  VPG_LAUNCH(k_parent_links, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), g->rows.get());
+  if (parent)
+    VPG_LAUNCH(k_set_parents, grid_for(n, 256), 256, 0, s, parent, n, g->rows.get());
+  else
+    VPG_LAUNCH(k_parent_links, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), g->rows.get());
   // solve chunks: cost prefix over the clusters (internal order)
   int64_t* cost = scratch_of<int64_t>(s, "chunk_cost", size_t(m) + 1);
   int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
@@ -359,6 +396,86 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
   const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
   VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst, m, g->n_chunks,
              int64_t(kChunkFloats), g->chunk_first.get());
+}
+
+void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,
+                 const int32_t* parent, const uint8_t* has_child, int64_t n_halo,
+                 const double* halo_ipt, cudaStream_t s) {
+  const int64_t n = rec.n;
+  VPG_REQUIRE(n < (int64_t(1) << 31) - 1 && n_halo >= 0 && n + n_halo < (int64_t(1) << 31) - 1,
+              VPG_ELIMIT, "more than 2^31-2 rows per shard");
+  VPG_REQUIRE(m >= 0 && (m > 0 || n == 0), VPG_EINVAL, "cluster count does not cover the rows");
+  g->n = n;
+  g->m = m;
+  g->n_halo = n_halo;
+  // host cluster geometry: offsets, padded kernel-block offsets, sizes
+  std::vector<int32_t> off(m + 1), size(m + 1, 0);
+  std::vector<int64_t> woff(m + 1);
+  int64_t q = 0, w = 0, nnz = 0;
+  int32_t smax = 0;
+  for (int64_t k = 0; k < m; ++k) {
+    const int32_t sz = cl_size_host[k];
+    VPG_REQUIRE(sz >= 1, VPG_EINVAL, "empty cluster in a shard-local partition");
+    off[k] = int32_t(q);
+    size[k] = sz;
+    woff[k] = w;
+    q += sz;
+    w += (int64_t(sz) * sz + 3) & ~int64_t(3);
+    nnz += int64_t(sz) * sz;
+    smax = std::max(smax, sz);
+  }
+  VPG_REQUIRE(q == n, VPG_EINVAL, "cluster sizes do not sum to the shard's row count");
+  off[m] = int32_t(q);
+  woff[m] = w;
+  g->nnz = nnz;
+  g->wt_len = w;
+  g->max_cluster = smax;
+  g->info.n_records = n;
+  g->info.n_clusters = m;
+  g->info.nnz = nnz;
+  g->K = std::max(1, (smax + 1) / 2);
+  const int block = 256;
+  g->perm.alloc(n + 1, s);
+  g->clpos.alloc(n + 1, s);
+  g->cluster_id.alloc(n + 1, s);
+  g->cl_off.alloc(m + 1, s);
+  g->cl_size.alloc(m + 1, s);
+  g->w_off.alloc(m + 1, s);
+  for (auto* v : {&g->cl_center, &g->ref_of, &g->internal_of}) v->alloc(m + 1, s);
+  VPG_CUDA(cudaMemcpyAsync(g->cl_off.get(), off.data(), sizeof(int32_t) * (m + 1),
+                           cudaMemcpyHostToDevice, s));
+  VPG_CUDA(cudaMemcpyAsync(g->cl_size.get(), size.data(), sizeof(int32_t) * (m + 1),
+                           cudaMemcpyHostToDevice, s));
+  VPG_CUDA(cudaMemcpyAsync(g->w_off.get(), woff.data(), sizeof(int64_t) * (m + 1),
+                           cudaMemcpyHostToDevice, s));
+  count_transfer(16 * (m + 1), 0);
+  if (n > 0) {
+    VPG_LAUNCH(k_iota32, grid_for(n, block), block, 0, s, g->perm.get(), n);
+    VPG_LAUNCH(k_iota32, grid_for(n, block), block, 0, s, g->clpos.get(), n);
+  }
+  if (m > 0) {
+    VPG_LAUNCH(k_iota32, grid_for(m, block), block, 0, s, g->ref_of.get(), m);
+    VPG_LAUNCH(k_iota32, grid_for(m, block), block, 0, s, g->internal_of.get(), m);
+    VPG_CUDA(cudaMemsetAsync(g->cl_center.get(), 0xFF, sizeof(int32_t) * m, s));  // unknown here
+    VPG_LAUNCH(k_cluster_of_rows, grid_for(m, block), block, 0, s, g->cl_off.get(), m,
+               g->cluster_id.get());
+  }
+  alloc_operator_buffers(g, std::max<int64_t>(w, 1), s);
+  if (n > 0) {
+    void* members = scratch(s, "members", member_bytes() * size_t(n) + 256);
+    pack_members(g, rec, nullptr, n, 0, members, s, has_child);
+    DBuf<int64_t> range(2, s);
+    const int64_t r[2] = {0, m};
+    VPG_CUDA(cudaMemcpyAsync(range.get(), r, sizeof(r), cudaMemcpyHostToDevice, s));
+    aggregate_range(g, members, range.get(), m, std::max(1, int(smax)), s);
+    if (n_halo > 0)
+      VPG_LAUNCH(k_halo_i0, grid_for(n_halo, block), block, 0, s, halo_ipt, n_halo,
+                 g->i0.get() + n);
+  }
+  finalize_operators_async(g, rec, s, parent);
+  VPG_CUDA(cudaStreamSynchronize(s));
+  finalize_chunks(g, s);
+  VPG_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace vpg

@@ -187,6 +187,7 @@ size_t vpg_struct_size(int32_t which) {
     case 3: return sizeof(vpg_graph_info);
     case 4: return sizeof(vpg_scene);
     case 5: return sizeof(vpg_trace_cfg);
+    case 6: return sizeof(vpg_graph_views);
     default: return 0;
   }
 }
@@ -354,6 +355,77 @@ int vpg_solve(vpg_graph* g, int32_t iterations, double tol, double* residuals, i
               void* stream) {
   return guarded([&] {
     vpg::solve(g, g->rec, iterations, tol, residuals, performed, as_stream(stream));
+  });
+}
+
+int vpg_graph_build_local(const vpg_records* rec, int64_t n_clusters, const int32_t* cl_size,
+                          const int32_t* parent, const uint8_t* has_child, int64_t n_halo,
+                          const double* halo_ipt, void* stream, vpg_graph** out) {
+  *out = nullptr;
+  vpg_graph* g = new vpg_graph();
+  const int rc = guarded([&] {
+    g->stream = as_stream(stream);
+    g->rec = *rec;
+    vpg::build_local(g, *rec, n_clusters, cl_size, parent, has_child, n_halo, halo_ipt, g->stream);
+  });
+  if (rc != VPG_OK) {
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return VPG_OK;
+}
+
+int vpg_graph_views_get(const vpg_graph* g, vpg_graph_views* v) {
+  return guarded([&] {
+    *v = vpg_graph_views{};
+    v->n = g->n;
+    v->m = g->m;
+    v->n_halo = g->n_halo;
+    v->perm = g->perm.get();
+    v->clpos = g->clpos.get();
+    v->cluster_id = g->cluster_id.get();
+    v->cl_off = g->cl_off.get();
+    v->cl_size = g->cl_size.get();
+    v->cl_center = g->cl_center.get();
+    v->ref_of = g->ref_of.get();
+    v->internal_of = g->internal_of.get();
+    v->i0 = reinterpret_cast<float*>(g->i0.get());
+    v->ibuf[0] = reinterpret_cast<float*>(g->ibuf[0].get());
+    v->ibuf[1] = reinterpret_cast<float*>(g->ibuf[1].get());
+    v->acc[0] = reinterpret_cast<float*>(g->acc[0].get());
+    v->acc[1] = reinterpret_cast<float*>(g->acc[1].get());
+    v->dbar = reinterpret_cast<float*>(g->dbar.get());
+    v->term_max = g->term_max.get();
+    v->red = g->red.get();
+    v->ctl = g->ctl.get();
+    v->performed = g->performed;
+  });
+}
+
+int vpg_solve_begin(vpg_graph* g, int32_t iterations, double tol, void* stream) {
+  return guarded([&] { vpg::solve_begin(g, g->rec, iterations, tol, as_stream(stream)); });
+}
+
+int vpg_solve_step(vpg_graph* g, int32_t t, void* stream) {
+  return guarded([&] { vpg::solve_step(g, t, as_stream(stream)); });
+}
+
+int vpg_solve_control(vpg_graph* g, int32_t t, void* stream) {
+  return guarded([&] { vpg::solve_control(g, t, as_stream(stream)); });
+}
+
+int vpg_solve_end(vpg_graph* g, double* residuals, int32_t* performed, void* stream) {
+  return guarded([&] { vpg::solve_end(g, residuals, performed, false, as_stream(stream)); });
+}
+
+int vpg_splat_arrays(const vpg_paths* paths, const double* coeff, const int32_t* clpos,
+                     const float* acc4, const float* dbar4, int64_t n_pixels, int32_t spp,
+                     int32_t direct_mode, double* image, void* stream) {
+  return guarded([&] {
+    vpg::splat_arrays(*paths, coeff, clpos, reinterpret_cast<const float4*>(acc4),
+                      reinterpret_cast<const float4*>(dbar4), n_pixels, spp, direct_mode, image,
+                      as_stream(stream));
   });
 }
 

@@ -49,6 +49,12 @@ struct vpg_graph {
   vpg::DBuf<int32_t> ctl;
   int32_t red_cap = 0;
   int32_t performed = -1;  // -1 = no solve yet
+  double tol = 0.0;        // of the solve in progress (vpg_solve_begin)
+  int32_t iterations = 0;
+  // shard-local graphs (vpg_graph_build_local): rows whose continuation
+  // parent lives on another shard propagate into halo slots n .. n+n_halo-1
+  // of the I vectors, which the caller exchanges between iterations
+  int64_t n_halo = 0;
   int32_t max_cluster = 0;
   vpg_graph_info info{};
   // the records the graph was built from (borrowed; the caller keeps them alive)
@@ -67,10 +73,16 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
 size_t member_bytes();
 void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s);
 void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
-                  int64_t off, void* members, cudaStream_t s);
+                  int64_t off, void* members, cudaStream_t s, const uint8_t* has_child = nullptr);
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
                      int S, cudaStream_t s);
 // parent links + chunk cost scan (async); chunk table once the host has the total
-void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s);
+void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s,
+                              const int32_t* parent = nullptr);
 void finalize_chunks(vpg_graph* g, cudaStream_t s);
+// shard-local graph from a given cluster partition (records already
+// cluster-major, clusters back to back), explicit parents and child flags
+void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,
+                 const int32_t* parent, const uint8_t* has_child, int64_t n_halo,
+                 const double* halo_ipt, cudaStream_t s);
 }  // namespace vpg

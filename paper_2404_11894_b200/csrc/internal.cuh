@@ -5,6 +5,14 @@
 namespace vpg {
 void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
            double* residuals, int32_t* performed, cudaStream_t s);
+void solve_begin(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
+                 cudaStream_t s);
+void solve_step(vpg_graph* g, int32_t t, cudaStream_t s);
+void solve_control(vpg_graph* g, int32_t t, cudaStream_t s);
+void solve_end(vpg_graph* g, double* residuals, int32_t* performed, bool empty, cudaStream_t s);
+void splat_arrays(const vpg_paths& P, const double* coeff, const int32_t* clpos, const float4* acc,
+                  const float4* dbar, int64_t npix, int spp, int mode, double* image,
+                  cudaStream_t s);
 void solve_export(const vpg_graph* g, const vpg_records& rec, double* incoming, double* i_bar,
                   cudaStream_t s);
 void aggregate_indirect(const vpg_graph* g, const vpg_records& rec, const double* incoming,

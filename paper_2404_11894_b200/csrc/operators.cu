@@ -557,16 +557,47 @@ int iterate_grid(int64_t m) {
 }  // namespace
 
 // ------------------------------------------------------------------ solve
-void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
-           double* residuals, int32_t* performed, cudaStream_t s) {
+// solve() = solve_begin + iterations x (solve_step + solve_control) + solve_end.
+// A shard-local graph runs the same pieces with the halo exchange and the
+// residual all-reduce between solve_step and solve_control (pathgraph/sharded.py).
+namespace {
+struct SolveLaunch {
+  int stage_floats = 0;
+  size_t smem = 0;
+  int grid = 0;
+};
+
+SolveLaunch solve_launch(const vpg_graph* g) {
+  // stage = one chunk: kChunkFloats plus the largest cluster's blocks + rows
+  SolveLaunch L;
+  const int smax = std::max(1, g->max_cluster);
+  L.stage_floats = kChunkFloats + ((smax * smax + 3) & ~3) + 16 * smax;
+  L.smem = 128 + size_t(kStages) * L.stage_floats * sizeof(float);
+  VPG_REQUIRE(L.smem <= 220 * 1024, VPG_ELIMIT, "clusters too large for the staged solve");
+  static size_t smem_set = 0;
+  if (L.smem > smem_set) {
+    VPG_CUDA(cudaFuncSetAttribute(k_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(L.smem)));
+    smem_set = L.smem;
+  }
+  L.grid = int(std::min<int64_t>(g->n_chunks, sm_count()));
+  return L;
+}
+}  // namespace
+
+void solve_begin(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
+                 cudaStream_t s) {
   VPG_REQUIRE(iterations >= 0, VPG_EINVAL, "iterations must be >= 0");
-  const int64_t n = g->n, m = g->m;
+  const int64_t n = g->n;
   if (g->red_cap < iterations + 1) {
     g->red.alloc(size_t(iterations + 1) * 8, s);
     g->resid.alloc(size_t(iterations + 1), s);
     g->red_cap = iterations + 1;
   }
   if (!g->ctl.get()) g->ctl.alloc(4, s);
+  g->tol = tol;
+  g->iterations = iterations;
+  g->performed = -1;
   VPG_CUDA(cudaMemsetAsync(g->red.get(), 0, g->red.bytes(), s));
   VPG_CUDA(cudaMemsetAsync(g->ctl.get(), 0, 4 * sizeof(int32_t), s));
   const int block = 256;
@@ -577,28 +608,28 @@ void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
       VPG_LAUNCH(k_own_indirect, grid_for(n, block), block, 0, s, rec, g->perm.get(), n,
                  g->acc[0].get());
   }
-  // stage = one chunk: kChunkFloats plus the largest cluster's blocks + rows
-  const int smax = std::max(1, g->max_cluster);
-  const int stage_floats = kChunkFloats + ((smax * smax + 3) & ~3) + 16 * smax;
-  const size_t smem = 128 + size_t(kStages) * stage_floats * sizeof(float);
-  VPG_REQUIRE(smem <= 220 * 1024, VPG_ELIMIT, "clusters too large for the staged solve");
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    VPG_CUDA(cudaFuncSetAttribute(k_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem)));
-    smem_set = smem;
-  }
-  const int grid = int(std::min<int64_t>(g->n_chunks, sm_count()));
-  for (int t = 0; t < iterations && n > 0; ++t) {
-    VPG_LAUNCH(k_solve_iter, grid, (kConsumers + 1) * 32, smem, s, g->cl_off.get(), g->w_off.get(),
-               g->chunk_first.get(), g->n_chunks, stage_floats, g->wt.get(), g->rows.get(),
-               g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
-               g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
-    VPG_LAUNCH(k_control, 1, 32, 0, s, t, tol, g->red.get(), g->term_max.get(), g->resid.get(),
-               g->ctl.get());
-  }
+}
+
+void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
+  VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
+  if (g->n == 0 || g->n_chunks == 0) return;
+  const SolveLaunch L = solve_launch(g);
+  VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->cl_off.get(),
+             g->w_off.get(), g->chunk_first.get(), g->n_chunks, L.stage_floats, g->wt.get(),
+             g->rows.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
+             g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
+}
+
+void solve_control(vpg_graph* g, int32_t t, cudaStream_t s) {
+  VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
+  VPG_LAUNCH(k_control, 1, 32, 0, s, t, g->tol, g->red.get(), g->term_max.get(), g->resid.get(),
+             g->ctl.get());
+}
+
+void solve_end(vpg_graph* g, double* residuals, int32_t* performed, bool empty, cudaStream_t s) {
+  const int32_t iterations = g->iterations;
   int32_t ctl_h[4] = {0, 0, 0, 0};
-  if (n > 0 && iterations > 0) {
+  if (!empty && iterations > 0) {
     VPG_CUDA(cudaMemcpyAsync(ctl_h, g->ctl.get(), sizeof(ctl_h), cudaMemcpyDeviceToHost, s));
     VPG_CUDA(cudaMemcpyAsync(residuals, g->resid.get(), sizeof(double) * iterations,
                              cudaMemcpyDeviceToHost, s));
@@ -606,12 +637,23 @@ void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
   } else if (iterations > 0) {
     // an empty graph: every residual is 0/1e-12 = 0 and the tol test stops at once
     for (int t = 0; t < iterations; ++t) residuals[t] = 0.0;
-    ctl_h[0] = tol > 0.0 ? 1 : iterations;
+    ctl_h[0] = g->tol > 0.0 ? 1 : iterations;
   }
   VPG_CUDA(cudaStreamSynchronize(s));
   g->performed = ctl_h[0];
   *performed = ctl_h[0];
   if (ctl_h[3]) throw Error(VPG_EDIVERGED, "fixed-point residuals grew over 3 consecutive iterations");
+}
+
+void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
+           double* residuals, int32_t* performed, cudaStream_t s) {
+  solve_begin(g, rec, iterations, tol, s);
+  const int64_t n = g->n;
+  for (int t = 0; t < iterations && n > 0; ++t) {
+    solve_step(g, t, s);
+    solve_control(g, t, s);
+  }
+  solve_end(g, residuals, performed, n == 0, s);
 }
 
 void solve_export(const vpg_graph* g, const vpg_records& rec, double* incoming, double* i_bar,
@@ -745,6 +787,15 @@ void splat(const vpg_graph* g, const vpg_records& rec, const vpg_paths& P, int w
   const int64_t npix = int64_t(w) * h;
   VPG_LAUNCH(k_splat, grid_for(npix, 128), 128, 0, s, P, rec.coeff, g->clpos.get(),
              g->acc[g->performed & 1].get(), g->dbar.get(), npix, spp, mode, image);
+}
+
+void splat_arrays(const vpg_paths& P, const double* coeff, const int32_t* clpos, const float4* acc,
+                  const float4* dbar, int64_t npix, int spp, int mode, double* image,
+                  cudaStream_t s) {
+  VPG_REQUIRE(spp >= 1 && P.n == npix * spp, VPG_EINVAL, "path table size != pixels*spp");
+  if (npix == 0) return;
+  VPG_LAUNCH(k_splat, grid_for(npix, 128), 128, 0, s, P, coeff, clpos, acc, dbar, npix, spp, mode,
+             image);
 }
 
 void splat_pt(const vpg_paths& P, int w, int h, int spp, double* image, cudaStream_t s) {

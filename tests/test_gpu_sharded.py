@@ -1,0 +1,101 @@
+"""The sharded (multi-GPU row-partition) path on the device: 1, 2 and 3 shards
+must give bit-identical images and solutions to the single-GPU render_pg.
+
+With one GPU on the test box the shards are processes sharing cuda:0 over a
+gloo group: every exchange is host-staged between kernel launches, so no
+kernel waits on another process (B200_PROFILING.md's rule for emulating
+ranks on fewer GPUs).  NCCL on one GPU per shard runs the same code."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1floor": dict(res=(24, 24), spp=2, max_depth=16, K=32, iters=6, seed=1),
+    "cloud": dict(res=(20, 20), spp=4, max_depth=64, K=16, iters=5, seed=2),
+}
+
+
+def _scene(name, res):
+    from paper_2404_11894_b200 import scenes as S
+
+    if name == "c1floor":
+        return S.scene_c1(res, floor=True)
+    return S.scene_c2(res, grid_n=16)
+
+
+def _config(c):
+    from paper_2404_11894_b200.harness.config import RenderConfig
+
+    return RenderConfig(mode="pg", spp=c["spp"], max_depth=c["max_depth"], seed=c["seed"],
+                        cluster_size=c["K"], iterations=c["iters"], tol=0.0)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _shard_worker(rank, world, port, name, out_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_11894_b200.pathgraph.sharded import ShardComm, render_pg_sharded
+
+        c = CASES[name]
+        out = render_pg_sharded(_scene(name, c["res"]), _config(c), ShardComm())
+        inc, ibar = out.graph.gather_solution()
+        if rank == 0:
+            np.savez(out_path, image=out.image, incoming=inc.cpu().numpy(),
+                     i_bar=ibar.cpu().numpy(), residuals=np.array(out.residuals),
+                     halo=out.graph.halo.n_halo, n_total=out.n_records_total)
+    finally:
+        dist.destroy_process_group()
+
+
+def _single(name):
+    from paper_2404_11894_b200.pathgraph import render_pg
+
+    c = CASES[name]
+    pg = render_pg(_scene(name, c["res"]), _config(c))
+    return pg
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_render_is_bit_identical(cuda, name, world):
+    import torch.multiprocessing as mp
+
+    ref = _single(name)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "shard0.npz")
+        if world == 1:
+            from paper_2404_11894_b200.pathgraph.sharded import ShardComm, render_pg_sharded
+
+            c = CASES[name]
+            out = render_pg_sharded(_scene(name, c["res"]), _config(c), ShardComm())
+            inc, ibar = out.graph.gather_solution()
+            got = dict(image=out.image, incoming=inc.cpu().numpy(), i_bar=ibar.cpu().numpy(),
+                       residuals=np.array(out.residuals), halo=0, n_total=out.n_records_total)
+        else:
+            mp.spawn(_shard_worker, args=(world, _free_port(), name, path), nprocs=world,
+                     join=True)
+            got = dict(np.load(path))
+    assert int(got["n_total"]) == ref.trace.records.n
+    if world > 1:
+        assert int(got["halo"]) > 0, "expected continuation edges across shards"
+    np.testing.assert_array_equal(got["image"], ref.image)
+    np.testing.assert_array_equal(got["incoming"], ref.result.incoming)
+    np.testing.assert_array_equal(got["i_bar"], ref.result.i_bar)
+    np.testing.assert_array_equal(got["residuals"], np.array(ref.result.residuals))
