@@ -28,7 +28,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
     f"-I{INCLUDE}",
 ]
 PER_FILE = {"tracer.cu": ["-fmad=false"]}

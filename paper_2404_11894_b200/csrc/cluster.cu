@@ -281,6 +281,33 @@ __device__ __forceinline__ void scan_cell(const GridParams& gp, const CellEntry*
 }
 
 
+// Z-order key of each center's cell: part A's clusters are laid out in this
+// order (any order is valid; ref_of keeps the reference numbering) so that
+// spatially close clusters -- and the continuation parents a row scatters
+// into during the solve -- are close in memory.
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
+  v &= 0x1FFFFFull;
+  v = (v | (v << 32)) & 0x1F00000000FFFFull;
+  v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+  v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+  v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__global__ void k_center_morton(const double* __restrict__ cpos, int m, GridParams gp,
+                                unsigned long long* __restrict__ keys, int32_t* __restrict__ ids) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    unsigned long long c[3];
+    for (int a = 0; a < 3; ++a) {
+      const long long v = cell_coord(cpos[j * 3 + a], gp.lo[a], gp.cell);
+      c[a] = (unsigned long long)(v < 0 ? 0 : (v > 0x1FFFFF ? 0x1FFFFF : v));
+    }
+    keys[j] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+    ids[j] = j;
+  }
+}
+
 // ------------------------------------ Generator.choice tail shuffle on device
 // numpy's partial Fisher-Yates (n > 10000, m > n // 50): step k swaps
 // positions i_k = n-1-k and j_k (drawn on the host).  Position i_k is final
@@ -662,21 +689,32 @@ struct OverCount {
   __host__ __device__ int64_t operator()(int32_t k) const { return info[k * 4 + 1]; }
 };
 
-// Gather members (record id + position) of the oversize groups for the host.
+// Gather the members of the oversize groups for the host split loop: record
+// id, position (SoA), squared distance to the group's center (fp64, the
+// reference's rounding, like the host dist2) and the slot of the center
+// among the members (slot_of[k], min over matches; >= staged means absent).
 __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
                                   const int64_t* __restrict__ seg, const int32_t* __restrict__ n_seg,
-                                  const double* __restrict__ pos, int32_t* __restrict__ out_rec,
-                                  double* __restrict__ out_pos) {
+                                  const int64_t* __restrict__ info, const double* __restrict__ pos,
+                                  int32_t* __restrict__ out_rec, double* __restrict__ ox,
+                                  double* __restrict__ oy, double* __restrict__ oz,
+                                  double* __restrict__ od0, int32_t* __restrict__ slot_of) {
   // seg[k*3+0] = source offset, seg[k*3+1] = count, seg[k*3+2] = destination offset
   const int nk = *n_seg;
   for (int k = blockIdx.x; k < nk; k += gridDim.x) {
     const int64_t src = seg[k * 3], cnt = seg[k * 3 + 1], dst = seg[k * 3 + 2];
+    const int32_t crec = int32_t(info[k * 4 + 3]);
+    const double cx = pos[int64_t(crec) * 3], cy = pos[int64_t(crec) * 3 + 1],
+                 cz = pos[int64_t(crec) * 3 + 2];
     for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) {
       const int32_t r = grp_rec[src + t];
+      const double px = pos[int64_t(r) * 3], py = pos[int64_t(r) * 3 + 1], pz = pos[int64_t(r) * 3 + 2];
       out_rec[dst + t] = r;
-      out_pos[(dst + t) * 3] = pos[int64_t(r) * 3];
-      out_pos[(dst + t) * 3 + 1] = pos[int64_t(r) * 3 + 1];
-      out_pos[(dst + t) * 3 + 2] = pos[int64_t(r) * 3 + 2];
+      ox[dst + t] = px;
+      oy[dst + t] = py;
+      oz[dst + t] = pz;
+      od0[dst + t] = dist2_exact(px, py, pz, cx, cy, cz);
+      if (r == crec) atomicMin(&slot_of[k], int32_t(dst + t));
     }
   }
 }
@@ -706,27 +744,41 @@ struct LayoutOf {
   }
 };
 
+struct LayoutOfPerm {  // LayoutOf of the groups taken in layout order
+  const int32_t* counts;
+  const int32_t* order;
+  int32_t max_size;
+  __host__ __device__ LayoutAcc operator()(int32_t i) const {
+    return LayoutOf{max_size}(counts[order[i]]);
+  }
+};
+
 // Device totals: acc = {A clusters, A rows, A kernel floats, non-empty groups}.
 // cls = per class {A begin, A end, reference base, non-empty groups}.
 __global__ void k_layout_a(const int32_t* __restrict__ counts, const int32_t* __restrict__ gstart,
                            const int32_t* __restrict__ crec, const LayoutAcc* __restrict__ pre,
+                           const int32_t* __restrict__ order, const LayoutAcc* __restrict__ pre_o,
                            int m, int32_t max_size, int64_t row_off, int64_t appended_before,
                            const int64_t* __restrict__ acc, int32_t* __restrict__ cl_off,
                            int32_t* __restrict__ cl_size, int64_t* __restrict__ w_off,
                            int64_t* __restrict__ cl_src, int32_t* __restrict__ cl_center,
                            int32_t* __restrict__ ref_of, int32_t* __restrict__ ne_prefix) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+  // i walks the layout order; pre_o is the layout scan, pre (group order) the
+  // reference numbering's count of non-empty groups before j
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int j = order[i];
     const int32_t size = counts[j];
-    const LayoutAcc e = pre[j];
-    ne_prefix[j] = e.ne;
+    const int32_t ne = pre[j].ne;
+    ne_prefix[j] = ne;
     if (size <= 0 || size > max_size) continue;
+    const LayoutAcc e = pre_o[i];
     const int64_t k = acc[0] + e.a;
     cl_off[k] = int32_t(acc[1] + e.rows);
     cl_size[k] = size;
     w_off[k] = acc[2] + e.w;
     cl_src[k] = row_off + gstart[j];
     cl_center[k] = crec[j];
-    ref_of[k] = int32_t(acc[3] + appended_before + e.ne);
+    ref_of[k] = int32_t(acc[3] + appended_before + ne);
   }
 }
 
@@ -1167,6 +1219,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                  cpos.get(), m, gp, spos.get(), table.get());
       VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
                  table.get());
+      // part A layout order (the table no longer needs skeys/sids)
+      VPG_LAUNCH(k_center_morton, grid_for(m, block), block, 0, s, cpos.get(), m, gp, keys.get(),
+                 ids.get());
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(),
+                                               sids.get(), m, 0, 63, s);
+      }, s);
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
                  rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start, run_len,
@@ -1237,13 +1296,22 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     // ---- part A of this class: layout (device)
     {
       LayoutAcc* pre = scratch_of<LayoutAcc>(s, "layout_pre", size_t(m) + 1);
+      LayoutAcc* pre_o = scratch_of<LayoutAcc>(s, "layout_pre_o", size_t(m) + 1);
       cub::TransformInputIterator<LayoutAcc, LayoutOf, const int32_t*> it(
           counts_c, LayoutOf{int32_t(max_size)});
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveScan(t, b, it, pre, LayoutSum(), LayoutAcc{0, 0, 0, 0}, m, s);
       }, s);
+      const int32_t* order = m > 1 ? sids.get() : ids.get();
+      cub::CountingInputIterator<int32_t> ci(0);
+      cub::TransformInputIterator<LayoutAcc, LayoutOfPerm, cub::CountingInputIterator<int32_t>> ito(
+          ci, LayoutOfPerm{counts_c, order, int32_t(max_size)});
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveScan(t, b, ito, pre_o, LayoutSum(), LayoutAcc{0, 0, 0, 0}, m,
+                                              s);
+      }, s);
       VPG_LAUNCH(k_layout_a, grid_for(m, block), block, 0, s, counts_c, gstart_c,
-                 crec_all.get() + p.center_off, pre, m, int32_t(max_size), p.row_off,
+                 crec_all.get() + p.center_off, pre, order, pre_o, m, int32_t(max_size), p.row_off,
                  appended_before, acc.get(), g->cl_off.get(), g->cl_size.get(), g->w_off.get(),
                  a_src.get(), g->cl_center.get(), g->ref_of.get(),
                  ne_prefix_all.get() + p.center_off);
@@ -1269,22 +1337,27 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     const int64_t staged = n_over > 0 ? h_scalars[3] : 0;
     // oversize members and positions to the host, queued ahead of part A
     HostBuf<int64_t> info(size_t(n_over) * 4 + 4);
-    HostBuf<int32_t> h_srec(size_t(staged) + 1);
-    HostBuf<double> xyz(size_t(staged) * 3 + 3);
+    HostBuf<int32_t> h_srec(size_t(staged) + 1), h_slot(size_t(n_over) + 1);
+    HostBuf<double> h_xyzd(size_t(staged) * 4 + 4);  // x | y | z | d0
     cudaEvent_t staged_ready;
     VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
     if (n_over > 0) {
       int32_t* d_srec = scratch_of<int32_t>(s, "staged_rec", size_t(staged) + 1);
-      double* d_spos = scratch_of<double>(s, "staged_pos", size_t(staged) * 3 + 3);
+      int32_t* d_slot = scratch_of<int32_t>(s, "staged_slot", size_t(n_over) + 1);
+      double* d_xyzd = scratch_of<double>(s, "staged_xyzd", size_t(staged) * 4 + 4);
+      VPG_CUDA(cudaMemsetAsync(d_slot, 0x7F, sizeof(int32_t) * n_over, s));
       VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec, over_seg,
-                 scalars.get() + 2, rec.pos, d_srec, d_spos);
+                 scalars.get() + 2, over_info.get(), rec.pos, d_srec, d_xyzd, d_xyzd + staged,
+                 d_xyzd + 2 * staged, d_xyzd + 3 * staged, d_slot);
       VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
                                cudaMemcpyDeviceToHost, s));
       VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec, sizeof(int32_t) * staged,
                                cudaMemcpyDeviceToHost, s));
-      VPG_CUDA(cudaMemcpyAsync(xyz.get(), d_spos, sizeof(double) * 3 * staged,
+      VPG_CUDA(cudaMemcpyAsync(h_slot.get(), d_slot, sizeof(int32_t) * n_over,
                                cudaMemcpyDeviceToHost, s));
-      count_transfer(0, 32 * n_over + 28 * staged);
+      VPG_CUDA(cudaMemcpyAsync(h_xyzd.get(), d_xyzd, sizeof(double) * 4 * staged,
+                               cudaMemcpyDeviceToHost, s));
+      count_transfer(0, 36 * n_over + 36 * staged);
     }
     VPG_CUDA(cudaEventRecord(staged_ready, s));
     // ---- part A of this class: permutation, pack, aggregate (device, async)
@@ -1305,30 +1378,21 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     int64_t appended_c = 0;
     if (n_over > 0) {
       dbg.mark("split: info+gather+D2H", false);
-      // initial center positions: the center is one of its group's members
-      // except with coincident centers (then it is fetched by record id)
       std::vector<SplitGroup> groups(n_over);
-      std::vector<double> c0(size_t(n_over) * 3);
+      std::vector<int64_t> cslot(n_over);
       int64_t b = 0;
       for (int k = 0; k < n_over; ++k) {
         const int64_t cnt = info[k * 4 + 1];
-        const int32_t crec = int32_t(info[k * 4 + 3]);
-        groups[k] = SplitGroup{b, cnt, crec};
-        int64_t t = b;
-        while (t < b + cnt && h_srec[t] != crec) ++t;
-        if (t < b + cnt) {
-          for (int a = 0; a < 3; ++a) c0[k * 3 + a] = xyz[t * 3 + a];
-        } else {
-          VPG_CUDA(cudaMemcpy(&c0[k * 3], rec.pos + int64_t(crec) * 3, 3 * sizeof(double),
-                              cudaMemcpyDeviceToHost));
-          count_transfer(0, 24);
-        }
+        groups[k] = SplitGroup{b, cnt, int32_t(info[k * 4 + 3])};
+        cslot[k] = h_slot[k] < staged ? int64_t(h_slot[k]) : -1;
         b += cnt;
       }
       g->info.n_staged += staged;
-      dbg.mark("split: center lookup", false);
-      n_splits += split_oversize(rng, h_srec.get(), xyz.get(), size_t(staged), groups, max_size,
-                                 c0.data(), &g->info.split_visits);
+      dbg.mark("split: groups", false);
+      double* xyzd = h_xyzd.get();
+      n_splits += split_oversize_soa(
+          rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
+          groups, cslot, max_size, &g->info.split_visits);
       dbg.mark("split: loop", false);
       const int64_t base_split = int64_t(split_rec.size());
       split_rec.insert(split_rec.end(), h_srec.get(), h_srec.get() + staged);

@@ -186,102 +186,116 @@ struct SplitGroup {
   int64_t center;  // member id of the center
 };
 
+// Flat member arrays of the split loop, structure of arrays so the distance
+// pass vectorises: id, position and the cached squared distance to the
+// member's current center.
+struct SplitMembers {
+  int32_t* id;
+  double *x, *y, *z, *d0;
+};
+
 // The LIFO split loop of clustering.py:58-85 over the oversize groups of one
-// compatibility class, on flat arrays.  `ids` holds the members of the
-// oversize groups back to back (each group ascending, groups in ascending
-// original order); `xyz` their positions (3 doubles per slot, moved with the
-// ids).  `groups` describes them; `center_xyz[3k..3k+3)` is the position of
-// groups[k].center.  Each split partitions its range in place (stable: kept
-// members compacted forward, moved ones appended after them), so every final
-// group stays a contiguous ascending range.  The squared distance of each
-// member to its current center is cached (a split only evaluates the
-// distance to the new center; moved members inherit it) and each group knows
-// the slot of its center, so no pass searches for it.  On return
-// groups[0..q) are the originals (possibly shrunk) and groups[q..) the
-// split-off groups in append order.  Returns the number of splits.
-inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
-                              std::vector<SplitGroup>& groups, int64_t max_size,
-                              const double* center_xyz, int64_t* visits = nullptr) {
-  std::unique_ptr<double[]> d0(new double[total + 1]);
-  std::vector<int64_t> cslot(groups.size(), -1);  // slot of each group's center, -1 if absent
-  for (size_t k = 0; k < groups.size(); ++k) {
-    const SplitGroup& gr = groups[k];
-    for (int64_t t = gr.begin; t < gr.begin + gr.size; ++t) {
-      d0[t] = dist2(&xyz[t * 3], center_xyz + k * 3);
-      if (ids[t] == gr.center && cslot[k] < 0) cslot[k] = t;
-    }
-  }
+// compatibility class.  `m` holds the members of the oversize groups back to
+// back (each group ascending, groups in ascending original order) with d0 =
+// squared distance to the group's center; `groups` describes them and
+// `cslot[k]` is the slot of groups[k]'s center among its members (-1 if the
+// center is not a member).  Each split partitions its range in place
+// (stable: kept members compacted forward, moved ones appended after them),
+// so every final group stays a contiguous ascending range; a split only
+// evaluates the distance to the new center (moved members inherit it as
+// their d0).  On return groups[0..q) are the originals (possibly shrunk) and
+// groups[q..) the split-off groups in append order.  Returns the number of
+// splits.
+inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGroup>& groups,
+                                  std::vector<int64_t>& cslot, int64_t max_size,
+                                  int64_t* visits = nullptr) {
   std::vector<int64_t> stack;
   for (int64_t c = 0; c < int64_t(groups.size()); ++c)
     if (groups[c].size > max_size) stack.push_back(c);
   std::vector<int32_t> mid;
-  std::vector<double> mxyz, md;
+  std::vector<double> mx, my, mz, md, vbuf;
+  std::vector<uint8_t> flag;
   int64_t splits = 0;
-  double* __restrict__ dd0 = d0.get();
+  int32_t* __restrict__ id = m.id;
+  double* __restrict__ X = m.x;
+  double* __restrict__ Y = m.y;
+  double* __restrict__ Z = m.z;
+  double* __restrict__ D0 = m.d0;
   while (!stack.empty()) {
     const int64_t c = stack.back();
     stack.pop_back();
     const SplitGroup gr = groups[c];
     if (gr.size <= max_size) continue;
-    const int64_t b = gr.begin, e = gr.begin + gr.size;
-    if (visits) *visits += gr.size;
+    const int64_t b = gr.begin, e = gr.begin + gr.size, sz = gr.size;
+    if (visits) *visits += sz;
     // candidates = members != old center, in member order (clustering.py:65-67)
     const int64_t at = cslot[c] >= 0 ? cslot[c] - b : -1;
-    const int64_t pool = at >= 0 ? gr.size - 1 : gr.size;
+    const int64_t pool = at >= 0 ? sz - 1 : sz;
     int64_t pick;
     if (pool > 0) {
       pick = int64_t(g.bounded(uint64_t(pool) - 1));
       if (at >= 0 && pick >= at) ++pick;
     } else {
-      pick = int64_t(g.bounded(uint64_t(gr.size) - 1));
+      pick = int64_t(g.bounded(uint64_t(sz) - 1));
     }
-    const int64_t new_center = ids[b + pick];
-    const double pn[3] = {xyz[(b + pick) * 3], xyz[(b + pick) * 3 + 1], xyz[(b + pick) * 3 + 2]};
-    // one pass: keep members compacted forward in place, moved ones to the side
-    if (int64_t(mid.size()) < gr.size) {
-      mid.resize(gr.size);
-      md.resize(gr.size);
-      mxyz.resize(gr.size * 3);
+    const int64_t new_center = id[b + pick];
+    const double px = X[b + pick], py = Y[b + pick], pz = Z[b + pick];
+    if (int64_t(mid.size()) < sz) {
+      for (auto* v : {&mx, &my, &mz, &md, &vbuf}) v->resize(sz);
+      mid.resize(sz);
+      flag.resize(sz);
     }
-    int64_t wk = b, wm = 0, keep_center = -1, moved_center = -1;
+    // pass 1 (vectorisable): distance to the new center, np.argmin over
+    // (old, new) with ties staying (clustering.py:69-74)
+    double* __restrict__ vb = vbuf.data();
+    uint8_t* __restrict__ fl = flag.data();
+    int64_t moved = 0;
+    for (int64_t i = 0; i < sz; ++i) {
+      const double dx = X[b + i] - px, dy = Y[b + i] - py, dz = Z[b + i] - pz;
+      const double v = (dx * dx + dy * dy) + dz * dz;
+      vb[i] = v;
+      const uint8_t f = v < D0[b + i];
+      fl[i] = f;
+      moved += f;
+    }
+    const int64_t kept = sz - moved;
     const int64_t old_slot = cslot[c], new_slot = b + pick;
-    for (int64_t t = b; t < e; ++t) {
-      const double v = dist2(&xyz[t * 3], pn);
-      if (v < dd0[t]) {  // np.argmin over (old, new): ties stay
-        if (t == new_slot) moved_center = wm;
-        mid[wm] = ids[t];
-        md[wm] = v;
-        mxyz[wm * 3] = xyz[t * 3];
-        mxyz[wm * 3 + 1] = xyz[t * 3 + 1];
-        mxyz[wm * 3 + 2] = xyz[t * 3 + 2];
-        ++wm;
-      } else {
-        if (t == old_slot) keep_center = wk;
-        if (wk != t) {
-          ids[wk] = ids[t];
-          dd0[wk] = dd0[t];
-          xyz[wk * 3] = xyz[t * 3];
-          xyz[wk * 3 + 1] = xyz[t * 3 + 1];
-          xyz[wk * 3 + 2] = xyz[t * 3 + 2];
-        }
-        ++wk;
-      }
-    }
-    const int64_t kept = wk - b, moved = wm;
     if (kept == 0 || moved == 0) {
-      // coincident points: halves (clustering.py:75-78).  Nothing was written
-      // back, so the range still holds the group in member order.  The second
-      // half takes the new center: its cached distances become d(., new).
-      const int64_t half = gr.size / 2;
-      for (int64_t t = b + half; t < e; ++t) dd0[t] = dist2(&xyz[t * 3], pn);
+      // coincident points: halves (clustering.py:75-78); the range still holds
+      // the group in member order.  The second half takes the new center: its
+      // cached distances become d(., new).
+      const int64_t half = sz / 2;
+      for (int64_t t = b + half; t < e; ++t) D0[t] = vb[t - b];
       groups[c].size = half;
       cslot[c] = (old_slot >= 0 && old_slot < b + half) ? old_slot : -1;
-      groups.push_back(SplitGroup{b + half, gr.size - half, new_center});
+      groups.push_back(SplitGroup{b + half, sz - half, new_center});
       cslot.push_back(new_slot >= b + half ? new_slot : -1);
     } else {
-      std::memcpy(ids + wk, mid.data(), sizeof(int32_t) * moved);
-      std::memcpy(dd0 + wk, md.data(), sizeof(double) * moved);
-      std::memcpy(xyz + wk * 3, mxyz.data(), sizeof(double) * 3 * moved);
+      // pass 2: stable partition, branch-free (every slot is written on both
+      // sides; a slot is only ever written at or before the one being read)
+      int32_t* __restrict__ Mi = mid.data();
+      double* __restrict__ MX = mx.data();
+      double* __restrict__ MY = my.data();
+      double* __restrict__ MZ = mz.data();
+      double* __restrict__ MD = md.data();
+      int64_t wk = b, wm = 0, keep_center = -1, moved_center = -1;
+      for (int64_t t = b; t < e; ++t) {
+        const int64_t i = t - b;
+        const int32_t f = fl[i];
+        const int32_t idv = id[t];
+        const double xv = X[t], yv = Y[t], zv = Z[t], d0v = D0[t];
+        id[wk] = idv; X[wk] = xv; Y[wk] = yv; Z[wk] = zv; D0[wk] = d0v;
+        Mi[wm] = idv; MX[wm] = xv; MY[wm] = yv; MZ[wm] = zv; MD[wm] = vb[i];
+        keep_center = (t == old_slot && !f) ? wk : keep_center;
+        moved_center = (t == new_slot && f) ? wm : moved_center;
+        wk += 1 - f;
+        wm += f;
+      }
+      std::memcpy(id + wk, Mi, sizeof(int32_t) * moved);
+      std::memcpy(X + wk, MX, sizeof(double) * moved);
+      std::memcpy(Y + wk, MY, sizeof(double) * moved);
+      std::memcpy(Z + wk, MZ, sizeof(double) * moved);
+      std::memcpy(D0 + wk, MD, sizeof(double) * moved);
       groups[c].size = kept;
       cslot[c] = keep_center;
       groups.push_back(SplitGroup{wk, moved, new_center});
@@ -292,6 +306,35 @@ inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
     if (groups.back().size > max_size) stack.push_back(int64_t(groups.size()) - 1);
   }
   return splits;
+}
+
+// AoS entry (tests, vpg_split_groups): positions 3 doubles per slot, the
+// centers' positions in center_xyz; d0 and the center slots computed here.
+inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
+                              std::vector<SplitGroup>& groups, int64_t max_size,
+                              const double* center_xyz, int64_t* visits = nullptr) {
+  std::vector<double> x(total + 1), y(total + 1), z(total + 1), d0(total + 1);
+  std::vector<int64_t> cslot(groups.size(), -1);
+  for (size_t t = 0; t < total; ++t) {
+    x[t] = xyz[t * 3];
+    y[t] = xyz[t * 3 + 1];
+    z[t] = xyz[t * 3 + 2];
+  }
+  for (size_t k = 0; k < groups.size(); ++k) {
+    const SplitGroup& gr = groups[k];
+    for (int64_t t = gr.begin; t < gr.begin + gr.size; ++t) {
+      d0[t] = dist2(&xyz[t * 3], center_xyz + k * 3);
+      if (ids[t] == gr.center && cslot[k] < 0) cslot[k] = t;
+    }
+  }
+  const int64_t n = split_oversize_soa(g, SplitMembers{ids, x.data(), y.data(), z.data(), d0.data()},
+                                       groups, cslot, max_size, visits);
+  for (size_t t = 0; t < total; ++t) {
+    xyz[t * 3] = x[t];
+    xyz[t * 3 + 1] = y[t];
+    xyz[t * 3 + 2] = z[t];
+  }
+  return n;
 }
 
 }  // namespace vpg
