@@ -240,28 +240,47 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
       const int j = idx / s, r = idx - j * s;
       wt[wb + idx] = float(double(pd[r * (S + 1) + j]) * wts[j]);
     }
-    // pass 2b: rows: D-bar and the solve vectors
-    for (int r = tid; r < s; r += blockDim.x) {
+    // pass 2b: rows: D-bar and the solve vectors, P2 threads per row each
+    // summing a slice of the columns, combined in a fixed order
+    const int P2 = s <= 32 ? 4 : 2;
+    const int slice2 = (s + P2 - 1) / P2;
+    for (int base = 0; base < P2 * s; base += blockDim.x) {
+      const int t = base + tid;
+      const bool active = t < P2 * s;
+      const int r = t / P2, h = t % P2;
       double dx = 0.0, dy = 0.0, dz = 0.0;
-      const float* prow = pd + r * (S + 1);
-      const float* erow = pe + r * (S + 1);
-      for (int j = 0; j < s; ++j) {
-        const double a = prow[j], b = erow[j];
-        dx += b * wts[S + j] + a * wts[4 * S + j];
-        dy += b * wts[2 * S + j] + a * wts[5 * S + j];
-        dz += b * wts[3 * S + j] + a * wts[6 * S + j];
+      if (active) {
+        const float* prow = pd + r * (S + 1);
+        const float* erow = pe + r * (S + 1);
+        const int j0 = h * slice2, j1 = min(s, j0 + slice2);
+        for (int j = j0; j < j1; ++j) {
+          const double a = prow[j], b = erow[j];
+          dx += b * wts[S + j] + a * wts[4 * S + j];
+          dy += b * wts[2 * S + j] + a * wts[5 * S + j];
+          dz += b * wts[3 * S + j] + a * wts[6 * S + j];
+        }
       }
-      const Member& mb = mem[q0 + r];
-      const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
-      const double bx = kx * dx, by = ky * dy, bz = kz * dz;
-      const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
-      const int64_t q = q0 + r;
-      dbar_o[q] = f4(bx, by, bz);
-      coeff_o[q] = f4(kx, ky, kz);
-      rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
-                                  __int_as_float(-1));  // parent set by k_parent_links
-      rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
-      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
+      dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
+      dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
+      dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
+      if (P2 == 4) {
+        dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 2);
+        dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
+        dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 2);
+      }
+      if (active && h == 0) {
+        const Member& mb = mem[q0 + r];
+        const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
+        const double bx = kx * dx, by = ky * dy, bz = kz * dz;
+        const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
+        const int64_t q = q0 + r;
+        dbar_o[q] = f4(bx, by, bz);
+        coeff_o[q] = f4(kx, ky, kz);
+        rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
+                                    __int_as_float(-1));  // parent set by k_parent_links
+        rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
+        i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
+      }
     }
     __syncthreads();
   }

@@ -378,6 +378,9 @@ struct EmitterSample {
   double rad[3];
 };
 
+// One shadow test (intersect + media transmittance) for every emitter type,
+// so the ratio-tracking loop exists once in the kernel: lanes that sampled
+// different emitter types reconverge in it (and it is cached once).
 __device__ EmitterSample sample_emitter(const vpg_scene& sc, const V3& p, Rng& rng) {
   const int n_em = sc.n_emit;
   const double u = rng.next();
@@ -387,6 +390,7 @@ __device__ EmitterSample sample_emitter(const vpg_scene& sc, const V3& p, Rng& r
   const double sel = double(n_em);
   EmitterSample out{V3{0.0, 0.0, 1.0}, 1.0, false, {0.0, 0.0, 0.0}};
   const int type = sc.em_type[e];
+  double clear, t_hi, factor;
   if (type == 1) {
     const double* q = sc.em_quad[e];
     const double u1 = rng.next(), u2 = rng.next();
@@ -402,38 +406,34 @@ __device__ EmitterSample sample_emitter(const vpg_scene& sc, const V3& p, Rng& r
     const double cos_q = -(nq[0] * out.w.x + nq[1] * out.w.y + nq[2] * out.w.z);
     out.pdf = d2 / (sc.em_area[e] * pymax(fabs(cos_q), 1e-12) * sel);
     if (cos_q <= 0.0) return out;
-    const double clear = dist - 1e-6 * pymax(1.0, dist);
-    int sid;
-    if (intersect(sc, p, out.w, kTEps, clear, sid) < clear) return out;
-    double tr[3];
-    media_transmittance(sc, p, out.w, 0.0, dist, rng, tr);
-    for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c];
-    return out;
-  }
-  out.delta = true;
-  if (type == 0) {
+    clear = dist - 1e-6 * pymax(1.0, dist);
+    t_hi = dist;
+    factor = 1.0;  // rad = val * tr
+  } else if (type == 0) {
+    out.delta = true;
     const double* lp = sc.em_pos[e];
     const double dx = lp[0] - p.x, dy = lp[1] - p.y, dz = lp[2] - p.z;
     const double d2 = dx * dx + dy * dy + dz * dz;
     if (d2 < 1e-16) return out;
     const double dist = sqrt(d2);
     out.w = V3{dx / dist, dy / dist, dz / dist};
-    const double clear = dist - 1e-6 * pymax(1.0, dist);
-    int sid;
-    if (intersect(sc, p, out.w, kTEps, clear, sid) < clear) return out;
-    double tr[3];
-    media_transmittance(sc, p, out.w, 0.0, dist, rng, tr);
-    const double inv_d2 = sel / d2;
-    for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c] * inv_d2;
-    return out;
+    clear = dist - 1e-6 * pymax(1.0, dist);
+    t_hi = dist;
+    factor = sel / d2;  // rad = val * tr * (sel / d2)
+  } else {
+    out.delta = true;
+    const double* ld = sc.em_pos[e];
+    out.w = V3{-ld[0], -ld[1], -ld[2]};
+    clear = kNoHit;
+    t_hi = kNoHit;
+    factor = sel;  // rad = val * tr * sel
   }
-  const double* ld = sc.em_pos[e];
-  out.w = V3{-ld[0], -ld[1], -ld[2]};
   int sid;
-  if (intersect(sc, p, out.w, kTEps, kNoHit, sid) < kNoHit) return out;
+  if (intersect(sc, p, out.w, kTEps, clear, sid) < clear) return out;
   double tr[3];
-  media_transmittance(sc, p, out.w, 0.0, kNoHit, rng, tr);
-  for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c] * sel;
+  media_transmittance(sc, p, out.w, 0.0, t_hi, rng, tr);
+  // x * 1.0 is exact, so the area light's val * tr rounds as before
+  for (int c = 0; c < 3; ++c) out.rad[c] = val[c] * tr[c] * factor;
   return out;
 }
 
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const v
 }
 
 // Single-pass capture: trace every path once, records into scratch slots.
-__global__ void __launch_bounds__(128) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
+__global__ void __launch_bounds__(128, 4) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                        int64_t* __restrict__ counts,
                                                        const vpg_records scratch,
                                                        const vpg_paths pth, Capture cap) {
