@@ -53,6 +53,8 @@ def parse():
                     help="square resolution of the CPU-baseline sample of the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-partitioned multi-GPU path even at N=1 (default for N>1)")
     return ap.parse_args()
 
 
@@ -223,8 +225,6 @@ def run_native(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl, cfg = workload_config(args.workload)
-    # multi-GPU: each rank renders its own frame of the workload (seed = rank)
-    cfg.seed = rank
     scene = wl.scene()
     stream = torch.cuda.current_stream()
 
@@ -233,8 +233,12 @@ def run_native(args):
         e.record(stream)
         return e
 
-    # ---- trace (setup; timed separately for ms/frame)
-    trace = render_pt(scene, cfg, with_records=True)
+    # ---- trace (setup; timed separately for ms/frame).  Each warm-up frame is
+    # dropped before the next so the timed one reuses its memory, as a render
+    # loop would.
+    for _ in range(2):
+        trace = render_pt(scene, cfg, with_records=True)
+        del trace
     torch.cuda.synchronize()
     e0 = ev()
     trace = render_pt(scene, cfg, with_records=True)
@@ -354,7 +358,7 @@ def run_native(args):
                    "max_depth": wl.max_depth, "cluster_size": cfg.cluster_size,
                    "iterations": cfg.iterations, "tol": 0.0, "vertices_per_gpu": n,
                    "clusters": int(gi["n_clusters"]), "nnz": int(gi["nnz"]),
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": "single",
                    "l2": "inputs larger than L2 (records 290 B/vertex, kernel blocks 4 B/nnz)"},
         "ms_per_frame": trace_ms + step_ms + splat_ms,
         "frame_breakdown_ms": {"trace": trace_ms, "build_plus_solve": step_ms, "splat": splat_ms},
@@ -382,10 +386,174 @@ def run_native(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------- sharded arm
+def run_sharded(args):
+    """N>1: one frame row-partitioned over the GPUs (pathgraph/sharded.py).
+
+    Weak scaling: the frame is the workload at spp x N, so every GPU traces
+    and owns about one C2 frame of records.  A step = the sharded build
+    (light all-gather, exact clustering, record all-to-all, shard-local
+    operators) + the solve with its per-iteration halo exchange.
+    """
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_11894_b200 import _native as N
+    from paper_2404_11894_b200.pathgraph.sharded import (ShardComm, ShardedPathGraph,
+                                                         pixel_ranges)
+    from paper_2404_11894_b200.scenecore.flatten import pack_scene
+    from paper_2404_11894_b200.transport.tracer import trace_records_device
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = ShardComm()
+    wl, cfg = workload_config(args.workload)
+    cfg.spp = wl.spp * world
+    scene = wl.scene()
+    packed = pack_scene(scene)
+    w, h, spp = packed.width, packed.height, cfg.spp
+    ranges = pixel_ranges(w * h, world)
+    p0, p1 = ranges[rank]
+    stream = torch.cuda.current_stream()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_ms(ms):
+        t = torch.tensor([ms], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    trace_records_device(scene, cfg, (p0 * spp, (p1 - p0) * spp))
+    barrier()
+    e0 = ev()
+    recs, paths, n_rec = trace_records_device(scene, cfg, (p0 * spp, (p1 - p0) * spp))
+    e1 = ev()
+    barrier()
+    trace_ms = max_ms(e0.elapsed_time(e1))
+
+    def step():
+        g = ShardedPathGraph.build(comm, recs, n_rec, cfg.cluster_size, seed=cfg.seed)
+        g.pix_ranges = ranges
+        g.solve(cfg.iterations, 0.0)
+        return g
+
+    for _ in range(args.warmup):
+        g = step()
+    del g
+    barrier()
+    launches0 = N.launch_count()
+    with ClockSampler(local) as clocks:
+        time.sleep(0.25)
+        barrier()
+        t_start = ev()
+        for _ in range(args.steps):
+            g = step()
+        t_end = ev()
+        barrier()
+    launches = N.launch_count() - launches0
+    step_ms = max_ms(t_start.elapsed_time(t_end) / args.steps)
+    n_total = int(g.row_off[-1])
+    n_own, n_halo = g.n, g.halo.n_halo
+    s0 = ev()
+    g.splat(paths, recs, (p0, p1), w, h, spp)
+    s1 = ev()
+    barrier()
+    splat_ms = max_ms(s0.elapsed_time(s1))
+    del g
+
+    # per-kernel device times of one step (after the timed region)
+    N.profile_reset()
+    N.profile(True)
+    g = step()
+    barrier()
+    prof = N.profile_read()
+    N.profile(False)
+    N.profile_reset()
+    hbm, peak_kind = peaks()
+    it_count, it_ms = prof.get("k_solve_iter", (0, 0.0))
+    it_avg = it_ms / max(it_count, 1)
+    achieved = ITER_BYTES_PER_VERTEX * g.n / (it_avg * 1e-3) / 1e9 if it_count else 0.0
+    prof_total = sum(ms for _, ms in prof.values())
+    del g
+
+    # end to end: this shard's records from pinned host memory, image to the host
+    host_recs = {k: v.cpu().pin_memory() for k, v in recs.items()}
+    host_paths = {k: v.cpu().pin_memory() for k, v in paths.items()}
+    h2d = sum(t.numel() * t.element_size() for t in list(host_recs.values()) +
+              list(host_paths.values()))
+
+    def e2e_once():
+        r = {k: v.to("cuda", non_blocking=True) for k, v in host_recs.items()}
+        pt = {k: v.to("cuda", non_blocking=True) for k, v in host_paths.items()}
+        g2 = ShardedPathGraph.build(comm, r, n_rec, cfg.cluster_size, seed=cfg.seed)
+        g2.pix_ranges = ranges
+        g2.solve(cfg.iterations, 0.0)
+        return g2.splat(pt, r, (p0, p1), w, h, spp).cpu()
+
+    e2e_once()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        img = e2e_once()
+    barrier()
+    e2e_s = max_ms((time.perf_counter() - t0) / args.e2e_steps * 1e3) / 1e3
+
+    value = n_total / (step_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (procedural fbm cloud scene, traced on device; no dataset)",
+        "config": {"workload": wl.name, "resolution": list(wl.res), "spp": spp,
+                   "max_depth": wl.max_depth, "cluster_size": cfg.cluster_size,
+                   "iterations": cfg.iterations, "tol": 0.0, "vertices_total": n_total,
+                   "vertices_per_gpu": n_total / world, "rows_owned_rank0": n_own,
+                   "halo_rows_rank0": n_halo, "parallelism": f"sharded{world}",
+                   "frame": f"{wl.name} scene at {w}x{h}, spp = {wl.spp} x {world} GPUs",
+                   "l2": "inputs larger than L2"},
+        "ms_per_frame": trace_ms + step_ms + splat_ms,
+        "frame_breakdown_ms": {"trace": trace_ms, "build_plus_solve": step_ms,
+                               "splat": splat_ms},
+        "roofline": {"kernel": "k_solve_iter", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_kind": peak_kind, "avg_launch_ms": it_avg,
+                     "share_of_step": it_ms / prof_total if prof_total else None},
+        "kernel_ms": {k: {"launches": c, "total_ms": ms} for k, (c, ms) in
+                      sorted(prof.items(), key=lambda kv: -kv[1][1])[:12]},
+        "e2e": {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(img.numel() * img.element_size()),
+                "ms_per_step": e2e_s * 1e3,
+                "path": "sharded build/solve/splat from pinned host records of each shard"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "cpu_baseline": None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.sharded or dist_env()[1] > 1:
+        run_sharded(args)
     else:
         run_native(args)
 

@@ -331,7 +331,8 @@ int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_r
  * in pass 1.  If *counter > capacity afterwards, records were dropped: retry
  * with capacity >= *counter (deterministic).  Then vpg_scatter_records moves
  * the n = *counter scratch records into path order, row = rec_start[path -
- * path_begin] + depth.  max_depth <= 128. */
+ * path_begin] + depth.  Any max_depth (a path's slots are linked in a scratch
+ * list for the backward i_pt sweep). */
 int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* scratch,
                       int64_t capacity, uint64_t* counter, int64_t* counts, const vpg_paths* paths,
                       void* stream);

@@ -30,7 +30,6 @@ constexpr uint64_t kSaltTrace = 0x7E;
 constexpr uint64_t kSaltExtra = 0xED;
 
 enum Mode { kOff = 0, kCount = 1, kFill = 2, kCapture = 3 };
-constexpr int kMaxCaptureDepth = 128;  // slot list per path in capture mode
 
 // ---------------------------------------------------------- rng (rng.py)
 struct Rng {
@@ -448,10 +447,16 @@ __device__ double emitter_dir_pdf_from_hit(const vpg_scene& sc, int sid, double 
   return t_hit * t_hit / (sc.em_area[e] * cos_q * sc.n_emit);
 }
 
+// Record and path-table stores are streaming (evict-first): the vertex buffer
+// is written once per frame and must not push the density grid out of L2.
 __device__ __forceinline__ void put3(double* a, int64_t row, double x, double y, double z) {
-  a[row * 3] = x;
-  a[row * 3 + 1] = y;
-  a[row * 3 + 2] = z;
+  __stcs(a + row * 3, x);
+  __stcs(a + row * 3 + 1, y);
+  __stcs(a + row * 3 + 2, z);
+}
+template <class T>
+__device__ __forceinline__ void put1(T* a, int64_t row, T v) {
+  __stcs(a + row, v);
 }
 
 struct PathResult {
@@ -466,6 +471,7 @@ struct PathResult {
 struct Capture {
   unsigned long long* counter;
   int64_t capacity;
+  int32_t* link;  // per slot: slot of the same path's previous record, -1 for its first
 };
 
 __device__ __forceinline__ int64_t claim_slot(const Capture& cap) {
@@ -478,18 +484,37 @@ __device__ __forceinline__ int64_t claim_slot(const Capture& cap) {
   return int64_t(base) + __popc(act & ((1u << lane) - 1u));
 }
 
+// The per-path state of trace_one (kernels.py:152-391) between bounces, so a
+// path can be advanced one bounce at a time: the capture kernel keeps every
+// lane busy by starting a new path in a lane whose path ended (the bounce code
+// is shared, so lanes at different depths of different paths still execute it
+// together).
 template <int kMode>
-__device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
-                                int64_t py, int64_t path_id, int64_t rec_offset,
-                                const vpg_records& rec, const vpg_paths& pth, int64_t slot,
-                                const Capture& cap = Capture{nullptr, 0}) {
-  constexpr bool kStore = kMode == kFill || kMode == kCapture;
-  int64_t rows[kMode == kCapture ? kMaxCaptureDepth : 1];
-  // row of record k of this path; -1 when a capture slot overflowed
-  auto row_of = [&](int k) -> int64_t { return kMode == kCapture ? rows[k] : rec_offset + k; };
-  Rng rng = make_stream(cfg.seed, path_id, kSaltTrace);
-  const double jx = rng.next();
-  const double jy = rng.next();
+struct PathState {
+  Rng rng;
+  V3 o, d;
+  double est[3], beta[3], dcam[3], camw[3], d0n[3], d0p[3], ext_fs[3];
+  double ext_pdf, rr_inv;
+  bool from_camera, allow_record;
+  int n_rec;
+  int64_t path_id, rec_offset, slot;
+  // capture: slot of the path's latest record (-1: none yet, or the scratch
+  // overflowed); earlier records are reached through Capture::link
+  int64_t last_row;
+  // row of the path's latest record
+  __device__ int64_t last() const { return kMode == kCapture ? last_row : rec_offset + n_rec - 1; }
+};
+
+template <int kMode>
+__device__ void path_begin(PathState<kMode>& st, const vpg_scene& sc, const vpg_trace_cfg& cfg,
+                           int64_t px, int64_t py, int64_t path_id, int64_t rec_offset,
+                           int64_t slot) {
+  st.path_id = path_id;
+  st.rec_offset = rec_offset;
+  st.slot = slot;
+  st.rng = make_stream(cfg.seed, path_id, kSaltTrace);
+  const double jx = st.rng.next();
+  const double jy = st.rng.next();
   const double* cam = sc.cam;
   const double width = cam[13], height = cam[14];
   const double aspect = width / height;
@@ -499,195 +524,238 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
   double dy = cam[4] + sx * cam[7] + sy * cam[10];
   double dz = cam[5] + sx * cam[8] + sy * cam[11];
   const double inv0 = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
-  V3 d{dx * inv0, dy * inv0, dz * inv0};
-  V3 o{cam[0], cam[1], cam[2]};
+  st.d = V3{dx * inv0, dy * inv0, dz * inv0};
+  st.o = V3{cam[0], cam[1], cam[2]};
+  for (int c = 0; c < 3; ++c) {
+    st.est[c] = 0.0;
+    st.beta[c] = 1.0;
+    st.dcam[c] = st.camw[c] = st.d0n[c] = st.d0p[c] = st.ext_fs[c] = 0.0;
+  }
+  st.ext_pdf = 1.0;
+  st.rr_inv = 1.0;
+  st.from_camera = true;
+  st.allow_record = true;
+  st.n_rec = 0;
+  st.last_row = -1;
+}
 
-  double est[3] = {0, 0, 0}, beta[3] = {1, 1, 1};
-  double dcam[3] = {0, 0, 0}, camw[3] = {0, 0, 0}, d0n[3] = {0, 0, 0}, d0p[3] = {0, 0, 0};
-  double ext_fs[3] = {0, 0, 0};
-  double ext_pdf = 1.0, rr_inv = 1.0;
-  bool from_camera = true, allow_record = true;
-  int n_rec = 0;
+// One iteration of the bounce loop; false when the path has ended.
+template <int kMode>
+__device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg_trace_cfg& cfg,
+                            const vpg_records& rec, const Capture& cap) {
+  constexpr bool kStore = kMode == kFill || kMode == kCapture;
+  Rng& rng = st.rng;
+  V3& o = st.o;
+  V3& d = st.d;
+  double* est = st.est;
+  double* beta = st.beta;
+  double* dcam = st.dcam;
+  double* camw = st.camw;
+  double* d0n = st.d0n;
+  double* d0p = st.d0p;
+  double* ext_fs = st.ext_fs;
+  double& ext_pdf = st.ext_pdf;
+  double& rr_inv = st.rr_inv;
+  bool& from_camera = st.from_camera;
+  bool& allow_record = st.allow_record;
+  int& n_rec = st.n_rec;
   const int max_depth = cfg.max_depth;
+  const int64_t path_id = st.path_id;
+  const int64_t rec_offset = st.rec_offset;
+  int sid;
+  const double t_hit = intersect(sc, o, d, kTEps, kNoHit, sid);
+  const double pe_at_dir = emitter_dir_pdf_from_hit(sc, sid, t_hit, d);
+  if (kStore && !from_camera) {
+    const int64_t prow = st.last();
+    if (prow >= 0) rec.pdf_emit_at_phase[prow] = pe_at_dir;
+  }
+  const MediaFlight mf = media_flight(sc, o, d, 0.0, t_hit, rng);
+  V3 v{o.x + mf.t * d.x, o.y + mf.t * d.y, o.z + mf.t * d.z};
+  bool volume = false;
+  double k[3] = {0, 0, 0};
+  double gpar = 0.0;
+  V3 nrm{0.0, 0.0, 0.0};
+  int class_id = -1;
 
-  while (true) {
-    int sid;
-    const double t_hit = intersect(sc, o, d, kTEps, kNoHit, sid);
-    const double pe_at_dir = emitter_dir_pdf_from_hit(sc, sid, t_hit, d);
-    if (kStore && !from_camera) {
-      const int64_t prow = row_of(n_rec - 1);
-      if (prow >= 0) rec.pdf_emit_at_phase[prow] = pe_at_dir;
-    }
-    const MediaFlight mf = media_flight(sc, o, d, 0.0, t_hit, rng);
-    V3 v{o.x + mf.t * d.x, o.y + mf.t * d.y, o.z + mf.t * d.z};
-    bool volume = false;
-    double k[3] = {0, 0, 0};
-    double gpar = 0.0;
-    V3 nrm{0.0, 0.0, 0.0};
-    int class_id = -1;
-
-    if (mf.scattered) {
-      if (!allow_record || n_rec >= max_depth) break;
-      const int mid = mf.medium;
-      const double* ss = sc.med_sigma_s[mid];
-      if (sc.med_kind[mid] == 0) {
-        k[0] = ss[0];
-        k[1] = ss[1];
-        k[2] = ss[2];
-      } else {
-        const double dens = grid_density(sc, mid, v) * sc.med_scale[mid];
-        k[0] = ss[0] * dens;
-        k[1] = ss[1] * dens;
-        k[2] = ss[2] * dens;
-      }
-      if (k[0] == 0.0 && k[1] == 0.0 && k[2] == 0.0) break;  // pure absorption
-      volume = true;
-      gpar = sc.med_g[mid];
-      class_id = mid;
+  if (mf.scattered) {
+    if (!allow_record || n_rec >= max_depth) return false;
+    const int mid = mf.medium;
+    const double* ss = sc.med_sigma_s[mid];
+    if (sc.med_kind[mid] == 0) {
+      k[0] = ss[0];
+      k[1] = ss[1];
+      k[2] = ss[2];
     } else {
-      if (sid < 0) break;
-      const int mat = sc.mat_type[sid];
-      v = V3{o.x + t_hit * d.x, o.y + t_hit * d.y, o.z + t_hit * d.z};
-      if (mat == 2) {
-        const V3 gn = surface_normal_at(sc, sid, v);
-        if (gn.x * d.x + gn.y * d.y + gn.z * d.z < 0.0) {
-          const double* ev = sc.em_value[sc.emitter_id[sid]];
-          if (from_camera) {
-            for (int c = 0; c < 3; ++c) {
-              dcam[c] = mf.w[c] * ev[c];
-              est[c] += dcam[c];
-            }
-          } else {
-            const double denom = ext_pdf + pe_at_dir;
-            double cc[3];
-            for (int c = 0; c < 3; ++c) {
-              cc[c] = ext_fs[c] * mf.w[c] * ev[c] / denom;
-              est[c] += beta[c] * cc[c];
-            }
-            if (n_rec == 1)
-              for (int c = 0; c < 3; ++c) d0p[c] = cc[c];
-            if (kStore) {
-              const int64_t row = row_of(n_rec - 1);
-              if (row >= 0) {
-                put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
-                for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
-              }
+      const double dens = grid_density(sc, mid, v) * sc.med_scale[mid];
+      k[0] = ss[0] * dens;
+      k[1] = ss[1] * dens;
+      k[2] = ss[2] * dens;
+    }
+    if (k[0] == 0.0 && k[1] == 0.0 && k[2] == 0.0) return false;  // pure absorption
+    volume = true;
+    gpar = sc.med_g[mid];
+    class_id = mid;
+  } else {
+    if (sid < 0) return false;
+    const int mat = sc.mat_type[sid];
+    v = V3{o.x + t_hit * d.x, o.y + t_hit * d.y, o.z + t_hit * d.z};
+    if (mat == 2) {
+      const V3 gn = surface_normal_at(sc, sid, v);
+      if (gn.x * d.x + gn.y * d.y + gn.z * d.z < 0.0) {
+        const double* ev = sc.em_value[sc.emitter_id[sid]];
+        if (from_camera) {
+          for (int c = 0; c < 3; ++c) {
+            dcam[c] = mf.w[c] * ev[c];
+            est[c] += dcam[c];
+          }
+        } else {
+          const double denom = ext_pdf + pe_at_dir;
+          double cc[3];
+          for (int c = 0; c < 3; ++c) {
+            cc[c] = ext_fs[c] * mf.w[c] * ev[c] / denom;
+            est[c] += beta[c] * cc[c];
+          }
+          if (n_rec == 1)
+            for (int c = 0; c < 3; ++c) d0p[c] = cc[c];
+          if (kStore) {
+            const int64_t row = st.last();
+            if (row >= 0) {
+              put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
+              for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
             }
           }
         }
-        break;
       }
-      if (mat == 1) break;  // black absorber
-      if (!allow_record || n_rec >= max_depth) break;
-      V3 gn = surface_normal_at(sc, sid, v);
-      if (gn.x * d.x + gn.y * d.y + gn.z * d.z > 0.0) gn = V3{-gn.x, -gn.y, -gn.z};
-      nrm = gn;
-      k[0] = sc.albedo[sid][0];
-      k[1] = sc.albedo[sid][1];
-      k[2] = sc.albedo[sid][2];
-      class_id = sid;
+      return false;
     }
-
-    // ---- record n_rec at v
-    double wc[3];
-    for (int c = 0; c < 3; ++c) wc[c] = mf.w[c] * rr_inv;
-    if (from_camera) {
-      for (int c = 0; c < 3; ++c) {
-        camw[c] = wc[c];
-        beta[c] = wc[c];
-      }
-    } else {
-      for (int c = 0; c < 3; ++c) beta[c] *= (ext_fs[c] / ext_pdf) * wc[c];
-    }
-    const V3 ax = d;  // arrival direction = phase anchor
-
-    const EmitterSample es = sample_emitter(sc, v, rng);
-    double rho_e;
-    if (volume) {
-      rho_e = hg_pdf(ax.x * es.w.x + ax.y * es.w.y + ax.z * es.w.z, gpar);
-    } else {
-      rho_e = pymax(0.0, nrm.x * es.w.x + nrm.y * es.w.y + nrm.z * es.w.z) * kInvPi;
-    }
-    const double p_p_at_e = rho_e;
-    double cn[3];
-    for (int c = 0; c < 3; ++c) {
-      const double fe = k[c] * rho_e;
-      cn[c] = es.delta ? fe * es.rad[c] : fe * es.rad[c] / (es.pdf + p_p_at_e);
-      est[c] += beta[c] * cn[c];
-    }
-    if (n_rec == 0)
-      for (int c = 0; c < 3; ++c) d0n[c] = cn[c];
-
-    const double u1 = rng.next();
-    const double u2 = rng.next();
-    V3 wp;
-    double pdf_p;
-    if (volume) {
-      wp = hg_sample_dir(gpar, ax, u1, u2);
-      pdf_p = hg_pdf(ax.x * wp.x + ax.y * wp.y + ax.z * wp.z, gpar);
-    } else {
-      wp = cosine_sample_dir(nrm, u1, u2);
-      pdf_p = pymax(0.0, nrm.x * wp.x + nrm.y * wp.y + nrm.z * wp.z) * kInvPi;
-    }
-    double fp[3];
-    for (int c = 0; c < 3; ++c) fp[c] = k[c] * pdf_p;
-
-    int64_t row = -1;
-    if (kMode == kFill) row = rec_offset + n_rec;
-    if (kMode == kCapture) {
-      const int64_t got = claim_slot(cap);
-      row = got < cap.capacity ? got : -1;
-      rows[n_rec] = row;
-    }
-    if (kStore && row >= 0) {
-      put3(rec.pos, row, v.x, v.y, v.z);
-      put3(rec.omega_out, row, -ax.x, -ax.y, -ax.z);
-      put3(rec.normal, row, nrm.x, nrm.y, nrm.z);
-      put3(rec.coeff, row, k[0], k[1], k[2]);
-      rec.g[row] = gpar;
-      put3(rec.phase_dir, row, wp.x, wp.y, wp.z);
-      rec.pdf_phase[row] = pdf_p;
-      rec.pdf_emit_at_phase[row] = 0.0;
-      put3(rec.emit_dir, row, es.w.x, es.w.y, es.w.z);
-      rec.pdf_emit[row] = es.pdf;
-      put3(rec.d_emit, row, es.rad[0], es.rad[1], es.rad[2]);
-      put3(rec.d_phase, row, 0.0, 0.0, 0.0);
-      put3(rec.i_pt, row, cn[0], cn[1], cn[2]);  // staged D-bar, replaced by the sweep
-      put3(rec.w_cont, row, wc[0], wc[1], wc[2]);
-      rec.kind[row] = volume ? 0 : 1;
-      rec.emit_delta[row] = es.delta ? 1 : 0;
-      rec.class_id[row] = class_id;
-      rec.path_idx[row] = path_id;
-      rec.depth[row] = n_rec;
-    }
-    ++n_rec;
-    if (pdf_p <= 0.0) break;  // degenerate sample, no continuation
-
-    rr_inv = 1.0;
-    allow_record = true;
-    if (n_rec >= cfg.rr_start) {
-      double q = (beta[0] * fp[0] / pdf_p + beta[1] * fp[1] / pdf_p + beta[2] * fp[2] / pdf_p) / 3.0;
-      if (q > 1.0) q = 1.0;
-      if (q < cfg.rr_floor) q = cfg.rr_floor;
-      const double u = rng.next();
-      if (u >= q) allow_record = false;
-      else rr_inv = 1.0 / q;
-    }
-    for (int c = 0; c < 3; ++c) ext_fs[c] = fp[c];
-    ext_pdf = pdf_p;
-    from_camera = false;
-    if (volume) {
-      o = v;
-    } else {
-      o = V3{v.x + wp.x * kSurfOffset, v.y + wp.y * kSurfOffset, v.z + wp.z * kSurfOffset};
-    }
-    d = wp;
+    if (mat == 1) return false;  // black absorber
+    if (!allow_record || n_rec >= max_depth) return false;
+    V3 gn = surface_normal_at(sc, sid, v);
+    if (gn.x * d.x + gn.y * d.y + gn.z * d.z > 0.0) gn = V3{-gn.x, -gn.y, -gn.z};
+    nrm = gn;
+    k[0] = sc.albedo[sid][0];
+    k[1] = sc.albedo[sid][1];
+    k[2] = sc.albedo[sid][2];
+    class_id = sid;
   }
 
+  // ---- record n_rec at v
+  double wc[3];
+  for (int c = 0; c < 3; ++c) wc[c] = mf.w[c] * rr_inv;
+  if (from_camera) {
+    for (int c = 0; c < 3; ++c) {
+      camw[c] = wc[c];
+      beta[c] = wc[c];
+    }
+  } else {
+    for (int c = 0; c < 3; ++c) beta[c] *= (ext_fs[c] / ext_pdf) * wc[c];
+  }
+  const V3 ax = d;  // arrival direction = phase anchor
+
+  const EmitterSample es = sample_emitter(sc, v, rng);
+  double rho_e;
+  if (volume) {
+    rho_e = hg_pdf(ax.x * es.w.x + ax.y * es.w.y + ax.z * es.w.z, gpar);
+  } else {
+    rho_e = pymax(0.0, nrm.x * es.w.x + nrm.y * es.w.y + nrm.z * es.w.z) * kInvPi;
+  }
+  const double p_p_at_e = rho_e;
+  double cn[3];
+  for (int c = 0; c < 3; ++c) {
+    const double fe = k[c] * rho_e;
+    cn[c] = es.delta ? fe * es.rad[c] : fe * es.rad[c] / (es.pdf + p_p_at_e);
+    est[c] += beta[c] * cn[c];
+  }
+  if (n_rec == 0)
+    for (int c = 0; c < 3; ++c) d0n[c] = cn[c];
+
+  const double u1 = rng.next();
+  const double u2 = rng.next();
+  V3 wp;
+  double pdf_p;
+  if (volume) {
+    wp = hg_sample_dir(gpar, ax, u1, u2);
+    pdf_p = hg_pdf(ax.x * wp.x + ax.y * wp.y + ax.z * wp.z, gpar);
+  } else {
+    wp = cosine_sample_dir(nrm, u1, u2);
+    pdf_p = pymax(0.0, nrm.x * wp.x + nrm.y * wp.y + nrm.z * wp.z) * kInvPi;
+  }
+  double fp[3];
+  for (int c = 0; c < 3; ++c) fp[c] = k[c] * pdf_p;
+
+  int64_t row = -1;
+  if (kMode == kFill) row = rec_offset + n_rec;
+  if (kMode == kCapture) {
+    const int64_t got = claim_slot(cap);
+    row = got < cap.capacity ? got : -1;
+    // the backward sweep walks the path's slots through the link list
+    if (row >= 0) cap.link[row] = int32_t(st.last_row);
+    st.last_row = row;
+  }
+  if (kStore && row >= 0) {
+    put3(rec.pos, row, v.x, v.y, v.z);
+    put3(rec.omega_out, row, -ax.x, -ax.y, -ax.z);
+    put3(rec.normal, row, nrm.x, nrm.y, nrm.z);
+    put3(rec.coeff, row, k[0], k[1], k[2]);
+    put1(rec.g, row, gpar);
+    put3(rec.phase_dir, row, wp.x, wp.y, wp.z);
+    put1(rec.pdf_phase, row, pdf_p);
+    put1(rec.pdf_emit_at_phase, row, 0.0);
+    put3(rec.emit_dir, row, es.w.x, es.w.y, es.w.z);
+    put1(rec.pdf_emit, row, es.pdf);
+    put3(rec.d_emit, row, es.rad[0], es.rad[1], es.rad[2]);
+    put3(rec.d_phase, row, 0.0, 0.0, 0.0);
+    put3(rec.i_pt, row, cn[0], cn[1], cn[2]);  // staged D-bar, replaced by the sweep
+    put3(rec.w_cont, row, wc[0], wc[1], wc[2]);
+    put1(reinterpret_cast<unsigned char*>(rec.kind), row, (unsigned char)(volume ? 0 : 1));
+    put1(reinterpret_cast<unsigned char*>(rec.emit_delta), row, (unsigned char)(es.delta ? 1 : 0));
+    put1(rec.class_id, row, int32_t(class_id));
+    put1(reinterpret_cast<long long*>(rec.path_idx), row, (long long)path_id);
+    put1(rec.depth, row, int32_t(n_rec));
+  }
+  ++n_rec;
+  if (pdf_p <= 0.0) return false;  // degenerate sample, no continuation
+
+  rr_inv = 1.0;
+  allow_record = true;
+  if (n_rec >= cfg.rr_start) {
+    double q = (beta[0] * fp[0] / pdf_p + beta[1] * fp[1] / pdf_p + beta[2] * fp[2] / pdf_p) / 3.0;
+    if (q > 1.0) q = 1.0;
+    if (q < cfg.rr_floor) q = cfg.rr_floor;
+    const double u = rng.next();
+    if (u >= q) allow_record = false;
+    else rr_inv = 1.0 / q;
+  }
+  for (int c = 0; c < 3; ++c) ext_fs[c] = fp[c];
+  ext_pdf = pdf_p;
+  from_camera = false;
+  if (volume) {
+    o = v;
+  } else {
+    o = V3{v.x + wp.x * kSurfOffset, v.y + wp.y * kSurfOffset, v.z + wp.z * kSurfOffset};
+  }
+  d = wp;
+  return true;
+}
+
+// Backward i_pt sweep (kernels.py:393-408) and the path-table row.
+template <int kMode>
+__device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, const vpg_paths& pth,
+                               const Capture& cap) {
+  constexpr bool kStore = kMode == kFill || kMode == kCapture;
+  const int n_rec = st.n_rec;
+  const int64_t slot = st.slot;
+  const double* est = st.est;
+  const double* dcam = st.dcam;
+  const double* camw = st.camw;
+  const double* d0n = st.d0n;
+  const double* d0p = st.d0p;
   if (kStore && n_rec > 0) {  // backward sweep (kernels.py:393-408)
     double in[3] = {0.0, 0.0, 0.0};
+    int64_t row = st.last_row;
     for (int kk = n_rec - 1; kk >= 0; --kk) {
-      const int64_t row = row_of(kk);
+      if (kMode != kCapture) row = st.rec_offset + kk;
+      else if (kk < n_rec - 1) row = cap.link[row];
       if (row < 0) break;  // overflowed capture: the host retries with room
       const double pp = rec.pdf_phase[row];
       for (int c = 0; c < 3; ++c) {
@@ -712,6 +780,18 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
   return res;
 }
 
+template <int kMode>
+__device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
+                                int64_t py, int64_t path_id, int64_t rec_offset,
+                                const vpg_records& rec, const vpg_paths& pth, int64_t slot,
+                                const Capture& cap = Capture{nullptr, 0, nullptr}) {
+  PathState<kMode> st;
+  path_begin(st, sc, cfg, px, py, path_id, rec_offset, slot);
+  while (path_bounce(st, sc, cfg, rec, cap)) {
+  }
+  return path_end(st, rec, pth, cap);
+}
+
 // count / fill over paths [path_begin, path_begin + path_count)
 template <int kMode>
 __global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const vpg_trace_cfg cfg,
@@ -731,45 +811,70 @@ __global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const v
 }
 
 // Single-pass capture: trace every path once, records into scratch slots.
+// A lane whose path ends starts its next path at once (the loop advances
+// every lane by one bounce per iteration), so lanes do not idle until the
+// longest path of their warp has finished.
 __global__ void __launch_bounds__(128, 4) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                        int64_t* __restrict__ counts,
                                                        const vpg_records scratch,
                                                        const vpg_paths pth, Capture cap) {
   const int64_t spp = cfg.spp;
   const int64_t width = sc.width;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cfg.path_count;
-       i += int64_t(gridDim.x) * blockDim.x) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= cfg.path_count) return;
+  PathState<kCapture> st;
+  {
     const int64_t path_id = cfg.path_begin + i;
     const int64_t pix = path_id / spp;
-    const PathResult r = trace_one<kCapture>(sc, cfg, pix % width, pix / width, path_id, 0,
-                                             scratch, pth, i, cap);
-    counts[i] = r.n_rec;
+    path_begin(st, sc, cfg, pix % width, pix / width, path_id, 0, i);
+  }
+  while (true) {
+    if (!path_bounce(st, sc, cfg, scratch, cap)) {
+      const PathResult r = path_end(st, scratch, pth, cap);
+      counts[i] = r.n_rec;
+      i += stride;
+      if (i >= cfg.path_count) break;
+      const int64_t path_id = cfg.path_begin + i;
+      const int64_t pix = path_id / spp;
+      path_begin(st, sc, cfg, pix % width, pix / width, path_id, 0, i);
+    }
   }
 }
 
-// Scratch slot -> its row in path order: rec_start[path] + depth.
-__global__ void k_scatter_records(const vpg_records src, int64_t n, const int64_t* __restrict__ rec_start,
-                                  int64_t path_begin, const vpg_records dst) {
+// Scratch slot -> its row in path order (rec_start[path] + depth), as an
+// inverse map, so the copy below writes the path-ordered records coalesced
+// and only the scratch reads are scattered (no partial-sector writes).
+__global__ void k_slot_of_row(const vpg_records src, int64_t n, const int64_t* __restrict__ rec_start,
+                              int64_t path_begin, int32_t* __restrict__ slot_of) {
   for (int64_t sidx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; sidx < n;
        sidx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t pid = src.path_idx[sidx];
-    const int64_t r = rec_start[pid - path_begin] + src.depth[sidx];
+    const int64_t pid = __ldcs(reinterpret_cast<const long long*>(src.path_idx) + sidx);
+    slot_of[rec_start[pid - path_begin] + __ldcs(src.depth + sidx)] = int32_t(sidx);
+  }
+}
+
+__global__ void k_gather_records(const vpg_records src, int64_t n,
+                                 const int32_t* __restrict__ slot_of, const vpg_records dst) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t sidx = slot_of[r];
     double* const v3d[10] = {dst.pos, dst.omega_out, dst.normal, dst.coeff, dst.phase_dir,
                              dst.emit_dir, dst.d_emit, dst.d_phase, dst.i_pt, dst.w_cont};
     const double* const v3s[10] = {src.pos, src.omega_out, src.normal, src.coeff, src.phase_dir,
                                    src.emit_dir, src.d_emit, src.d_phase, src.i_pt, src.w_cont};
 #pragma unroll
     for (int f = 0; f < 10; ++f)
-      for (int c = 0; c < 3; ++c) v3d[f][r * 3 + c] = v3s[f][sidx * 3 + c];
-    dst.g[r] = src.g[sidx];
-    dst.pdf_phase[r] = src.pdf_phase[sidx];
-    dst.pdf_emit_at_phase[r] = src.pdf_emit_at_phase[sidx];
-    dst.pdf_emit[r] = src.pdf_emit[sidx];
+      for (int c = 0; c < 3; ++c) v3d[f][r * 3 + c] = __ldcs(v3s[f] + sidx * 3 + c);
+    dst.g[r] = __ldcs(src.g + sidx);
+    dst.pdf_phase[r] = __ldcs(src.pdf_phase + sidx);
+    dst.pdf_emit_at_phase[r] = __ldcs(src.pdf_emit_at_phase + sidx);
+    dst.pdf_emit[r] = __ldcs(src.pdf_emit + sidx);
     dst.kind[r] = src.kind[sidx];
     dst.emit_delta[r] = src.emit_delta[sidx];
-    dst.class_id[r] = src.class_id[sidx];
-    dst.path_idx[r] = pid;
-    dst.depth[r] = src.depth[sidx];
+    dst.class_id[r] = __ldcs(src.class_id + sidx);
+    dst.path_idx[r] = src.path_idx[sidx];
+    dst.depth[r] = __ldcs(src.depth + sidx);
   }
 }
 
@@ -862,17 +967,18 @@ void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_reco
                    int64_t capacity, unsigned long long* counter, int64_t* counts,
                    const vpg_paths& pth, cudaStream_t s) {
   check_scene(sc);
-  VPG_REQUIRE(cfg.max_depth <= kMaxCaptureDepth, VPG_ELIMIT,
-              "single-pass capture supports max_depth <= 128 (use the count/fill passes)");
   VPG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
   VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts, scratch, pth,
-             Capture{counter, capacity});
+             Capture{counter, capacity, scratch_of<int32_t>(s, "capture_link", size_t(capacity))});
 }
 
 void scatter_records(const vpg_records& scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s) {
-  VPG_LAUNCH(k_scatter_records, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin,
-             out);
+  if (n <= 0) return;
+  VPG_REQUIRE(n < (int64_t(1) << 31), VPG_ELIMIT, "more than 2^31 records per trace");
+  int32_t* slot_of = scratch_of<int32_t>(s, "slot_of_row", size_t(n));
+  VPG_LAUNCH(k_slot_of_row, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin, slot_of);
+  VPG_LAUNCH(k_gather_records, grid_for(n, 256), 256, 0, s, scratch, n, slot_of, out);
 }
 
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,

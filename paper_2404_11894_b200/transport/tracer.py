@@ -48,7 +48,6 @@ def _struct(cls, tensors, n):
 
 
 _CAPACITY_HINT: dict = {}  # (scene id, spp, depth, seed, range) -> record count of the last trace
-MAX_CAPTURE_DEPTH = 128
 # Capture scratch, kept across calls (grow-only): re-allocating ~290 B x
 # capacity every frame costs more than the scatter itself.
 _SCRATCH: dict = {"capacity": 0, "tensors": None}
@@ -67,13 +66,13 @@ def release_scratch():
     _SCRATCH["tensors"], _SCRATCH["capacity"] = None, 0
 
 
-def trace_records_device(scene, config: RenderConfig, path_range=None):
+def trace_records_device(scene, config: RenderConfig, path_range=None, capture: bool = True):
     """Record-capturing trace; returns (records dict, paths dict, n_records) on the device.
 
-    Single pass: records land in scratch slots, then are scattered into path
-    order (rec_start = exclusive scan of the per-path counts).  Deeper paths
-    than the capture slot list (max_depth > 128) use the reference's two
-    passes (count, then re-trace and fill at the prefix-sum offsets).
+    Single pass (default): records land in scratch slots, then are gathered
+    into path order (rec_start = exclusive scan of the per-path counts).
+    capture=False runs the reference's two passes instead (count, then
+    re-trace and fill at the prefix-sum offsets; tracer.py:58-70).
     """
     torch = N.require_cuda()
     packed = pack_scene(scene)
@@ -86,7 +85,7 @@ def trace_records_device(scene, config: RenderConfig, path_range=None):
     stream = N.stream_handle()
     lib = N.lib()
     counts = torch.empty(count, dtype=torch.int64, device="cuda")
-    if int(config.max_depth) <= MAX_CAPTURE_DEPTH:
+    if capture:
         key = (id(scene), int(config.spp), int(config.max_depth), int(config.seed), begin, count)
         capacity = _CAPACITY_HINT.get(key, max(64, 6 * count))
         counter = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -112,7 +111,7 @@ def trace_records_device(scene, config: RenderConfig, path_range=None):
     paths["pixel_idx"].copy_(torch.arange(begin, begin + count, device="cuda") // int(config.spp))
     recs = _alloc(N.RECORD_FIELDS, n_rec, torch, zero=False)
     rst = _struct(N.Records, recs, n_rec)
-    if int(config.max_depth) <= MAX_CAPTURE_DEPTH:
+    if capture:
         if n_rec:
             N.check(lib.vpg_scatter_records(ctypes.byref(sst), n_rec, paths["rec_start"].data_ptr(),
                                             begin, ctypes.byref(rst), stream))

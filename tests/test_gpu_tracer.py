@@ -137,3 +137,18 @@ def test_device_trace_graph_matches_oracle_on_same_records(cuda):
     assert_rel(img, O.splat(og, ib), 1e-4, what="image")
     info = g.info()
     assert info["n_clusters"] == len(og.clusters) and info["nnz"] == og.w.nnz
+
+
+def test_two_pass_trace_equals_single_pass_capture(cuda):
+    """count + fill (the reference's two passes) and the one-pass capture give
+    the same record set, field for field."""
+    from paper_2404_11894_b200.transport.tracer import trace_records_device
+
+    scene, cfg, _ = _trace("cloud_16")
+    a, pa, na = trace_records_device(scene, cfg, capture=True)
+    b, pb, nb = trace_records_device(scene, cfg, capture=False)
+    assert na == nb
+    for k in a:
+        assert bool((a[k][:na] == b[k][:nb]).all()), k
+    for k in pa:
+        assert bool((pa[k] == pb[k]).all()), k
