@@ -170,6 +170,12 @@ typedef struct vpg_graph_info {
  * until vpg_graph_free. */
 int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng,
                     int32_t flags, void* stream, vpg_graph** out);
+/* The same, for records still being uploaded: only pos, kind and class_id
+ * must be valid when the call starts; the stream waits on `fields_ready`
+ * (a cudaEvent_t) before the build first reads any other field, so the
+ * clustering overlaps the rest of the host->device transfer. */
+int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng,
+                         int32_t flags, void* stream, void* fields_ready, vpg_graph** out);
 int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out);
 int vpg_graph_free(vpg_graph* g);
 

@@ -128,6 +128,8 @@ _SIGNATURES = {
                                    c_p, c_p, c_p, c_p]),
     "vpg_graph_build": (C.c_int, [C.POINTER(Records), c_i32, C.POINTER(Pcg64State), c_i32, c_p,
                                   C.POINTER(c_p)]),
+    "vpg_graph_build_wait": (C.c_int, [C.POINTER(Records), c_i32, C.POINTER(Pcg64State), c_i32, c_p,
+                                       c_p, C.POINTER(c_p)]),
     "vpg_graph_info_get": (C.c_int, [c_p, C.POINTER(GraphInfo)]),
     "vpg_graph_free": (C.c_int, [c_p]),
     "vpg_graph_export_clusters": (C.c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),

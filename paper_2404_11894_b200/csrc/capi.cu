@@ -306,15 +306,16 @@ int vpg_split_groups(vpg_pcg64* rng, const double* pos, int64_t n_groups, const 
   });
 }
 
-int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng, int32_t flags,
-                    void* stream, vpg_graph** out) {
+int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng,
+                         int32_t flags, void* stream, void* fields_ready, vpg_graph** out) {
   *out = nullptr;
   vpg_graph* g = new vpg_graph();
   const int rc = guarded([&] {
     g->stream = as_stream(stream);
     g->rec = *rec;
     vpg::build_graph(g, *rec, cluster_size, rng, (flags & VPG_BUILD_TIMINGS) != 0,
-                     !(flags & VPG_BUILD_CLUSTERS_ONLY), g->stream);
+                     !(flags & VPG_BUILD_CLUSTERS_ONLY), g->stream,
+                     static_cast<cudaEvent_t>(fields_ready));
     g->info.n_records = g->n;
     g->info.n_clusters = g->m;
     g->info.nnz = g->nnz;
@@ -325,6 +326,11 @@ int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng
   }
   *out = g;
   return VPG_OK;
+}
+
+int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng, int32_t flags,
+                    void* stream, vpg_graph** out) {
+  return vpg_graph_build_wait(rec, cluster_size, rng, flags, stream, nullptr, out);
 }
 
 int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out) {

@@ -878,6 +878,37 @@ void to_device(T* d, const std::vector<T>& h, cudaStream_t s) {
   count_transfer(h.size() * sizeof(T), 0);
 }
 
+// Host -> device copies that must not queue behind a bulk transfer on the
+// copy engine (the async record upload the build overlaps): the kernel reads
+// the pinned host buffer directly (UVA-mapped) instead of a memcpy.
+__global__ void k_copy_host(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                            int64_t words) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < words;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+struct HostUpload {
+  std::vector<std::unique_ptr<HostBuf<uint32_t>>> keep;  // alive until the build syncs
+  // source already pinned (HostBuf): no staging copy
+  template <class T>
+  void pinned(T* d, const T* h, size_t n, cudaStream_t s) {
+    static_assert(sizeof(T) % 4 == 0, "word-sized elements");
+    const int64_t words = int64_t(n * sizeof(T) / 4);
+    if (!words) return;
+    VPG_LAUNCH(k_copy_host, grid_for(words, 256, 1024), 256, 0, s,
+               reinterpret_cast<const uint32_t*>(h), reinterpret_cast<uint32_t*>(d), words);
+    count_transfer(n * sizeof(T), 0);
+  }
+  template <class T>
+  void put(T* d, const T* h, size_t n, cudaStream_t s) {
+    if (!n) return;
+    keep.emplace_back(new HostBuf<uint32_t>((n * sizeof(T) + 3) / 4));
+    std::memcpy(keep.back()->get(), h, n * sizeof(T));
+    pinned(d, reinterpret_cast<const T*>(keep.back()->get()), n, s);
+  }
+};
+
 int bits_for(uint64_t max_value) {
   int b = 1;
   while (b < 64 && (max_value >> b)) ++b;
@@ -969,7 +1000,7 @@ GridParams make_grid(const ClassPlan& p) {
 }  // namespace
 
 void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng_state,
-                 bool timings, bool with_ops, cudaStream_t s) {
+                 bool timings, bool with_ops, cudaStream_t s, cudaEvent_t fields_ready) {
   const int64_t n = rec.n;
   VPG_REQUIRE(K >= 1, VPG_EINVAL, "cluster size K must be >= 1");
   VPG_REQUIRE(n < (int64_t(1) << 31) - 1, VPG_ELIMIT, "more than 2^31-2 records per device");
@@ -977,6 +1008,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   g->K = K;
   for (double& t : g->info.build_ms) t = 0.0;
   StageClock clk(timings, s, g->info.build_ms);
+  HostUpload up;
   Pcg64 rng(*rng_state);
   const int block = 256;
 
@@ -1021,7 +1053,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   g->info.n_classes = n_cls;
 
   DBuf<uint32_t> d_slots(n_cls, s);
-  to_device(d_slots.get(), slots, s);
+  up.put(d_slots.get(), slots.data(), slots.size(), s);
   DBuf<unsigned long long> stats(n_cls * 7, s);
   {
     std::vector<unsigned long long> init(n_cls * 7);
@@ -1032,7 +1064,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
         init[4 * n_cls + c * 3 + a] = 0ull;
       }
     }
-    to_device(stats.get(), init, s);
+    up.put(stats.get(), init.data(), init.size(), s);
   }
   DBuf<uint8_t> cls_idx;
   if (n_cls > 1) cls_idx.alloc(n, s);
@@ -1090,7 +1122,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   {
     std::vector<int64_t> cco(n_cls + 1, 0);
     for (int c = 0; c < n_cls; ++c) cco[c] = plan[c].center_off;
-    to_device(class_center_off.get(), cco, s);
+    up.put(class_center_off.get(), cco.data(), cco.size(), s);
   }
   const int64_t max_size = 2 * int64_t(K);
   const int S = int(std::max<int64_t>(1, std::min<int64_t>(max_size, n)));
@@ -1171,9 +1203,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       unsigned long long* d_keys = scratch_of<unsigned long long>(s, "swap_keys", steps + 1);
       unsigned long long* d_sk = scratch_of<unsigned long long>(s, "swap_sorted", steps + 1);
       int32_t* d_prev = scratch_of<int32_t>(s, "swap_prev", steps + 1);
-      VPG_CUDA(cudaMemcpyAsync(d_target, targets.get(), sizeof(int32_t) * steps,
-                               cudaMemcpyHostToDevice, s));
-      count_transfer(sizeof(int32_t) * steps, 0);
+      up.pinned(d_target, targets.get(), size_t(steps), s);
       VPG_LAUNCH(k_swap_keys, grid_for(steps, block), block, 0, s, d_target, steps, d_keys);
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortKeys(t, b, d_keys, d_sk, int(steps), 0, 64, s);
@@ -1187,9 +1217,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       HostBuf<int32_t> picks32(m);
       rng_choice(rng, p.n, p.m, picks.get());
       for (int j = 0; j < m; ++j) picks32[j] = int32_t(picks[j]);
-      VPG_CUDA(cudaMemcpyAsync(d_local.get(), picks32.get(), sizeof(int32_t) * m,
-                               cudaMemcpyHostToDevice, s));
-      count_transfer(sizeof(int32_t) * m, 0);
+      up.pinned(d_local.get(), picks32.get(), size_t(m), s);
       VPG_CUDA(cudaStreamSynchronize(s));
     }
     clk.mark(1);
@@ -1365,6 +1393,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
                g->clpos.get(), g->cluster_id.get());
     if (with_ops) {
+      // the operator fields may still be in flight (async upload): the
+      // clustering above only needed pos, kind and class_id
+      if (fields_ready && c == 0) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
       pack_members(g, rec, rows_p ? rows_p + p.row_off : nullptr, p.n, p.row_off, members, s);
       aggregate_range(g, members, ranges.get() + 2 * c, m, S, s);
     }
@@ -1451,11 +1482,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     hs.alloc(split_rec.size());
     std::copy(part_b.begin(), part_b.end(), hb.get());
     std::copy(split_rec.begin(), split_rec.end(), hs.get());
-    VPG_CUDA(cudaMemcpyAsync(d_b.get(), hb.get(), sizeof(int64_t) * part_b.size(),
-                             cudaMemcpyHostToDevice, s));
-    VPG_CUDA(cudaMemcpyAsync(d_split.get(), hs.get(), sizeof(int32_t) * split_rec.size(),
-                             cudaMemcpyHostToDevice, s));
-    count_transfer(8 * part_b.size() + 4 * split_rec.size(), 0);
+    up.pinned(d_b.get(), hb.get(), part_b.size(), s);
+    up.pinned(d_split.get(), hs.get(), split_rec.size(), s);
     VPG_LAUNCH(k_layout_b, grid_for(nb, block), block, 0, s, d_b.get(), nb, acc.get(),
                cls_info.get(), ne_prefix_all.get(), class_center_off.get(), g->cl_off.get(),
                g->cl_size.get(), g->w_off.get(), a_src.get(), g->cl_center.get(), g->ref_of.get());
@@ -1491,6 +1519,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   VPG_CUDA(cudaMemcpyAsync(&h_tot[0], d_nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VPG_CUDA(cudaMemcpyAsync(&h_tot[1], g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (with_ops && fields_ready) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
   if (with_ops) finalize_operators_async(g, rec, s);
   VPG_CUDA(cudaStreamSynchronize(s));
   count_transfer(0, 20);

@@ -68,7 +68,7 @@ constexpr int kChunkFloats = 8192;
 // below, overlapped with the host split loop); `with_operators` = false for
 // cluster_points.
 void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng, bool timings,
-                 bool with_operators, cudaStream_t s);
+                 bool with_operators, cudaStream_t s, cudaEvent_t fields_ready = nullptr);
 // aggregation.cu
 size_t member_bytes();
 void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s);

@@ -34,11 +34,18 @@ class NativeGraph:
     @classmethod
     def build(cls, records: RecordSoA, cluster_size: int, rng: np.random.Generator,
               flags: int = 0) -> "NativeGraph":
-        st = records.device()
+        # the clustering needs only pos/kind/class_id: with an upload in flight
+        # the native build waits for the other fields itself, just before it
+        # first reads them
+        st = records.device(wait="early")
+        fields = records.ready_event("all")
+        if flags & N.VPG_BUILD_CLUSTERS_ONLY:
+            fields = None  # never read; later device() calls wait for them
         state = N.Pcg64State.from_generator(rng)
         out = ctypes.c_void_p()
-        N.check(N.lib().vpg_graph_build(ctypes.byref(st), int(cluster_size), ctypes.byref(state),
-                                        int(flags), N.stream_handle(), ctypes.byref(out)))
+        N.check(N.lib().vpg_graph_build_wait(
+            ctypes.byref(st), int(cluster_size), ctypes.byref(state), int(flags), N.stream_handle(),
+            fields.cuda_event if fields is not None else None, ctypes.byref(out)))
         state.store_into(rng)
         return cls(out.value, records.device_tensors(), st, records.n)
 

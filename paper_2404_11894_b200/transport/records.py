@@ -107,19 +107,63 @@ class _DualSoA:
         object.__setattr__(self, "_pinned", pinned)
         return self
 
-    def device(self, stream=None):
-        """Device tensors of every field (uploaded on first use) and the ABI struct."""
+    # fields a consumer may need before the rest (RecordSoA: the clustering's)
+    _EARLY: tuple = ()
+
+    def upload_async(self):
+        """Start the host->device copies of a pinned SoA on the copy stream:
+        the _EARLY fields first, then the rest, each group closed by an event
+        ("early", "all").  Consumers wait on the group they need (device()
+        waits on "all"), so compute that needs only the early fields overlaps
+        the rest of the transfer."""
+        if self._dev is not None:
+            return
+        torch = N.require_cuda()
+        if self._pinned is None:
+            self.device()
+            return
+        main = torch.cuda.current_stream()
+        copy = _copy_stream(torch)
+        copy.wait_stream(main)
+        dev, events = {}, {}
+        order = [f for f in self._FIELDS if f[0] in self._EARLY] + \
+                [f for f in self._FIELDS if f[0] not in self._EARLY]
+        with torch.cuda.stream(copy):
+            for k, (name, width, code) in enumerate(order):
+                t = self._pinned[name].to("cuda", non_blocking=True)
+                t.record_stream(main)  # used on the main stream: no early reuse
+                dev[name] = t
+                if k + 1 == len(self._EARLY):
+                    events["early"] = torch.cuda.Event()
+                    events["early"].record(copy)
+            events["all"] = torch.cuda.Event()
+            events["all"].record(copy)
+        object.__setattr__(self, "_dev", dev)
+        object.__setattr__(self, "_events", events)
+        object.__setattr__(self, "_struct", None)
+
+    def ready_event(self, group: str = "all"):
+        """The upload event of a field group, None when nothing is in flight."""
+        ev = self.__dict__.get("_events")
+        return ev.get(group, ev.get("all")) if ev else None
+
+    def device(self, stream=None, wait: str = "all"):
+        """Device tensors of every field (uploaded on first use) and the ABI struct.
+        The current stream waits for the field group `wait` of an async upload."""
         if self._dev is None:
             torch = N.require_cuda()
-            dev = {}
-            for name, width, code in self._FIELDS:
-                if self._pinned is not None:
-                    src = self._pinned[name]
-                else:
+            if self._pinned is not None:
+                self.upload_async()
+            else:
+                dev = {}
+                for name, width, code in self._FIELDS:
                     src = torch.from_numpy(np.ascontiguousarray(self._get(name)))
-                dev[name] = src.to("cuda", non_blocking=self._pinned is not None)
-            object.__setattr__(self, "_dev", dev)
-            object.__setattr__(self, "_struct", None)
+                    dev[name] = src.to("cuda")
+                object.__setattr__(self, "_dev", dev)
+                object.__setattr__(self, "_struct", None)
+        ev = self.ready_event(wait)
+        if ev is not None:
+            _torch().cuda.current_stream().wait_event(ev)
         if self._struct is None:
             st = self._STRUCT()
             st.n = self._n
@@ -140,6 +184,16 @@ class _DualSoA:
 
     def host_arrays(self) -> dict:
         return {name: self._get(name) for name, _, _ in self._FIELDS}
+
+
+_COPY = {}
+
+
+def _copy_stream(torch):
+    dev = torch.cuda.current_device()
+    if dev not in _COPY:
+        _COPY[dev] = torch.cuda.Stream()
+    return _COPY[dev]
 
 
 def _install_fields(cls):
@@ -168,6 +222,7 @@ class RecordSoA(_DualSoA):
 
     _FIELDS = N.RECORD_FIELDS
     _STRUCT = N.Records
+    _EARLY = ("pos", "kind", "class_id")  # all the clustering reads
 
     def __init__(self, *args, cluster_id=None, _dev=None, _n=None, **kwargs):
         host = {}
