@@ -335,14 +335,17 @@ int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_r
  * and its records go to scratch slots (capacity `capacity`) claimed through
  * the device `counter`; counts (path_count) and the path table are written as
  * in pass 1.  If *counter > capacity afterwards, records were dropped: retry
- * with capacity >= *counter (deterministic).  Then vpg_scatter_records moves
- * the n = *counter scratch records into path order, row = rec_start[path -
- * path_begin] + depth.  Any max_depth (a path's slots are linked in a scratch
- * list for the backward i_pt sweep). */
-int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* scratch,
+ * with capacity >= *counter (deterministic).  The scratch (device) holds one
+ * record per slot, VPG_SCRATCH_DOUBLES doubles each (a slot-major layout, so
+ * a path's stores land in its own slot).  vpg_scatter_records then writes the
+ * n = *counter scratch records, in path order (row = rec_start[path -
+ * path_begin] + depth), into the SoA `out`.  Any max_depth (a path's slots
+ * are linked in a scratch list for the backward i_pt sweep). */
+#define VPG_SCRATCH_DOUBLES 40
+int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, double* scratch,
                       int64_t capacity, uint64_t* counter, int64_t* counts, const vpg_paths* paths,
                       void* stream);
-int vpg_scatter_records(const vpg_records* scratch, int64_t n, const int64_t* rec_start,
+int vpg_scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                         int64_t path_begin, const vpg_records* out, void* stream);
 /* extra_direct_kernel (kernels.py:499-553). */
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,

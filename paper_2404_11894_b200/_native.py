@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libvolpg_b200.so")
 VPG_OK, VPG_EINVAL, VPG_ECUDA, VPG_EDIVERGED, VPG_ENOMEM, VPG_ELIMIT = 0, -1, -2, -3, -4, -5
 VPG_BUILD_TIMINGS = 1
 VPG_BUILD_CLUSTERS_ONLY = 2
+SCRATCH_DOUBLES = 40  # VPG_SCRATCH_DOUBLES: one capture-scratch record
 DIRECT_PT, DIRECT_EXTRA, DIRECT_AGGREGATED = 0, 1, 2
 MAX_SURF, MAX_EMIT, MAX_MED = 32, 16, 8
 
@@ -148,9 +149,9 @@ _SIGNATURES = {
                                  C.POINTER(Paths), c_p]),
     "vpg_extra_direct": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(Records), C.POINTER(Paths),
                                    c_i64, c_i32, c_p]),
-    "vpg_trace_capture": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(TraceCfg), C.POINTER(Records),
+    "vpg_trace_capture": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(TraceCfg), c_p,
                                     c_i64, c_p, c_p, C.POINTER(Paths), c_p]),
-    "vpg_scatter_records": (C.c_int, [C.POINTER(Records), c_i64, c_p, c_i64, C.POINTER(Records),
+    "vpg_scatter_records": (C.c_int, [c_p, c_i64, c_p, c_i64, C.POINTER(Records),
                                       c_p]),
     "vpg_graph_build_local": (C.c_int, [C.POINTER(Records), c_i64, c_p, c_p, c_p, c_i64, c_p, c_p,
                                         C.POINTER(c_p)]),

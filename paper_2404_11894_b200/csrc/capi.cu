@@ -474,20 +474,20 @@ int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_r
   return guarded([&] { vpg::trace_fill(*scene, *cfg, *rec, *paths, as_stream(stream)); });
 }
 
-int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_records* scratch,
+int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, double* scratch,
                       int64_t capacity, uint64_t* counter, int64_t* counts, const vpg_paths* paths,
                       void* stream) {
   return guarded([&] {
-    vpg::trace_capture(*scene, *cfg, *scratch, capacity,
+    vpg::trace_capture(*scene, *cfg, scratch, capacity,
                        reinterpret_cast<unsigned long long*>(counter), counts, *paths,
                        as_stream(stream));
   });
 }
 
-int vpg_scatter_records(const vpg_records* scratch, int64_t n, const int64_t* rec_start,
+int vpg_scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                         int64_t path_begin, const vpg_records* out, void* stream) {
   return guarded([&] {
-    vpg::scatter_records(*scratch, n, rec_start, path_begin, *out, as_stream(stream));
+    vpg::scatter_records(scratch, n, rec_start, path_begin, *out, as_stream(stream));
   });
 }
 

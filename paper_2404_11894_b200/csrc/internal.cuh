@@ -32,10 +32,10 @@ void trace_count(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t* counts,
                  const vpg_paths& pth, cudaStream_t s);
 void trace_fill(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& rec,
                 const vpg_paths& pth, cudaStream_t s);
-void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& scratch,
+void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratch,
                    int64_t capacity, unsigned long long* counter, int64_t* counts,
                    const vpg_paths& pth, cudaStream_t s);
-void scatter_records(const vpg_records& scratch, int64_t n, const int64_t* rec_start,
+void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
                   int n_extra, cudaStream_t s);

@@ -472,6 +472,65 @@ struct Capture {
   unsigned long long* counter;
   int64_t capacity;
   int32_t* link;  // per slot: slot of the same path's previous record, -1 for its first
+  double* aos;    // capacity x kScratchDoubles: one record per slot (see RecView)
+};
+
+// Record fields.  The capture scratch holds one record per slot, structure
+// of arrays would scatter every field store of a path; a slot is
+// kScratchDoubles doubles (10 sectors): the doubles at these offsets, then
+// path_idx (int64 bits), {class_id, depth} (2 x int32), {kind, emit_delta}.
+enum : int {
+  kFPos = 0, kFOmega = 3, kFNormal = 6, kFCoeff = 9, kFPhaseDir = 12, kFEmitDir = 15,
+  kFDEmit = 18, kFDPhase = 21, kFIpt = 24, kFWcont = 27, kFG = 30, kFPdfPhase = 31,
+  kFPdfEap = 32, kFPdfEmit = 33, kFPath = 34, kFClassDepth = 35, kFKind = 36
+};
+
+template <int kMode>
+struct RecView {
+  const vpg_records& soa;
+  double* aos;
+  // address of field `fld` (component 0) of record `row`
+  __device__ __forceinline__ double* f(int fld, int64_t row) const {
+    if (kMode == kCapture) return aos + row * VPG_SCRATCH_DOUBLES + fld;
+    switch (fld) {
+      case kFPos: return soa.pos + row * 3;
+      case kFOmega: return soa.omega_out + row * 3;
+      case kFNormal: return soa.normal + row * 3;
+      case kFCoeff: return soa.coeff + row * 3;
+      case kFPhaseDir: return soa.phase_dir + row * 3;
+      case kFEmitDir: return soa.emit_dir + row * 3;
+      case kFDEmit: return soa.d_emit + row * 3;
+      case kFDPhase: return soa.d_phase + row * 3;
+      case kFIpt: return soa.i_pt + row * 3;
+      case kFWcont: return soa.w_cont + row * 3;
+      case kFG: return soa.g + row;
+      case kFPdfPhase: return soa.pdf_phase + row;
+      case kFPdfEap: return soa.pdf_emit_at_phase + row;
+      default: return soa.pdf_emit + row;
+    }
+  }
+  __device__ __forceinline__ void put3(int fld, int64_t row, double x, double y, double z) const {
+    double* p = f(fld, row);
+    p[0] = x;
+    p[1] = y;
+    p[2] = z;
+  }
+  __device__ __forceinline__ void put1(int fld, int64_t row, double v) const { *f(fld, row) = v; }
+  __device__ __forceinline__ void put_ints(int64_t row, int64_t path, int32_t cls, int32_t depth,
+                                           uint8_t kind, uint8_t delta) const {
+    if (kMode == kCapture) {
+      double* p = aos + row * VPG_SCRATCH_DOUBLES;
+      reinterpret_cast<long long*>(p)[kFPath] = path;
+      reinterpret_cast<int2*>(p + kFClassDepth)[0] = make_int2(cls, depth);
+      reinterpret_cast<uchar2*>(p + kFKind)[0] = make_uchar2(kind, delta);
+    } else {
+      soa.path_idx[row] = path;
+      soa.class_id[row] = cls;
+      soa.depth[row] = depth;
+      soa.kind[row] = kind;
+      soa.emit_delta[row] = delta;
+    }
+  }
 };
 
 __device__ __forceinline__ int64_t claim_slot(const Capture& cap) {
@@ -562,12 +621,13 @@ __device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg
   const int max_depth = cfg.max_depth;
   const int64_t path_id = st.path_id;
   const int64_t rec_offset = st.rec_offset;
+  const RecView<kMode> rv{rec, cap.aos};
   int sid;
   const double t_hit = intersect(sc, o, d, kTEps, kNoHit, sid);
   const double pe_at_dir = emitter_dir_pdf_from_hit(sc, sid, t_hit, d);
   if (kStore && !from_camera) {
     const int64_t prow = st.last();
-    if (prow >= 0) rec.pdf_emit_at_phase[prow] = pe_at_dir;
+    if (prow >= 0) rv.put1(kFPdfEap, prow, pe_at_dir);
   }
   const MediaFlight mf = media_flight(sc, o, d, 0.0, t_hit, rng);
   V3 v{o.x + mf.t * d.x, o.y + mf.t * d.y, o.z + mf.t * d.z};
@@ -620,8 +680,9 @@ __device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg
           if (kStore) {
             const int64_t row = st.last();
             if (row >= 0) {
-              put3(rec.d_phase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
-              for (int c = 0; c < 3; ++c) rec.i_pt[row * 3 + c] += cc[c];  // staged D-bar
+              rv.put3(kFDPhase, row, mf.w[0] * ev[0], mf.w[1] * ev[1], mf.w[2] * ev[2]);
+              double* ip = rv.f(kFIpt, row);
+              for (int c = 0; c < 3; ++c) ip[c] += cc[c];  // staged D-bar
             }
           }
         }
@@ -693,25 +754,22 @@ __device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg
     st.last_row = row;
   }
   if (kStore && row >= 0) {
-    put3(rec.pos, row, v.x, v.y, v.z);
-    put3(rec.omega_out, row, -ax.x, -ax.y, -ax.z);
-    put3(rec.normal, row, nrm.x, nrm.y, nrm.z);
-    put3(rec.coeff, row, k[0], k[1], k[2]);
-    put1(rec.g, row, gpar);
-    put3(rec.phase_dir, row, wp.x, wp.y, wp.z);
-    put1(rec.pdf_phase, row, pdf_p);
-    put1(rec.pdf_emit_at_phase, row, 0.0);
-    put3(rec.emit_dir, row, es.w.x, es.w.y, es.w.z);
-    put1(rec.pdf_emit, row, es.pdf);
-    put3(rec.d_emit, row, es.rad[0], es.rad[1], es.rad[2]);
-    put3(rec.d_phase, row, 0.0, 0.0, 0.0);
-    put3(rec.i_pt, row, cn[0], cn[1], cn[2]);  // staged D-bar, replaced by the sweep
-    put3(rec.w_cont, row, wc[0], wc[1], wc[2]);
-    put1(reinterpret_cast<unsigned char*>(rec.kind), row, (unsigned char)(volume ? 0 : 1));
-    put1(reinterpret_cast<unsigned char*>(rec.emit_delta), row, (unsigned char)(es.delta ? 1 : 0));
-    put1(rec.class_id, row, int32_t(class_id));
-    put1(reinterpret_cast<long long*>(rec.path_idx), row, (long long)path_id);
-    put1(rec.depth, row, int32_t(n_rec));
+    rv.put3(kFPos, row, v.x, v.y, v.z);
+    rv.put3(kFOmega, row, -ax.x, -ax.y, -ax.z);
+    rv.put3(kFNormal, row, nrm.x, nrm.y, nrm.z);
+    rv.put3(kFCoeff, row, k[0], k[1], k[2]);
+    rv.put1(kFG, row, gpar);
+    rv.put3(kFPhaseDir, row, wp.x, wp.y, wp.z);
+    rv.put1(kFPdfPhase, row, pdf_p);
+    rv.put1(kFPdfEap, row, 0.0);
+    rv.put3(kFEmitDir, row, es.w.x, es.w.y, es.w.z);
+    rv.put1(kFPdfEmit, row, es.pdf);
+    rv.put3(kFDEmit, row, es.rad[0], es.rad[1], es.rad[2]);
+    rv.put3(kFDPhase, row, 0.0, 0.0, 0.0);
+    rv.put3(kFIpt, row, cn[0], cn[1], cn[2]);  // staged D-bar, replaced by the sweep
+    rv.put3(kFWcont, row, wc[0], wc[1], wc[2]);
+    rv.put_ints(row, path_id, int32_t(class_id), int32_t(n_rec), uint8_t(volume ? 0 : 1),
+                uint8_t(es.delta ? 1 : 0));
   }
   ++n_rec;
   if (pdf_p <= 0.0) return false;  // degenerate sample, no continuation
@@ -745,6 +803,7 @@ __device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, con
   constexpr bool kStore = kMode == kFill || kMode == kCapture;
   const int n_rec = st.n_rec;
   const int64_t slot = st.slot;
+  const RecView<kMode> rv{rec, cap.aos};
   const double* est = st.est;
   const double* dcam = st.dcam;
   const double* camw = st.camw;
@@ -757,13 +816,16 @@ __device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, con
       if (kMode != kCapture) row = st.rec_offset + kk;
       else if (kk < n_rec - 1) row = cap.link[row];
       if (row < 0) break;  // overflowed capture: the host retries with room
-      const double pp = rec.pdf_phase[row];
+      const double pp = *rv.f(kFPdfPhase, row);
+      double* ip = rv.f(kFIpt, row);
+      const double* kcp = rv.f(kFCoeff, row);
+      const double* wcp = rv.f(kFWcont, row);
       for (int c = 0; c < 3; ++c) {
-        const double dbar = rec.i_pt[row * 3 + c];
-        rec.i_pt[row * 3 + c] = in[c];
-        const double kc = rec.coeff[row * 3 + c];
+        const double dbar = ip[c];
+        ip[c] = in[c];
+        const double kc = kcp[c];
         const double fpp = pp > 0.0 ? kc * pp / pp : 0.0;
-        in[c] = rec.w_cont[row * 3 + c] * (dbar + fpp * in[c]);
+        in[c] = wcp[c] * (dbar + fpp * in[c]);
       }
     }
   }
@@ -784,7 +846,7 @@ template <int kMode>
 __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
                                 int64_t py, int64_t path_id, int64_t rec_offset,
                                 const vpg_records& rec, const vpg_paths& pth, int64_t slot,
-                                const Capture& cap = Capture{nullptr, 0, nullptr}) {
+                                const Capture& cap = Capture{nullptr, 0, nullptr, nullptr}) {
   PathState<kMode> st;
   path_begin(st, sc, cfg, px, py, path_id, rec_offset, slot);
   while (path_bounce(st, sc, cfg, rec, cap)) {
@@ -843,38 +905,61 @@ __global__ void __launch_bounds__(128, 4) k_trace_capture(const vpg_scene sc, co
 }
 
 // Scratch slot -> its row in path order (rec_start[path] + depth), as an
-// inverse map, so the copy below writes the path-ordered records coalesced
-// and only the scratch reads are scattered (no partial-sector writes).
-__global__ void k_slot_of_row(const vpg_records src, int64_t n, const int64_t* __restrict__ rec_start,
-                              int64_t path_begin, int32_t* __restrict__ slot_of) {
+// inverse map, so the copy below writes the path-ordered records coalesced.
+__global__ void k_slot_of_row(const double* __restrict__ aos, int64_t n,
+                              const int64_t* __restrict__ rec_start, int64_t path_begin,
+                              int32_t* __restrict__ slot_of) {
   for (int64_t sidx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; sidx < n;
        sidx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t pid = __ldcs(reinterpret_cast<const long long*>(src.path_idx) + sidx);
-    slot_of[rec_start[pid - path_begin] + __ldcs(src.depth + sidx)] = int32_t(sidx);
+    const double* p = aos + sidx * VPG_SCRATCH_DOUBLES;
+    const long long pid = reinterpret_cast<const long long*>(p)[kFPath];
+    const int depth = reinterpret_cast<const int2*>(p + kFClassDepth)->y;
+    slot_of[rec_start[pid - path_begin] + depth] = int32_t(sidx);
   }
 }
 
-__global__ void k_gather_records(const vpg_records src, int64_t n,
-                                 const int32_t* __restrict__ slot_of, const vpg_records dst) {
-  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
-       r += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t sidx = slot_of[r];
-    double* const v3d[10] = {dst.pos, dst.omega_out, dst.normal, dst.coeff, dst.phase_dir,
-                             dst.emit_dir, dst.d_emit, dst.d_phase, dst.i_pt, dst.w_cont};
-    const double* const v3s[10] = {src.pos, src.omega_out, src.normal, src.coeff, src.phase_dir,
-                                   src.emit_dir, src.d_emit, src.d_phase, src.i_pt, src.w_cont};
+// Path-ordered SoA records from the slot-major scratch: a warp stages 32
+// records (10 full sectors each) in shared memory, then writes every field
+// of its 32 consecutive rows coalesced (lane = row).
+constexpr int kGatherWarps = 4;
+constexpr int kSlotStride = VPG_SCRATCH_DOUBLES + 1;  // odd stride: conflict-free row reads
+__global__ void __launch_bounds__(kGatherWarps * 32)
+k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __restrict__ slot_of,
+                 const vpg_records dst) {
+  __shared__ double buf[kGatherWarps][32 * kSlotStride];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* b = buf[wid];
+  const int64_t step = int64_t(gridDim.x) * kGatherWarps * 32;
+  for (int64_t base = (int64_t(blockIdx.x) * kGatherWarps + wid) * 32; base < n; base += step) {
+    const int cnt = int(n - base < 32 ? n - base : 32);
+    for (int idx = lane; idx < cnt * VPG_SCRATCH_DOUBLES; idx += 32) {
+      const int j = idx / VPG_SCRATCH_DOUBLES, w = idx - j * VPG_SCRATCH_DOUBLES;
+      b[j * kSlotStride + w] = __ldcs(aos + int64_t(slot_of[base + j]) * VPG_SCRATCH_DOUBLES + w);
+    }
+    __syncwarp();
+    if (lane < cnt) {
+      const int64_t r = base + lane;
+      const double* q = b + lane * kSlotStride;
+      double* const v3[10] = {dst.pos, dst.omega_out, dst.normal, dst.coeff, dst.phase_dir,
+                              dst.emit_dir, dst.d_emit, dst.d_phase, dst.i_pt, dst.w_cont};
+      const int off[10] = {kFPos, kFOmega, kFNormal, kFCoeff, kFPhaseDir,
+                           kFEmitDir, kFDEmit, kFDPhase, kFIpt, kFWcont};
 #pragma unroll
-    for (int f = 0; f < 10; ++f)
-      for (int c = 0; c < 3; ++c) v3d[f][r * 3 + c] = __ldcs(v3s[f] + sidx * 3 + c);
-    dst.g[r] = __ldcs(src.g + sidx);
-    dst.pdf_phase[r] = __ldcs(src.pdf_phase + sidx);
-    dst.pdf_emit_at_phase[r] = __ldcs(src.pdf_emit_at_phase + sidx);
-    dst.pdf_emit[r] = __ldcs(src.pdf_emit + sidx);
-    dst.kind[r] = src.kind[sidx];
-    dst.emit_delta[r] = src.emit_delta[sidx];
-    dst.class_id[r] = __ldcs(src.class_id + sidx);
-    dst.path_idx[r] = src.path_idx[sidx];
-    dst.depth[r] = __ldcs(src.depth + sidx);
+      for (int f = 0; f < 10; ++f)
+        for (int c = 0; c < 3; ++c) v3[f][r * 3 + c] = q[off[f] + c];
+      dst.g[r] = q[kFG];
+      dst.pdf_phase[r] = q[kFPdfPhase];
+      dst.pdf_emit_at_phase[r] = q[kFPdfEap];
+      dst.pdf_emit[r] = q[kFPdfEmit];
+      dst.path_idx[r] = __double_as_longlong(q[kFPath]);
+      const long long cd = __double_as_longlong(q[kFClassDepth]);
+      dst.class_id[r] = int32_t(cd & 0xFFFFFFFFll);
+      dst.depth[r] = int32_t(cd >> 32);
+      const long long kd = __double_as_longlong(q[kFKind]);
+      dst.kind[r] = uint8_t(kd & 0xFF);
+      dst.emit_delta[r] = uint8_t((kd >> 8) & 0xFF);
+    }
+    __syncwarp();
   }
 }
 
@@ -963,22 +1048,27 @@ void trace_fill(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records
              pth);
 }
 
-void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, const vpg_records& scratch,
+void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratch,
                    int64_t capacity, unsigned long long* counter, int64_t* counts,
                    const vpg_paths& pth, cudaStream_t s) {
   check_scene(sc);
+  VPG_REQUIRE(capacity >= 0 && capacity < (int64_t(1) << 31), VPG_ELIMIT,
+              "capture scratch capacity must be below 2^31 slots");
   VPG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
-  VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts, scratch, pth,
-             Capture{counter, capacity, scratch_of<int32_t>(s, "capture_link", size_t(capacity))});
+  int32_t* link = scratch_of<int32_t>(s, "capture_link", size_t(capacity) + 1);
+  VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts,
+             vpg_records{}, pth, Capture{counter, capacity, link, scratch});
 }
 
-void scatter_records(const vpg_records& scratch, int64_t n, const int64_t* rec_start,
+void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s) {
   if (n <= 0) return;
   VPG_REQUIRE(n < (int64_t(1) << 31), VPG_ELIMIT, "more than 2^31 records per trace");
   int32_t* slot_of = scratch_of<int32_t>(s, "slot_of_row", size_t(n));
-  VPG_LAUNCH(k_slot_of_row, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin, slot_of);
-  VPG_LAUNCH(k_gather_records, grid_for(n, 256), 256, 0, s, scratch, n, slot_of, out);
+  VPG_LAUNCH(k_slot_of_row, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin,
+             slot_of);
+  VPG_LAUNCH(k_gather_records, int((n + 127) / 128 < sm_count() * 8 ? (n + 127) / 128 : sm_count() * 8),
+             kGatherWarps * 32, 0, s, scratch, n, slot_of, out);
 }
 
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,

@@ -54,9 +54,11 @@ _SCRATCH: dict = {"capacity": 0, "tensors": None}
 
 
 def _scratch(capacity, torch):
+    """Slot-major capture scratch: capacity x SCRATCH_DOUBLES float64."""
     if _SCRATCH["capacity"] < capacity or _SCRATCH["tensors"] is None:
         _SCRATCH["tensors"] = None
-        _SCRATCH["tensors"] = _alloc(N.RECORD_FIELDS, capacity, torch, zero=False)
+        _SCRATCH["tensors"] = torch.empty((max(capacity, 1), N.SCRATCH_DOUBLES),
+                                          dtype=torch.float64, device="cuda")
         _SCRATCH["capacity"] = capacity
     return _SCRATCH["tensors"], _SCRATCH["capacity"]
 
@@ -91,8 +93,7 @@ def trace_records_device(scene, config: RenderConfig, path_range=None, capture: 
         counter = torch.zeros(1, dtype=torch.int64, device="cuda")
         while True:
             scratch, capacity = _scratch(capacity, torch)
-            sst = _struct(N.Records, scratch, capacity)
-            N.check(lib.vpg_trace_capture(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(sst),
+            N.check(lib.vpg_trace_capture(ctypes.byref(sc), ctypes.byref(cfg), scratch.data_ptr(),
                                           capacity, counter.data_ptr(), counts.data_ptr(),
                                           ctypes.byref(pst), stream))
             n_rec = int(counter.item())
@@ -113,7 +114,7 @@ def trace_records_device(scene, config: RenderConfig, path_range=None, capture: 
     rst = _struct(N.Records, recs, n_rec)
     if capture:
         if n_rec:
-            N.check(lib.vpg_scatter_records(ctypes.byref(sst), n_rec, paths["rec_start"].data_ptr(),
+            N.check(lib.vpg_scatter_records(scratch.data_ptr(), n_rec, paths["rec_start"].data_ptr(),
                                             begin, ctypes.byref(rst), stream))
     else:
         N.check(lib.vpg_trace_fill(ctypes.byref(sc), ctypes.byref(cfg), ctypes.byref(rst),
