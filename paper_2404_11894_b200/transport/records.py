@@ -376,12 +376,16 @@ def load_records(path, pin: bool = False) -> TraceOutput:
         version, n_rec, n_path, width, height, spp = struct.unpack("<IQQIII", f.read(32))
         if version != VPGR_VERSION:
             raise IOError(f"{path}: unsupported VPGR version {version}")
-        rec = np.frombuffer(f.read(RECORD_DTYPE.itemsize * n_rec), dtype=RECORD_DTYPE)
-        if rec.size != n_rec:
+        # a short block is a truncated dump (IOError, as the reference raises
+        # for a block cut at a record boundary) wherever the cut falls
+        raw = f.read(RECORD_DTYPE.itemsize * n_rec)
+        if len(raw) != RECORD_DTYPE.itemsize * n_rec:
             raise IOError(f"{path}: truncated record block")
-        pth = np.frombuffer(f.read(PATH_DTYPE.itemsize * n_path), dtype=PATH_DTYPE)
-        if pth.size != n_path:
+        rec = np.frombuffer(raw, dtype=RECORD_DTYPE)
+        raw = f.read(PATH_DTYPE.itemsize * n_path)
+        if len(raw) != PATH_DTYPE.itemsize * n_path:
             raise IOError(f"{path}: truncated path block")
+        pth = np.frombuffer(raw, dtype=PATH_DTYPE)
     records = RecordSoA(**{name: np.ascontiguousarray(rec[name]) for name, _, _ in N.RECORD_FIELDS})
     paths = PathSoA(**{name: np.ascontiguousarray(pth[name]) for name, _, _ in N.PATH_FIELDS})
     if pin:

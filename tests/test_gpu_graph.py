@@ -179,3 +179,18 @@ def test_cluster_points_edge_cases_match_oracle(cuda, seed):
         assert [c.center for c in cl] == [c.center for c in cl_ref]
         assert r_gpu.bit_generator.state == r_ref.bit_generator.state
         assert max(len(c.members) for c in cl) <= 2 * K
+
+
+def test_k1_pipeline_reproduces_path_tracing(cuda):
+    """K = 1 (every record its own cluster): the fixed point equals the PT
+    estimate (SPEC K=1 identity; reference: 5e-16 in fp64) -- here within the
+    fp32 iteration's 1e-4."""
+    from paper_2404_11894_b200 import scenes as S
+    from paper_2404_11894_b200.harness.config import RenderConfig
+    from paper_2404_11894_b200.pathgraph import render_pg
+
+    cfg = RenderConfig(mode="pg", spp=2, max_depth=12, seed=5, cluster_size=1, iterations=13,
+                       tol=0.0)
+    pg = render_pg(S.scene_c1((12, 12), floor=True), cfg)
+    err = np.abs(pg.image - pg.pt_image)
+    assert float(err.max()) <= 1e-4 * float(np.abs(pg.pt_image).max())
