@@ -128,9 +128,13 @@ __device__ __forceinline__ double strategy_pdf(const double* __restrict__ geo, i
   const double cs = dot3(geo[l], geo[S + l], geo[2 * S + l], dx, dy, dz);
   if (!volume) return cs > 0.0 ? __dmul_rn(cs, kInvPi) : 0.0;
   const double den = __dsub_rn(geo[10 * S + l], __dmul_rn(geo[11 * S + l], cs));
-  // num / (den * sqrt(den)) as num * rsqrt(den)^3: within ~2 ulp of the
-  // reference's sqrt-and-divide, at a fraction of the fp64 issue cost
-  const double rs = rsqrt(den);
+  // num / (den * sqrt(den)) as num * rsqrt(den)^3, rsqrt from the fp32
+  // MUFU estimate (rel. error < 2.4e-7) and one fp64 Newton step (rel.
+  // error < 1e-13): den itself -- where the cancellation at g -> 1 lives --
+  // stays fp64.  Far inside the 1e-4 radiance bar, at a fraction of the
+  // fp64 rsqrt's issue cost.
+  const double r0 = double(rsqrtf(float(den)));
+  const double rs = r0 * (1.5 - 0.5 * den * r0 * r0);
   return geo[9 * S + l] * (rs * rs * rs);
 }
 

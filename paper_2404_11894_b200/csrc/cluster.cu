@@ -465,23 +465,66 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
       }
       __syncwarp();
     } else {
-      // crowded neighbourhood: every lane scans the 27 cells itself
-      for (int t = lane; t < len; t += 32) {
-        const int32_t i = sorted_ids[b + t];
-        const int64_t r = class_row(rows, row_off, i);
-        const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
+      // crowded neighbourhood (dense regions): 32 points at a time scan the
+      // candidate list in shared-memory chunks staged by the whole warp --
+      // candidate idx belongs to neighbour cell k = #lanes whose inclusive
+      // count is <= idx.  The lexicographic (d2, center) minimum does not
+      // depend on the chunking.
+      for (int pb = 0; pb < len; pb += 32) {
+        const int t = pb + lane;
+        const bool active = t < len;
+        int32_t i = 0;
+        double px = 0.0, py = 0.0, pz = 0.0;
+        if (active) {
+          i = sorted_ids[b + t];
+          const int64_t r = class_row(rows, row_off, i);
+          px = pos[r * 3];
+          py = pos[r * 3 + 1];
+          pz = pos[r * 3 + 2];
+        }
         Best best{INFINITY, 0x7FFFFFFF};
-        for (int dx = -1; dx <= 1; ++dx)
-          for (int dy = -1; dy <= 1; ++dy)
-            for (int dz = -1; dz <= 1; ++dz)
-              scan_cell(gp, table, spos, cx + dx, cy + dy, cz + dz, px, py, pz, best);
-        if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
-          fb_list[atomicAdd(fb_count, 1)] = i;
-          assign[i] = -1;
-        } else {
-          assign[i] = best.j;
+        for (int base = 0; base < total; base += kCandCap) {
+          const int cnt = total - base < kCandCap ? total - base : kCandCap;
+          __syncwarp();
+          for (int rd = 0; rd < cnt; rd += 32) {
+            const int idx = base + rd + lane;
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+              const int v = __shfl_sync(0xFFFFFFFFu, incl, k + step - 1);
+              if (v <= idx) k += step;
+            }
+            const int k_start = __shfl_sync(0xFFFFFFFFu, c_start, k);
+            const int k_first = __shfl_sync(0xFFFFFFFFu, incl - c_cnt, k);
+            if (rd + lane < cnt) {
+              const double4 c = spos[k_start + (idx - k_first)];
+              const bool keep = gp.packed ||
+                                (cell_coord(c.x, gp.lo[0], gp.cell) == cx + k / 9 - 1 &&
+                                 cell_coord(c.y, gp.lo[1], gp.cell) == cy + (k / 3) % 3 - 1 &&
+                                 cell_coord(c.z, gp.lo[2], gp.cell) == cz + k % 3 - 1);
+              cand[wid][rd + lane] = keep ? c : make_double4(INFINITY, INFINITY, INFINITY,
+                                                             __longlong_as_double(0x7FFFFFFFLL));
+            }
+          }
+          __syncwarp();
+          if (active)
+            for (int q = 0; q < cnt; ++q) {
+              const double4 c = cand[wid][q];
+              const int j = int(__double_as_longlong(c.w));
+              if (j == 0x7FFFFFFF) continue;
+              best_update(best, dist2_exact(px, py, pz, c.x, c.y, c.z), j);
+            }
+        }
+        if (active) {
+          if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
+            fb_list[atomicAdd(fb_count, 1)] = i;
+            assign[i] = -1;
+          } else {
+            assign[i] = best.j;
+          }
         }
       }
+      __syncwarp();
     }
   }
 }
