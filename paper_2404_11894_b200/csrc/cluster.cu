@@ -1188,8 +1188,17 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     members = scratch(s, "members", member_bytes() * size_t(n) + 256);
   }
 
-  std::vector<int32_t> split_rec;    // members of every split group, back to back
-  std::vector<int64_t> part_b;       // 8 int64 per split group, see k_layout_b
+  // per class: the split groups' members back to back, and 8 int64 per split
+  // group (see k_layout_b) -- kept in the pinned buffers they were produced
+  // in, so part B reads them from the device without host-side concatenation
+  struct SplitChunk {
+    std::unique_ptr<HostBuf<int32_t>> rec;
+    int64_t n_rec;
+    std::unique_ptr<HostBuf<int64_t>> b;
+    int64_t n_b;
+  };
+  std::vector<SplitChunk> chunks;
+  int64_t split_total = 0, nb_total = 0;
   int64_t rows_b = 0, w_b = 0, appended_before = 0;
   int64_t n_splits = 0;
   HostBuf<int64_t> h_acc(8);
@@ -1408,7 +1417,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     const int64_t staged = n_over > 0 ? h_scalars[3] : 0;
     // oversize members and positions to the host, queued ahead of part A
     HostBuf<int64_t> info(size_t(n_over) * 4 + 4);
-    HostBuf<int32_t> h_srec(size_t(staged) + 1), h_slot(size_t(n_over) + 1);
+    auto h_srec_own = std::make_unique<HostBuf<int32_t>>(size_t(staged) + 1);
+    HostBuf<int32_t>& h_srec = *h_srec_own;
+    HostBuf<int32_t> h_slot(size_t(n_over) + 1);
     HostBuf<double> h_xyzd(size_t(staged) * 4 + 4);  // x | y | z | d0
     cudaEvent_t staged_ready;
     VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
@@ -1468,17 +1479,22 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
           rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
           groups, cslot, max_size, &g->info.split_visits);
       dbg.mark("split: loop", false);
-      const int64_t base_split = int64_t(split_rec.size());
-      split_rec.insert(split_rec.end(), h_srec.get(), h_srec.get() + staged);
+      const int64_t base_split = split_total;
+      auto hb_own = std::make_unique<HostBuf<int64_t>>(groups.size() * 8 + 8);
+      int64_t* hb = hb_own->get();
       for (size_t k = 0; k < groups.size(); ++k) {
         const int64_t sz = groups[k].size;
         const int64_t j = k < size_t(n_over) ? info[k * 4] : -1 - (int64_t(k) - n_over);
         const int64_t e[8] = {c, j, sz, rows_b, w_b, base_split + groups[k].begin,
                               groups[k].center, 0};
-        part_b.insert(part_b.end(), e, e + 8);
+        std::memcpy(hb + 8 * k, e, sizeof(e));
         rows_b += sz;
         w_b += (sz * sz + 3) & ~int64_t(3);
       }
+      chunks.push_back(SplitChunk{std::move(h_srec_own), staged, std::move(hb_own),
+                                  int64_t(groups.size())});
+      split_total += staged;
+      nb_total += int64_t(groups.size());
       appended_c = int64_t(groups.size()) - n_over;
       dbg.mark("split: mods", false);
     }
@@ -1492,7 +1508,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   VPG_CUDA(cudaEventSynchronize(acc_ready));
   cudaEventDestroy(acc_ready);
   const int64_t m_a = h_acc[0];
-  const int64_t nb = int64_t(part_b.size()) / 8;
+  const int64_t nb = nb_total;
   const int64_t M = m_a + nb;
   g->m = M;
   {
@@ -1515,18 +1531,17 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     g->w_off = std::move(f_w);
     a_src = std::move(f_src);
   }
-  HostBuf<int64_t> hb;
-  HostBuf<int32_t> hs;
-  DBuf<int64_t> d_b(part_b.size() + 8, s);
-  DBuf<int32_t> d_split(split_rec.size() + 1, s);
+  DBuf<int64_t> d_b(size_t(nb) * 8 + 8, s);
+  DBuf<int32_t> d_split(size_t(split_total) + 1, s);
   DBuf<int64_t> range_b(2, s);
   if (nb) {
-    hb.alloc(part_b.size());
-    hs.alloc(split_rec.size());
-    std::copy(part_b.begin(), part_b.end(), hb.get());
-    std::copy(split_rec.begin(), split_rec.end(), hs.get());
-    up.pinned(d_b.get(), hb.get(), part_b.size(), s);
-    up.pinned(d_split.get(), hs.get(), split_rec.size(), s);
+    int64_t ob = 0, os = 0;
+    for (const SplitChunk& ch : chunks) {
+      up.pinned(d_b.get() + ob, ch.b->get(), size_t(ch.n_b) * 8, s);
+      up.pinned(d_split.get() + os, ch.rec->get(), size_t(ch.n_rec), s);
+      ob += ch.n_b * 8;
+      os += ch.n_rec;
+    }
     VPG_LAUNCH(k_layout_b, grid_for(nb, block), block, 0, s, d_b.get(), nb, acc.get(),
                cls_info.get(), ne_prefix_all.get(), class_center_off.get(), g->cl_off.get(),
                g->cl_size.get(), g->w_off.get(), a_src.get(), g->cl_center.get(), g->ref_of.get());
@@ -1538,7 +1553,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, d_split.get(),
                g->perm.get(), g->clpos.get(), g->cluster_id.get());
     if (with_ops) {
-      pack_members(g, rec, d_split.get(), int64_t(split_rec.size()), 0, members, s);
+      pack_members(g, rec, d_split.get(), split_total, 0, members, s);
       aggregate_range(g, members, range_b.get(), nb, S, s);
     }
   }
