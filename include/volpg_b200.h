@@ -62,6 +62,9 @@ int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* to
  * 0 vpg_pcg64, 1 vpg_records, 2 vpg_paths, 3 vpg_graph_info, 4 vpg_scene, 5 vpg_trace_cfg,
  * 6 vpg_graph_views */
 size_t vpg_struct_size(int32_t which);
+/* Every profiled launch in order: start (ms after the first) and duration. */
+int vpg_profile_timeline(char* names, int64_t names_cap, double* start_ms, double* dur_ms,
+                         int64_t cap, int64_t* n_launches);
 
 /* ------------------------------------------------- numpy Generator replica
  * Bit-exact replica of numpy.random.Generator(PCG64) for the two calls the

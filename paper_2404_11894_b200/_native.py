@@ -123,6 +123,7 @@ _SIGNATURES = {
     "vpg_profile_enable": (None, [c_i32]),
     "vpg_profile_reset": (C.c_int, []),
     "vpg_profile_read": (C.c_int, [C.c_char_p, c_i64, c_p, c_p, c_i64, C.POINTER(c_i64)]),
+    "vpg_profile_timeline": (C.c_int, [C.c_char_p, c_i64, c_p, c_p, c_i64, C.POINTER(c_i64)]),
     "vpg_rng_choice": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,
@@ -212,6 +213,19 @@ def check(rc: int) -> None:
 
         raise SolveDivergence(msg)
     raise NativeError(msg)
+
+
+def profile_timeline():
+    """[(name, start_ms, dur_ms)] of every profiled launch, in launch order."""
+    cap = 1 << 16
+    names = C.create_string_buffer(cap * 48)
+    st = np.zeros(cap)
+    du = np.zeros(cap)
+    n = c_i64()
+    check(lib().vpg_profile_timeline(names, len(names), st.ctypes.data, du.ctypes.data, cap,
+                                     C.byref(n)))
+    keys = names.value.decode().split("\n")
+    return [(keys[i], float(st[i]), float(du[i])) for i in range(min(n.value, cap))]
 
 
 def launch_count() -> int:

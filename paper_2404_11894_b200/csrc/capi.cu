@@ -205,6 +205,31 @@ int vpg_profile_reset(void) {
   });
 }
 
+int vpg_profile_timeline(char* names, int64_t names_cap, double* start_ms, double* dur_ms,
+                         int64_t cap, int64_t* n_launches) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(vpg::g_prof_mu);
+    std::string joined;
+    int64_t k = 0;
+    for (auto& e : vpg::g_prof) {
+      VPG_CUDA(cudaEventSynchronize(e.stop));
+      float t0 = 0.f, d = 0.f;
+      VPG_CUDA(cudaEventElapsedTime(&t0, vpg::g_prof.front().start, e.start));
+      VPG_CUDA(cudaEventElapsedTime(&d, e.start, e.stop));
+      if (k < cap) {
+        start_ms[k] = t0;
+        dur_ms[k] = d;
+        joined += e.name;
+        joined += '\n';
+      }
+      ++k;
+    }
+    *n_launches = k;
+    VPG_REQUIRE(int64_t(joined.size()) < names_cap, VPG_ELIMIT, "profile name buffer too small");
+    memcpy(names, joined.c_str(), joined.size() + 1);
+  });
+}
+
 int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* total_ms,
                      int64_t cap, int64_t* n_kernels) {
   return guarded([&] {
