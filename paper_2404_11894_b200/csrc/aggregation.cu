@@ -29,6 +29,8 @@ namespace {
 constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 constexpr double kInvPi = 1.0 / 3.14159265358979323846;
 constexpr int kAggThreads = 128;
+// dynamic shared memory of k_aggregate for the largest supported cluster (2K = 160)
+constexpr size_t kAggSmemMax = 226 * 1024;
 
 struct __align__(32) Member {
   double ax, ay, az;  // -omega_out (volume) or the oriented normal (surface)
@@ -372,12 +374,12 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
                      int S, cudaStream_t s) {
   if (max_count <= 0) return;
   const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
-  VPG_REQUIRE(smem <= 200 * 1024, VPG_ELIMIT,
+  VPG_REQUIRE(smem <= kAggSmemMax, VPG_ELIMIT,
               "clusters larger than 160 members (cluster_size > 80) are not supported");
   static bool attr_set = false;
   if (!attr_set) {
     VPG_CUDA(cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
+                                  int(kAggSmemMax)));
     attr_set = true;
   }
   const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
@@ -410,7 +412,20 @@ void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t
 
 void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchronised
   const int64_t m = g->m;
-  g->n_chunks = (g->chunk_total + kChunkFloats - 1) / kChunkFloats;
+  // the largest chunk (<= kChunkFloatsMax) with which 3, else 2, else 1
+  // stages of chunk + the largest cluster's blocks and rows fit
+  const int64_t smax = std::max<int64_t>(1, g->max_cluster);
+  const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + 16 * smax;
+  g->n_stages = 0;
+  for (int st = 3; st >= 1 && !g->n_stages; --st) {
+    const int64_t room = int64_t((kSolveSmem - 128) / (sizeof(float) * st)) - extra;
+    if (room >= kChunkFloatsMin) {
+      g->n_stages = st;
+      g->chunk_floats = int32_t(std::min<int64_t>(kChunkFloatsMax, room & ~int64_t(3)));
+    }
+  }
+  VPG_REQUIRE(g->n_stages > 0, VPG_ELIMIT, "clusters too large for the staged solve");
+  g->n_chunks = (g->chunk_total + g->chunk_floats - 1) / g->chunk_floats;
   g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
   if (g->n == 0) {
     VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
@@ -418,7 +433,7 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
   }
   const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
   VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst, m, g->n_chunks,
-             int64_t(kChunkFloats), g->chunk_first.get());
+             int64_t(g->chunk_floats), g->chunk_first.get());
 }
 
 void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,

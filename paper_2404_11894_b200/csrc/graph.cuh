@@ -25,7 +25,7 @@
 //     i0 = i_pt, dbar = D-bar, coeff (float4)
 //   ibuf[2], acc[2]: double-buffered I and W*I (acc = i_bar / coeff).
 //   chunk_first[c]: first cluster of solve chunk c; chunks cut the cost prefix
-//     sum(pad4(s^2) + 16 s) floats at multiples of kChunkFloats, so one chunk's
+//     sum(pad4(s^2) + 16 s) floats at multiples of chunk_floats, so one chunk's
 //     kernel blocks + row data fit a shared-memory stage (TMA bulk copies).
 #pragma once
 #include "common.cuh"
@@ -42,6 +42,7 @@ struct vpg_graph {
   vpg::DBuf<float4> rows;  // 2 float4 per row: (a.xyz, par bits), (b.xyz, 0)
   vpg::DBuf<int32_t> chunk_first;
   int64_t n_chunks = 0, chunk_total = 0;
+  int32_t chunk_floats = 0, n_stages = 0;  // solve staging (finalize_chunks)
   vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows
   // solve state (device): red[t*8 + 0..5] float bits, ctl = {performed, stop, grow, diverged}
   vpg::DBuf<uint32_t> red;
@@ -62,8 +63,12 @@ struct vpg_graph {
 };
 
 namespace vpg {
-// floats of kernel blocks + row data per solve chunk (one shared-memory stage)
-constexpr int kChunkFloats = 8192;
+// floats of kernel blocks + row data per solve chunk (one shared-memory stage):
+// chosen per graph so that n_stages stages of chunk + the largest cluster fit
+// the shared memory (kSolveSmem); larger chunks keep more bytes in flight
+constexpr int kChunkFloatsMax = 12288;
+constexpr int kChunkFloatsMin = 2048;
+constexpr size_t kSolveSmem = 220 * 1024;
 // cluster.cu: the whole build (clusters, layout, and the operator passes
 // below, overlapped with the host split loop); `with_operators` = false for
 // cluster_points.

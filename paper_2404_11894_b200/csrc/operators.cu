@@ -91,7 +91,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 // warp and kConsumers consumer warps:
 //  - the producer streams each chunk's kernel blocks, static row data
 //    {a, b, par}, its slice of I and (t > 0) of the previous W*I into a
-//    shared-memory stage with cp.async.bulk, kStages chunks ahead; a stage
+//    shared-memory stage with cp.async.bulk, n_stages chunks ahead; a stage
 //    is refilled once every cluster of its chunk has been consumed;
 //  - consumer warps pull clusters one at a time from a CTA-wide counter (in
 //    chunk order, so a warp never waits on a slower warp), wait on the
@@ -101,12 +101,13 @@ __device__ __forceinline__ void fence_proxy_async() {
 //    to HBM, with the residual maxima of solve.py:54-61.  The old I[par] is
 //    recomputed from the previous W*I (same arithmetic as when it was stored)
 //    instead of gathered.
-constexpr int kConsumers = 12;
-constexpr int kStages = 3;
+constexpr int kConsumers = 16;
+constexpr int kMaxStages = 3;  // the stage count is chosen per graph (graph.cuh)
 
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
 k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
-             const int32_t* __restrict__ chunk_first, int64_t n_chunks, int stage_floats,
+             const int32_t* __restrict__ chunk_first, int64_t n_chunks, int n_stages,
+             int stage_floats,
              const float* __restrict__ wt, const float4* __restrict__ rows,
              const float4* __restrict__ i_in, float4* __restrict__ i_out,
              const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
@@ -114,16 +115,16 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
              const int32_t* __restrict__ ctl) {
   if (ctl[1]) return;  // converged or diverged earlier
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // kStages barriers
-  int* done = reinterpret_cast<int*>(smem + 64);                  // kStages counters
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // n_stages (<= 3) barriers
+  int* done = reinterpret_cast<int*>(smem + 64);                  // n_stages counters
   int* next_item = reinterpret_cast<int*>(smem + 96);
-  int* issued = reinterpret_cast<int*>(smem + 104);               // kStages chunk ids
+  int* issued = reinterpret_cast<int*>(smem + 104);               // n_stages chunk ids
   float* stage0 = reinterpret_cast<float*>(smem + 128);
   __shared__ float blk[kConsumers][6];
   __shared__ unsigned blk_nan[kConsumers];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < n_stages; ++st) {
       mbar_init(&full[st], 1);
       done[st] = 0;
       issued[st] = -1;
@@ -140,9 +141,9 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
       for (int64_t i = 0;; ++i) {
         const int64_t c = blockIdx.x + i * G;
         if (c >= n_chunks) break;
-        const int st = int(i % kStages);
-        if (i >= kStages) {
-          const int64_t cp = c - kStages * G;  // the chunk that last used this stage
+        const int st = int(i % n_stages);
+        if (i >= n_stages) {
+          const int64_t cp = c - n_stages * G;  // the chunk that last used this stage
           const int need = chunk_first[cp + 1] - chunk_first[cp];
           while (*reinterpret_cast<volatile int*>(&done[st]) < need) __nanosleep(64);
           done[st] = 0;
@@ -203,11 +204,11 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
         }
       }
       if (finished) break;
-      const int st = int(ci % kStages);
+      const int st = int(ci % n_stages);
       if (waited != ci) {
         // never wait on a phase parity two uses ahead: first see the chunk issued
         while (*reinterpret_cast<volatile int*>(&issued[st]) != int(ci)) __nanosleep(32);
-        mbar_wait(&full[st], uint32_t((ci / kStages) & 1));
+        mbar_wait(&full[st], uint32_t((ci / n_stages) & 1));
         waited = ci;
       }
       const float* buf = stage0 + st * int64_t(stage_floats);
@@ -568,12 +569,12 @@ struct SolveLaunch {
 };
 
 SolveLaunch solve_launch(const vpg_graph* g) {
-  // stage = one chunk: kChunkFloats plus the largest cluster's blocks + rows
+  // stage = one chunk (g->chunk_floats) plus the largest cluster's blocks + rows
   SolveLaunch L;
   const int smax = std::max(1, g->max_cluster);
-  L.stage_floats = kChunkFloats + ((smax * smax + 3) & ~3) + 16 * smax;
-  L.smem = 128 + size_t(kStages) * L.stage_floats * sizeof(float);
-  VPG_REQUIRE(L.smem <= 220 * 1024, VPG_ELIMIT, "clusters too large for the staged solve");
+  L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + 16 * smax;
+  L.smem = 128 + size_t(g->n_stages) * L.stage_floats * sizeof(float);
+  VPG_REQUIRE(L.smem <= kSolveSmem, VPG_ELIMIT, "clusters too large for the staged solve");
   static size_t smem_set = 0;
   if (L.smem > smem_set) {
     VPG_CUDA(cudaFuncSetAttribute(k_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -615,7 +616,8 @@ void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
   if (g->n == 0 || g->n_chunks == 0) return;
   const SolveLaunch L = solve_launch(g);
   VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->cl_off.get(),
-             g->w_off.get(), g->chunk_first.get(), g->n_chunks, L.stage_floats, g->wt.get(),
+             g->w_off.get(), g->chunk_first.get(), g->n_chunks, g->n_stages, L.stage_floats,
+             g->wt.get(),
              g->rows.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
              g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
 }

@@ -194,3 +194,22 @@ def test_k1_pipeline_reproduces_path_tracing(cuda):
     pg = render_pg(S.scene_c1((12, 12), floor=True), cfg)
     err = np.abs(pg.image - pg.pt_image)
     assert float(err.max()) <= 1e-4 * float(np.abs(pg.pt_image).max())
+
+
+@pytest.mark.parametrize("K", [48, 80])
+def test_large_cluster_sizes(cuda, K):
+    """Clusters up to 2K = 160 members: the solve stages fewer, smaller chunks
+    (fewer stages when the largest cluster's block needs the shared memory)."""
+    from paper_2404_11894_b200.pathgraph import build_graph, solve, splat_output
+
+    z = golden("c1floor_16")
+    trace = _trace_from_golden(z)
+    g = build_graph(trace, K, seed=3)
+    res = solve(g, iterations=6, tol=0.0)
+    img = splat_output(g, res)
+    rec, paths = O.load_golden_records(z)
+    og = O.build_graph(rec, paths, int(z["width"]), int(z["height"]), int(z["spp"]), K, 3)
+    assert np.array_equal(trace.records.cluster_id, og.cluster_id)
+    inc, ib, _, _ = O.solve(og, 6, 0.0)
+    assert_rel(res.incoming, inc, 1e-4, what="incoming")
+    assert_rel(img, O.splat(og, ib), 1e-4, what="image")
