@@ -762,6 +762,57 @@ __global__ void k_gather_oversize(const int32_t* __restrict__ grp_rec,
   }
 }
 
+// First-split outcomes of every oversize group for every possible pick: bit
+// m of row p of group k = (member m is strictly closer to member p than to
+// the group's center), i.e. "m moves if p is the new center"
+// (clustering.py:69-74) with the host loop's exact fp64 distances.  82% of
+// the split loop's splits are first splits; with these rows the host only
+// draws the pick and partitions.  mask_off = exclusive scan of
+// cnt * ceil(cnt / 64) words (MaskWords).
+struct MaskWords {
+  const int64_t* info;
+  const int32_t* n_over;
+  __host__ __device__ int64_t operator()(int32_t k) const {
+    if (k >= *n_over) return 0;
+    const int64_t cnt = info[k * 4 + 1];
+    return cnt * ((cnt + 63) / 64);
+  }
+};
+
+__global__ void k_mask_total(const int64_t* __restrict__ mask_off, const int64_t* __restrict__ info,
+                             const int32_t* __restrict__ n_over, int64_t* __restrict__ total) {
+  const int n = *n_over;
+  if (n == 0) {
+    *total = 0;
+    return;
+  }
+  const int64_t cnt = info[(n - 1) * 4 + 1];
+  *total = mask_off[n - 1] + cnt * ((cnt + 63) / 64);
+}
+
+__global__ void k_first_split_masks(const int64_t* __restrict__ seg, const int32_t* __restrict__ n_over,
+                                    const int64_t* __restrict__ mask_off,
+                                    const double* __restrict__ x, const double* __restrict__ y,
+                                    const double* __restrict__ z, const double* __restrict__ d0,
+                                    unsigned long long* __restrict__ masks) {
+  const int nk = *n_over;
+  for (int k = blockIdx.x; k < nk; k += gridDim.x) {
+    const int64_t cnt = seg[k * 3 + 1], b = seg[k * 3 + 2];
+    const int64_t words = (cnt + 63) / 64;
+    unsigned long long* mk = masks + mask_off[k];
+    for (int64_t item = threadIdx.x; item < cnt * words; item += blockDim.x) {
+      const int64_t p = item / words, w = item - p * words;
+      const double px = x[b + p], py = y[b + p], pz = z[b + p];
+      unsigned long long bits = 0;
+      const int64_t m0 = w * 64, m1 = m0 + 64 < cnt ? m0 + 64 : cnt;
+      for (int64_t mm = m0; mm < m1; ++mm)
+        if (dist2_exact(x[b + mm], y[b + mm], z[b + mm], px, py, pz) < d0[b + mm])
+          bits |= 1ull << (mm - m0);
+      mk[item] = bits;
+    }
+  }
+}
+
 // ------------------------------------------------------------ layout
 // Internal cluster order: part A = every group that needed no split, class by
 // class in group order; part B = the split loop's results (modified groups and
@@ -1158,6 +1209,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   DBuf<int32_t> ne_prefix_all(center_total + 1, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
   DBuf<int32_t> far_count(1, s);
+  DBuf<int64_t> mask_total(1, s);
   DBuf<int64_t> acc(8, s), cls_info(size_t(4) * n_cls + 4, s), ranges(size_t(2) * n_cls + 2, s);
   DBuf<int64_t> class_center_off(n_cls + 1, s);
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
@@ -1372,6 +1424,17 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     }
     VPG_LAUNCH(k_oversize_seg, grid_for(m, block), block, 0, s, over_info.get(), scalars.get() + 2,
                over_dst, p.row_off, over_seg, scalars.get());
+    int64_t* mask_off = scratch_of<int64_t>(s, "mask_off", size_t(m) + 1);
+    {
+      cub::CountingInputIterator<int32_t> it0(0);
+      cub::TransformInputIterator<int64_t, MaskWords, cub::CountingInputIterator<int32_t>> mw_it(
+          it0, MaskWords{over_info.get(), scalars.get() + 2});
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, mw_it, mask_off, m, s);
+      }, s);
+      VPG_LAUNCH(k_mask_total, 1, 1, 0, s, mask_off, over_info.get(), scalars.get() + 2,
+                 mask_total.get());
+    }
 
     // ---- part A of this class: layout (device)
     {
@@ -1408,9 +1471,12 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     }
     // sizes of the oversize staging (nothing heavy is queued before this sync)
     HostBuf<int32_t> h_scalars(4);
+    HostBuf<int64_t> h_mask_total(1);
     VPG_CUDA(cudaMemcpyAsync(h_scalars.get(), scalars.get(), 4 * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, s));
-    count_transfer(0, 16);
+    VPG_CUDA(cudaMemcpyAsync(h_mask_total.get(), mask_total.get(), sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+    count_transfer(0, 24);
     VPG_CUDA(cudaStreamSynchronize(s));
     g->info.n_fallback += h_scalars[0];
     const int n_over = h_scalars[2];
@@ -1421,6 +1487,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     HostBuf<int32_t>& h_srec = *h_srec_own;
     HostBuf<int32_t> h_slot(size_t(n_over) + 1);
     HostBuf<double> h_xyzd(size_t(staged) * 4 + 4);  // x | y | z | d0
+    const int64_t n_mask = n_over > 0 ? h_mask_total[0] : 0;
+    HostBuf<unsigned long long> h_masks(size_t(n_mask) + 1);
     cudaEvent_t staged_ready;
     VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
     if (n_over > 0) {
@@ -1439,7 +1507,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                                cudaMemcpyDeviceToHost, s));
       VPG_CUDA(cudaMemcpyAsync(h_xyzd.get(), d_xyzd, sizeof(double) * 4 * staged,
                                cudaMemcpyDeviceToHost, s));
-      count_transfer(0, 36 * n_over + 36 * staged);
+      auto* d_masks = scratch_of<unsigned long long>(s, "split_masks", size_t(n_mask) + 1);
+      VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, s, over_seg,
+                 scalars.get() + 2, mask_off, d_xyzd, d_xyzd + staged, d_xyzd + 2 * staged,
+                 d_xyzd + 3 * staged, d_masks);
+      VPG_CUDA(cudaMemcpyAsync(h_masks.get(), d_masks, sizeof(unsigned long long) * n_mask,
+                               cudaMemcpyDeviceToHost, s));
+      count_transfer(0, 36 * n_over + 36 * staged + 8 * n_mask);
     }
     VPG_CUDA(cudaEventRecord(staged_ready, s));
     // ---- part A of this class: permutation, pack, aggregate (device, async)
@@ -1477,7 +1551,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       double* xyzd = h_xyzd.get();
       n_splits += split_oversize_soa(
           rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
-          groups, cslot, max_size, &g->info.split_visits);
+          groups, cslot, max_size, &g->info.split_visits, h_masks.get());
       dbg.mark("split: loop", false);
       const int64_t base_split = split_total;
       auto hb_own = std::make_unique<HostBuf<int64_t>>(groups.size() * 8 + 8);

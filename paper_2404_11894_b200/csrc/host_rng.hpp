@@ -206,9 +206,23 @@ struct SplitMembers {
 // their d0).  On return groups[0..q) are the originals (possibly shrunk) and
 // groups[q..) the split-off groups in append order.  Returns the number of
 // splits.
+//
+// `masks` (optional) holds, for every original group k in order, cnt_k rows
+// of ceil(cnt_k / 64) words: bit m of row p = (member m is strictly closer to
+// member p than to the group's center) -- the outcome of the group's FIRST
+// split for every possible pick, precomputed on the device.  A first split
+// then only draws the pick and partitions; later splits compute as usual.
 inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGroup>& groups,
                                   std::vector<int64_t>& cslot, int64_t max_size,
-                                  int64_t* visits = nullptr) {
+                                  int64_t* visits = nullptr,
+                                  const unsigned long long* masks = nullptr) {
+  const size_t n_orig = groups.size();
+  std::vector<int64_t> moff(masks ? n_orig : 0);
+  std::vector<uint8_t> fresh(masks ? n_orig : 0, 1);
+  for (size_t k = 0, o = 0; k < moff.size(); ++k) {
+    moff[k] = int64_t(o);
+    o += size_t(groups[k].size) * size_t((groups[k].size + 63) / 64);
+  }
   std::vector<int64_t> stack;
   for (int64_t c = 0; c < int64_t(groups.size()); ++c)
     if (groups[c].size > max_size) stack.push_back(c);
@@ -244,6 +258,62 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
       for (auto* v : {&mx, &my, &mz, &md, &vbuf}) v->resize(sz);
       mid.resize(sz);
       flag.resize(sz);
+    }
+    if (masks && size_t(c) < n_orig && fresh[c]) {
+      // first split of an original group: the moved set is row `pick`
+      fresh[c] = 0;
+      const int64_t words = (sz + 63) / 64;
+      const unsigned long long* row = masks + moff[c] + pick * words;
+      int64_t moved = 0;
+      for (int64_t w = 0; w < words; ++w) moved += __builtin_popcountll(row[w]);
+      const int64_t kept = sz - moved;
+      const int64_t old_slot = cslot[c], new_slot = b + pick;
+      if (kept > 0 && moved > 0) {
+        // stable partition by the row's bits; positions and distances move
+        // too only when a half will be split again (its d0 = distance to its
+        // center: unchanged for the kept half, to the pick for the moved one)
+        const bool again = kept > max_size || moved > max_size;
+        int32_t* __restrict__ Mi = mid.data();
+        double* __restrict__ MX = mx.data();
+        double* __restrict__ MY = my.data();
+        double* __restrict__ MZ = mz.data();
+        double* __restrict__ MD = md.data();
+        int64_t wk = b, wm = 0, keep_center = -1, moved_center = -1;
+        for (int64_t t = b; t < e; ++t) {
+          const int i = int(t - b);
+          const int f = int((row[i >> 6] >> (i & 63)) & 1ull);
+          const int32_t idv = id[t];
+          if (again) {
+            const double xv = X[t], yv = Y[t], zv = Z[t];
+            const double dx = xv - px, dy = yv - py, dz = zv - pz;
+            X[wk] = xv; Y[wk] = yv; Z[wk] = zv; D0[wk] = D0[t];
+            MX[wm] = xv; MY[wm] = yv; MZ[wm] = zv; MD[wm] = (dx * dx + dy * dy) + dz * dz;
+          }
+          id[wk] = idv;
+          Mi[wm] = idv;
+          keep_center = (t == old_slot && !f) ? wk : keep_center;
+          moved_center = (t == new_slot && f) ? wm : moved_center;
+          wk += 1 - f;
+          wm += f;
+        }
+        std::memcpy(id + wk, Mi, sizeof(int32_t) * moved);
+        if (again) {
+          std::memcpy(X + wk, MX, sizeof(double) * moved);
+          std::memcpy(Y + wk, MY, sizeof(double) * moved);
+          std::memcpy(Z + wk, MZ, sizeof(double) * moved);
+          std::memcpy(D0 + wk, MD, sizeof(double) * moved);
+        }
+        groups[c].size = kept;
+        cslot[c] = keep_center;
+        groups.push_back(SplitGroup{wk, moved, new_center});
+        cslot.push_back(moved_center >= 0 ? wk + moved_center : -1);
+        ++splits;
+        if (groups[c].size > max_size) stack.push_back(c);
+        if (groups.back().size > max_size) stack.push_back(int64_t(groups.size()) - 1);
+        continue;
+      }
+      // coincident points (all or nothing moves): the general path below
+      // reproduces the halving with exact distances
     }
     // pass 1 (vectorisable): distance to the new center, np.argmin over
     // (old, new) with ties staying (clustering.py:69-74)
@@ -327,8 +397,21 @@ inline int64_t split_oversize(Pcg64& g, int32_t* ids, double* xyz, size_t total,
       if (ids[t] == gr.center && cslot[k] < 0) cslot[k] = t;
     }
   }
+  // the first-split rows the device precomputes in the build (same
+  // definition), so this entry exercises the same fast path
+  std::vector<unsigned long long> masks;
+  for (size_t k = 0; k < groups.size(); ++k) {
+    const int64_t b = groups[k].begin, cnt = groups[k].size, words = (cnt + 63) / 64;
+    for (int64_t p = 0; p < cnt; ++p)
+      for (int64_t w = 0; w < words; ++w) {
+        unsigned long long bits = 0;
+        for (int64_t mm = w * 64; mm < std::min(cnt, w * 64 + 64); ++mm)
+          if (dist2(&xyz[(b + mm) * 3], &xyz[(b + p) * 3]) < d0[b + mm]) bits |= 1ull << (mm - w * 64);
+        masks.push_back(bits);
+      }
+  }
   const int64_t n = split_oversize_soa(g, SplitMembers{ids, x.data(), y.data(), z.data(), d0.data()},
-                                       groups, cslot, max_size, visits);
+                                       groups, cslot, max_size, visits, masks.data());
   for (size_t t = 0; t < total; ++t) {
     xyz[t * 3] = x[t];
     xyz[t * 3 + 1] = y[t];
