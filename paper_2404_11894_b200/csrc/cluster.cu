@@ -1029,12 +1029,24 @@ struct StageClock {
   }
 };
 
+// A non-blocking stream per device for host transfers that must not hold up
+// the compute stream.
+cudaStream_t side_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  VPG_CUDA(cudaGetDevice(&dev));
+  if (!streams[dev]) VPG_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  return streams[dev];
+}
+
 template <class F>
 void cub_call(F&& f, cudaStream_t s) {
   size_t bytes = 0;
   VPG_CUDA(f(nullptr, bytes));
   void* tmp = scratch(s, "cub_temp", bytes + 256);
+  const int tok = profiling() ? prof_begin("cub", s) : -1;
   VPG_CUDA(f(tmp, bytes));
+  if (tok >= 0) prof_end(tok, s);
   count_launch(2);
 }
 
@@ -1495,27 +1507,37 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       int32_t* d_srec = scratch_of<int32_t>(s, "staged_rec", size_t(staged) + 1);
       int32_t* d_slot = scratch_of<int32_t>(s, "staged_slot", size_t(n_over) + 1);
       double* d_xyzd = scratch_of<double>(s, "staged_xyzd", size_t(staged) * 4 + 4);
+      auto* d_masks = scratch_of<unsigned long long>(s, "split_masks", size_t(n_mask) + 1);
       VPG_CUDA(cudaMemsetAsync(d_slot, 0x7F, sizeof(int32_t) * n_over, s));
       VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec, over_seg,
                  scalars.get() + 2, over_info.get(), rec.pos, d_srec, d_xyzd, d_xyzd + staged,
                  d_xyzd + 2 * staged, d_xyzd + 3 * staged, d_slot);
-      VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
-                               cudaMemcpyDeviceToHost, s));
-      VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec, sizeof(int32_t) * staged,
-                               cudaMemcpyDeviceToHost, s));
-      VPG_CUDA(cudaMemcpyAsync(h_slot.get(), d_slot, sizeof(int32_t) * n_over,
-                               cudaMemcpyDeviceToHost, s));
-      VPG_CUDA(cudaMemcpyAsync(h_xyzd.get(), d_xyzd, sizeof(double) * 4 * staged,
-                               cudaMemcpyDeviceToHost, s));
-      auto* d_masks = scratch_of<unsigned long long>(s, "split_masks", size_t(n_mask) + 1);
       VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, s, over_seg,
                  scalars.get() + 2, mask_off, d_xyzd, d_xyzd + staged, d_xyzd + 2 * staged,
                  d_xyzd + 3 * staged, d_masks);
+      // the staging goes to the host on a side stream, so part A's kernels
+      // (queued next on s) do not wait behind the copies
+      cudaStream_t side = side_stream();
+      cudaEvent_t gathered;
+      VPG_CUDA(cudaEventCreateWithFlags(&gathered, cudaEventDisableTiming));
+      VPG_CUDA(cudaEventRecord(gathered, s));
+      VPG_CUDA(cudaStreamWaitEvent(side, gathered, 0));
+      cudaEventDestroy(gathered);
+      VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
+                               cudaMemcpyDeviceToHost, side));
+      VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec, sizeof(int32_t) * staged,
+                               cudaMemcpyDeviceToHost, side));
+      VPG_CUDA(cudaMemcpyAsync(h_slot.get(), d_slot, sizeof(int32_t) * n_over,
+                               cudaMemcpyDeviceToHost, side));
+      VPG_CUDA(cudaMemcpyAsync(h_xyzd.get(), d_xyzd, sizeof(double) * 4 * staged,
+                               cudaMemcpyDeviceToHost, side));
       VPG_CUDA(cudaMemcpyAsync(h_masks.get(), d_masks, sizeof(unsigned long long) * n_mask,
-                               cudaMemcpyDeviceToHost, s));
+                               cudaMemcpyDeviceToHost, side));
       count_transfer(0, 36 * n_over + 36 * staged + 8 * n_mask);
+      VPG_CUDA(cudaEventRecord(staged_ready, side));
+    } else {
+      VPG_CUDA(cudaEventRecord(staged_ready, s));
     }
-    VPG_CUDA(cudaEventRecord(staged_ready, s));
     // ---- part A of this class: permutation, pack, aggregate (device, async)
     VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
