@@ -110,7 +110,12 @@ __global__ void k_class_bitmap(const uint8_t* __restrict__ kind, const int32_t* 
     }
     const uint32_t slot = uint32_t(k * kSlotsPerKind + c);
     const unsigned peers = __match_any_sync(__activemask(), slot);
-    if ((__ffs(peers) - 1) == int(threadIdx.x & 31)) atomicOr(&bitmap[slot >> 5], 1u << (slot & 31));
+    // one lane per distinct class, and only while its bit is still clear (the
+    // few classes would otherwise serialise every warp on one word)
+    const uint32_t bit = 1u << (slot & 31);
+    if ((__ffs(peers) - 1) == int(threadIdx.x & 31) &&
+        !(*reinterpret_cast<volatile uint32_t*>(&bitmap[slot >> 5]) & bit))
+      atomicOr(&bitmap[slot >> 5], bit);
   }
 }
 
