@@ -364,6 +364,13 @@ def run_native(args):
         "frame_breakdown_ms": {"trace": trace_ms, "build_plus_solve": step_ms, "splat": splat_ms},
         "roofline": {"kernel": it_name, "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     # the block-dense layout moves fewer bytes than the CSR-based
+                     # algorithmic figure (frac can exceed 1): the measured DRAM
+                     # traffic over the same launch time is the hardware fraction
+                     "traffic_gbs": (traffic / (it_avg_ms * 1e-3) / 1e9
+                                     if traffic and it_count else None),
+                     "traffic_frac": (traffic / (it_avg_ms * 1e-3) / 1e9 / hbm
+                                      if traffic and it_count else None),
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": ITER_BYTES_PER_VERTEX * n,
                      "avg_launch_ms": it_avg_ms,
