@@ -97,6 +97,28 @@ int vpg_split_groups(vpg_pcg64* rng, const double* pos, int64_t n_groups,
                      int64_t cap_groups, int64_t* out_n_groups,
                      int64_t* out_off, int64_t* out_members, int64_t* out_center);
 
+/* The split loop on structure-of-arrays input (the sharded build gathers the
+ * oversize groups of a class from every shard): ids (n_total, int32, groups
+ * back to back, each ascending; reordered in place so every final group is a
+ * contiguous ascending run), x/y/z/d0 (member positions and squared distance
+ * to the group's center), per group its size, center record id and the slot
+ * of the center among its members (-1 if absent).  Out: final groups
+ * (originals first, split-off groups appended, clustering.py:58-85) as
+ * begin/size/center, capacity cap_groups. */
+int vpg_split_groups_soa(vpg_pcg64* rng, int32_t* ids, const double* x, const double* y,
+                         const double* z, const double* d0, int64_t n_groups, const int64_t* sizes,
+                         const int64_t* centers, const int64_t* cslot, int64_t max_size,
+                         int64_t cap_groups, int64_t* out_n_groups, int64_t* out_begin,
+                         int64_t* out_size, int64_t* out_center, int64_t* n_splits);
+
+/* Exact nearest center (ties -> lowest index; clustering.py:96-148) of n
+ * points against m centers, all device (n x 3, m x 3 float64); bounds (host,
+ * 6 doubles: lo xyz, hi xyz) size the hash grid like the class bounding box.
+ * assign: n int32 (device).  n_fallback (host, optional): points the
+ * neighbourhood search could not decide. */
+int vpg_assign_nearest(const double* pos, int64_t n, const double* centers, int64_t m,
+                       const double* bounds, int32_t* assign, int64_t* n_fallback, void* stream);
+
 /* ------------------------------------------------------- vertex records
  * Device SoA mirroring RecordSoA (records.py:75-126).  `n` records, stored
  * contiguous per path and depth-ordered (records.py:3-5). */

@@ -128,6 +128,10 @@ _SIGNATURES = {
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,
                                    c_p, c_p, c_p, c_p]),
+    "vpg_split_groups_soa": (C.c_int, [C.POINTER(Pcg64State), c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
+                                       c_p, c_p, c_i64, c_i64, C.POINTER(c_i64), c_p, c_p, c_p,
+                                       C.POINTER(c_i64)]),
+    "vpg_assign_nearest": (C.c_int, [c_p, c_i64, c_p, c_i64, c_p, c_p, C.POINTER(c_i64), c_p]),
     "vpg_graph_build": (C.c_int, [C.POINTER(Records), c_i32, C.POINTER(Pcg64State), c_i32, c_p,
                                   C.POINTER(c_p)]),
     "vpg_graph_build_wait": (C.c_int, [C.POINTER(Records), c_i32, C.POINTER(Pcg64State), c_i32, c_p,

@@ -353,6 +353,47 @@ int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64
   return VPG_OK;
 }
 
+int vpg_split_groups_soa(vpg_pcg64* rng, int32_t* ids, const double* x, const double* y,
+                         const double* z, const double* d0, int64_t n_groups, const int64_t* sizes,
+                         const int64_t* centers, const int64_t* cslot, int64_t max_size,
+                         int64_t cap_groups, int64_t* out_n_groups, int64_t* out_begin,
+                         int64_t* out_size, int64_t* out_center, int64_t* n_splits) {
+  return guarded([&] {
+    vpg::Pcg64 g(*rng);
+    std::vector<vpg::SplitGroup> groups(static_cast<size_t>(n_groups));
+    std::vector<int64_t> slot(static_cast<size_t>(n_groups));
+    int64_t total = 0;
+    for (int64_t k = 0; k < n_groups; ++k) {
+      groups[k] = vpg::SplitGroup{total, sizes[k], centers[k]};
+      slot[k] = cslot[k];
+      total += sizes[k];
+    }
+    std::vector<double> X(x, x + total), Y(y, y + total), Z(z, z + total), D(d0, d0 + total);
+    const int64_t n = vpg::split_oversize_soa(
+        g, vpg::SplitMembers{ids, X.data(), Y.data(), Z.data(), D.data()}, groups, slot, max_size);
+    VPG_REQUIRE(int64_t(groups.size()) <= cap_groups, VPG_ELIMIT, "output group capacity exceeded");
+    for (size_t k = 0; k < groups.size(); ++k) {
+      out_begin[k] = groups[k].begin;
+      out_size[k] = groups[k].size;
+      out_center[k] = groups[k].center;
+    }
+    *out_n_groups = int64_t(groups.size());
+    *n_splits = n;
+    g.store(rng);
+  });
+}
+
+int vpg_assign_nearest(const double* pos, int64_t n, const double* centers, int64_t m,
+                       const double* bounds, int32_t* assign, int64_t* n_fallback, void* stream) {
+  return guarded([&] {
+    VPG_REQUIRE(m >= 1 && m < (int64_t(1) << 31) && n < (int64_t(1) << 31), VPG_ELIMIT,
+                "assign_nearest: sizes out of range");
+    const int64_t fb = vpg::assign_nearest(pos, n, centers, int(m), bounds, bounds + 3, assign,
+                                           as_stream(stream));
+    if (n_fallback) *n_fallback = fb;
+  });
+}
+
 int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng, int32_t flags,
                     void* stream, vpg_graph** out) {
   return vpg_graph_build_wait(rec, cluster_size, rng, flags, stream, nullptr, out);

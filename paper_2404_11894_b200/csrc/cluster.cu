@@ -209,6 +209,17 @@ __global__ void k_center_setup(const int32_t* __restrict__ local, int m, const i
   }
 }
 
+// Cell keys of given centers (assign_nearest).
+__global__ void k_center_keys(const double* __restrict__ cpos, int m, GridParams gp,
+                              unsigned long long* __restrict__ keys, int32_t* __restrict__ ids) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    keys[j] = cell_key(gp, cell_coord(cpos[j * 3], gp.lo[0], gp.cell),
+                       cell_coord(cpos[j * 3 + 1], gp.lo[1], gp.cell),
+                       cell_coord(cpos[j * 3 + 2], gp.lo[2], gp.cell));
+    ids[j] = j;
+  }
+}
+
 // Sorted centers -> packed positions; run heads inserted into the cell table.
 __global__ void k_center_table(const unsigned long long* __restrict__ skeys,
                                const int32_t* __restrict__ sids, const double* __restrict__ cpos,
@@ -1688,6 +1699,87 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   clk.mark(5);
   if (with_ops) finalize_chunks(g, s);
   clk.mark(6);
+}
+
+// Exact nearest center (lowest index on ties) of every point against given
+// centers -- the assignment step of clustering.py:96-148 on its own, for a
+// shard's rows against the replicated centers of a class.  The result does
+// not depend on the grid; lo/hi (the class bounding box) only size it like
+// the single-device build.
+int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, const double* lo,
+                       const double* hi, int32_t* assign, cudaStream_t s) {
+  if (n <= 0) return 0;
+  VPG_REQUIRE(m >= 1, VPG_EINVAL, "no centers");
+  if (m == 1) {  // a single center takes every point (clustering.py:100-101)
+    VPG_CUDA(cudaMemsetAsync(assign, 0, sizeof(int32_t) * n, s));
+    return 0;
+  }
+  const int block = 256;
+  ClassPlan p{};
+  p.n = n;
+  p.m = m;
+  for (int a = 0; a < 3; ++a) {
+    p.lo[a] = lo[a];
+    p.hi[a] = hi[a];
+  }
+  const GridParams gp = make_grid(p);
+  DBuf<int32_t> scalars(4, s);
+  DBuf<int32_t> far_count(1, s);
+  VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, scalars.bytes(), s));
+  unsigned long long* pkeys = scratch_of<unsigned long long>(s, "an_pkeys", n);
+  unsigned long long* pkeys_sorted = scratch_of<unsigned long long>(s, "an_pkeys_sorted", n);
+  int32_t* pids = scratch_of<int32_t>(s, "an_pids", n);
+  int32_t* pids_sorted = scratch_of<int32_t>(s, "an_pids_sorted", n);
+  int32_t* run_start = scratch_of<int32_t>(s, "an_run_start", n + 1);
+  int32_t* run_len = scratch_of<int32_t>(s, "an_run_len", n + 1);
+  int32_t* fb_list = scratch_of<int32_t>(s, "an_fb_list", n + 1);
+  VPG_LAUNCH(k_point_keys, grid_for(n, block), block, 0, s, nullptr, 0, n, pos, gp, pkeys, pids);
+  int end_bits = 64;
+  if (gp.packed)
+    end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted, int(n), 0,
+                                           end_bits, s);
+  }, s);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
+                                              scalars.get() + 1, int(n), s);
+  }, s);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(n), s);
+  }, s);
+  DBuf<unsigned long long> keys(m, s), skeys(m, s);
+  DBuf<int32_t> ids(m, s), sids(m, s);
+  DBuf<double4> spos(m, s);
+  DBuf<CellEntry> table(gp.table_mask + 1, s);
+  VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+  VPG_LAUNCH(k_center_keys, grid_for(m, block), block, 0, s, cpos, m, gp, keys.get(), ids.get());
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(), sids.get(), m,
+                                           0, 64, s);
+  }, s);
+  VPG_LAUNCH(k_center_table, grid_for(m, block), block, 0, s, skeys.get(), sids.get(), cpos, m, gp,
+             spos.get(), table.get());
+  VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
+             table.get());
+  VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, nullptr, 0, pos, gp,
+             table.get(), spos.get(), pids_sorted, run_start, run_len, scalars.get() + 1, assign,
+             fb_list, scalars.get());
+  int32_t* far_list = scratch_of<int32_t>(s, "an_far_list", n + 1);
+  auto* far_d = scratch_of<unsigned long long>(s, "an_far_d", n + 1);
+  int32_t* far_j = scratch_of<int32_t>(s, "an_far_j", n + 1);
+  VPG_CUDA(cudaMemsetAsync(far_count.get(), 0, sizeof(int32_t), s));
+  VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, nullptr, 0, pos, gp, table.get(),
+             spos.get(), fb_list, scalars.get(), assign, far_list, far_count.get(), far_d, far_j);
+  for (int pass = 0; pass < 2; ++pass)
+    VPG_LAUNCH(k_far_tiles, sm_count() * 4, 256, 0, s, nullptr, 0, pos, spos.get(), m, far_list,
+               far_count.get(), far_d, far_j, pass);
+  VPG_LAUNCH(k_far_store, sm_count() * 2, 256, 0, s, far_list, far_count.get(), far_j, assign);
+  int32_t h_fb = 0;
+  VPG_CUDA(cudaMemcpyAsync(&h_fb, scalars.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaStreamSynchronize(s));
+  count_transfer(0, 4);
+  return h_fb;
 }
 
 }  // namespace vpg

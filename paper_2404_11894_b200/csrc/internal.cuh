@@ -37,6 +37,8 @@ void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratc
                    const vpg_paths& pth, cudaStream_t s);
 void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s);
+int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, const double* lo,
+                       const double* hi, int32_t* assign, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
                   int n_extra, cudaStream_t s);
 }  // namespace vpg

@@ -207,34 +207,6 @@ def plan_owners(cl_size, center_pos, world: int) -> OwnerPlan:
                      [int(x) for x in clusters_per.tolist()])
 
 
-def row_destinations(perm, cl_off, plan: OwnerPlan):
-    """(dest_shard, dest_row) of every record (global record order)."""
-    import torch
-
-    n = int(perm.shape[0])
-    m = int(cl_off.shape[0]) - 1
-    dev = perm.device
-    off = cl_off.to(torch.int64)
-    sizes = off[1:] - off[:-1]
-    k_of_q = torch.repeat_interleave(torch.arange(m, device=dev), sizes)
-    within = torch.arange(n, device=dev) - off[k_of_q]
-    rec = perm.to(torch.int64)
-    dest_shard = torch.empty(n, dtype=torch.int64, device=dev)
-    dest_row = torch.empty(n, dtype=torch.int64, device=dev)
-    dest_shard[rec] = plan.owner[k_of_q]
-    dest_row[rec] = plan.local_start[k_of_q] + within
-    return dest_shard, dest_row
-
-
-def recv_counts_for(dest_shard, row_counts, me: int, world: int):
-    """Rows shard `me` receives from each source shard (rows are in shard order)."""
-    import torch
-
-    src = torch.repeat_interleave(torch.arange(world, device=dest_shard.device),
-                                  torch.as_tensor(row_counts, device=dest_shard.device))
-    return torch.bincount(src[dest_shard == me], minlength=world).tolist()
-
-
 class HaloExchange:
     """Continuation edges that cross shards (solve.py:78-83 propagation).
 
@@ -270,13 +242,200 @@ class HaloExchange:
             i_out[self.recv_rows] = got
 
 
+# ------------------------------------------------------ distributed clustering
+def _sq_dist(a, b):
+    """fp64 squared distance rounded like numpy's ((a-b)**2).sum(-1): ((dx*dx + dy*dy) + dz*dz),
+    one IEEE op at a time (no contraction)."""
+    d = a - b
+    sq = d * d
+    return (sq[:, 0] + sq[:, 1]) + sq[:, 2]
+
+
+@dataclass
+class GlobalClusters:
+    """The clusters of the whole frame (replicated on every shard) and this
+    shard's rows' places in them."""
+    sizes: "object"       # (M,) int64, reference cluster order
+    center_pos: "object"  # (M, 3) float64
+    row_cluster: "object"  # (n_local,) int64
+    row_rank: "object"     # (n_local,) int64 rank in the cluster (ascending global row)
+    n_splits: int
+
+
+def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_size: int,
+                        rng: np.random.Generator) -> GlobalClusters:
+    """cluster_points (clustering.py:28-148) over the shards' records without
+    gathering them: per class (ascending keys) the centers are drawn with the
+    replicated Generator (numpy's own choice, the same stream on every
+    shard), their positions all-gathered from the shards holding them, every
+    shard assigns its own rows (exact nearest, lowest index on ties), the
+    group sizes are all-reduced, and only the oversize groups' members are
+    gathered for the split loop, which runs replicated on the shared stream.
+    Same clusters as the single-device build."""
+    import torch
+
+    dev = pos.device
+    me, world = comm.rank, comm.world
+    K = int(cluster_size)
+    max_size = 2 * K
+    n = int(pos.shape[0])
+    keys = (kind.to(torch.int64) << 32) | class_id.to(torch.int64)
+    loc_keys = torch.unique(keys) if n else keys[:0]
+    cnt = comm.all_gather_ints([int(loc_keys.numel())])[:, 0].tolist()
+    all_keys = comm.all_gather_rows(loc_keys, cnt)
+    classes = sorted(set(int(x) for x in all_keys.cpu().tolist()))
+    sizes_all, cpos_all = [], []
+    row_cluster = torch.full((n,), -1, dtype=torch.int64, device=dev)
+    row_rank = torch.full((n,), -1, dtype=torch.int64, device=dev)
+    base = 0
+    n_splits = 0
+    lib = N.lib()
+    stream = N.stream_handle()
+    for key in classes:
+        rows = torch.nonzero(keys == key).reshape(-1)  # ascending = ascending global row
+        counts = comm.all_gather_ints([int(rows.numel())])[:, 0]
+        n_c = int(counts.sum())
+        pref = int(counts[:me].sum())
+        my_n = int(rows.numel())
+        m = -(-n_c // K)
+        # centers: Generator.choice(n, m, replace=False) (clustering.py:51)
+        idx = torch.as_tensor(rng.choice(n_c, m, replace=False), dtype=torch.int64, device=dev)
+        mine = torch.nonzero((idx >= pref) & (idx < pref + my_n)).reshape(-1)
+        c_rows = rows[idx[mine] - pref]
+        msg = torch.cat([mine.to(torch.float64).reshape(-1, 1), pos[c_rows],
+                         (c_rows + g0).to(torch.float64).reshape(-1, 1)], 1)
+        got = comm.all_gather_rows(msg, comm.all_gather_ints([int(mine.numel())])[:, 0])
+        order = got[:, 0].to(torch.int64)
+        cpos = torch.empty((m, 3), dtype=torch.float64, device=dev)
+        cpos[order] = got[:, 1:4]
+        # class bounding box (sizes the hash grid like the single-device build)
+        p_c = pos[rows].contiguous()
+        lo = p_c.min(0).values if my_n else torch.full((3,), float("inf"), dtype=torch.float64,
+                                                         device=dev)
+        hi = p_c.max(0).values if my_n else torch.full((3,), -float("inf"), dtype=torch.float64,
+                                                         device=dev)
+        bb = torch.cat([-lo, hi])
+        comm.all_reduce_max_(bb)
+        bounds = torch.cat([-bb[:3], bb[3:]]).cpu().numpy()
+        assign = torch.empty(my_n, dtype=torch.int32, device=dev)
+        if my_n:
+            N.check(lib.vpg_assign_nearest(p_c.data_ptr(), my_n, cpos.contiguous().data_ptr(), m,
+                                           bounds.ctypes.data, assign.data_ptr(), None, stream))
+        a64 = assign.to(torch.int64)
+        hist = torch.bincount(a64, minlength=m) if my_n else torch.zeros(m, dtype=torch.int64,
+                                                                            device=dev)
+        hists = comm.all_gather_rows(hist.reshape(1, -1), [1] * world)  # (world, m)
+        gsize = hists.sum(0)
+        before = hists[:me].sum(0)
+        # rank of each row among its group's members (ascending global row)
+        srt = torch.argsort(a64, stable=True)
+        first = torch.cumsum(hist, 0) - hist
+        lrank = torch.empty(my_n, dtype=torch.int64, device=dev)
+        lrank[srt] = torch.arange(my_n, device=dev) - first[a64[srt]]
+        over = torch.nonzero(gsize > max_size).reshape(-1)
+        n_over = int(over.numel())
+        # reference numbering: non-empty groups in center order, then the
+        # split-off groups of this class (clustering.py:87-93)
+        nonempty = gsize > 0
+        cid_of_j = torch.cumsum(nonempty.to(torch.int64), 0) - 1 + base
+        n_ne = int(nonempty.sum())
+        cl_sizes = gsize[nonempty].clone()
+        cl_pos = cpos[nonempty].clone()
+        is_over = torch.zeros(m, dtype=torch.bool, device=dev)
+        is_over[over] = True
+        plain = ~is_over[a64]
+        row_cluster[rows[plain]] = cid_of_j[a64[plain]]
+        row_rank[rows[plain]] = before[a64[plain]] + lrank[plain]
+        appended = []
+        if n_over:
+            om = torch.nonzero(is_over[a64]).reshape(-1)
+            grow = (rows[om] + g0)
+            mem = torch.cat([a64[om].to(torch.float64).reshape(-1, 1),
+                             grow.to(torch.float64).reshape(-1, 1), p_c[om],
+                             _sq_dist(p_c[om], cpos[a64[om]]).reshape(-1, 1)], 1)
+            allm = comm.all_gather_rows(mem, comm.all_gather_ints([int(om.numel())])[:, 0])
+            gj = allm[:, 0].to(torch.int64)
+            gr = allm[:, 1].to(torch.int64)
+            srt2 = torch.argsort(gj * (1 << 40) + gr)
+            allm, gj, gr = allm[srt2], gj[srt2], gr[srt2]
+            crec = torch.empty(m, dtype=torch.int64, device=dev)
+            crec[order] = got[:, 4].to(torch.int64)
+            osz = gsize[over]
+            ostart = torch.cumsum(osz, 0) - osz
+            # slot of each group's center among its members (-1: not a member)
+            cslot = torch.full((n_over,), -1, dtype=torch.int64, device=dev)
+            hit = torch.nonzero(gr == crec[gj]).reshape(-1)
+            if hit.numel():
+                kk = torch.searchsorted(over, gj[hit])
+                cslot[kk] = hit  # members ascending: one hit per group
+            ids = torch.arange(allm.shape[0], dtype=torch.int32).numpy().copy()
+            h = allm[:, 2:6].cpu().numpy()
+            x, y, z, d0 = (np.ascontiguousarray(h[:, i]) for i in range(4))
+            st = N.Pcg64State.from_generator(rng)
+            cap = int(allm.shape[0]) + n_over + 1
+            o_n = ctypes.c_int64()
+            o_b = np.zeros(cap, np.int64)
+            o_s = np.zeros(cap, np.int64)
+            o_c = np.zeros(cap, np.int64)
+            nspl = ctypes.c_int64()
+            sz_h = osz.cpu().numpy().astype(np.int64)
+            cen_h = crec[over].cpu().numpy().astype(np.int64)
+            cs_h = cslot.cpu().numpy().astype(np.int64)
+            N.check(lib.vpg_split_groups_soa(ctypes.byref(st), ids.ctypes.data, x.ctypes.data,
+                                             y.ctypes.data, z.ctypes.data, d0.ctypes.data, n_over,
+                                             sz_h.ctypes.data, cen_h.ctypes.data,
+                                             cs_h.ctypes.data, max_size, cap, ctypes.byref(o_n),
+                                             o_b.ctypes.data, o_s.ctypes.data, o_c.ctypes.data,
+                                             ctypes.byref(nspl)))
+            st.store_into(rng)
+            n_splits += nspl.value
+            ng = o_n.value
+            # final groups: members (staged index) in order; cluster ids: the
+            # originals keep their slot among the non-empty groups, split-off
+            # groups are appended
+            ids_t = torch.as_tensor(ids.astype(np.int64), device=dev)
+            fg = torch.as_tensor(np.repeat(np.arange(ng), o_s[:ng]), device=dev)
+            fpos = torch.as_tensor(np.concatenate([np.arange(sz) for sz in o_s[:ng]]) if ng else
+                                   np.zeros(0, np.int64), device=dev)
+            member_idx = torch.cat([ids_t[int(b):int(b) + int(sz)] for b, sz in
+                                    zip(o_b[:ng], o_s[:ng])]) if ng else ids_t[:0]
+            g_cid = torch.empty(ng, dtype=torch.int64, device=dev)
+            g_cid[:n_over] = cid_of_j[over]
+            g_cid[n_over:] = base + n_ne + torch.arange(ng - n_over, device=dev)
+            # sizes / centers of the originals (shrunk) and the appended groups
+            cl_sizes[(cid_of_j[over] - base)] = torch.as_tensor(o_s[:n_over], device=dev)
+            center_rec = torch.as_tensor(o_c[:ng], device=dev)
+            # (the originals keep their centers; a split-off group's center is
+            # one of the class's oversize members)
+            srt_gr, srt_i = torch.sort(gr)
+            cidx = srt_i[torch.searchsorted(srt_gr, center_rec[n_over:])]
+            appended = [(torch.as_tensor(o_s[n_over:ng], device=dev), allm[cidx, 2:5])]
+            # my rows in oversize groups: their final group and rank
+            mem_grow = gr[member_idx]
+            my_lo, my_hi = g0, g0 + n
+            mine2 = torch.nonzero((mem_grow >= my_lo) & (mem_grow < my_hi)).reshape(-1)
+            lr = mem_grow[mine2] - g0
+            row_cluster[lr] = g_cid[fg[mine2]]
+            row_rank[lr] = fpos[mine2]
+        sizes_all.append(cl_sizes)
+        cpos_all.append(cl_pos)
+        for sz, cp in appended:
+            sizes_all.append(sz)
+            cpos_all.append(cp)
+        base += n_ne + sum(int(sz.numel()) for sz, _ in appended)
+    sizes = torch.cat(sizes_all) if sizes_all else torch.zeros(0, dtype=torch.int64, device=dev)
+    center_pos = torch.cat(cpos_all) if cpos_all else torch.zeros((0, 3), dtype=torch.float64,
+                                                                  device=dev)
+    return GlobalClusters(sizes, center_pos, row_cluster, row_rank, n_splits)
+
+
 # ------------------------------------------------------------ record payload
 def _payload_columns():
     cols = []
     for name, width, code in N.RECORD_FIELDS:
         cols.append((name, width, code))
     cols += [("parent_ipt", 3, "f8"), ("has_child", 1, "i8"), ("grow", 1, "i8"),
-             ("dest_row", 1, "i8")]
+             ("par_shard", 1, "i8"), ("par_row", 1, "i8"), ("dest_row", 1, "i8")]
     return cols
 
 
@@ -352,54 +511,46 @@ class ShardedPathGraph:
         self.row_counts = counts
         self.row_off = [0] + list(np.cumsum(counts))
         n_all = int(self.row_off[-1])
-        # light columns of every record, then the exact clustering on all of them
-        pos = comm.all_gather_rows(recs["pos"][:n_rec], counts)
-        kind = comm.all_gather_rows(recs["kind"][:n_rec], counts)
-        cls_id = comm.all_gather_rows(recs["class_id"][:n_rec], counts)
-        light = N.Records()
-        light.n = n_all
-        if n_all:
-            light.pos, light.kind, light.class_id = pos.data_ptr(), kind.data_ptr(), cls_id.data_ptr()
+        # the exact clustering, distributed (cluster_distributed)
         rng = np.random.default_rng(np.random.SeedSequence([seed & 0xFFFFFFFF, 0xC1A5]))
-        st = N.Pcg64State.from_generator(rng)
-        gc = ctypes.c_void_p()
-        N.check(lib.vpg_graph_build(ctypes.byref(light), int(cluster_size), ctypes.byref(st),
-                                    N.VPG_BUILD_CLUSTERS_ONLY, stream, ctypes.byref(gc)))
-        try:
-            v = N.GraphViews()
-            N.check(lib.vpg_graph_views_get(gc.value, ctypes.byref(v)))
-            m = int(v.m)
-            perm = _view(v.perm, (n_all,), "<i4").clone()
-            cl_off = _view(v.cl_off, (m + 1,), "<i4").clone()
-            center = _view(v.cl_center, (m,), "<i4").clone()
-        finally:
-            lib.vpg_graph_free(gc.value)
-        self.n_clusters_total = m
-        sizes = (cl_off[1:] - cl_off[:-1]).to(torch.int64)
-        plan = plan_owners(sizes, pos[center.to(torch.int64)] if m else pos[:0], world)
-        dest_shard, dest_row = row_destinations(perm, cl_off, plan)
-        self.plan = plan
-        del pos, kind, cls_id, perm
-
-        # this shard's records, with what the owner needs beyond them
-        n = n_rec
         g0 = int(self.row_off[me])
+        gcl = cluster_distributed(comm, recs["pos"][:n_rec], recs["kind"][:n_rec],
+                                  recs["class_id"][:n_rec], g0, cluster_size, rng)
+        sizes = gcl.sizes
+        m = int(sizes.numel())
+        self.n_clusters_total = m
+        self.n_splits = gcl.n_splits
+        plan = plan_owners(sizes, gcl.center_pos, world)
+        self.plan = plan
+        dest_shard = plan.owner[gcl.row_cluster]
+        dest_row = plan.local_start[gcl.row_cluster] + gcl.row_rank
+
+        # this shard's records, with what the owner needs beyond them: the
+        # continuation parent (record r-1 of the same path) is on this shard,
+        # so its destination travels with the child
+        n = n_rec
         cols = {name: recs[name][:n] for name, _, _ in N.RECORD_FIELDS}
         pidx = cols["path_idx"]
         has_child = torch.zeros(n, dtype=torch.int64, device="cuda")
         if n > 1:
             has_child[:-1] = (pidx[1:] == pidx[:-1]).to(torch.int64)
         parent_ipt = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+        par_shard = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+        par_row = torch.full((n,), -1, dtype=torch.int64, device="cuda")
         if n > 1:
             parent_ipt[1:] = cols["i_pt"][:-1]
-        parent_ipt[cols["depth"] == 0] = 0.0
+            par_shard[1:] = dest_shard[:-1]
+            par_row[1:] = dest_row[:-1]
+        first = cols["depth"] == 0
+        parent_ipt[first] = 0.0
+        par_shard[first] = -1
         grow = torch.arange(g0, g0 + n, dtype=torch.int64, device="cuda")
-        cols.update(parent_ipt=parent_ipt, has_child=has_child, grow=grow,
-                    dest_row=dest_row[g0:g0 + n])
-        dst = dest_shard[g0:g0 + n]
-        order = torch.argsort(dst, stable=True)
-        send_counts = torch.bincount(dst, minlength=world).tolist() if n else [0] * world
-        recv_counts = recv_counts_for(dest_shard, counts, me, world)
+        cols.update(parent_ipt=parent_ipt, has_child=has_child, grow=grow, par_shard=par_shard,
+                    par_row=par_row, dest_row=dest_row)
+        order = torch.argsort(dest_shard, stable=True)
+        send_counts = torch.bincount(dest_shard, minlength=world).tolist() if n else [0] * world
+        sc = torch.tensor(send_counts, dtype=torch.int64, device="cuda").reshape(-1, 1)
+        recv_counts = comm.all_to_all(sc, [1] * world, [1] * world).reshape(-1).tolist()
         payload = pack_payload(cols, n)
         got = comm.all_to_all(payload[order], send_counts, recv_counts)
         n_own = int(plan.rows[me])
@@ -411,13 +562,10 @@ class ShardedPathGraph:
         self.n = n_own
 
         # continuation parents: local row, or a halo slot for a remote one
-        depth = own["depth"].to(torch.int64)
-        has_par = depth > 0
-        par_g = own["grow"] - 1
         parent = torch.full((n_own,), -1, dtype=torch.int64, device="cuda")
-        rows_with = torch.nonzero(has_par).reshape(-1)
-        p_shard = dest_shard[par_g[rows_with]]
-        p_row = dest_row[par_g[rows_with]]
+        rows_with = torch.nonzero(own["par_shard"] >= 0).reshape(-1)
+        p_shard = own["par_shard"][rows_with]
+        p_row = own["par_row"][rows_with]
         local_mask = p_shard == me
         parent[rows_with[local_mask]] = p_row[local_mask]
         remote = ~local_mask

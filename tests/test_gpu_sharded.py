@@ -18,13 +18,15 @@ pytestmark = pytest.mark.gpu
 CASES = {
     "c1floor": dict(res=(24, 24), spp=2, max_depth=16, K=32, iters=6, seed=1),
     "cloud": dict(res=(20, 20), spp=4, max_depth=64, K=16, iters=5, seed=2),
+    # small K: many oversize groups and deep split chains in both classes
+    "c1floor_k4": dict(res=(16, 16), spp=2, max_depth=16, K=4, iters=4, seed=5),
 }
 
 
 def _scene(name, res):
     from paper_2404_11894_b200 import scenes as S
 
-    if name == "c1floor":
+    if name.startswith("c1floor"):
         return S.scene_c1(res, floor=True)
     return S.scene_c2(res, grid_n=16)
 
@@ -59,7 +61,8 @@ def _shard_worker(rank, world, port, name, out_path):
         if rank == 0:
             np.savez(out_path, image=out.image, incoming=inc.cpu().numpy(),
                      i_bar=ibar.cpu().numpy(), residuals=np.array(out.residuals),
-                     halo=out.graph.halo.n_halo, n_total=out.n_records_total)
+                     halo=out.graph.halo.n_halo, n_total=out.n_records_total,
+                     n_clusters=out.graph.n_clusters_total, n_splits=out.graph.n_splits)
     finally:
         dist.destroy_process_group()
 
@@ -87,12 +90,16 @@ def test_sharded_render_is_bit_identical(cuda, name, world):
             out = render_pg_sharded(_scene(name, c["res"]), _config(c), ShardComm())
             inc, ibar = out.graph.gather_solution()
             got = dict(image=out.image, incoming=inc.cpu().numpy(), i_bar=ibar.cpu().numpy(),
-                       residuals=np.array(out.residuals), halo=0, n_total=out.n_records_total)
+                       residuals=np.array(out.residuals), halo=0, n_total=out.n_records_total,
+                       n_clusters=out.graph.n_clusters_total, n_splits=out.graph.n_splits)
         else:
             mp.spawn(_shard_worker, args=(world, _free_port(), name, path), nprocs=world,
                      join=True)
             got = dict(np.load(path))
     assert int(got["n_total"]) == ref.trace.records.n
+    info = ref.graph.info()
+    assert int(got["n_clusters"]) == info["n_clusters"]
+    assert int(got["n_splits"]) == info["n_splits"]
     if world > 1:
         assert int(got["halo"]) > 0, "expected continuation edges across shards"
     np.testing.assert_array_equal(got["image"], ref.image)

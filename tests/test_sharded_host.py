@@ -46,6 +46,21 @@ def _problem(seed=0, n_paths=300, k=8):
                 centers=centers, pos=pos, a=a, b=b, i0=i0, w=w, n=n, m=m)
 
 
+def _destinations(P, plan):
+    """(shard, row) of every record: its cluster's shard, the cluster's first
+    row there plus the record's rank among the members (as the sharded build
+    derives them from cluster_distributed's row_cluster/row_rank)."""
+    n, m = P["n"], P["m"]
+    k_of = np.empty(n, np.int64)
+    rank = np.empty(n, np.int64)
+    for k in range(m):
+        mem = P["perm"][P["cl_off"][k]:P["cl_off"][k + 1]]
+        k_of[mem] = k
+        rank[mem] = np.arange(mem.size)
+    k_of, rank = torch.tensor(k_of), torch.tensor(rank)
+    return plan.owner[k_of], plan.local_start[k_of] + rank
+
+
 def _global_iterate(P, T):
     """Reference emulation: I[parent(r)] = a[r] * (W I)[r] + b[r], record order."""
     n = P["n"]
@@ -78,9 +93,7 @@ def _worker(rank, world, port, T, out_q):
         counts = [cuts[r + 1] - cuts[r] for r in range(world)]
         sizes = torch.tensor(P["sizes"])
         plan = S.plan_owners(sizes, torch.tensor(P["pos"][P["centers"]]), world)
-        perm = torch.tensor(P["perm"], dtype=torch.int32)
-        cl_off = torch.tensor(P["cl_off"], dtype=torch.int32)
-        dest_shard, dest_row = S.row_destinations(perm, cl_off, plan)
+        dest_shard, dest_row = _destinations(P, plan)
         # every shard owns a permutation of its rows; members stay ascending
         mine = torch.nonzero(dest_shard == rank).reshape(-1)
         assert sorted(dest_row[mine].tolist()) == list(range(plan.rows[rank]))
@@ -95,7 +108,8 @@ def _worker(rank, world, port, T, out_q):
         dst = dest_shard[grow]
         order = torch.argsort(dst, stable=True)
         send_counts = torch.bincount(dst, minlength=world).tolist()
-        recv_counts = S.recv_counts_for(dest_shard, counts, rank, world)
+        sc = torch.tensor(send_counts, dtype=torch.int64).reshape(-1, 1)
+        recv_counts = comm.all_to_all(sc, [1] * world, [1] * world).reshape(-1).tolist()
         got = comm.all_to_all(torch.stack([grow, dest_row[grow]], 1)[order], send_counts,
                               recv_counts)
         own = torch.empty(plan.rows[rank], dtype=torch.int64)
