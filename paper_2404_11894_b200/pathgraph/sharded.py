@@ -298,8 +298,14 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         pref = int(counts[:me].sum())
         my_n = int(rows.numel())
         m = -(-n_c // K)
-        # centers: Generator.choice(n, m, replace=False) (clustering.py:51)
-        idx = torch.as_tensor(rng.choice(n_c, m, replace=False), dtype=torch.int64, device=dev)
+        # centers: Generator.choice(n, m, replace=False) (clustering.py:51), by
+        # the native bit-exact replica (numpy's own tail shuffle builds an
+        # n-element index array)
+        idx_h = np.empty(m, dtype=np.int64)
+        st0 = N.Pcg64State.from_generator(rng)
+        N.check(lib.vpg_rng_choice(ctypes.byref(st0), n_c, m, idx_h.ctypes.data))
+        st0.store_into(rng)
+        idx = torch.as_tensor(idx_h, device=dev)
         mine = torch.nonzero((idx >= pref) & (idx < pref + my_n)).reshape(-1)
         c_rows = rows[idx[mine] - pref]
         msg = torch.cat([mine.to(torch.float64).reshape(-1, 1), pos[c_rows],
@@ -368,9 +374,8 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             if hit.numel():
                 kk = torch.searchsorted(over, gj[hit])
                 cslot[kk] = hit  # members ascending: one hit per group
-            ids = torch.arange(allm.shape[0], dtype=torch.int32).numpy().copy()
-            h = allm[:, 2:6].cpu().numpy()
-            x, y, z, d0 = (np.ascontiguousarray(h[:, i]) for i in range(4))
+            ids = np.arange(allm.shape[0], dtype=np.int32)
+            x, y, z, d0 = allm[:, 2:6].t().contiguous().cpu().numpy()  # SoA rows
             st = N.Pcg64State.from_generator(rng)
             cap = int(allm.shape[0]) + n_over + 1
             o_n = ctypes.c_int64()
@@ -393,12 +398,15 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             # final groups: members (staged index) in order; cluster ids: the
             # originals keep their slot among the non-empty groups, split-off
             # groups are appended
+            # the final groups' ranges tile the staged array: each position's
+            # group is the last range starting at or before it
             ids_t = torch.as_tensor(ids.astype(np.int64), device=dev)
-            fg = torch.as_tensor(np.repeat(np.arange(ng), o_s[:ng]), device=dev)
-            fpos = torch.as_tensor(np.concatenate([np.arange(sz) for sz in o_s[:ng]]) if ng else
-                                   np.zeros(0, np.int64), device=dev)
-            member_idx = torch.cat([ids_t[int(b):int(b) + int(sz)] for b, sz in
-                                    zip(o_b[:ng], o_s[:ng])]) if ng else ids_t[:0]
+            b_t = torch.as_tensor(o_b[:ng], device=dev)
+            order_b = torch.argsort(b_t)
+            posn = torch.arange(ids_t.numel(), device=dev)
+            fg = order_b[torch.searchsorted(b_t[order_b], posn, right=True) - 1]
+            fpos = posn - b_t[fg]
+            member_idx = ids_t
             g_cid = torch.empty(ng, dtype=torch.int64, device=dev)
             g_cid[:n_over] = cid_of_j[over]
             g_cid[n_over:] = base + n_ne + torch.arange(ng - n_over, device=dev)
