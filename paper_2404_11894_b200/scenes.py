@@ -73,6 +73,26 @@ def scene_c1(res=(64, 64), floor: bool = False) -> Scene:
     return Scene(_camera(32.0, res), [med], surfaces, [light])
 
 
+def scene_mixed(res=(12, 12)) -> Scene:
+    """Test scene covering what the configs do not: a chromatic, anisotropic
+    homogeneous medium, sphere and box surfaces (Lambertian and black), a
+    floor, and a point light beside the area light (delta and non-delta
+    emitters, several surface compatibility classes)."""
+    quad, light = _area_light()
+    med = Medium("homogeneous", (2.0, 1.5, 1.0), (1.6, 1.2, 0.7), 0.5, (-1, -1, -1, 1, 1, 1),
+                 name="haze")
+    surfaces = [
+        quad,
+        Surface("sphere", (0.35, -0.3, 0.2, 0.35), "lambertian", albedo=(0.8, 0.5, 0.3)),
+        Surface("box", (-0.8, -0.9, -0.3, -0.4, -0.5, 0.3), "lambertian", albedo=(0.3, 0.6, 0.9)),
+        Surface("box", (0.3, 0.4, -0.6, 0.6, 0.7, -0.2), "black"),
+        Surface("quad", (-3.0, -1.2, 3.0, 6.0, 0.0, 0.0, 0.0, 0.0, -6.0), "lambertian",
+                albedo=(0.6, 0.6, 0.6)),
+    ]
+    point = Emitter("point", (3.0, 2.5, 2.0), position=(-0.5, 0.8, -1.5))
+    return Scene(_camera(32.0, res), [med], surfaces, [light, point])
+
+
 def scene_c2(res=(512, 512), grid_n: int = 256) -> Scene:
     quad, light = _area_light()
     sun = Emitter("directional", (3.0, 2.9, 2.6), direction=(0.3, -1.0, 0.2))

@@ -59,6 +59,7 @@ CASES = {
     "c1floor_16": (lambda: S.scene_c1((16, 16), floor=True), 4, 16, 1, [32], 3),
     "cloud_16": (lambda: S.scene_c2((16, 16), grid_n=16), 4, 64, 2, [32], 0),
     "dense_12": (lambda: S.scene_c3((12, 12)), 2, 64, 0, [32], 0),
+    "mixed_12": (lambda: S.scene_mixed((12, 12)), 4, 32, 4, [16], 2),
 }
 
 

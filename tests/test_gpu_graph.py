@@ -16,6 +16,7 @@ from oracle import pathgraph_oracle as O
 pytestmark = pytest.mark.gpu
 
 CASES = [("c1_16", 32), ("c1_16", 8), ("c1_16", 1), ("c1floor_16", 32), ("cloud_16", 32),
+         ("mixed_12", 16),
          ("dense_12", 32)]
 
 

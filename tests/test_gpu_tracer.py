@@ -19,6 +19,7 @@ TRACE_CASES = {
     "c1floor_16": (lambda: S.scene_c1((16, 16), floor=True), 4, 16, 1),
     "cloud_16": (lambda: S.scene_c2((16, 16), grid_n=16), 4, 64, 2),
     "dense_12": (lambda: S.scene_c3((12, 12)), 2, 64, 0),
+    "mixed_12": (lambda: S.scene_mixed((12, 12)), 4, 32, 4),
 }
 VEC = ["pos", "omega_out", "normal", "coeff", "g", "phase_dir", "pdf_phase", "pdf_emit_at_phase",
        "emit_dir", "pdf_emit", "d_emit", "d_phase", "i_pt", "w_cont"]

@@ -8,6 +8,7 @@ from conftest import golden
 from oracle import pathgraph_oracle as O
 
 CASES = [("c1_16", 32), ("c1_16", 8), ("c1_16", 1), ("c1floor_16", 32), ("cloud_16", 32),
+         ("mixed_12", 16),
          ("dense_12", 32)]
 
 
@@ -89,3 +90,32 @@ def test_oracle_pt_image_and_k1_identity():
     g = O.build_graph(rec, paths, w, h, spp, 1, int(z["seed"]))
     inc, ib, _, _ = O.solve(g, 10, 0.0)
     np.testing.assert_allclose(O.splat(g, ib), z["pt_image"], rtol=1e-5, atol=1e-12)
+
+
+# the C tracer restatement vs the reference's own records (same scenes and
+# settings as tests/golden/make_golden.py)
+TRACE_GOLDENS = {
+    "c1_16": ("scene_c1", dict(res=(16, 16)), 4, 16, 0),
+    "c1floor_16": ("scene_c1", dict(res=(16, 16), floor=True), 4, 16, 1),
+    "cloud_16": ("scene_c2", dict(res=(16, 16), grid_n=16), 4, 64, 2),
+    "dense_12": ("scene_c3", dict(res=(12, 12)), 2, 64, 0),
+    "mixed_12": ("scene_mixed", dict(res=(12, 12)), 4, 32, 4),
+}
+
+
+@pytest.mark.parametrize("name", list(TRACE_GOLDENS))
+def test_tracer_oracle_matches_reference_records(name):
+    from oracle import tracer_oracle as T
+    from paper_2404_11894_b200 import scenes as S
+    from paper_2404_11894_b200.harness.config import RenderConfig
+
+    fac, kw, spp, md, seed = TRACE_GOLDENS[name]
+    z = golden(name)
+    rec, paths = T.trace_records(getattr(S, fac)(**kw), RenderConfig(spp=spp, max_depth=md,
+                                                                       seed=seed))
+    ref_rec, ref_paths = O.load_golden_records(z)
+    assert np.array_equal(paths["rec_count"], ref_paths["rec_count"])
+    for f, v in rec.items():
+        np.testing.assert_allclose(v, ref_rec[f], rtol=1e-12, atol=0, err_msg=f)
+    for f in ("cam_weight", "d_cam", "direct0", "pt_estimate"):
+        np.testing.assert_allclose(paths[f], ref_paths[f], rtol=1e-12, atol=0, err_msg=f)
