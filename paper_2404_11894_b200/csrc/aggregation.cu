@@ -143,7 +143,8 @@ __device__ __forceinline__ double strategy_pdf(const double* __restrict__ geo, i
 // Dynamic shared memory for clusters of up to S members:
 //   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2
 //   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
-//   pd, pe  S*(S+1) floats each (pair densities, row-padded)
+//   pd     S*(S+1) floats (phase-direction pair densities, row-padded; the
+//          emitter-direction ones are recomputed in pass 2b)
 __global__ void __launch_bounds__(kAggThreads)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
@@ -155,7 +156,6 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   double* geo = reinterpret_cast<double*>(smem);
   double* wts = geo + 12 * S;
   float* pd = reinterpret_cast<float*>(wts + 7 * S);
-  float* pe = pd + S * (S + 1);
   __shared__ int s_volume;
   const int tid = threadIdx.x;
 
@@ -205,7 +205,6 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
           const double a = strategy_pdf(geo, S, l, volume, dpx, dpy, dpz);
           const double b = strategy_pdf(geo, S, l, volume, dex, dey, dez);
           pd[l * (S + 1) + j] = float(a);
-          pe[l * (S + 1) + j] = float(b);
           sp = __dadd_rn(sp, a);
           se = __dadd_rn(se, b);
         }
@@ -257,10 +256,13 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
       double dx = 0.0, dy = 0.0, dz = 0.0;
       if (active) {
         const float* prow = pd + r * (S + 1);
-        const float* erow = pe + r * (S + 1);
         const int j0 = h * slice2, j1 = min(s, j0 + slice2);
         for (int j = j0; j < j1; ++j) {
-          const double a = prow[j], b = erow[j];
+          // the emitter-direction density is recomputed rather than kept in
+          // shared memory: half the pair storage, 8 CTAs per SM instead of 5
+          const double a = prow[j];
+          const double b = strategy_pdf(geo, S, r, volume, geo[6 * S + j], geo[7 * S + j],
+                                        geo[8 * S + j]);
           dx += b * wts[S + j] + a * wts[4 * S + j];
           dy += b * wts[2 * S + j] + a * wts[5 * S + j];
           dz += b * wts[3 * S + j] + a * wts[6 * S + j];
@@ -373,7 +375,7 @@ void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
                      int S, cudaStream_t s) {
   if (max_count <= 0) return;
-  const size_t smem = size_t(19) * S * sizeof(double) + size_t(2) * S * (S + 1) * sizeof(float);
+  const size_t smem = size_t(19) * S * sizeof(double) + size_t(S) * (S + 1) * sizeof(float);
   VPG_REQUIRE(smem <= kAggSmemMax, VPG_ELIMIT,
               "clusters larger than 160 members (cluster_size > 80) are not supported");
   static bool attr_set = false;
