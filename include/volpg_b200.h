@@ -372,6 +372,24 @@ int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, double* 
                       void* stream);
 int vpg_scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                         int64_t path_begin, const vpg_records* out, void* stream);
+/* ------------------------------------------------------------ VPGR codec
+ * Packed rows (a VPGR dump's record or path block, records.py:191-256) <->
+ * per-field device arrays, on the device: `packed` (device) holds n rows of
+ * row_bytes; field f occupies bytes [offset, offset+bytes) of a row and
+ * fields[f].ptr (device) is its array (row i at ptr + i*bytes).  Loading a
+ * dump is one host->device copy of the block plus vpg_unpack_rows; saving
+ * from the device is vpg_pack_rows plus one device->host copy. */
+#define VPG_CODEC_MAX_FIELDS 24
+typedef struct vpg_codec_field {
+  int32_t offset;
+  int32_t bytes;
+  void* ptr;
+} vpg_codec_field;
+int vpg_unpack_rows(const void* packed, int64_t n, int32_t row_bytes,
+                    const vpg_codec_field* fields, int32_t n_fields, void* stream);
+int vpg_pack_rows(void* packed, int64_t n, int32_t row_bytes, const vpg_codec_field* fields,
+                  int32_t n_fields, void* stream);
+
 /* extra_direct_kernel (kernels.py:499-553). */
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream);

@@ -85,6 +85,10 @@ class GraphViews(C.Structure):
                  ("red", c_p), ("ctl", c_p), ("performed", c_i32), ("_pad", c_i32)])
 
 
+class CodecField(C.Structure):
+    _fields_ = [("offset", c_i32), ("bytes", c_i32), ("ptr", c_p)]
+
+
 def _arr(t, *dims):
     for d in reversed(dims):
         t = t * d
@@ -128,6 +132,8 @@ _SIGNATURES = {
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,
                                    c_p, c_p, c_p, c_p]),
+    "vpg_unpack_rows": (C.c_int, [c_p, c_i64, c_i32, C.POINTER(CodecField), c_i32, c_p]),
+    "vpg_pack_rows": (C.c_int, [c_p, c_i64, c_i32, C.POINTER(CodecField), c_i32, c_p]),
     "vpg_split_groups_soa": (C.c_int, [C.POINTER(Pcg64State), c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
                                        c_p, c_p, c_i64, c_i64, C.POINTER(c_i64), c_p, c_p, c_p,
                                        C.POINTER(c_i64)]),

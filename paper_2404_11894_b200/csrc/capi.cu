@@ -353,6 +353,22 @@ int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64
   return VPG_OK;
 }
 
+int vpg_unpack_rows(const void* packed, int64_t n, int32_t row_bytes,
+                    const vpg_codec_field* fields, int32_t n_fields, void* stream) {
+  return guarded([&] {
+    vpg::codec_rows(true, static_cast<uint8_t*>(const_cast<void*>(packed)), n, row_bytes, fields,
+                    n_fields, as_stream(stream));
+  });
+}
+
+int vpg_pack_rows(void* packed, int64_t n, int32_t row_bytes, const vpg_codec_field* fields,
+                  int32_t n_fields, void* stream) {
+  return guarded([&] {
+    vpg::codec_rows(false, static_cast<uint8_t*>(packed), n, row_bytes, fields, n_fields,
+                    as_stream(stream));
+  });
+}
+
 int vpg_split_groups_soa(vpg_pcg64* rng, int32_t* ids, const double* x, const double* y,
                          const double* z, const double* d0, int64_t n_groups, const int64_t* sizes,
                          const int64_t* centers, const int64_t* cslot, int64_t max_size,

@@ -39,6 +39,8 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s);
 int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, const double* lo,
                        const double* hi, int32_t* assign, cudaStream_t s);
+void codec_rows(bool unpack, uint8_t* packed, int64_t n, int32_t row_bytes,
+                const vpg_codec_field* fields, int32_t n_fields, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
                   int n_extra, cudaStream_t s);
 }  // namespace vpg

@@ -349,8 +349,113 @@ def splat_pt_image(paths: PathSoA, width: int, height: int, spp: int) -> np.ndar
     return img.cpu().numpy()
 
 
+_CODEC_CHUNK = 32 << 20  # bytes of packed rows per staged chunk
+_STAGING = {}
+
+
+def _staging(torch, nbytes):
+    """Two (pinned host, device, event) staging buffers, cached per device."""
+    key = torch.cuda.current_device()
+    cur = _STAGING.get(key)
+    if cur is None or cur[0][0].numel() < nbytes:
+        cur = [(torch.empty(nbytes, dtype=torch.uint8).pin_memory(),
+                torch.empty(nbytes, dtype=torch.uint8, device="cuda"), torch.cuda.Event())
+               for _ in range(2)]
+        for _, _, ev in cur:
+            ev.record()
+        _STAGING[key] = cur
+    return cur
+
+
+def _codec_table(dtype, dev: dict, r0: int):
+    """CodecField array of a packed dtype against device arrays, rows from r0."""
+    names = dtype.names
+    table = (N.CodecField * len(names))()
+    for i, name in enumerate(names):
+        off = dtype.fields[name][1]
+        nbytes = dtype.fields[name][0].itemsize
+        table[i].offset = off
+        table[i].bytes = nbytes
+        table[i].ptr = dev[name].data_ptr() + r0 * nbytes
+    return table
+
+
+def _block_to_device(f, path, n, dtype, dev, torch, stream, what):
+    """Stream n packed rows from the file into the device arrays: chunked
+    reads into pinned staging, async upload and vpg_unpack_rows on `stream`,
+    double-buffered so the read of chunk k+1 overlaps chunk k on the device."""
+    row = dtype.itemsize
+    per = max(1, _CODEC_CHUNK // row)
+    bufs = _staging(torch, per * row)
+    lib = N.lib()
+    for c, r0 in enumerate(range(0, n, per)):
+        host, devbuf, ev = bufs[c % 2]
+        ev.synchronize()
+        cnt = min(per, n - r0)
+        nb = cnt * row
+        got = f.readinto(memoryview(host.numpy())[:nb])
+        if got != nb:
+            raise IOError(f"{path}: truncated {what} block")
+        with torch.cuda.stream(stream):
+            devbuf[:nb].copy_(host[:nb], non_blocking=True)
+            table = _codec_table(dtype, dev, r0)
+            N.check(lib.vpg_unpack_rows(devbuf.data_ptr(), cnt, row, table, len(table),
+                                        N.stream_handle()))
+            ev.record(stream)
+
+
+def _block_from_device(f, n, dtype, dev, torch, stream):
+    """Write n rows of the device arrays as packed rows: vpg_pack_rows into a
+    device staging chunk, async download to pinned memory, file write of the
+    previous chunk while the next one packs."""
+    row = dtype.itemsize
+    per = max(1, _CODEC_CHUNK // row)
+    bufs = _staging(torch, per * row)
+    lib = N.lib()
+    pending = None
+    for c, r0 in enumerate(range(0, n, per)):
+        host, devbuf, ev = bufs[c % 2]
+        ev.synchronize()
+        cnt = min(per, n - r0)
+        nb = cnt * row
+        with torch.cuda.stream(stream):
+            table = _codec_table(dtype, dev, r0)
+            N.check(lib.vpg_pack_rows(devbuf.data_ptr(), cnt, row, table, len(table),
+                                      N.stream_handle()))
+            host[:nb].copy_(devbuf[:nb], non_blocking=True)
+            ev.record(stream)
+        if pending is not None:
+            pending[1].synchronize()
+            f.write(memoryview(pending[0].numpy())[:pending[2]])
+        pending = (host, ev, nb)
+    if pending is not None:
+        pending[1].synchronize()
+        f.write(memoryview(pending[0].numpy())[:pending[2]])
+
+
+def _write_header(f, out: TraceOutput):
+    f.write(VPGR_MAGIC)
+    f.write(struct.pack("<IQQIII", VPGR_VERSION, out.records.n, out.paths.n, out.width,
+                        out.height, out.spp))
+
+
 def save_records(path, out: TraceOutput) -> None:
-    """Write the versioned VPGR dump (reference: records.py:191-217)."""
+    """Write the versioned VPGR dump (reference: records.py:191-217).
+
+    Device-resident records (a device trace, or a device load) are packed on
+    the device (vpg_pack_rows) and streamed to the file in chunks; host
+    records are packed with numpy.  Either way the file is byte-identical to
+    the reference's dump of the same records."""
+    if out.records.on_device() and out.paths.on_device():
+        torch = N.require_cuda()
+        rdev, pdev = out.records.device_tensors(), out.paths.device_tensors()
+        stream = _copy_stream(torch)
+        stream.wait_stream(torch.cuda.current_stream())
+        with open(path, "wb") as f:
+            _write_header(f, out)
+            _block_from_device(f, out.records.n, RECORD_DTYPE, rdev, torch, stream)
+            _block_from_device(f, out.paths.n, PATH_DTYPE, pdev, torch, stream)
+        return
     rec = np.zeros(out.records.n, dtype=RECORD_DTYPE)
     for name, _, _ in N.RECORD_FIELDS:
         rec[name] = out.records._get(name)
@@ -358,24 +463,58 @@ def save_records(path, out: TraceOutput) -> None:
     for name, _, _ in N.PATH_FIELDS:
         pth[name] = out.paths._get(name)
     with open(path, "wb") as f:
-        f.write(VPGR_MAGIC)
-        f.write(struct.pack("<IQQIII", VPGR_VERSION, out.records.n, out.paths.n,
-                            out.width, out.height, out.spp))
+        _write_header(f, out)
         f.write(rec.tobytes())
         f.write(pth.tobytes())
 
 
-def load_records(path, pin: bool = False) -> TraceOutput:
-    """Read a VPGR dump (reference: records.py:220-256) into host SoA arrays.
+def _read_header(f, path):
+    if f.read(4) != VPGR_MAGIC:
+        raise IOError(f"{path}: not a VPGR record dump")
+    head = f.read(32)
+    if len(head) != 32:
+        raise IOError(f"{path}: truncated VPGR header")
+    version, n_rec, n_path, width, height, spp = struct.unpack("<IQQIII", head)
+    if version != VPGR_VERSION:
+        raise IOError(f"{path}: unsupported VPGR version {version}")
+    return n_rec, n_path, width, height, spp
 
-    pin=True places the arrays in page-locked memory for asynchronous upload.
+
+def _device_empty(torch, fields, n):
+    out = {}
+    for name, width, code in fields:
+        np_dt = np.dtype("<" + code)
+        t_dt = {np.dtype("<f8"): torch.float64, np.dtype("<i4"): torch.int32,
+                np.dtype("<i8"): torch.int64, np.dtype("<u1"): torch.uint8}[np_dt]
+        shape = (n, width) if width > 1 else (n,)
+        out[name] = torch.empty(shape, dtype=t_dt, device="cuda")
+    return out
+
+
+def load_records(path, pin: bool = False, device: bool = False) -> TraceOutput:
+    """Read a VPGR dump (reference: records.py:220-256).
+
+    Host load (default): numpy SoA arrays; pin=True places them in
+    page-locked memory for asynchronous upload.  device=True loads straight
+    into HBM: the packed blocks are streamed through pinned staging chunks
+    and transposed to SoA on the device (vpg_unpack_rows), so the records
+    never exist as host SoA arrays (they materialise on first host read).
+    A short or cut block raises IOError either way.
     """
     with open(path, "rb") as f:
-        if f.read(4) != VPGR_MAGIC:
-            raise IOError(f"{path}: not a VPGR record dump")
-        version, n_rec, n_path, width, height, spp = struct.unpack("<IQQIII", f.read(32))
-        if version != VPGR_VERSION:
-            raise IOError(f"{path}: unsupported VPGR version {version}")
+        n_rec, n_path, width, height, spp = _read_header(f, path)
+        if device:
+            torch = N.require_cuda()
+            main = torch.cuda.current_stream()
+            stream = _copy_stream(torch)
+            rdev = _device_empty(torch, N.RECORD_FIELDS, n_rec)
+            pdev = _device_empty(torch, N.PATH_FIELDS, n_path)
+            stream.wait_stream(main)
+            _block_to_device(f, path, n_rec, RECORD_DTYPE, rdev, torch, stream, "record")
+            _block_to_device(f, path, n_path, PATH_DTYPE, pdev, torch, stream, "path")
+            main.wait_stream(stream)
+            return TraceOutput(None, RecordSoA.from_device(rdev, n_rec),
+                               PathSoA.from_device(pdev, n_path), width, height, spp)
         # a short block is a truncated dump (IOError, as the reference raises
         # for a block cut at a record boundary) wherever the cut falls
         raw = f.read(RECORD_DTYPE.itemsize * n_rec)

@@ -61,3 +61,69 @@ def test_solve_from_records_on_reference_dump(cuda):
     assert_rel(image, z["image"], 1e-4, what="image")
     assert_rel(result.incoming, z["incoming"], 1e-4, what="incoming")
     assert_rel(result.i_bar, z["i_bar"], 1e-4, what="i_bar")
+
+
+@pytest.mark.gpu
+def test_device_load_matches_host_load(cuda, monkeypatch):
+    import paper_2404_11894_b200.transport.records as R
+
+    host = load_records(DUMP)
+    # small staging chunks so the double-buffered path runs several chunks
+    monkeypatch.setattr(R, "_CODEC_CHUNK", 290 * 37)
+    monkeypatch.setattr(R, "_STAGING", {})
+    dev = load_records(DUMP, device=True)
+    assert dev.records.on_device() and dev.paths.on_device()
+    assert (dev.width, dev.height, dev.spp) == (host.width, host.height, host.spp)
+    for soa_h, soa_d in ((host.records, dev.records), (host.paths, dev.paths)):
+        th = soa_h.host_arrays()
+        td = {k: v.cpu().numpy() for k, v in soa_d.device_tensors().items()}
+        for name in th:
+            assert td[name].dtype == th[name].dtype, name
+            np.testing.assert_array_equal(td[name], th[name], err_msg=name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", [290 * 5, 32 << 20])
+def test_device_save_is_byte_identical(cuda, monkeypatch, tmp_path, chunk):
+    import paper_2404_11894_b200.transport.records as R
+
+    monkeypatch.setattr(R, "_CODEC_CHUNK", chunk)
+    monkeypatch.setattr(R, "_STAGING", {})
+    dev = load_records(DUMP, device=True)
+    dev.records.drop_host()
+    out = tmp_path / "dev.vpgr"
+    save_records(str(out), dev)
+    assert out.read_bytes() == open(DUMP, "rb").read()
+
+
+@pytest.mark.gpu
+def test_device_trace_dump_round_trip(cuda, tmp_path):
+    """A device trace saved from HBM and loaded back into HBM is bit-identical
+    field by field, and the host save of the same trace is the same file."""
+    from paper_2404_11894_b200 import scenes as S
+    from paper_2404_11894_b200.harness.config import RenderConfig
+    from paper_2404_11894_b200.transport import render_pt
+
+    t = render_pt(S.scene_mixed((12, 12)), RenderConfig(spp=2, max_depth=24, seed=3),
+                  with_records=True)
+    assert t.records.on_device()
+    a, b = tmp_path / "dev.vpgr", tmp_path / "host.vpgr"
+    save_records(str(a), t)
+    back = load_records(str(a), device=True)
+    for soa, soa2 in ((t.records, back.records), (t.paths, back.paths)):
+        d1, d2 = soa.device_tensors(), soa2.device_tensors()
+        for name in d1:
+            assert cuda.equal(d1[name], d2[name]), name
+    host = load_records(str(a))
+    save_records(str(b), host)
+    assert a.read_bytes() == b.read_bytes()
+
+
+@pytest.mark.gpu
+def test_device_load_truncated_raises(cuda, tmp_path):
+    raw = open(DUMP, "rb").read()
+    for cut in (100, 290 * 491 // 2):
+        p = tmp_path / f"cut{cut}.vpgr"
+        p.write_bytes(raw[:-cut])
+        with pytest.raises(IOError):
+            load_records(str(p), device=True)
