@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -123,28 +124,192 @@ __global__ void k_parent_links(vpg_records rec, const int32_t* __restrict__ clpo
   }
 }
 
-// Member l's strategy density toward direction d (graph.py:82-91), fp64 in
-// the reference's rounding order.
-__device__ __forceinline__ double strategy_pdf(const double* __restrict__ geo, int S, int l,
-                                               bool volume, double dx, double dy, double dz) {
+// Member l's strategy density toward direction d (graph.py:82-91).  Surface
+// members (Lambertian, max(0, n.d)/pi) follow the reference's fp64 rounding
+// order exactly, so the zero pattern (and with it the inclusion masks) is
+// the reference's.
+__device__ __forceinline__ double surface_pdf(const double* __restrict__ geo, int S, int l,
+                                              double dx, double dy, double dz) {
   const double cs = dot3(geo[l], geo[S + l], geo[2 * S + l], dx, dy, dz);
-  if (!volume) return cs > 0.0 ? __dmul_rn(cs, kInvPi) : 0.0;
-  const double den = __dsub_rn(geo[10 * S + l], __dmul_rn(geo[11 * S + l], cs));
-  // num / (den * sqrt(den)) as num * rsqrt(den)^3, rsqrt from the fp32
-  // MUFU estimate (rel. error < 2.4e-7) and one fp64 Newton step (rel.
-  // error < 1e-13): den itself -- where the cancellation at g -> 1 lives --
-  // stays fp64.  Far inside the 1e-4 radiance bar, at a fraction of the
-  // fp64 rsqrt's issue cost.
-  const double r0 = double(rsqrtf(float(den)));
-  const double rs = r0 * (1.5 - 0.5 * den * r0 * r0);
-  return geo[9 * S + l] * (rs * rs * rs);
+  return cs > 0.0 ? __dmul_rn(cs, kInvPi) : 0.0;
+}
+
+// Volume members: HG (phase.py:17-21), num / (den * sqrt(den)) with
+// den = 1 + g^2 - 2 g cos.  The cosine and den -- where the cancellation at
+// g -> 1 lives -- stay fp64; den^-3/2 and the product are fp32 (MUFU rsqrt,
+// rel. error ~1e-7 on den's fp32 rounding), which is ~1e-6 on the density,
+// far inside the 1e-4 radiance bar, at a quarter of the fp64 issue cost.
+// A pdf is never 0 here unless num is (g = +-1), and then in both.
+__device__ __forceinline__ float hg_pdf(double ax, double ay, double az, double c1, double c2,
+                                        float num, double dx, double dy, double dz) {
+  const double cs = fma(az, dz, fma(ay, dy, ax * dx));
+  const double den = fma(-c2, cs, c1);
+  const float r = rsqrtf(float(den));
+  return num * (r * r * r);
 }
 
 // Dynamic shared memory for clusters of up to S members:
-//   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2
+//   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2 (num also
+//         as fp32 in the low word of its slot's float view, see below)
 //   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
+//          (volume clusters keep them as fp32 in the same region)
 //   pd     S*(S+1) floats (phase-direction pair densities, row-padded; the
 //          emitter-direction ones are recomputed in pass 2b)
+template <bool kVol>
+__device__ __forceinline__ void aggregate_cluster(
+    const Member* __restrict__ mem, int32_t q0, int s, int64_t wb, int64_t n, int S,
+    double* __restrict__ geo, double* __restrict__ wts, float* __restrict__ pd,
+    float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
+    float4* __restrict__ coeff_o, float4* __restrict__ rows_o, float4* __restrict__ i0_o) {
+  using acc_t = typename std::conditional<kVol, float, double>::type;
+  const int tid = threadIdx.x;
+  const float* numf = reinterpret_cast<const float*>(geo + 12 * S);  // S floats after geo
+  float* wtsf = reinterpret_cast<float*>(wts);
+  const double ks = double(s);
+
+  // pass 1: columns j, P threads per column (P = 4 for s <= 32, else 2) each
+  // summing a contiguous slice of l; the slices combine in a fixed order
+  // (((p0 + p1) + (p2 + p3))), so p-hat is deterministic.  The loop trip
+  // count is uniform so every lane reaches the shuffles.
+  const int P = s <= 32 ? 4 : 2;
+  const int slice = (s + P - 1) / P;
+  for (int base = 0; base < P * s; base += blockDim.x) {
+    const int t = base + tid;
+    const bool active = t < P * s;
+    const int j = t / P, h = t % P;
+    acc_t sp = 0, se = 0;
+    if (active) {
+      const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
+      const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
+      const int l0 = h * slice, l1 = min(s, l0 + slice);
+      for (int l = l0; l < l1; ++l) {
+        if constexpr (kVol) {
+          const double ax = geo[l], ay = geo[S + l], az = geo[2 * S + l];
+          const double c1 = geo[10 * S + l], c2 = geo[11 * S + l];
+          const float a = hg_pdf(ax, ay, az, c1, c2, numf[l], dpx, dpy, dpz);
+          const float b = hg_pdf(ax, ay, az, c1, c2, numf[l], dex, dey, dez);
+          pd[l * (S + 1) + j] = a;
+          sp += a;
+          se += b;
+        } else {
+          const double a = surface_pdf(geo, S, l, dpx, dpy, dpz);
+          const double b = surface_pdf(geo, S, l, dex, dey, dez);
+          pd[l * (S + 1) + j] = float(a);
+          sp = __dadd_rn(sp, a);
+          se = __dadd_rn(se, b);
+        }
+      }
+    }
+    sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 1);
+    se += __shfl_xor_sync(0xFFFFFFFFu, se, 1);
+    if (P == 4) {
+      sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 2);
+      se += __shfl_xor_sync(0xFFFFFFFFu, se, 2);
+    }
+    if (active && h == 0) {
+      const Member& mb = mem[q0 + j];
+      const double p_ind = double(sp);
+      const double p_dp = __dadd_rn(p_ind, __dmul_rn(ks, mb.pdf_eap));
+      const double p_de = (mb.flags & 1u) ? ks : __dadd_rn(double(se), __dmul_rn(ks, mb.pdf_e));
+      const int64_t q = q0 + j;
+      phat[q] = p_ind;
+      phat[n + q] = p_dp;
+      phat[2 * n + q] = p_de;
+      const bool inc_p = isfinite(p_ind) && p_ind > 0.0;
+      const bool inc_e = isfinite(p_de) && p_de > 0.0;
+      const bool ok_dp = inc_p && isfinite(p_dp) && p_dp > 0.0;
+      const double ie = inc_e ? __ddiv_rn(1.0, p_de) : 0.0;
+      const double ip = ok_dp ? __ddiv_rn(1.0, p_dp) : 0.0;
+      const double iw = inc_p ? __ddiv_rn(1.0, p_ind) : 0.0;
+      if constexpr (kVol) {
+        wtsf[j] = float(iw);
+        wtsf[S + j] = float(double(mb.de[0]) * ie);
+        wtsf[2 * S + j] = float(double(mb.de[1]) * ie);
+        wtsf[3 * S + j] = float(double(mb.de[2]) * ie);
+        wtsf[4 * S + j] = float(double(mb.dp[0]) * ip);
+        wtsf[5 * S + j] = float(double(mb.dp[1]) * ip);
+        wtsf[6 * S + j] = float(double(mb.dp[2]) * ip);
+      } else {
+        wts[j] = iw;
+        wts[S + j] = double(mb.de[0]) * ie;
+        wts[2 * S + j] = double(mb.de[1]) * ie;
+        wts[3 * S + j] = double(mb.de[2]) * ie;
+        wts[4 * S + j] = double(mb.dp[0]) * ip;
+        wts[5 * S + j] = double(mb.dp[1]) * ip;
+        wts[6 * S + j] = double(mb.dp[2]) * ip;
+      }
+    }
+  }
+  __syncthreads();
+
+  // pass 2a: the kernel block, transposed (wt[wb + j*s + r] = W[r, j])
+  for (int idx = tid; idx < s * s; idx += blockDim.x) {
+    const int j = idx / s, r = idx - j * s;
+    if constexpr (kVol)
+      wt[wb + idx] = pd[r * (S + 1) + j] * wtsf[j];
+    else
+      wt[wb + idx] = float(double(pd[r * (S + 1) + j]) * wts[j]);
+  }
+  // pass 2b: rows: D-bar and the solve vectors, P2 threads per row each
+  // summing a slice of the columns, combined in a fixed order
+  const int P2 = s <= 32 ? 4 : 2;
+  const int slice2 = (s + P2 - 1) / P2;
+  for (int base = 0; base < P2 * s; base += blockDim.x) {
+    const int t = base + tid;
+    const bool active = t < P2 * s;
+    const int r = t / P2, h = t % P2;
+    acc_t dx = 0, dy = 0, dz = 0;
+    if (active) {
+      const float* prow = pd + r * (S + 1);
+      const int j0 = h * slice2, j1 = min(s, j0 + slice2);
+      // the emitter-direction density is recomputed rather than kept in
+      // shared memory: half the pair storage, 8 CTAs per SM instead of 5
+      if constexpr (kVol) {
+        const double ax = geo[r], ay = geo[S + r], az = geo[2 * S + r];
+        const double c1 = geo[10 * S + r], c2 = geo[11 * S + r];
+        const float num = numf[r];
+        for (int j = j0; j < j1; ++j) {
+          const float a = prow[j];
+          const float b = hg_pdf(ax, ay, az, c1, c2, num, geo[6 * S + j], geo[7 * S + j],
+                                 geo[8 * S + j]);
+          dx += b * wtsf[S + j] + a * wtsf[4 * S + j];
+          dy += b * wtsf[2 * S + j] + a * wtsf[5 * S + j];
+          dz += b * wtsf[3 * S + j] + a * wtsf[6 * S + j];
+        }
+      } else {
+        for (int j = j0; j < j1; ++j) {
+          const double a = prow[j];
+          const double b = surface_pdf(geo, S, r, geo[6 * S + j], geo[7 * S + j], geo[8 * S + j]);
+          dx += b * wts[S + j] + a * wts[4 * S + j];
+          dy += b * wts[2 * S + j] + a * wts[5 * S + j];
+          dz += b * wts[3 * S + j] + a * wts[6 * S + j];
+        }
+      }
+    }
+    dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
+    dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
+    dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
+    if (P2 == 4) {
+      dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 2);
+      dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
+      dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 2);
+    }
+    if (active && h == 0) {
+      const Member& mb = mem[q0 + r];
+      const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
+      const double bx = kx * double(dx), by = ky * double(dy), bz = kz * double(dz);
+      const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
+      const int64_t q = q0 + r;
+      dbar_o[q] = f4(bx, by, bz);
+      coeff_o[q] = f4(kx, ky, kz);
+      rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
+                                  __int_as_float(-1));  // parent set by k_parent_links
+      rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
+      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kAggThreads)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
@@ -154,7 +319,8 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             float4* __restrict__ i0_o) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* geo = reinterpret_cast<double*>(smem);
-  double* wts = geo + 12 * S;
+  float* numf = reinterpret_cast<float*>(geo + 12 * S);
+  double* wts = geo + 12 * S + (S + 1) / 2;
   float* pd = reinterpret_cast<float*>(wts + 7 * S);
   __shared__ int s_volume;
   const int tid = threadIdx.x;
@@ -177,119 +343,20 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
       geo[8 * S + l] = mb.ez;
       const double g = mb.g;
       const double g2 = __dmul_rn(g, g);
-      geo[9 * S + l] = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
+      const double num = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
+      geo[9 * S + l] = num;
+      numf[l] = float(num);
       geo[10 * S + l] = __dadd_rn(1.0, g2);
       geo[11 * S + l] = __dmul_rn(2.0, g);
       if (l == 0) s_volume = (mb.flags & 4u) ? 0 : 1;
     }
     __syncthreads();
-    const bool volume = s_volume != 0;
-    const double ks = double(s);
-
-    // pass 1: columns j, P threads per column (P = 4 for s <= 32, else 2) each
-    // summing a contiguous slice of l; the slices combine in a fixed order
-    // (((p0 + p1) + (p2 + p3))), so p-hat is deterministic.  The loop trip
-    // count is uniform so every lane reaches the shuffles.
-    const int P = s <= 32 ? 4 : 2;
-    const int slice = (s + P - 1) / P;
-    for (int base = 0; base < P * s; base += blockDim.x) {
-      const int t = base + tid;
-      const bool active = t < P * s;
-      const int j = t / P, h = t % P;
-      double sp = 0.0, se = 0.0;
-      if (active) {
-        const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
-        const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
-        const int l0 = h * slice, l1 = min(s, l0 + slice);
-        for (int l = l0; l < l1; ++l) {
-          const double a = strategy_pdf(geo, S, l, volume, dpx, dpy, dpz);
-          const double b = strategy_pdf(geo, S, l, volume, dex, dey, dez);
-          pd[l * (S + 1) + j] = float(a);
-          sp = __dadd_rn(sp, a);
-          se = __dadd_rn(se, b);
-        }
-      }
-      sp = __dadd_rn(sp, __shfl_xor_sync(0xFFFFFFFFu, sp, 1));
-      se = __dadd_rn(se, __shfl_xor_sync(0xFFFFFFFFu, se, 1));
-      if (P == 4) {
-        sp = __dadd_rn(sp, __shfl_xor_sync(0xFFFFFFFFu, sp, 2));
-        se = __dadd_rn(se, __shfl_xor_sync(0xFFFFFFFFu, se, 2));
-      }
-      if (active && h == 0) {
-        const Member& mb = mem[q0 + j];
-        const double p_ind = sp;
-        const double p_dp = __dadd_rn(p_ind, __dmul_rn(ks, mb.pdf_eap));
-        const double p_de = (mb.flags & 1u) ? ks : __dadd_rn(se, __dmul_rn(ks, mb.pdf_e));
-        const int64_t q = q0 + j;
-        phat[q] = p_ind;
-        phat[n + q] = p_dp;
-        phat[2 * n + q] = p_de;
-        const bool inc_p = isfinite(p_ind) && p_ind > 0.0;
-        const bool inc_e = isfinite(p_de) && p_de > 0.0;
-        const bool ok_dp = inc_p && isfinite(p_dp) && p_dp > 0.0;
-        const double ie = inc_e ? __ddiv_rn(1.0, p_de) : 0.0;
-        const double ip = ok_dp ? __ddiv_rn(1.0, p_dp) : 0.0;
-        wts[j] = inc_p ? __ddiv_rn(1.0, p_ind) : 0.0;
-        wts[S + j] = double(mb.de[0]) * ie;
-        wts[2 * S + j] = double(mb.de[1]) * ie;
-        wts[3 * S + j] = double(mb.de[2]) * ie;
-        wts[4 * S + j] = double(mb.dp[0]) * ip;
-        wts[5 * S + j] = double(mb.dp[1]) * ip;
-        wts[6 * S + j] = double(mb.dp[2]) * ip;
-      }
-    }
-    __syncthreads();
-
-    // pass 2a: the kernel block, transposed (wt[wb + j*s + r] = W[r, j])
-    for (int idx = tid; idx < s * s; idx += blockDim.x) {
-      const int j = idx / s, r = idx - j * s;
-      wt[wb + idx] = float(double(pd[r * (S + 1) + j]) * wts[j]);
-    }
-    // pass 2b: rows: D-bar and the solve vectors, P2 threads per row each
-    // summing a slice of the columns, combined in a fixed order
-    const int P2 = s <= 32 ? 4 : 2;
-    const int slice2 = (s + P2 - 1) / P2;
-    for (int base = 0; base < P2 * s; base += blockDim.x) {
-      const int t = base + tid;
-      const bool active = t < P2 * s;
-      const int r = t / P2, h = t % P2;
-      double dx = 0.0, dy = 0.0, dz = 0.0;
-      if (active) {
-        const float* prow = pd + r * (S + 1);
-        const int j0 = h * slice2, j1 = min(s, j0 + slice2);
-        for (int j = j0; j < j1; ++j) {
-          // the emitter-direction density is recomputed rather than kept in
-          // shared memory: half the pair storage, 8 CTAs per SM instead of 5
-          const double a = prow[j];
-          const double b = strategy_pdf(geo, S, r, volume, geo[6 * S + j], geo[7 * S + j],
-                                        geo[8 * S + j]);
-          dx += b * wts[S + j] + a * wts[4 * S + j];
-          dy += b * wts[2 * S + j] + a * wts[5 * S + j];
-          dz += b * wts[3 * S + j] + a * wts[6 * S + j];
-        }
-      }
-      dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
-      dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
-      dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
-      if (P2 == 4) {
-        dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 2);
-        dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
-        dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 2);
-      }
-      if (active && h == 0) {
-        const Member& mb = mem[q0 + r];
-        const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
-        const double bx = kx * dx, by = ky * dy, bz = kz * dz;
-        const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
-        const int64_t q = q0 + r;
-        dbar_o[q] = f4(bx, by, bz);
-        coeff_o[q] = f4(kx, ky, kz);
-        rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
-                                    __int_as_float(-1));  // parent set by k_parent_links
-        rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
-        i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
-      }
-    }
+    if (s_volume)
+      aggregate_cluster<true>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+                              rows_o, i0_o);
+    else
+      aggregate_cluster<false>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+                               rows_o, i0_o);
     __syncthreads();
   }
 }
@@ -375,7 +442,8 @@ void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
                      int S, cudaStream_t s) {
   if (max_count <= 0) return;
-  const size_t smem = size_t(19) * S * sizeof(double) + size_t(S) * (S + 1) * sizeof(float);
+  const size_t smem = (size_t(19) * S + (S + 1) / 2) * sizeof(double) +
+                      size_t(S) * (S + 1) * sizeof(float);
   VPG_REQUIRE(smem <= kAggSmemMax, VPG_ELIMIT,
               "clusters larger than 160 members (cluster_size > 80) are not supported");
   static bool attr_set = false;

@@ -1591,6 +1591,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
           rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
           groups, cslot, max_size, &g->info.split_visits, h_masks.get());
       dbg.mark("split: loop", false);
+      if (dbg.on)
+        fprintf(stderr, "[vpg] class %d: %lld oversize groups, %lld staged members, %lld groups after\n",
+                c, (long long)n_over, (long long)staged, (long long)groups.size());
       const int64_t base_split = split_total;
       auto hb_own = std::make_unique<HostBuf<int64_t>>(groups.size() * 8 + 8);
       int64_t* hb = hb_own->get();
