@@ -42,7 +42,8 @@ struct __align__(32) Member {
   float coeff[3], wc[3];
   float ipt[3];
   uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface
-  uint32_t pad[8];
+  int32_t parent;  // cluster-major row of the continuation parent, -1 none / not yet known
+  uint32_t pad[7];
 };
 static_assert(sizeof(Member) == 192, "Member must stay 6 sectors");
 
@@ -100,7 +101,11 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
     const bool terminal = has_child ? !has_child[r]
                                     : !(r + 1 < n && rec.path_idx[r + 1] == rec.path_idx[r]);
     m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u);
-    for (int k = 0; k < 8; ++k) m.pad[k] = 0;
+    // continuation parent r-1 (records.py:128-140) when its row is already
+    // placed; a parent placed later (a split group) links its children in
+    // k_child_links.  Shard-local builds get theirs from k_set_parents.
+    m.parent = (!has_child && r > 0 && rec.path_idx[r - 1] == rec.path_idx[r]) ? clpos[r - 1] : -1;
+    for (int k = 0; k < 7; ++k) m.pad[k] = 0;
     out[q] = m;
     if (terminal)
       for (int c = 0; c < 3; ++c) tmax[c] = fmaxf(tmax[c], fabsf(m.ipt[c]));
@@ -109,6 +114,24 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
     float v = tmax[c];
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
     if (lane == 0 && v > 0.f) atomicMax(reinterpret_cast<unsigned int*>(&term_max[c]), __float_as_uint(v));
+  }
+}
+
+// Children of the records in `list` that were packed before their parent was
+// placed (k_pack_members left them -1): row clpos[r+1] propagates into
+// clpos[r] when r+1 is on the same path.  Records not placed yet are skipped
+// (their own pack links them); a child packed in the same pass already
+// carries the same value, so the order against its aggregate is free.
+__global__ void k_child_links(vpg_records rec, const int32_t* __restrict__ clpos,
+                              const int32_t* __restrict__ list, int64_t list_n,
+                              float4* __restrict__ rows) {
+  const int64_t n = rec.n;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < list_n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = list[i];
+    if (r + 1 >= n || rec.path_idx[r + 1] != rec.path_idx[r]) continue;
+    const int32_t q = clpos[r], qc = clpos[r + 1];
+    if (q >= 0 && qc >= 0) reinterpret_cast<int32_t*>(rows)[8 * int64_t(qc) + 3] = q;
   }
 }
 
@@ -303,7 +326,7 @@ __device__ __forceinline__ void aggregate_cluster(
       dbar_o[q] = f4(bx, by, bz);
       coeff_o[q] = f4(kx, ky, kz);
       rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
-                                  __int_as_float(-1));  // parent set by k_parent_links
+                                  __int_as_float(mb.parent));
       rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
       i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
@@ -458,14 +481,21 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
              g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get());
 }
 
+void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
+                   cudaStream_t s) {
+  if (list_n <= 0) return;
+  VPG_LAUNCH(k_child_links, grid_for(list_n, 256), 256, 0, s, rec, g->clpos.get(), list, list_n,
+             g->rows.get());
+}
+
 void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s,
-                              const int32_t* parent) {
+                              const int32_t* parent, bool linked) {
   const int64_t n = g->n, m = g->m;
   g->chunk_total = 0;
   if (n == 0) return;
   if (parent)
     VPG_LAUNCH(k_set_parents, grid_for(n, 256), 256, 0, s, parent, n, g->rows.get());
-  else
+  else if (!linked)
     VPG_LAUNCH(k_parent_links, grid_for(n, 256), 256, 0, s, rec, g->clpos.get(), g->rows.get());
   // solve chunks: cost prefix over the clusters (internal order)
   int64_t* cost = scratch_of<int64_t>(s, "chunk_cost", size_t(m) + 1);

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <vector>
 
 #include "graph.cuh"
@@ -795,22 +796,36 @@ struct MaskWords {
   }
 };
 
+// Mask total, and the bulk staging's transfer pieces: piece j holds the
+// oversize groups [n*j/P, n*(j+1)/P) -- bounds[j] = {first group, its staged
+// offset, its mask offset}, bounds[P] the totals.
+constexpr int kBulkPieces = 8;
 __global__ void k_mask_total(const int64_t* __restrict__ mask_off, const int64_t* __restrict__ info,
-                             const int32_t* __restrict__ n_over, int64_t* __restrict__ total) {
+                             const int32_t* __restrict__ n_over, const int64_t* __restrict__ seg,
+                             int64_t* __restrict__ total) {
   const int n = *n_over;
+  int64_t* bounds = total + 1;
   if (n == 0) {
     *total = 0;
+    for (int j = 0; j <= kBulkPieces; ++j) bounds[3 * j] = bounds[3 * j + 1] = bounds[3 * j + 2] = 0;
     return;
   }
   const int64_t cnt = info[(n - 1) * 4 + 1];
   *total = mask_off[n - 1] + cnt * ((cnt + 63) / 64);
+  for (int j = 0; j <= kBulkPieces; ++j) {
+    const int64_t gk = int64_t(n) * j / kBulkPieces;
+    bounds[3 * j] = gk;
+    bounds[3 * j + 1] = gk < n ? seg[gk * 3 + 2] : seg[(n - 1) * 3 + 2] + cnt;
+    bounds[3 * j + 2] = gk < n ? mask_off[gk] : *total;
+  }
 }
 
 __global__ void k_first_split_masks(const int64_t* __restrict__ seg, const int32_t* __restrict__ n_over,
                                     const int64_t* __restrict__ mask_off,
                                     const double* __restrict__ x, const double* __restrict__ y,
                                     const double* __restrict__ z, const double* __restrict__ d0,
-                                    unsigned long long* __restrict__ masks) {
+                                    unsigned long long* __restrict__ masks,
+                                    int32_t* __restrict__ moved) {
   const int nk = *n_over;
   for (int k = blockIdx.x; k < nk; k += gridDim.x) {
     const int64_t cnt = seg[k * 3 + 1], b = seg[k * 3 + 2];
@@ -825,7 +840,47 @@ __global__ void k_first_split_masks(const int64_t* __restrict__ seg, const int32
         if (dist2_exact(x[b + mm], y[b + mm], z[b + mm], px, py, pz) < d0[b + mm])
           bits |= 1ull << (mm - m0);
       mk[item] = bits;
+      // the size of the moved half for pick p (moved[] zeroed beforehand)
+      if (bits) atomicAdd(&moved[b + p], __popcll(bits));
     }
+  }
+}
+
+// The first splits the host booked without moving members (DeferredSplit:
+// staged begin, size, pick's mask row): stable partition of the staged
+// record ids in place, kept members first, then the moved ones -- exactly
+// the host's partition.  Block per split, <= 3 members per thread.
+constexpr int kApplyThreads = 128;
+__global__ void __launch_bounds__(kApplyThreads)
+k_apply_first_splits(const int64_t* __restrict__ dsplit, int64_t n_split,
+                     const unsigned long long* __restrict__ masks, int32_t* __restrict__ ids) {
+  for (int64_t i = blockIdx.x; i < n_split; i += gridDim.x) {
+    const int64_t b = dsplit[3 * i], sz = dsplit[3 * i + 1];
+    const unsigned long long* row = masks + dsplit[3 * i + 2];
+    const int words = int((sz + 63) / 64);
+    int moved_total = 0;
+    for (int w = 0; w < words; ++w) moved_total += __popcll(row[w]);
+    const int kept_total = int(sz) - moved_total;
+    int32_t v[3];
+    int dst[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int t = threadIdx.x + u * kApplyThreads;
+      dst[u] = -1;
+      if (t < sz) {
+        v[u] = ids[b + t];
+        const int w = t >> 6;
+        int before = __popcll(row[w] & ((1ull << (t & 63)) - 1ull));
+        for (int w2 = 0; w2 < w; ++w2) before += __popcll(row[w2]);
+        const bool f = (row[w] >> (t & 63)) & 1ull;
+        dst[u] = f ? kept_total + before : t - before;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (dst[u] >= 0) ids[b + dst[u]] = v[u];
+    __syncthreads();
   }
 }
 
@@ -1237,7 +1292,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   DBuf<int32_t> ne_prefix_all(center_total + 1, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
   DBuf<int32_t> far_count(1, s);
-  DBuf<int64_t> mask_total(1, s);
+  DBuf<int64_t> mask_total(1 + 3 * (kBulkPieces + 1), s);
   DBuf<int64_t> acc(8, s), cls_info(size_t(4) * n_cls + 4, s), ranges(size_t(2) * n_cls + 2, s);
   DBuf<int64_t> class_center_off(n_cls + 1, s);
   VPG_CUDA(cudaMemsetAsync(counts_all.get(), 0, counts_all.bytes(), s));
@@ -1276,6 +1331,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     int64_t n_rec;
     std::unique_ptr<HostBuf<int64_t>> b;
     int64_t n_b;
+    std::unique_ptr<HostBuf<int64_t>> deferred;  // DeferredSplit triples
+    int64_t n_deferred;
+    std::unique_ptr<DBuf<unsigned long long>> masks;  // the class's first-split rows
   };
   std::vector<SplitChunk> chunks;
   int64_t split_total = 0, nb_total = 0;
@@ -1460,7 +1518,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveSum(t, b, mw_it, mask_off, m, s);
       }, s);
-      VPG_LAUNCH(k_mask_total, 1, 1, 0, s, mask_off, over_info.get(), scalars.get() + 2,
+      VPG_LAUNCH(k_mask_total, 1, 1, 0, s, mask_off, over_info.get(), scalars.get() + 2, over_seg,
                  mask_total.get());
     }
 
@@ -1499,12 +1557,12 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     }
     // sizes of the oversize staging (nothing heavy is queued before this sync)
     HostBuf<int32_t> h_scalars(4);
-    HostBuf<int64_t> h_mask_total(1);
+    HostBuf<int64_t> h_mask_total(1 + 3 * (kBulkPieces + 1));
     VPG_CUDA(cudaMemcpyAsync(h_scalars.get(), scalars.get(), 4 * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, s));
-    VPG_CUDA(cudaMemcpyAsync(h_mask_total.get(), mask_total.get(), sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, s));
-    count_transfer(0, 24);
+    VPG_CUDA(cudaMemcpyAsync(h_mask_total.get(), mask_total.get(),
+                             sizeof(int64_t) * (1 + 3 * (kBulkPieces + 1)), cudaMemcpyDeviceToHost, s));
+    count_transfer(0, 16 + 8 * (1 + 3 * (kBulkPieces + 1)));
     VPG_CUDA(cudaStreamSynchronize(s));
     g->info.n_fallback += h_scalars[0];
     const int n_over = h_scalars[2];
@@ -1517,20 +1575,29 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     HostBuf<double> h_xyzd(size_t(staged) * 4 + 4);  // x | y | z | d0
     const int64_t n_mask = n_over > 0 ? h_mask_total[0] : 0;
     HostBuf<unsigned long long> h_masks(size_t(n_mask) + 1);
+    HostBuf<int32_t> h_moved(size_t(staged) + 1);
+    // kept until part B applies the deferred first splits
+    auto d_masks_own = std::make_unique<DBuf<unsigned long long>>(size_t(n_mask) + 1, s);
     cudaEvent_t staged_ready;
     VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
+    // positions, distances and mask rows go in pieces, last groups first (the
+    // split loop pops them first); piece_ready[j] closes piece j
+    std::vector<cudaEvent_t> piece_ready(n_over > 0 ? kBulkPieces : 0);
+    const int64_t* bounds = h_mask_total.get() + 1;
     if (n_over > 0) {
       int32_t* d_srec = scratch_of<int32_t>(s, "staged_rec", size_t(staged) + 1);
       int32_t* d_slot = scratch_of<int32_t>(s, "staged_slot", size_t(n_over) + 1);
       double* d_xyzd = scratch_of<double>(s, "staged_xyzd", size_t(staged) * 4 + 4);
-      auto* d_masks = scratch_of<unsigned long long>(s, "split_masks", size_t(n_mask) + 1);
+      unsigned long long* d_masks = d_masks_own->get();
+      int32_t* d_moved = scratch_of<int32_t>(s, "first_moved", size_t(staged) + 1);
+      VPG_CUDA(cudaMemsetAsync(d_moved, 0, sizeof(int32_t) * staged, s));
       VPG_CUDA(cudaMemsetAsync(d_slot, 0x7F, sizeof(int32_t) * n_over, s));
       VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec, over_seg,
                  scalars.get() + 2, over_info.get(), rec.pos, d_srec, d_xyzd, d_xyzd + staged,
                  d_xyzd + 2 * staged, d_xyzd + 3 * staged, d_slot);
       VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, s, over_seg,
                  scalars.get() + 2, mask_off, d_xyzd, d_xyzd + staged, d_xyzd + 2 * staged,
-                 d_xyzd + 3 * staged, d_masks);
+                 d_xyzd + 3 * staged, d_masks, d_moved);
       // the staging goes to the host on a side stream, so part A's kernels
       // (queued next on s) do not wait behind the copies
       cudaStream_t side = side_stream();
@@ -1545,12 +1612,24 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                                cudaMemcpyDeviceToHost, side));
       VPG_CUDA(cudaMemcpyAsync(h_slot.get(), d_slot, sizeof(int32_t) * n_over,
                                cudaMemcpyDeviceToHost, side));
-      VPG_CUDA(cudaMemcpyAsync(h_xyzd.get(), d_xyzd, sizeof(double) * 4 * staged,
+      VPG_CUDA(cudaMemcpyAsync(h_moved.get(), d_moved, sizeof(int32_t) * staged,
                                cudaMemcpyDeviceToHost, side));
-      VPG_CUDA(cudaMemcpyAsync(h_masks.get(), d_masks, sizeof(unsigned long long) * n_mask,
-                               cudaMemcpyDeviceToHost, side));
-      count_transfer(0, 36 * n_over + 36 * staged + 8 * n_mask);
       VPG_CUDA(cudaEventRecord(staged_ready, side));
+      for (int j = kBulkPieces - 1; j >= 0; --j) {
+        const int64_t s0 = bounds[3 * j + 1], s1 = bounds[3 * j + 4];
+        const int64_t k0 = bounds[3 * j + 2], k1 = bounds[3 * j + 5];
+        if (s1 > s0)
+          for (int a = 0; a < 4; ++a)
+            VPG_CUDA(cudaMemcpyAsync(h_xyzd.get() + a * staged + s0, d_xyzd + a * staged + s0,
+                                     sizeof(double) * (s1 - s0), cudaMemcpyDeviceToHost, side));
+        if (k1 > k0)
+          VPG_CUDA(cudaMemcpyAsync(h_masks.get() + k0, d_masks + k0,
+                                   sizeof(unsigned long long) * (k1 - k0), cudaMemcpyDeviceToHost,
+                                   side));
+        VPG_CUDA(cudaEventCreateWithFlags(&piece_ready[j], cudaEventDisableTiming));
+        VPG_CUDA(cudaEventRecord(piece_ready[j], side));
+      }
+      count_transfer(0, 36 * n_over + 40 * staged + 8 * n_mask);
     } else {
       VPG_CUDA(cudaEventRecord(staged_ready, s));
     }
@@ -1564,6 +1643,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       if (fields_ready && c == 0) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
       pack_members(g, rec, rows_p ? rows_p + p.row_off : nullptr, p.n, p.row_off, members, s);
       aggregate_range(g, members, ranges.get() + 2 * c, m, S, s);
+      // children in earlier classes were packed before these parents existed
+      if (c > 0 && rows_p) link_children(g, rec, rows_p + p.row_off, p.n, s);
     }
     clk.mark(3);
 
@@ -1587,13 +1668,35 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       g->info.n_staged += staged;
       dbg.mark("split: groups", false);
       double* xyzd = h_xyzd.get();
+      SplitStats st;
+      std::vector<DeferredSplit> deferred;
+      // the bulk piece holding original group k, waited for on first use
+      int waited_from = kBulkPieces;
+      const std::function<void(int64_t)> need_bulk = [&](int64_t k) {
+        int j = kBulkPieces - 1;
+        while (j > 0 && bounds[3 * j] > k) --j;
+        while (waited_from > j) {
+          --waited_from;
+          VPG_CUDA(cudaEventSynchronize(piece_ready[waited_from]));
+        }
+      };
       n_splits += split_oversize_soa(
           rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
-          groups, cslot, max_size, &g->info.split_visits, h_masks.get());
+          groups, cslot, max_size, &g->info.split_visits, h_masks.get(), dbg.on ? &st : nullptr,
+          h_moved.get(), 2 * max_size <= 3 * kApplyThreads ? &deferred : nullptr, &need_bulk);
+      for (int j = 0; j < kBulkPieces; ++j) {
+        VPG_CUDA(cudaEventSynchronize(piece_ready[j]));  // host buffers outlive no copy
+        cudaEventDestroy(piece_ready[j]);
+      }
       dbg.mark("split: loop", false);
-      if (dbg.on)
+      if (dbg.on) {
         fprintf(stderr, "[vpg] class %d: %lld oversize groups, %lld staged members, %lld groups after\n",
                 c, (long long)n_over, (long long)staged, (long long)groups.size());
+        const char* kinds[3] = {"first split, final", "first split, again", "later split"};
+        for (int q = 0; q < 3; ++q)
+          fprintf(stderr, "[vpg]   %-20s %6lld splits %8lld members %8.3f ms\n", kinds[q],
+                  (long long)st.n[q], (long long)st.members[q], st.ns[q] * 1e-6);
+      }
       const int64_t base_split = split_total;
       auto hb_own = std::make_unique<HostBuf<int64_t>>(groups.size() * 8 + 8);
       int64_t* hb = hb_own->get();
@@ -1606,8 +1709,15 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
         rows_b += sz;
         w_b += (sz * sz + 3) & ~int64_t(3);
       }
+      auto hd_own = std::make_unique<HostBuf<int64_t>>(deferred.size() * 3 + 3);
+      for (size_t k = 0; k < deferred.size(); ++k) {
+        hd_own->get()[3 * k] = deferred[k].begin;
+        hd_own->get()[3 * k + 1] = deferred[k].size;
+        hd_own->get()[3 * k + 2] = deferred[k].row;
+      }
       chunks.push_back(SplitChunk{std::move(h_srec_own), staged, std::move(hb_own),
-                                  int64_t(groups.size())});
+                                  int64_t(groups.size()), std::move(hd_own),
+                                  int64_t(deferred.size()), std::move(d_masks_own)});
       split_total += staged;
       nb_total += int64_t(groups.size());
       appended_c = int64_t(groups.size()) - n_over;
@@ -1654,6 +1764,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     for (const SplitChunk& ch : chunks) {
       up.pinned(d_b.get() + ob, ch.b->get(), size_t(ch.n_b) * 8, s);
       up.pinned(d_split.get() + os, ch.rec->get(), size_t(ch.n_rec), s);
+      if (ch.n_deferred) {
+        int64_t* d_def = scratch_of<int64_t>(s, "deferred_splits", size_t(ch.n_deferred) * 3);
+        up.pinned(d_def, ch.deferred->get(), size_t(ch.n_deferred) * 3, s);
+        VPG_LAUNCH(k_apply_first_splits, int(std::min<int64_t>(ch.n_deferred, 65535)),
+                   kApplyThreads, 0, s, d_def, ch.n_deferred, ch.masks->get(),
+                   d_split.get() + os);
+      }
       ob += ch.n_b * 8;
       os += ch.n_rec;
     }
@@ -1670,6 +1787,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     if (with_ops) {
       pack_members(g, rec, d_split.get(), split_total, 0, members, s);
       aggregate_range(g, members, range_b.get(), nb, S, s);
+      link_children(g, rec, d_split.get(), split_total, s);
     }
   }
   g->internal_of.alloc(M + 1, s);
@@ -1693,7 +1811,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   VPG_CUDA(cudaMemcpyAsync(&h_tot[1], g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   if (with_ops && fields_ready) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
-  if (with_ops) finalize_operators_async(g, rec, s);
+  if (with_ops) finalize_operators_async(g, rec, s, nullptr, true);
   VPG_CUDA(cudaStreamSynchronize(s));
   count_transfer(0, 20);
   g->nnz = h_tot[0];

@@ -82,8 +82,11 @@ void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
                      int S, cudaStream_t s);
 // parent links + chunk cost scan (async); chunk table once the host has the total
+// linked: k_pack_members + link_children already set every parent
 void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s,
-                              const int32_t* parent = nullptr);
+                              const int32_t* parent = nullptr, bool linked = false);
+void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
+                   cudaStream_t s);
 void finalize_chunks(vpg_graph* g, cudaStream_t s);
 // shard-local graph from a given cluster partition (records already
 // cluster-major, clusters back to back), explicit parents and child flags

@@ -17,6 +17,8 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <chrono>
+#include <functional>
 #include <vector>
 
 #include "../../include/volpg_b200.h"
@@ -212,10 +214,25 @@ struct SplitMembers {
 // member p than to the group's center) -- the outcome of the group's FIRST
 // split for every possible pick, precomputed on the device.  A first split
 // then only draws the pick and partitions; later splits compute as usual.
+struct SplitStats {  // diagnostics (VPG_DEBUG_TIMING): count / ns / members per split kind
+  int64_t n[3] = {0, 0, 0}, ns[3] = {0, 0, 0}, members[3] = {0, 0, 0};
+};
+
+// A first split whose two halves both end at most max_size members: the host
+// only draws the pick and books the halves; the members are partitioned on
+// the device afterwards (begin, size, offset of the pick's mask row).
+struct DeferredSplit {
+  int64_t begin, size, row;
+};
+
 inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGroup>& groups,
                                   std::vector<int64_t>& cslot, int64_t max_size,
                                   int64_t* visits = nullptr,
-                                  const unsigned long long* masks = nullptr) {
+                                  const unsigned long long* masks = nullptr,
+                                  SplitStats* stats = nullptr,
+                                  const int32_t* first_moved = nullptr,
+                                  std::vector<DeferredSplit>* deferred = nullptr,
+                                  const std::function<void(int64_t)>* need_bulk = nullptr) {
   const size_t n_orig = groups.size();
   std::vector<int64_t> moff(masks ? n_orig : 0);
   std::vector<uint8_t> fresh(masks ? n_orig : 0, 1);
@@ -226,6 +243,10 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
   std::vector<int64_t> stack;
   for (int64_t c = 0; c < int64_t(groups.size()); ++c)
     if (groups[c].size > max_size) stack.push_back(c);
+  // the original group every group's members came from (positions, distances
+  // and mask rows may arrive late: need_bulk(original) before touching them)
+  std::vector<int32_t> root(need_bulk ? groups.size() : 0);
+  for (size_t c = 0; c < root.size(); ++c) root[c] = int32_t(c);
   std::vector<int32_t> mid;
   std::vector<double> mx, my, mz, md, vbuf;
   std::vector<uint8_t> flag;
@@ -240,6 +261,15 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
     stack.pop_back();
     const SplitGroup gr = groups[c];
     if (gr.size <= max_size) continue;
+    const auto t_start = stats ? std::chrono::steady_clock::now()
+                               : std::chrono::steady_clock::time_point();
+    auto stat = [&](int kind) {
+      if (!stats) return;
+      stats->n[kind] += 1;
+      stats->members[kind] += gr.size;
+      stats->ns[kind] += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                             std::chrono::steady_clock::now() - t_start).count();
+    };
     const int64_t b = gr.begin, e = gr.begin + gr.size, sz = gr.size;
     if (visits) *visits += sz;
     // candidates = members != old center, in member order (clustering.py:65-67)
@@ -252,14 +282,45 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
     } else {
       pick = int64_t(g.bounded(uint64_t(sz) - 1));
     }
+    const bool first = masks && size_t(c) < n_orig && fresh[c];
+    if (first && first_moved) {
+      // the staging is fresh from DMA (not in any CPU cache) and originals
+      // are popped in descending order: pull a later group's lines in now
+      const int64_t ahead = c - 12;
+      if (ahead >= 0) {
+        const SplitGroup& ga = groups[ahead];
+        for (int64_t t = ga.begin; t < ga.begin + ga.size; t += 16) {
+          __builtin_prefetch(first_moved + t);
+          __builtin_prefetch(id + t);
+        }
+      }
+    }
     const int64_t new_center = id[b + pick];
+    if (first && first_moved && deferred) {
+      // first split of an original group, its size known without the row: a
+      // final one is booked only (members partitioned on the device)
+      const int64_t moved = first_moved[b + pick], kept = sz - moved;
+      if (kept > 0 && moved > 0 && kept <= max_size && moved <= max_size) {
+        fresh[c] = 0;
+        deferred->push_back(DeferredSplit{b, sz, moff[c] + pick * ((sz + 63) / 64)});
+        groups[c].size = kept;
+        cslot[c] = -1;
+        groups.push_back(SplitGroup{b + kept, moved, new_center});
+        cslot.push_back(-1);
+        if (need_bulk) root.push_back(root[c]);
+        ++splits;
+        stat(0);
+        continue;
+      }
+    }
+    if (need_bulk) (*need_bulk)(root[c]);
     const double px = X[b + pick], py = Y[b + pick], pz = Z[b + pick];
     if (int64_t(mid.size()) < sz) {
       for (auto* v : {&mx, &my, &mz, &md, &vbuf}) v->resize(sz);
       mid.resize(sz);
       flag.resize(sz);
     }
-    if (masks && size_t(c) < n_orig && fresh[c]) {
+    if (first) {
       // first split of an original group: the moved set is row `pick`
       fresh[c] = 0;
       const int64_t words = (sz + 63) / 64;
@@ -307,9 +368,11 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
         cslot[c] = keep_center;
         groups.push_back(SplitGroup{wk, moved, new_center});
         cslot.push_back(moved_center >= 0 ? wk + moved_center : -1);
+        if (need_bulk) root.push_back(root[c]);
         ++splits;
         if (groups[c].size > max_size) stack.push_back(c);
         if (groups.back().size > max_size) stack.push_back(int64_t(groups.size()) - 1);
+        stat(again ? 1 : 0);
         continue;
       }
       // coincident points (all or nothing moves): the general path below
@@ -340,6 +403,7 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
       cslot[c] = (old_slot >= 0 && old_slot < b + half) ? old_slot : -1;
       groups.push_back(SplitGroup{b + half, sz - half, new_center});
       cslot.push_back(new_slot >= b + half ? new_slot : -1);
+      if (need_bulk) root.push_back(root[c]);
     } else {
       // pass 2: stable partition, branch-free (every slot is written on both
       // sides; a slot is only ever written at or before the one being read)
@@ -370,10 +434,12 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
       cslot[c] = keep_center;
       groups.push_back(SplitGroup{wk, moved, new_center});
       cslot.push_back(moved_center >= 0 ? wk + moved_center : -1);
+      if (need_bulk) root.push_back(root[c]);
     }
     ++splits;
     if (groups[c].size > max_size) stack.push_back(c);
     if (groups.back().size > max_size) stack.push_back(int64_t(groups.size()) - 1);
+    stat(2);
   }
   return splits;
 }
