@@ -263,12 +263,15 @@ def run_native(args):
         time.sleep(0.25)  # let the sampler start before the timed region
         torch.cuda.synchronize()
         t_start = ev()
+        marks = []
         for _ in range(args.steps):
             g, res = step()
-        t_end = ev()
+            marks.append(ev())
+        t_end = marks[-1] if marks else ev()
         torch.cuda.synchronize()
     launches = N.launch_count() - launches0
     step_ms = t_start.elapsed_time(t_end) / args.steps
+    each_ms = [round(a.elapsed_time(b), 3) for a, b in zip([t_start] + marks[:-1], marks)]
     if dist:
         t = torch.tensor([step_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -351,7 +354,7 @@ def run_native(args):
     step_bytes = (BUILD_BYTES_PER_VERTEX + ITER_BYTES_PER_VERTEX * cfg.iterations) * n
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": step_ms, "step_ms_each": each_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (procedural fbm cloud scene, traced on device; no dataset)",
         "config": {"workload": wl.name, "resolution": list(wl.res), "spp": wl.spp,
