@@ -1102,12 +1102,13 @@ struct StageClock {
 
 // A non-blocking stream per device for host transfers that must not hold up
 // the compute stream.
-cudaStream_t side_stream() {
-  static cudaStream_t streams[64] = {};
+cudaStream_t side_stream(int which = 0) {
+  static cudaStream_t streams[2][64] = {};
   int dev = 0;
   VPG_CUDA(cudaGetDevice(&dev));
-  if (!streams[dev]) VPG_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-  return streams[dev];
+  cudaStream_t& st = streams[which][dev];
+  if (!st) VPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  return st;
 }
 
 template <class F>
@@ -1342,6 +1343,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   HostBuf<int64_t> h_acc(8);
   cudaEvent_t acc_ready;
   VPG_CUDA(cudaEventCreateWithFlags(&acc_ready, cudaEventDisableTiming));
+  cudaEvent_t placed, b_done;
+  VPG_CUDA(cudaEventCreateWithFlags(&placed, cudaEventDisableTiming));
+  VPG_CUDA(cudaEventCreateWithFlags(&b_done, cudaEventDisableTiming));
 
   for (int c = 0; c < n_cls; ++c) {
     const ClassPlan& p = plan[c];
@@ -1637,6 +1641,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
                g->clpos.get(), g->cluster_id.get());
+    // part B (split results) may start once this class's rows are placed
+    VPG_CUDA(cudaEventRecord(placed, s));
     if (with_ops) {
       // the operator fields may still be in flight (async upload): the
       // clustering above only needed pos, kind and class_id
@@ -1736,12 +1742,20 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   const int64_t nb = nb_total;
   const int64_t M = m_a + nb;
   g->m = M;
+  // Part B runs on a second stream, concurrently with part A's pack and
+  // aggregate (still running on s): it only needs part A's placement (the
+  // `placed` event) and writes disjoint rows.  Its buffers are allocated on sb
+  // and handed to s for their release; s joins sb before anything reads them.
+  cudaStream_t sb = side_stream(1);
+  VPG_CUDA(cudaStreamWaitEvent(sb, placed, 0));
+  if (with_ops && fields_ready) VPG_CUDA(cudaStreamWaitEvent(sb, fields_ready, 0));
   {
-    // final cluster arrays: part A copied over, part B written below
-    DBuf<int32_t> f_off(M + 1, s), f_size(M + 1, s), f_center(M + 1, s), f_ref(M + 1, s);
-    DBuf<int64_t> f_w(M + 1, s), f_src(M + 1, s);
+    // final cluster arrays: part A copied over, part B written below (the
+    // old part A arrays are freed on s, after part A's aggregate)
+    DBuf<int32_t> f_off(M + 1, sb), f_size(M + 1, sb), f_center(M + 1, sb), f_ref(M + 1, sb);
+    DBuf<int64_t> f_w(M + 1, sb), f_src(M + 1, sb);
     auto copy_a = [&](void* dst, const void* src, size_t elem) {
-      if (m_a) VPG_CUDA(cudaMemcpyAsync(dst, src, elem * m_a, cudaMemcpyDeviceToDevice, s));
+      if (m_a) VPG_CUDA(cudaMemcpyAsync(dst, src, elem * m_a, cudaMemcpyDeviceToDevice, sb));
     };
     copy_a(f_off.get(), g->cl_off.get(), 4);
     copy_a(f_size.get(), g->cl_size.get(), 4);
@@ -1749,6 +1763,14 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     copy_a(f_ref.get(), g->ref_of.get(), 4);
     copy_a(f_w.get(), g->w_off.get(), 8);
     copy_a(f_src.get(), a_src.get(), 8);
+    for (auto* b : {&f_off, &f_size, &f_center, &f_ref}) b->s = s;
+    for (auto* b : {&f_w, &f_src}) b->s = s;
+    // the old arrays are released on s: only after sb has copied them
+    cudaEvent_t copied;
+    VPG_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    VPG_CUDA(cudaEventRecord(copied, sb));
+    VPG_CUDA(cudaStreamWaitEvent(s, copied, 0));
+    cudaEventDestroy(copied);
     g->cl_off = std::move(f_off);
     g->cl_size = std::move(f_size);
     g->cl_center = std::move(f_center);
@@ -1756,40 +1778,46 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     g->w_off = std::move(f_w);
     a_src = std::move(f_src);
   }
-  DBuf<int64_t> d_b(size_t(nb) * 8 + 8, s);
-  DBuf<int32_t> d_split(size_t(split_total) + 1, s);
-  DBuf<int64_t> range_b(2, s);
+  DBuf<int64_t> d_b(size_t(nb) * 8 + 8, sb);
+  DBuf<int32_t> d_split(size_t(split_total) + 1, sb);
+  DBuf<int64_t> range_b(2, sb);
   if (nb) {
     int64_t ob = 0, os = 0;
     for (const SplitChunk& ch : chunks) {
-      up.pinned(d_b.get() + ob, ch.b->get(), size_t(ch.n_b) * 8, s);
-      up.pinned(d_split.get() + os, ch.rec->get(), size_t(ch.n_rec), s);
+      up.pinned(d_b.get() + ob, ch.b->get(), size_t(ch.n_b) * 8, sb);
+      up.pinned(d_split.get() + os, ch.rec->get(), size_t(ch.n_rec), sb);
       if (ch.n_deferred) {
-        int64_t* d_def = scratch_of<int64_t>(s, "deferred_splits", size_t(ch.n_deferred) * 3);
-        up.pinned(d_def, ch.deferred->get(), size_t(ch.n_deferred) * 3, s);
+        int64_t* d_def = scratch_of<int64_t>(sb, "deferred_splits", size_t(ch.n_deferred) * 3);
+        up.pinned(d_def, ch.deferred->get(), size_t(ch.n_deferred) * 3, sb);
         VPG_LAUNCH(k_apply_first_splits, int(std::min<int64_t>(ch.n_deferred, 65535)),
-                   kApplyThreads, 0, s, d_def, ch.n_deferred, ch.masks->get(),
+                   kApplyThreads, 0, sb, d_def, ch.n_deferred, ch.masks->get(),
                    d_split.get() + os);
       }
       ob += ch.n_b * 8;
       os += ch.n_rec;
     }
-    VPG_LAUNCH(k_layout_b, grid_for(nb, block), block, 0, s, d_b.get(), nb, acc.get(),
+    VPG_LAUNCH(k_layout_b, grid_for(nb, block), block, 0, sb, d_b.get(), nb, acc.get(),
                cls_info.get(), ne_prefix_all.get(), class_center_off.get(), g->cl_off.get(),
                g->cl_size.get(), g->w_off.get(), a_src.get(), g->cl_center.get(), g->ref_of.get());
   }
-  VPG_LAUNCH(k_layout_close, 1, 1, 0, s, nb, rows_b, w_b, acc.get(), g->cl_off.get(),
+  VPG_LAUNCH(k_layout_close, 1, 1, 0, sb, nb, rows_b, w_b, acc.get(), g->cl_off.get(),
              g->w_off.get(), range_b.get());
   if (nb) {
-    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, range_b.get(), g->cl_off.get(),
+    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, sb, range_b.get(), g->cl_off.get(),
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, d_split.get(),
                g->perm.get(), g->clpos.get(), g->cluster_id.get());
     if (with_ops) {
-      pack_members(g, rec, d_split.get(), split_total, 0, members, s);
-      aggregate_range(g, members, range_b.get(), nb, S, s);
-      link_children(g, rec, d_split.get(), split_total, s);
+      pack_members(g, rec, d_split.get(), split_total, 0, members, sb);
+      aggregate_range(g, members, range_b.get(), nb, S, sb);
     }
   }
+  VPG_CUDA(cudaEventRecord(b_done, sb));
+  VPG_CUDA(cudaStreamWaitEvent(s, b_done, 0));
+  cudaEventDestroy(placed);
+  cudaEventDestroy(b_done);
+  // children in part A of the split results' records: after part A's
+  // aggregate wrote those rows (stream order on s)
+  if (with_ops && nb) link_children(g, rec, d_split.get(), split_total, s);
   g->internal_of.alloc(M + 1, s);
   VPG_LAUNCH(k_invert_ref, grid_for(M, block), block, 0, s, g->ref_of.get(), M,
              g->internal_of.get());
