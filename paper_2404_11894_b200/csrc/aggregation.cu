@@ -420,7 +420,7 @@ __global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, int64_t m,
        k += int64_t(gridDim.x) * blockDim.x) {
     if (k == m) { cost[k] = 0; continue; }
     const int64_t s = cl_off[k + 1] - cl_off[k];
-    cost[k] = ((s * s + 3) & ~int64_t(3)) + 16 * s;
+    cost[k] = ((s * s + 3) & ~int64_t(3)) + 16 * s + 4;
   }
 }
 
@@ -436,6 +436,35 @@ __global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_
       if (cst[mid] < target) lo = mid + 1; else hi = mid;
     }
     first[c] = int32_t(lo);
+  }
+}
+
+// Chunk descriptors (one 32-byte load per chunk for the solve's producer) and
+// the per-cluster table staged with each chunk.  Cluster k is in chunk
+// floor(cst[k] / chunk_floats) (chunk_first[c] = first k with cst[k] >= c F).
+__global__ void k_chunk_desc(const int32_t* __restrict__ first, int64_t n_chunks,
+                             const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
+                             int4* __restrict__ desc) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_chunks;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t k0 = first[c], k1 = first[c + 1];
+    const int64_t w0 = w_off[k0];
+    const int32_t q0 = cl_off[k0];
+    desc[2 * c] = make_int4(int(uint32_t(uint64_t(w0))), int(uint32_t(uint64_t(w0) >> 32)), k0,
+                            k1 - k0);
+    desc[2 * c + 1] = make_int4(q0, cl_off[k1] - q0, int(w_off[k1] - w0), 0);
+  }
+}
+
+__global__ void k_cluster_meta(const int64_t* __restrict__ cst, int64_t m, int64_t chunk_floats,
+                               const int32_t* __restrict__ first,
+                               const int32_t* __restrict__ cl_off,
+                               const int64_t* __restrict__ w_off, int4* __restrict__ meta) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < m;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t k0 = first[cst[k] / chunk_floats];
+    meta[k] = make_int4(cl_off[k] - cl_off[k0], int(w_off[k] - w_off[k0]), cl_off[k + 1] - cl_off[k],
+                        0);
   }
 }
 
@@ -515,7 +544,7 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
   // the largest chunk (<= kChunkFloatsMax) with which 3, else 2, else 1
   // stages of chunk + the largest cluster's blocks and rows fit
   const int64_t smax = std::max<int64_t>(1, g->max_cluster);
-  const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + 16 * smax;
+  const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + 16 * smax + 4;
   g->n_stages = 0;
   for (int st = 3; st >= 1 && !g->n_stages; --st) {
     const int64_t room = int64_t((kSolveSmem - 128) / (sizeof(float) * st)) - extra;
@@ -527,6 +556,8 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
   VPG_REQUIRE(g->n_stages > 0, VPG_ELIMIT, "clusters too large for the staged solve");
   g->n_chunks = (g->chunk_total + g->chunk_floats - 1) / g->chunk_floats;
   g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
+  g->chunk_desc.alloc(size_t(2 * g->n_chunks + 2), s);
+  g->cl_meta.alloc(size_t(m + 1), s);
   if (g->n == 0) {
     VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
     return;
@@ -534,6 +565,10 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
   const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
   VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst, m, g->n_chunks,
              int64_t(g->chunk_floats), g->chunk_first.get());
+  VPG_LAUNCH(k_chunk_desc, grid_for(g->n_chunks, 256), 256, 0, s, g->chunk_first.get(),
+             g->n_chunks, g->cl_off.get(), g->w_off.get(), g->chunk_desc.get());
+  VPG_LAUNCH(k_cluster_meta, grid_for(m, 256), 256, 0, s, cst, m, int64_t(g->chunk_floats),
+             g->chunk_first.get(), g->cl_off.get(), g->w_off.get(), g->cl_meta.get());
 }
 
 void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,

@@ -25,8 +25,13 @@
 //     i0 = i_pt, dbar = D-bar, coeff (float4)
 //   ibuf[2], acc[2]: double-buffered I and W*I (acc = i_bar / coeff).
 //   chunk_first[c]: first cluster of solve chunk c; chunks cut the cost prefix
-//     sum(pad4(s^2) + 16 s) floats at multiples of chunk_floats, so one chunk's
-//     kernel blocks + row data fit a shared-memory stage (TMA bulk copies).
+//     sum(pad4(s^2) + 16 s + 4) floats at multiples of chunk_floats, so one
+//     chunk's cluster table, kernel blocks and row data fit a shared-memory
+//     stage (TMA bulk copies).
+//   chunk_desc[c]: {w0, k0, nk, q0, R, wc}: the chunk's first W float, first
+//     cluster, cluster count, first row, row count, W floats -- one load.
+//   cl_meta[k]: {first row - chunk's q0, W offset - chunk's w0, size, 0}, staged
+//     with the chunk so a consumer never reads cluster metadata from HBM.
 #pragma once
 #include "common.cuh"
 
@@ -41,6 +46,8 @@ struct vpg_graph {
   vpg::DBuf<float4> i0, dbar, coeff, ibuf[2], acc[2];
   vpg::DBuf<float4> rows;  // 2 float4 per row: (a.xyz, par bits), (b.xyz, 0)
   vpg::DBuf<int32_t> chunk_first;
+  vpg::DBuf<int4> chunk_desc;  // 2 int4 per chunk (see above)
+  vpg::DBuf<int4> cl_meta;
   int64_t n_chunks = 0, chunk_total = 0;
   int32_t chunk_floats = 0, n_stages = 0;  // solve staging (finalize_chunks)
   vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows

@@ -105,9 +105,8 @@ constexpr int kConsumers = 16;
 constexpr int kMaxStages = 3;  // the stage count is chosen per graph (graph.cuh)
 
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
-k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
-             const int32_t* __restrict__ chunk_first, int64_t n_chunks, int n_stages,
-             int stage_floats,
+k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64_t n_chunks,
+             int n_stages, int stage_floats,
              const float* __restrict__ wt, const float4* __restrict__ rows,
              const float4* __restrict__ i_in, float4* __restrict__ i_out,
              const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
@@ -137,56 +136,91 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
 
   if (wid == kConsumers) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      for (int64_t i = 0;; ++i) {
-        const int64_t c = blockIdx.x + i * G;
-        if (c >= n_chunks) break;
-        const int st = int(i % n_stages);
-        if (i >= n_stages) {
-          const int64_t cp = c - n_stages * G;  // the chunk that last used this stage
-          const int need = chunk_first[cp + 1] - chunk_first[cp];
-          while (*reinterpret_cast<volatile int*>(&done[st]) < need) __nanosleep(64);
-          done[st] = 0;
-          fence_proxy_async();  // consumers' generic reads before the async refill
-        }
-        uint64_t* bar = &full[st];
-        float* buf = stage0 + st * int64_t(stage_floats);
-        const int32_t k0 = chunk_first[c], k1 = chunk_first[c + 1];
-        // the stage's previous phase has completed (its chunk was consumed), so
-        // a consumer that sees issued == i waits on this chunk's phase
-        *reinterpret_cast<volatile int*>(&issued[st]) = int(i);
-        if (k0 == k1) {
-          mbar_arrive(bar);
-          continue;
-        }
-        const int64_t w0 = w_off[k0], wc = w_off[k1] - w0;
-        const int32_t q0 = cl_off[k0], R = cl_off[k1] - q0;
-        const uint32_t wb = uint32_t(wc * 4), rb = uint32_t(R) * 32u, ib = uint32_t(R) * 16u;
-        mbar_expect_tx(bar, wb + rb + ib + (t > 0 ? ib : 0u));
-        if (wb) bulk_g2s(buf, wt + w0, wb, bar);
-        bulk_g2s(buf + wc, rows + 2 * int64_t(q0), rb, bar);
-        bulk_g2s(buf + wc + 8 * int64_t(R), i_in + q0, ib, bar);
-        if (t > 0) bulk_g2s(buf + wc + 12 * int64_t(R), acc_prev + q0, ib, bar);
+    // The warp loads the descriptors of its next 32 chunks at once (one
+    // 32-byte load per lane), so no dependent metadata load sits between
+    // two refills; lane 0 issues the copies.
+    int prev_nk[3] = {0, 0, 0};  // cluster count of the chunk last issued per stage
+    for (int64_t i0c = 0;; i0c += 32) {
+      const int64_t cl = blockIdx.x + (i0c + lane) * G;
+      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
+      if (cl < n_chunks) {
+        d0 = desc[2 * cl];
+        d1 = desc[2 * cl + 1];
       }
+      bool finished = false;
+      for (int j = 0; j < 32; ++j) {
+        const int64_t i = i0c + j;
+        if (blockIdx.x + i * G >= n_chunks) {
+          finished = true;
+          break;
+        }
+        const uint32_t w0lo = __shfl_sync(0xFFFFFFFFu, uint32_t(d0.x), j);
+        const uint32_t w0hi = __shfl_sync(0xFFFFFFFFu, uint32_t(d0.y), j);
+        const int nk = __shfl_sync(0xFFFFFFFFu, d0.w, j);
+        const int k0 = __shfl_sync(0xFFFFFFFFu, d0.z, j);
+        const int q0 = __shfl_sync(0xFFFFFFFFu, d1.x, j);
+        const int R = __shfl_sync(0xFFFFFFFFu, d1.y, j);
+        const int wc = __shfl_sync(0xFFFFFFFFu, d1.z, j);
+        const int st = int(i % n_stages);
+        if (lane == 0) {
+          if (i >= n_stages) {
+            // the stage's previous chunk must be fully consumed
+            const int need = st == 0 ? prev_nk[0] : (st == 1 ? prev_nk[1] : prev_nk[2]);
+            while (*reinterpret_cast<volatile int*>(&done[st]) < need) __nanosleep(32);
+            done[st] = 0;
+            fence_proxy_async();  // consumers' generic reads before the async refill
+          }
+          uint64_t* bar = &full[st];
+          float* buf = stage0 + st * int64_t(stage_floats);
+          // the stage's previous phase has completed (its chunk was consumed), so
+          // a consumer that sees issued == i waits on this chunk's phase
+          *reinterpret_cast<volatile int*>(&issued[st]) = int(i);
+          if (nk == 0) {
+            mbar_arrive(bar);
+          } else {
+            const int64_t w0 = int64_t((uint64_t(w0hi) << 32) | w0lo);
+            const uint32_t mb = uint32_t(nk) * 16u, wb = uint32_t(wc) * 4u,
+                           rb = uint32_t(R) * 32u, ib = uint32_t(R) * 16u;
+            mbar_expect_tx(bar, mb + wb + rb + ib + (t > 0 ? ib : 0u));
+            bulk_g2s(buf, meta + k0, mb, bar);
+            float* p = buf + 4 * nk;
+            if (wb) bulk_g2s(p, wt + w0, wb, bar);
+            p += wc;
+            bulk_g2s(p, rows + 2 * int64_t(q0), rb, bar);
+            p += 8 * R;
+            bulk_g2s(p, i_in + q0, ib, bar);
+            if (t > 0) bulk_g2s(p + 4 * R, acc_prev + q0, ib, bar);
+          }
+        }
+        // every lane tracks the counts (only lane 0 reads them)
+        if (st == 0) prev_nk[0] = nk;
+        else if (st == 1) prev_nk[1] = nk;
+        else prev_nk[2] = nk;
+      }
+      if (finished) break;
     }
   } else {
     // ----------------------------------------------------------- consumers
     float dmax[3] = {0.f, 0.f, 0.f}, smax[3] = {0.f, 0.f, 0.f};
     unsigned nan_bits = 0;  // numpy's max propagates NaN per channel: remember it
     int64_t ci = 0, cbase = 0, waited = -1;  // current chunk (local index), its first item
-    int32_t ck0 = 0, ck1 = 0;
+    int nk = 0, R = 0, wc = 0, cq0 = 0;      // of chunk ci
     {
       const int64_t c = blockIdx.x;
       if (c < n_chunks) {
-        ck0 = chunk_first[c];
-        ck1 = chunk_first[c + 1];
+        const int4 d0 = desc[2 * c], d1 = desc[2 * c + 1];
+        nk = d0.w;
+        cq0 = d1.x;
+        R = d1.y;
+        wc = d1.z;
       }
     }
     for (;;) {
       int x = 0;
       if (lane == 0) x = atomicAdd(next_item, 1);
       x = __shfl_sync(0xFFFFFFFFu, x, 0);
-      // advance to the chunk holding item x
+      // advance to the chunk holding item x (immutable descriptors: no race
+      // with the producer reusing a stage)
       bool finished = false;
       while (true) {
         const int64_t c = blockIdx.x + ci * G;
@@ -194,13 +228,16 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
           finished = true;
           break;
         }
-        if (x < cbase + (ck1 - ck0)) break;
-        cbase += ck1 - ck0;
+        if (x < cbase + nk) break;
+        cbase += nk;
         ++ci;
         const int64_t c2 = blockIdx.x + ci * G;
         if (c2 < n_chunks) {
-          ck0 = chunk_first[c2];
-          ck1 = chunk_first[c2 + 1];
+          const int4 d0 = desc[2 * c2], d1 = desc[2 * c2 + 1];
+          nk = d0.w;
+          cq0 = d1.x;
+          R = d1.y;
+          wc = d1.z;
         }
       }
       if (finished) break;
@@ -212,16 +249,15 @@ k_solve_iter(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_o
         waited = ci;
       }
       const float* buf = stage0 + st * int64_t(stage_floats);
-      const int64_t w0 = w_off[ck0], wc = w_off[ck1] - w0;
-      const int32_t cq0 = cl_off[ck0], R = cl_off[ck1] - cq0;
-      const float4* srow = reinterpret_cast<const float4*>(buf + wc);
-      const float4* sin = reinterpret_cast<const float4*>(buf + wc + 8 * int64_t(R));
-      const float4* sprev = reinterpret_cast<const float4*>(buf + wc + 12 * int64_t(R));
-      const int32_t k = ck0 + int32_t(x - cbase);
-      const int32_t q0 = cl_off[k];
-      const int s = cl_off[k + 1] - q0;
-      const float* w = buf + (w_off[k] - w0);
-      const int rl = q0 - cq0;
+      const int4 mk = reinterpret_cast<const int4*>(buf)[x - cbase];
+      const float* wbase = buf + 4 * nk;
+      const float4* srow = reinterpret_cast<const float4*>(wbase + wc);
+      const float4* sin = reinterpret_cast<const float4*>(wbase + wc + 8 * int64_t(R));
+      const float4* sprev = reinterpret_cast<const float4*>(wbase + wc + 12 * int64_t(R));
+      const int rl = mk.x;
+      const int s = mk.z;
+      const int64_t q0 = int64_t(cq0) + rl;
+      const float* w = wbase + mk.y;
       for (int rc = 0; rc < s; rc += 64) {
         const int r0 = rc + lane, r1 = rc + lane + 32;
         float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
@@ -572,7 +608,7 @@ SolveLaunch solve_launch(const vpg_graph* g) {
   // stage = one chunk (g->chunk_floats) plus the largest cluster's blocks + rows
   SolveLaunch L;
   const int smax = std::max(1, g->max_cluster);
-  L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + 16 * smax;
+  L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + 16 * smax + 4;
   L.smem = 128 + size_t(g->n_stages) * L.stage_floats * sizeof(float);
   VPG_REQUIRE(L.smem <= kSolveSmem, VPG_ELIMIT, "clusters too large for the staged solve");
   static size_t smem_set = 0;
@@ -615,9 +651,8 @@ void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
   VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
   if (g->n == 0 || g->n_chunks == 0) return;
   const SolveLaunch L = solve_launch(g);
-  VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->cl_off.get(),
-             g->w_off.get(), g->chunk_first.get(), g->n_chunks, g->n_stages, L.stage_floats,
-             g->wt.get(),
+  VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->chunk_desc.get(),
+             g->cl_meta.get(), g->n_chunks, g->n_stages, L.stage_floats, g->wt.get(),
              g->rows.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
              g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
 }

@@ -11,7 +11,8 @@ cfg = RenderConfig(spp=wl.spp, max_depth=wl.max_depth, seed=0)
 out = render_pt(wl.scene(), cfg, with_records=True)
 bt, st = [], []
 g = None
-for rep in range(25):
+import os
+for rep in range(int(os.environ.get("REPS", "25"))):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     g = build_graph(out, 32, seed=0)
     torch.cuda.synchronize(); t1 = time.perf_counter()
