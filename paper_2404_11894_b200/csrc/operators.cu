@@ -261,18 +261,31 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64
       for (int rc = 0; rc < s; rc += 64) {
         const int r0 = rc + lane, r1 = rc + lane + 32;
         float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
+        if (s - rc <= 32) {
+          // one row per lane (most clusters: s <= 2K = 64, mean K)
+          const float* colr = w + r0;
 #pragma unroll 4
-        for (int j = 0; j < s; ++j) {
-          const float4 ij = sin[rl + j];
-          const float* col = w + j * s;
-          const float w0v = r0 < s ? col[r0] : 0.f;
-          const float w1v = r1 < s ? col[r1] : 0.f;
-          acc0.x = fmaf(w0v, ij.x, acc0.x);
-          acc0.y = fmaf(w0v, ij.y, acc0.y);
-          acc0.z = fmaf(w0v, ij.z, acc0.z);
-          acc1.x = fmaf(w1v, ij.x, acc1.x);
-          acc1.y = fmaf(w1v, ij.y, acc1.y);
-          acc1.z = fmaf(w1v, ij.z, acc1.z);
+          for (int j = 0; j < s; ++j) {
+            const float4 ij = sin[rl + j];
+            const float w0v = r0 < s ? colr[j * s] : 0.f;
+            acc0.x = fmaf(w0v, ij.x, acc0.x);
+            acc0.y = fmaf(w0v, ij.y, acc0.y);
+            acc0.z = fmaf(w0v, ij.z, acc0.z);
+          }
+        } else {
+#pragma unroll 4
+          for (int j = 0; j < s; ++j) {
+            const float4 ij = sin[rl + j];
+            const float* col = w + j * s;
+            const float w0v = r0 < s ? col[r0] : 0.f;
+            const float w1v = r1 < s ? col[r1] : 0.f;
+            acc0.x = fmaf(w0v, ij.x, acc0.x);
+            acc0.y = fmaf(w0v, ij.y, acc0.y);
+            acc0.z = fmaf(w0v, ij.z, acc0.z);
+            acc1.x = fmaf(w1v, ij.x, acc1.x);
+            acc1.y = fmaf(w1v, ij.y, acc1.y);
+            acc1.z = fmaf(w1v, ij.z, acc1.z);
+          }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
