@@ -73,9 +73,9 @@ namespace vpg {
 // floats of kernel blocks + row data per solve chunk (one shared-memory stage):
 // chosen per graph so that n_stages stages of chunk + the largest cluster fit
 // the shared memory (kSolveSmem); larger chunks keep more bytes in flight
-constexpr int kChunkFloatsMax = 12288;
+constexpr int kChunkFloatsMax = 16384;
 constexpr int kChunkFloatsMin = 2048;
-constexpr size_t kSolveSmem = 220 * 1024;
+constexpr size_t kSolveSmem = 226 * 1024;
 // cluster.cu: the whole build (clusters, layout, and the operator passes
 // below, overlapped with the host split loop); `with_operators` = false for
 // cluster_points.

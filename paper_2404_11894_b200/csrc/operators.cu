@@ -102,7 +102,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 //    recomputed from the previous W*I (same arithmetic as when it was stored)
 //    instead of gathered.
 constexpr int kConsumers = 16;
-constexpr int kMaxStages = 3;  // the stage count is chosen per graph (graph.cuh)
+constexpr int kMaxStages = 4;  // the stage count is chosen per graph (graph.cuh)
 
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
 k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64_t n_chunks,
@@ -114,7 +114,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64
              const int32_t* __restrict__ ctl) {
   if (ctl[1]) return;  // converged or diverged earlier
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // n_stages (<= 3) barriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // n_stages (<= 4) barriers
   int* done = reinterpret_cast<int*>(smem + 64);                  // n_stages counters
   int* next_item = reinterpret_cast<int*>(smem + 96);
   int* issued = reinterpret_cast<int*>(smem + 104);               // n_stages chunk ids
@@ -139,7 +139,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64
     // The warp loads the descriptors of its next 32 chunks at once (one
     // 32-byte load per lane), so no dependent metadata load sits between
     // two refills; lane 0 issues the copies.
-    int prev_nk[3] = {0, 0, 0};  // cluster count of the chunk last issued per stage
+    __shared__ int prev_nk[kMaxStages];  // cluster count of the chunk last issued per stage
     for (int64_t i0c = 0;; i0c += 32) {
       const int64_t cl = blockIdx.x + (i0c + lane) * G;
       int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
@@ -165,8 +165,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64
         if (lane == 0) {
           if (i >= n_stages) {
             // the stage's previous chunk must be fully consumed
-            const int need = st == 0 ? prev_nk[0] : (st == 1 ? prev_nk[1] : prev_nk[2]);
-            while (*reinterpret_cast<volatile int*>(&done[st]) < need) __nanosleep(32);
+            while (*reinterpret_cast<volatile int*>(&done[st]) < prev_nk[st]) __nanosleep(32);
             done[st] = 0;
             fence_proxy_async();  // consumers' generic reads before the async refill
           }
@@ -192,10 +191,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64
             if (t > 0) bulk_g2s(p + 4 * R, acc_prev + q0, ib, bar);
           }
         }
-        // every lane tracks the counts (only lane 0 reads them)
-        if (st == 0) prev_nk[0] = nk;
-        else if (st == 1) prev_nk[1] = nk;
-        else prev_nk[2] = nk;
+        if (lane == 0) prev_nk[st] = nk;
       }
       if (finished) break;
     }
