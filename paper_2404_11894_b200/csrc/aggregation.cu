@@ -424,9 +424,12 @@ __global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, int64_t m,
   }
 }
 
-__global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_t n_chunks,
-                              int64_t chunk_floats, int32_t* __restrict__ first) {
-  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c <= n_chunks;
+__global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_t cap,
+                              int64_t chunk_floats, int32_t* __restrict__ first,
+                              int64_t* __restrict__ n_chunks_out) {
+  const int64_t n_chunks = (cst[m] + chunk_floats - 1) / chunk_floats;  // <= cap
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_chunks_out = n_chunks;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c <= n_chunks && c <= cap;
        c += int64_t(gridDim.x) * blockDim.x) {
     if (c == n_chunks) { first[c] = int32_t(m); continue; }
     const int64_t target = c * chunk_floats;
@@ -442,9 +445,10 @@ __global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_
 // Chunk descriptors (one 32-byte load per chunk for the solve's producer) and
 // the per-cluster table staged with each chunk.  Cluster k is in chunk
 // floor(cst[k] / chunk_floats) (chunk_first[c] = first k with cst[k] >= c F).
-__global__ void k_chunk_desc(const int32_t* __restrict__ first, int64_t n_chunks,
+__global__ void k_chunk_desc(const int32_t* __restrict__ first, const int64_t* __restrict__ n_chunks_p,
                              const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
                              int4* __restrict__ desc) {
+  const int64_t n_chunks = *n_chunks_p;
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_chunks;
        c += int64_t(gridDim.x) * blockDim.x) {
     const int32_t k0 = first[c], k1 = first[c + 1];
@@ -520,7 +524,6 @@ void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, in
 void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t s,
                               const int32_t* parent, bool linked) {
   const int64_t n = g->n, m = g->m;
-  g->chunk_total = 0;
   if (n == 0) return;
   if (parent)
     VPG_LAUNCH(k_set_parents, grid_for(n, 256), 256, 0, s, parent, n, g->rows.get());
@@ -535,14 +538,12 @@ void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t
   void* tmp = scratch(s, "cub_temp", bytes + 256);
   VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cost, cst, int(m + 1), s));
   count_launch(1);
-  VPG_CUDA(cudaMemcpyAsync(&g->chunk_total, cst + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  count_transfer(0, 8);
 }
 
-void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchronised
-  const int64_t m = g->m;
+void finalize_chunks(vpg_graph* g, cudaStream_t s) {
+  const int64_t m = g->m, n = g->n;
   // the largest chunk (<= kChunkFloatsMax) with which 3, else 2, else 1
-  // stages of chunk + the largest cluster's blocks and rows fit
+  // stages of chunk + the largest cluster's table, blocks and rows fit
   const int64_t smax = std::max<int64_t>(1, g->max_cluster);
   const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + 16 * smax + 4;
   g->n_stages = 0;
@@ -554,19 +555,23 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {  // after the stream synchr
     }
   }
   VPG_REQUIRE(g->n_stages > 0, VPG_ELIMIT, "clusters too large for the staged solve");
-  g->n_chunks = (g->chunk_total + g->chunk_floats - 1) / g->chunk_floats;
-  g->chunk_first.alloc(size_t(g->n_chunks + 1), s);
-  g->chunk_desc.alloc(size_t(2 * g->n_chunks + 2), s);
+  // sum over clusters of pad4(s^2) + 16 s + 4 <= smax n + 16 n + 7 m
+  const int64_t bound = smax * n + 16 * n + 7 * m;
+  g->chunk_cap = bound / g->chunk_floats + 2;
+  g->chunk_first.alloc(size_t(g->chunk_cap + 1), s);
+  g->chunk_desc.alloc(size_t(2 * g->chunk_cap + 2), s);
   g->cl_meta.alloc(size_t(m + 1), s);
-  if (g->n == 0) {
+  g->n_chunks_dev.alloc(1, s);
+  if (n == 0) {
     VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
+    VPG_CUDA(cudaMemsetAsync(g->n_chunks_dev.get(), 0, sizeof(int64_t), s));
     return;
   }
   const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
-  VPG_LAUNCH(k_chunk_first, grid_for(g->n_chunks + 1, 256), 256, 0, s, cst, m, g->n_chunks,
-             int64_t(g->chunk_floats), g->chunk_first.get());
-  VPG_LAUNCH(k_chunk_desc, grid_for(g->n_chunks, 256), 256, 0, s, g->chunk_first.get(),
-             g->n_chunks, g->cl_off.get(), g->w_off.get(), g->chunk_desc.get());
+  VPG_LAUNCH(k_chunk_first, grid_for(g->chunk_cap + 1, 256), 256, 0, s, cst, m, g->chunk_cap,
+             int64_t(g->chunk_floats), g->chunk_first.get(), g->n_chunks_dev.get());
+  VPG_LAUNCH(k_chunk_desc, grid_for(g->chunk_cap, 256), 256, 0, s, g->chunk_first.get(),
+             g->n_chunks_dev.get(), g->cl_off.get(), g->w_off.get(), g->chunk_desc.get());
   VPG_LAUNCH(k_cluster_meta, grid_for(m, 256), 256, 0, s, cst, m, int64_t(g->chunk_floats),
              g->chunk_first.get(), g->cl_off.get(), g->w_off.get(), g->cl_meta.get());
 }

@@ -343,7 +343,7 @@ int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64
                      static_cast<cudaEvent_t>(fields_ready));
     g->info.n_records = g->n;
     g->info.n_clusters = g->m;
-    g->info.nnz = g->nnz;
+    if (!g->tot_pending) g->info.nnz = g->nnz;
   });
   if (rc != VPG_OK) {
     delete g;
@@ -416,7 +416,10 @@ int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng
 }
 
 int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out) {
-  return guarded([&] { *out = g->info; });
+  return guarded([&] {
+    g->sync_totals();
+    *out = g->info;
+  });
 }
 
 int vpg_graph_free(vpg_graph* g) {

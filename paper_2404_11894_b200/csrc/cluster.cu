@@ -1204,7 +1204,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     if (with_ops) alloc_operator_buffers(g, 1, s);
     g->chunk_first.alloc(1, s);
     VPG_CUDA(cudaMemsetAsync(g->chunk_first.get(), 0, sizeof(int32_t), s));
-    g->n_chunks = 0;
+    g->n_chunks_dev.alloc(1, s);
+    VPG_CUDA(cudaMemsetAsync(g->n_chunks_dev.get(), 0, sizeof(int64_t), s));
     rng.store(rng_state);
     return;
   }
@@ -1821,32 +1822,38 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   g->internal_of.alloc(M + 1, s);
   VPG_LAUNCH(k_invert_ref, grid_for(M, block), block, 0, s, g->ref_of.get(), M,
              g->internal_of.get());
-  // totals: nnz (sum of s^2), padded kernel length, largest cluster
-  DBuf<int64_t> d_nnz(1, s);
-  DBuf<int32_t> d_max(1, s);
+  // totals: nnz (sum of s^2) and the padded kernel length, to pinned memory
+  // without waiting (vpg_graph::sync_totals); the staging needs only the
+  // bound on the cluster size (every cluster has at most 2K members)
+  g->tot_host.alloc(2);
   {
+    int64_t* d_tot = scratch_of<int64_t>(s, "nnz_total", 2);
     cub::TransformInputIterator<int64_t, SquareOp, const int32_t*> sq_it(g->cl_size.get(), SquareOp());
     cub_call([&](void* t, size_t& b) {
-      return cub::DeviceReduce::Sum(t, b, sq_it, d_nnz.get(), int(M), s);
+      return cub::DeviceReduce::Sum(t, b, sq_it, d_tot, int(M), s);
     }, s);
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceReduce::Reduce(t, b, g->cl_size.get(), d_max.get(), int(M), MaxOp(), 0, s);
-    }, s);
+    VPG_CUDA(cudaMemcpyAsync(d_tot + 1, g->w_off.get() + M, sizeof(int64_t),
+                             cudaMemcpyDeviceToDevice, s));
+    VPG_CUDA(cudaMemcpyAsync(g->tot_host.get(), d_tot, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             s));
+    count_transfer(0, 16);
   }
-  int64_t h_tot[2] = {0, 0};
-  int32_t h_max = 0;
-  VPG_CUDA(cudaMemcpyAsync(&h_tot[0], d_nnz.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  VPG_CUDA(cudaMemcpyAsync(&h_tot[1], g->w_off.get() + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  VPG_CUDA(cudaMemcpyAsync(&h_max, d_max.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  g->max_cluster = int32_t(std::min<int64_t>(max_size, std::max<int64_t>(n, 1)));
   if (with_ops && fields_ready) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
   if (with_ops) finalize_operators_async(g, rec, s, nullptr, true);
-  VPG_CUDA(cudaStreamSynchronize(s));
-  count_transfer(0, 20);
-  g->nnz = h_tot[0];
-  g->wt_len = h_tot[1];
-  g->max_cluster = h_max;
   clk.mark(5);
   if (with_ops) finalize_chunks(g, s);
+  // pinned inputs part B's kernels read from the host stay with the graph
+  for (SplitChunk& ch : chunks) {
+    g->hold_host(std::move(ch.rec));
+    g->hold_host(std::move(ch.b));
+    g->hold_host(std::move(ch.deferred));
+  }
+  for (auto& k : up.keep) g->hold_host(std::move(k));
+  up.keep.clear();
+  VPG_CUDA(cudaEventCreateWithFlags(&g->done_ev, cudaEventDisableTiming));
+  VPG_CUDA(cudaEventRecord(g->done_ev, s));
+  g->tot_pending = true;
   clk.mark(6);
 }
 

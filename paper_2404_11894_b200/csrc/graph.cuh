@@ -33,6 +33,9 @@
 //   cl_meta[k]: {first row - chunk's q0, W offset - chunk's w0, size, 0}, staged
 //     with the chunk so a consumer never reads cluster metadata from HBM.
 #pragma once
+#include <memory>
+#include <vector>
+
 #include "common.cuh"
 
 struct vpg_graph {
@@ -48,7 +51,8 @@ struct vpg_graph {
   vpg::DBuf<int32_t> chunk_first;
   vpg::DBuf<int4> chunk_desc;  // 2 int4 per chunk (see above)
   vpg::DBuf<int4> cl_meta;
-  int64_t n_chunks = 0, chunk_total = 0;
+  vpg::DBuf<int64_t> n_chunks_dev;  // the chunk count, computed on the device
+  int64_t chunk_cap = 0;            // capacity of the chunk arrays (a host-side bound)
   int32_t chunk_floats = 0, n_stages = 0;  // solve staging (finalize_chunks)
   vpg::DBuf<float> term_max;   // 3: max |i_pt| over terminal rows
   // solve state (device): red[t*8 + 0..5] float bits, ctl = {performed, stop, grow, diverged}
@@ -67,6 +71,36 @@ struct vpg_graph {
   vpg_graph_info info{};
   // the records the graph was built from (borrowed; the caller keeps them alive)
   vpg_records rec{};
+  // The build returns without waiting for the device: its totals arrive in
+  // pinned memory (sync_totals() before reading nnz / wt_len), and pinned
+  // inputs its last kernels still read are held until done_ev.
+  mutable vpg::HostBuf<int64_t> tot_host;
+  mutable bool tot_pending = false;
+  cudaEvent_t done_ev = nullptr;
+  std::vector<std::shared_ptr<void>> hold;
+
+  void sync_totals() const {
+    if (!tot_pending) return;
+    cudaEventSynchronize(done_ev);
+    auto* self = const_cast<vpg_graph*>(this);
+    self->nnz = tot_host[0];
+    self->wt_len = tot_host[1];
+    self->info.nnz = nnz;
+    tot_pending = false;
+  }
+  template <class T>
+  void hold_host(std::unique_ptr<vpg::HostBuf<T>> b) {
+    if (b) hold.push_back(std::shared_ptr<void>(b.release(), [](void* p) {
+      delete static_cast<vpg::HostBuf<T>*>(p);
+    }));
+  }
+  ~vpg_graph() {
+    if (done_ev) {
+      cudaEventSynchronize(done_ev);
+      cudaEventDestroy(done_ev);
+    }
+    hold.clear();
+  }
 };
 
 namespace vpg {
@@ -94,6 +128,8 @@ void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t
                               const int32_t* parent = nullptr, bool linked = false);
 void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
                    cudaStream_t s);
+// chunk table, descriptors and cluster table on the device (no host sync;
+// g->max_cluster must bound the largest cluster)
 void finalize_chunks(vpg_graph* g, cudaStream_t s);
 // shard-local graph from a given cluster partition (records already
 // cluster-major, clusters back to back), explicit parents and child flags

@@ -105,14 +105,16 @@ constexpr int kConsumers = 16;
 constexpr int kMaxStages = 4;  // the stage count is chosen per graph (graph.cuh)
 
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
-k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta, int64_t n_chunks,
-             int n_stages, int stage_floats,
+k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
+             const int64_t* __restrict__ n_chunks_p, int n_stages, int stage_floats,
              const float* __restrict__ wt, const float4* __restrict__ rows,
              const float4* __restrict__ i_in, float4* __restrict__ i_out,
              const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
              const float4* __restrict__ i0, int t, uint32_t* __restrict__ red,
              const int32_t* __restrict__ ctl) {
   if (ctl[1]) return;  // converged or diverged earlier
+  const int64_t n_chunks = *n_chunks_p;
+  if (int64_t(blockIdx.x) >= n_chunks) return;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // n_stages (<= 4) barriers
   int* done = reinterpret_cast<int*>(smem + 64);                  // n_stages counters
@@ -626,7 +628,7 @@ SolveLaunch solve_launch(const vpg_graph* g) {
                                   int(L.smem)));
     smem_set = L.smem;
   }
-  L.grid = int(std::min<int64_t>(g->n_chunks, sm_count()));
+  L.grid = sm_count();  // persistent; CTAs past the (device-side) chunk count exit
   return L;
 }
 }  // namespace
@@ -658,10 +660,10 @@ void solve_begin(vpg_graph* g, const vpg_records& rec, int32_t iterations, doubl
 
 void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
   VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
-  if (g->n == 0 || g->n_chunks == 0) return;
+  if (g->n == 0) return;
   const SolveLaunch L = solve_launch(g);
   VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->chunk_desc.get(),
-             g->cl_meta.get(), g->n_chunks, g->n_stages, L.stage_floats, g->wt.get(),
+             g->cl_meta.get(), g->n_chunks_dev.get(), g->n_stages, L.stage_floats, g->wt.get(),
              g->rows.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
              g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
 }
@@ -806,6 +808,7 @@ void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, dou
     }
     if (indptr) VPG_CUDA(cudaMemcpyAsync(indptr, ip.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
     if (indices || data) {
+      g->sync_totals();
       DBuf<int64_t> ind(size_t(g->nnz) + 1, s);
       DBuf<double> dat(size_t(g->nnz) + 1, s);
       VPG_LAUNCH(k_export_csr, grid_for(n * 32, block), block, 0, s, g->cluster_id.get(),
