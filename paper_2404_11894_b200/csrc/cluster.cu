@@ -86,8 +86,9 @@ struct GridParams {
 
 __device__ __forceinline__ uint64_t cell_key(const GridParams& gp, long long x, long long y,
                                              long long z) {
-  if (gp.packed)
-    return (uint64_t(x + 1) << 42) | (uint64_t(y + 1) << 21) | uint64_t(z + 1);
+  if (gp.packed)  // dense index over the grid padded by two cells per side
+    return (uint64_t(x + 2) * uint64_t(gp.dims[1] + 4) + uint64_t(y + 2)) * uint64_t(gp.dims[2] + 4) +
+           uint64_t(z + 2);
   uint64_t h = mix64(uint64_t(x) * 0x9E3779B97F4A7C15ull ^ mix64(uint64_t(y) + 0x632BE59BD9B4E019ull) ^
                      mix64(uint64_t(z) * 0xD1342543DE82EF95ull + 7));
   return h & 0x7FFFFFFFFFFFFFFFull;
@@ -390,12 +391,10 @@ constexpr int kCandCap = 128;  // candidate centers staged per warp
 constexpr long long kShellBudget = 4096;  // cells one fallback point may enumerate
 constexpr int kAssignWarps = 8;
 
-// Sort key of a point's cell: a dense linear index over the padded grid when
-// the grid is packed, else the hashed key (ties only cost extra candidates).
+// Sort key of a point's cell: the cell key (dense over the padded grid when
+// packed, else hashed: ties only cost extra candidates).
 __device__ __forceinline__ unsigned long long sort_key(const GridParams& gp, long long x,
                                                        long long y, long long z) {
-  if (gp.packed)
-    return (unsigned long long)(((x + 1) * (gp.dims[1] + 2) + (y + 1)) * (gp.dims[2] + 2) + (z + 1));
   return cell_key(gp, x, y, z);
 }
 
@@ -409,6 +408,49 @@ __global__ void k_point_keys(const int32_t* rows, int64_t row_off, int64_t n,
                        cell_coord(pos[r * 3 + 1], gp.lo[1], gp.cell),
                        cell_coord(pos[r * 3 + 2], gp.lo[2], gp.cell));
     ids[i] = int32_t(i);
+  }
+}
+
+// Counting sort of the points by cell (dense packed keys): count, scan,
+// scatter.  Points of one cell land in arbitrary order, which the assignment
+// does not see (each point's nearest center is exact on its own).
+__global__ void k_cell_count(const int32_t* rows, int64_t row_off, int64_t n,
+                             const double* __restrict__ pos, GridParams gp,
+                             int32_t* __restrict__ counts, int32_t* __restrict__ pkey) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = class_row(rows, row_off, i);
+    const int32_t key = int32_t(cell_key(gp, cell_coord(pos[r * 3], gp.lo[0], gp.cell),
+                                         cell_coord(pos[r * 3 + 1], gp.lo[1], gp.cell),
+                                         cell_coord(pos[r * 3 + 2], gp.lo[2], gp.cell)));
+    pkey[i] = key;
+    atomicAdd(&counts[key], 1);
+  }
+}
+
+__global__ void k_cell_scatter(int64_t n, const int32_t* __restrict__ pkey,
+                               const int32_t* __restrict__ offs, int32_t* __restrict__ counts,
+                               int32_t* __restrict__ sorted_ids) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t key = pkey[i];
+    sorted_ids[offs[key] + atomicSub(&counts[key], 1) - 1] = int32_t(i);
+  }
+}
+
+struct CellNonEmpty {
+  const int32_t* offs;
+  __host__ __device__ bool operator()(int32_t c) const { return offs[c + 1] > offs[c]; }
+};
+
+__global__ void k_cell_runs(const int32_t* __restrict__ cells, const int32_t* __restrict__ n_sel,
+                            const int32_t* __restrict__ offs, int32_t* __restrict__ run_start,
+                            int32_t* __restrict__ run_len) {
+  const int n = *n_sel;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t c = cells[i];
+    run_start[i] = offs[c];
+    run_len[i] = offs[c + 1] - offs[c];
   }
 }
 
@@ -1080,6 +1122,12 @@ int bits_for(uint64_t max_value) {
   return b;
 }
 
+// radix bits of the dense packed cell keys (cell_key)
+int packed_key_bits(const GridParams& gp) {
+  const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
+  return cells < 1.8e19 ? bits_for(uint64_t(cells)) : 64;
+}
+
 struct StageClock {
   bool on;
   cudaStream_t s;
@@ -1367,22 +1415,46 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       pids_sorted = scratch_of<int32_t>(s, "pids_sorted", p.n);
       run_start = scratch_of<int32_t>(s, "run_start", p.n + 1);
       run_len = scratch_of<int32_t>(s, "run_len", p.n + 1);
-      VPG_LAUNCH(k_point_keys, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n, rec.pos,
-                 gp, pkeys, pids);
-      if (gp.packed)
-        end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
+      if (gp.packed) end_bits = packed_key_bits(gp);
       const int64_t nn = p.n;
-      cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted, int(nn),
-                                               0, end_bits, s);
-      }, s);
-      cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
-                                                  scalars.get() + 1, int(nn), s);
-      }, s);
-      cub_call([&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(nn), s);
-      }, s);
+      const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
+      if (gp.packed && cells <= 4.0 * double(p.n) + 4096.0 && cells < 2.0e9) {
+        // counting sort over the dense cell keys
+        const int64_t nc = int64_t(cells);
+        int32_t* counts = scratch_of<int32_t>(s, "cell_counts", size_t(nc) + 1);
+        int32_t* offs = scratch_of<int32_t>(s, "cell_offs", size_t(nc) + 1);
+        int32_t* pkey = reinterpret_cast<int32_t*>(pkeys);
+        VPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nc + 1), s));
+        VPG_LAUNCH(k_cell_count, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
+                   rec.pos, gp, counts, pkey);
+        cub_call([&](void* t, size_t& b) {
+          return cub::DeviceScan::ExclusiveSum(t, b, counts, offs, int(nc + 1), s);
+        }, s);
+        VPG_LAUNCH(k_cell_scatter, grid_for(p.n, block), block, 0, s, p.n, pkey, offs, counts,
+                   pids_sorted);
+        int32_t* sel = reinterpret_cast<int32_t*>(pkeys_sorted);
+        cub::CountingInputIterator<int32_t> ci(0);
+        cub_call([&](void* t, size_t& b) {
+          return cub::DeviceSelect::If(t, b, ci, sel, scalars.get() + 1, int(nc), CellNonEmpty{offs},
+                                       s);
+        }, s);
+        VPG_LAUNCH(k_cell_runs, grid_for(p.n, block), block, 0, s, sel, scalars.get() + 1, offs,
+                   run_start, run_len);
+      } else {
+        VPG_LAUNCH(k_point_keys, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
+                   rec.pos, gp, pkeys, pids);
+        cub_call([&](void* t, size_t& b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted,
+                                                 int(nn), 0, end_bits, s);
+        }, s);
+        cub_call([&](void* t, size_t& b) {
+          return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
+                                                    scalars.get() + 1, int(nn), s);
+        }, s);
+        cub_call([&](void* t, size_t& b) {
+          return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(nn), s);
+        }, s);
+      }
     }
 
     // m centers = Generator.choice(n, m) (clustering.py:51)
@@ -1400,8 +1472,11 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       int32_t* d_prev = scratch_of<int32_t>(s, "swap_prev", steps + 1);
       up.pinned(d_target, targets.get(), size_t(steps), s);
       VPG_LAUNCH(k_swap_keys, grid_for(steps, block), block, 0, s, d_target, steps, d_keys);
+      // by position only (bits 32..): the sort is stable and the keys arrive in
+      // step order, so equal positions stay in step order
+      const int pos_bits = bits_for(uint64_t(p.n > 1 ? p.n - 1 : 1));
       cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, d_keys, d_sk, int(steps), 0, 64, s);
+        return cub::DeviceRadixSort::SortKeys(t, b, d_keys, d_sk, int(steps), 32, 32 + pos_bits, s);
       }, s);
       VPG_LAUNCH(k_swap_links, grid_for(steps, block), block, 0, s, d_sk, steps, p.n, d_prev);
       VPG_LAUNCH(k_swap_resolve, grid_for(steps, block), block, 0, s, d_target, d_sk, d_prev, steps,
@@ -1436,7 +1511,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                  ids.get());
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(),
-                                               sids.get(), m, 0, 64, s);
+                                               sids.get(), m, 0, end_bits, s);
       }, s);
       VPG_LAUNCH(k_center_table, grid_for(m, block), block, 0, s, skeys.get(), sids.get(),
                  cpos.get(), m, gp, spos.get(), table.get());
@@ -1445,9 +1520,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       // part A layout order (the table no longer needs skeys/sids)
       VPG_LAUNCH(k_center_morton, grid_for(m, block), block, 0, s, cpos.get(), m, gp, keys.get(),
                  ids.get());
+      // Morton bits: cell coordinates are clamped to [0, 2^21) per axis
+      long long max_dim = 1;
+      for (int a = 0; a < 3; ++a) max_dim = std::max(max_dim, gp.dims[a]);
+      const int morton_bits = 3 * std::min(21, bits_for(uint64_t(max_dim)));
       cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(),
-                                               sids.get(), m, 0, 63, s);
+                                               sids.get(), m, 0, morton_bits, s);
       }, s);
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
@@ -1891,8 +1970,7 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
   int32_t* fb_list = scratch_of<int32_t>(s, "an_fb_list", n + 1);
   VPG_LAUNCH(k_point_keys, grid_for(n, block), block, 0, s, nullptr, 0, n, pos, gp, pkeys, pids);
   int end_bits = 64;
-  if (gp.packed)
-    end_bits = bits_for(uint64_t((gp.dims[0] + 3) * (gp.dims[1] + 2) * (gp.dims[2] + 2)));
+  if (gp.packed) end_bits = packed_key_bits(gp);
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted, int(n), 0,
                                            end_bits, s);
