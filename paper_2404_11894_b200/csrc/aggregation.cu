@@ -30,6 +30,8 @@ namespace {
 constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 constexpr double kInvPi = 1.0 / 3.14159265358979323846;
 constexpr int kAggThreads = 128;
+// HG densities are evaluated all in fp32 for |g| <= kG32 (see hg_pdf32)
+constexpr float kG32 = 0.95f;
 // dynamic shared memory of k_aggregate for the largest supported cluster (2K = 160)
 constexpr size_t kAggSmemMax = 226 * 1024;
 
@@ -41,7 +43,7 @@ struct __align__(32) Member {
   float de[3], dp[3];  // d_emit, d_phase
   float coeff[3], wc[3];
   float ipt[3];
-  uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface
+  uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface, 8 |g| > kG32
   int32_t parent;  // cluster-major row of the continuation parent, -1 none / not yet known
   uint32_t pad[7];
 };
@@ -100,7 +102,8 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
     // no continuation child (records.py:128-140); shard-local records carry it
     const bool terminal = has_child ? !has_child[r]
                                     : !(r + 1 < n && rec.path_idx[r + 1] == rec.path_idx[r]);
-    m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u);
+    m.flags = (rec.emit_delta[r] ? 1u : 0u) | (terminal ? 2u : 0u) | (volume ? 0u : 4u) |
+              (fabs(m.g) > double(kG32) ? 8u : 0u);
     // continuation parent r-1 (records.py:128-140) when its row is already
     // placed; a parent placed later (a split group) links its children in
     // k_child_links.  Shard-local builds get theirs from k_set_parents.
@@ -171,22 +174,44 @@ __device__ __forceinline__ float hg_pdf(double ax, double ay, double az, double 
   return num * (r * r * r);
 }
 
+// HG density with every operand fp32, for |g| <= kG32: den = 1 + g^2 - 2g cos
+// is evaluated as |d - g a|^2 + (1 - |d|^2) + g^2 (1 - |a|^2), an identity
+// for any vectors (the corrections are ~1e-16 for the unit directions the
+// tracer writes and exact for a zero direction), in which nothing cancels:
+// for |g| <= 0.95 the components of d - g a are >= ~0.05 in the forward
+// peak, so the fp32 rounding of the inputs costs < 1e-5 relative on the
+// density (measured ~1e-6), inside the 1e-4 radiance bar.  Larger |g| keeps
+// the fp64 cosine and denominator (hg_pdf above).
+__device__ __forceinline__ float hg_pdf32(float ax, float ay, float az, float g, float num,
+                                          float g2ca, float dx, float dy, float dz, float cd) {
+  const float ux = fmaf(-g, ax, dx), uy = fmaf(-g, ay, dy), uz = fmaf(-g, az, dz);
+  const float den = fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, cd + g2ca)));
+  const float r = rsqrtf(den);
+  return num * (r * r * r);
+}
+
 // Dynamic shared memory for clusters of up to S members:
 //   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2 (num also
-//         as fp32 in the low word of its slot's float view, see below)
+//         as fp32 after them); mode kVol32 keeps its fp32 operands in the same
+//         region instead: ax ay az px py pz ex ey ez g num g^2(1-|a|^2)
+//         (1-|p|^2) (1-|e|^2), S floats each
 //   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
 //          (volume clusters keep them as fp32 in the same region)
 //   pd     S*(S+1) floats (phase-direction pair densities, row-padded; the
 //          emitter-direction ones are recomputed in pass 2b)
-template <bool kVol>
+enum AggMode { kSurface = 0, kVol64 = 1, kVol32 = 2 };
+
+template <int kMode>
 __device__ __forceinline__ void aggregate_cluster(
     const Member* __restrict__ mem, int32_t q0, int s, int64_t wb, int64_t n, int S,
     double* __restrict__ geo, double* __restrict__ wts, float* __restrict__ pd,
     float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
     float4* __restrict__ coeff_o, float4* __restrict__ rows_o, float4* __restrict__ i0_o) {
+  constexpr bool kVol = kMode != kSurface;
   using acc_t = typename std::conditional<kVol, float, double>::type;
   const int tid = threadIdx.x;
   const float* numf = reinterpret_cast<const float*>(geo + 12 * S);  // S floats after geo
+  const float* g32 = reinterpret_cast<const float*>(geo);            // kVol32 operands
   float* wtsf = reinterpret_cast<float*>(wts);
   const double ks = double(s);
 
@@ -202,24 +227,39 @@ __device__ __forceinline__ void aggregate_cluster(
     const int j = t / P, h = t % P;
     acc_t sp = 0, se = 0;
     if (active) {
-      const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
-      const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
       const int l0 = h * slice, l1 = min(s, l0 + slice);
-      for (int l = l0; l < l1; ++l) {
-        if constexpr (kVol) {
-          const double ax = geo[l], ay = geo[S + l], az = geo[2 * S + l];
-          const double c1 = geo[10 * S + l], c2 = geo[11 * S + l];
-          const float a = hg_pdf(ax, ay, az, c1, c2, numf[l], dpx, dpy, dpz);
-          const float b = hg_pdf(ax, ay, az, c1, c2, numf[l], dex, dey, dez);
+      if constexpr (kMode == kVol32) {
+        const float dpx = g32[3 * S + j], dpy = g32[4 * S + j], dpz = g32[5 * S + j];
+        const float dex = g32[6 * S + j], dey = g32[7 * S + j], dez = g32[8 * S + j];
+        const float cp = g32[12 * S + j], ce = g32[13 * S + j];
+        for (int l = l0; l < l1; ++l) {
+          const float ax = g32[l], ay = g32[S + l], az = g32[2 * S + l];
+          const float g = g32[9 * S + l], num = g32[10 * S + l], g2ca = g32[11 * S + l];
+          const float a = hg_pdf32(ax, ay, az, g, num, g2ca, dpx, dpy, dpz, cp);
+          const float b = hg_pdf32(ax, ay, az, g, num, g2ca, dex, dey, dez, ce);
           pd[l * (S + 1) + j] = a;
           sp += a;
           se += b;
-        } else {
-          const double a = surface_pdf(geo, S, l, dpx, dpy, dpz);
-          const double b = surface_pdf(geo, S, l, dex, dey, dez);
-          pd[l * (S + 1) + j] = float(a);
-          sp = __dadd_rn(sp, a);
-          se = __dadd_rn(se, b);
+        }
+      } else {
+        const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
+        const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
+        for (int l = l0; l < l1; ++l) {
+          if constexpr (kMode == kVol64) {
+            const double ax = geo[l], ay = geo[S + l], az = geo[2 * S + l];
+            const double c1 = geo[10 * S + l], c2 = geo[11 * S + l];
+            const float a = hg_pdf(ax, ay, az, c1, c2, numf[l], dpx, dpy, dpz);
+            const float b = hg_pdf(ax, ay, az, c1, c2, numf[l], dex, dey, dez);
+            pd[l * (S + 1) + j] = a;
+            sp += a;
+            se += b;
+          } else {
+            const double a = surface_pdf(geo, S, l, dpx, dpy, dpz);
+            const double b = surface_pdf(geo, S, l, dex, dey, dez);
+            pd[l * (S + 1) + j] = float(a);
+            sp = __dadd_rn(sp, a);
+            se = __dadd_rn(se, b);
+          }
         }
       }
     }
@@ -265,16 +305,9 @@ __device__ __forceinline__ void aggregate_cluster(
   }
   __syncthreads();
 
-  // pass 2a: the kernel block, transposed (wt[wb + j*s + r] = W[r, j])
-  for (int idx = tid; idx < s * s; idx += blockDim.x) {
-    const int j = idx / s, r = idx - j * s;
-    if constexpr (kVol)
-      wt[wb + idx] = pd[r * (S + 1) + j] * wtsf[j];
-    else
-      wt[wb + idx] = float(double(pd[r * (S + 1) + j]) * wts[j]);
-  }
-  // pass 2b: rows: D-bar and the solve vectors, P2 threads per row each
-  // summing a slice of the columns, combined in a fixed order
+  // pass 2: rows: the kernel block (transposed, wt[wb + j*s + r] = W[r, j]),
+  // D-bar and the solve vectors, P2 threads per row each covering a slice
+  // of the columns, the D-bar sums combined in a fixed order
   const int P2 = s <= 32 ? 4 : 2;
   const int slice2 = (s + P2 - 1) / P2;
   for (int base = 0; base < P2 * s; base += blockDim.x) {
@@ -287,12 +320,25 @@ __device__ __forceinline__ void aggregate_cluster(
       const int j0 = h * slice2, j1 = min(s, j0 + slice2);
       // the emitter-direction density is recomputed rather than kept in
       // shared memory: half the pair storage, 8 CTAs per SM instead of 5
-      if constexpr (kVol) {
+      if constexpr (kMode == kVol32) {
+        const float ax = g32[r], ay = g32[S + r], az = g32[2 * S + r];
+        const float g = g32[9 * S + r], num = g32[10 * S + r], g2ca = g32[11 * S + r];
+        for (int j = j0; j < j1; ++j) {
+          const float a = prow[j];
+          wt[wb + j * s + r] = a * wtsf[j];
+          const float b = hg_pdf32(ax, ay, az, g, num, g2ca, g32[6 * S + j], g32[7 * S + j],
+                                   g32[8 * S + j], g32[13 * S + j]);
+          dx += b * wtsf[S + j] + a * wtsf[4 * S + j];
+          dy += b * wtsf[2 * S + j] + a * wtsf[5 * S + j];
+          dz += b * wtsf[3 * S + j] + a * wtsf[6 * S + j];
+        }
+      } else if constexpr (kMode == kVol64) {
         const double ax = geo[r], ay = geo[S + r], az = geo[2 * S + r];
         const double c1 = geo[10 * S + r], c2 = geo[11 * S + r];
         const float num = numf[r];
         for (int j = j0; j < j1; ++j) {
           const float a = prow[j];
+          wt[wb + j * s + r] = a * wtsf[j];
           const float b = hg_pdf(ax, ay, az, c1, c2, num, geo[6 * S + j], geo[7 * S + j],
                                  geo[8 * S + j]);
           dx += b * wtsf[S + j] + a * wtsf[4 * S + j];
@@ -302,6 +348,7 @@ __device__ __forceinline__ void aggregate_cluster(
       } else {
         for (int j = j0; j < j1; ++j) {
           const double a = prow[j];
+          wt[wb + j * s + r] = float(a * wts[j]);
           const double b = surface_pdf(geo, S, r, geo[6 * S + j], geo[7 * S + j], geo[8 * S + j]);
           dx += b * wts[S + j] + a * wts[4 * S + j];
           dy += b * wts[2 * S + j] + a * wts[5 * S + j];
@@ -343,9 +390,9 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   extern __shared__ __align__(16) unsigned char smem[];
   double* geo = reinterpret_cast<double*>(smem);
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
+  float* g32 = reinterpret_cast<float*>(geo);
   double* wts = geo + 12 * S + (S + 1) / 2;
   float* pd = reinterpret_cast<float*>(wts + 7 * S);
-  __shared__ int s_volume;
   const int tid = threadIdx.x;
 
   const int64_t k_end = range[1];
@@ -353,33 +400,74 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
     const int32_t q0 = cl_off[k];
     const int s = cl_size[k];
     const int64_t wb = w_off[k];
+    {
+      // pull the next cluster's members towards L2 while this one computes
+      const int64_t kn = k + gridDim.x;
+      if (kn < k_end) {
+        const int32_t qn = cl_off[kn], sn = cl_size[kn];
+        const char* base = reinterpret_cast<const char*>(mem + qn);
+        const int lines = (sn * int(sizeof(Member)) + 127) / 128;
+        for (int i = tid; i < lines; i += blockDim.x)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * i));
+      }
+    }
+    // the cluster's mode: Lambertian, HG with fp64 denominators (some
+    // |g| > kG32), or HG all in fp32 -- every warp reduces the member flags
+    // itself, so no block barrier is needed
+    uint32_t fl = 0;
+    for (int l = tid & 31; l < s; l += 32) fl |= mem[q0 + l].flags;
+    const bool surface = __any_sync(0xFFFFFFFFu, fl & 4u);
+    const bool need64 = __any_sync(0xFFFFFFFFu, fl & 8u);
+    const int mode = surface ? kSurface : (need64 ? kVol64 : kVol32);
     for (int l = tid; l < s; l += blockDim.x) {
       const Member& mb = mem[q0 + l];
-      geo[l] = mb.ax;
-      geo[S + l] = mb.ay;
-      geo[2 * S + l] = mb.az;
-      geo[3 * S + l] = mb.px;
-      geo[4 * S + l] = mb.py;
-      geo[5 * S + l] = mb.pz;
-      geo[6 * S + l] = mb.ex;
-      geo[7 * S + l] = mb.ey;
-      geo[8 * S + l] = mb.ez;
       const double g = mb.g;
       const double g2 = __dmul_rn(g, g);
       const double num = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
-      geo[9 * S + l] = num;
-      numf[l] = float(num);
-      geo[10 * S + l] = __dadd_rn(1.0, g2);
-      geo[11 * S + l] = __dmul_rn(2.0, g);
-      if (l == 0) s_volume = (mb.flags & 4u) ? 0 : 1;
+      if (mode == kVol32) {
+        g32[l] = float(mb.ax);
+        g32[S + l] = float(mb.ay);
+        g32[2 * S + l] = float(mb.az);
+        g32[3 * S + l] = float(mb.px);
+        g32[4 * S + l] = float(mb.py);
+        g32[5 * S + l] = float(mb.pz);
+        g32[6 * S + l] = float(mb.ex);
+        g32[7 * S + l] = float(mb.ey);
+        g32[8 * S + l] = float(mb.ez);
+        g32[9 * S + l] = float(g);
+        g32[10 * S + l] = float(num);
+        const double na = fma(mb.ax, mb.ax, fma(mb.ay, mb.ay, mb.az * mb.az));
+        const double np = fma(mb.px, mb.px, fma(mb.py, mb.py, mb.pz * mb.pz));
+        const double ne = fma(mb.ex, mb.ex, fma(mb.ey, mb.ey, mb.ez * mb.ez));
+        g32[11 * S + l] = float(g2 * (1.0 - na));
+        g32[12 * S + l] = float(1.0 - np);
+        g32[13 * S + l] = float(1.0 - ne);
+      } else {
+        geo[l] = mb.ax;
+        geo[S + l] = mb.ay;
+        geo[2 * S + l] = mb.az;
+        geo[3 * S + l] = mb.px;
+        geo[4 * S + l] = mb.py;
+        geo[5 * S + l] = mb.pz;
+        geo[6 * S + l] = mb.ex;
+        geo[7 * S + l] = mb.ey;
+        geo[8 * S + l] = mb.ez;
+        geo[9 * S + l] = num;
+        numf[l] = float(num);
+        geo[10 * S + l] = __dadd_rn(1.0, g2);
+        geo[11 * S + l] = __dmul_rn(2.0, g);
+      }
     }
     __syncthreads();
-    if (s_volume)
-      aggregate_cluster<true>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
-                              rows_o, i0_o);
+    if (mode == kVol32)
+      aggregate_cluster<kVol32>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+                                rows_o, i0_o);
+    else if (mode == kVol64)
+      aggregate_cluster<kVol64>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+                                rows_o, i0_o);
     else
-      aggregate_cluster<false>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
-                               rows_o, i0_o);
+      aggregate_cluster<kSurface>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+                                  rows_o, i0_o);
     __syncthreads();
   }
 }
