@@ -231,7 +231,7 @@ __global__ void k_center_table(const unsigned long long* __restrict__ skeys,
     const int j = sids[i];
     spos[i] = make_double4(cpos[j * 3], cpos[j * 3 + 1], cpos[j * 3 + 2], __longlong_as_double((long long)j));
     const unsigned long long key = skeys[i];
-    if (i == 0 || skeys[i - 1] != key) {
+    if (table && (i == 0 || skeys[i - 1] != key)) {
       uint64_t slot = table_slot(key, gp.table_mask);
       while (true) {
         const unsigned long long prev = atomicCAS(&table[slot].key, kEmpty, key);
@@ -254,6 +254,37 @@ __device__ __forceinline__ const CellEntry* table_find(const CellEntry* table, u
     if (k == key) return e;
     if (k == kEmpty) return nullptr;
     slot = (slot + 1) & mask;
+  }
+}
+
+// Cell -> [first, end) of its centers among the key-sorted centers: a direct
+// array over the dense packed keys when the grid is small enough (one load),
+// else the hash table.
+struct CellIndex {
+  const CellEntry* hash;
+  const int2* dense;
+  uint64_t mask;
+  __device__ __forceinline__ bool find(uint64_t key, int& start, int& end) const {
+    if (dense) {
+      const int2 e = dense[key];
+      start = e.x;
+      end = e.y;
+      return e.y > e.x;
+    }
+    const CellEntry* e = table_find(hash, key, mask);
+    if (!e) return false;
+    start = e->start;
+    end = e->end;
+    return true;
+  }
+};
+
+__global__ void k_center_dense(const unsigned long long* __restrict__ skeys, int m,
+                               int2* __restrict__ dense) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long key = skeys[i];
+    if (i == 0 || skeys[i - 1] != key) dense[key].x = i;
+    if (i == m - 1 || skeys[i + 1] != key) dense[key].y = i + 1;
   }
 }
 
@@ -280,13 +311,12 @@ __device__ __forceinline__ void best_update(Best& b, double d2, int j) {
 }
 
 // Scan the centers of one cell (key) into `b`.
-__device__ __forceinline__ void scan_cell(const GridParams& gp, const CellEntry* table,
+__device__ __forceinline__ void scan_cell(const GridParams& gp, const CellIndex& table,
                                           const double4* __restrict__ spos, long long cx,
                                           long long cy, long long cz, double px, double py,
                                           double pz, Best& b) {
-  const CellEntry* e = table_find(table, cell_key(gp, cx, cy, cz), gp.table_mask);
-  if (!e) return;
-  const int start = e->start, end = e->end;
+  int start, end;
+  if (!table.find(cell_key(gp, cx, cy, cz), start, end)) return;
   for (int t = start; t < end; ++t) {
     const double4 c = spos[t];
     if (!gp.packed) {  // hashed keys: confirm the cell really matches
@@ -460,7 +490,7 @@ __global__ void k_cell_runs(const int32_t* __restrict__ cells, const int32_t* __
 // -- exactly the reference's per-cell candidate list (clustering.py:121-137).
 __global__ void __launch_bounds__(kAssignWarps * 32)
 k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ pos, GridParams gp,
-               const CellEntry* __restrict__ table, const double4* __restrict__ spos,
+               CellIndex table, const double4* __restrict__ spos,
                const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ run_start,
                const int32_t* __restrict__ run_len, const int32_t* __restrict__ n_runs,
                int32_t* __restrict__ assign, int32_t* __restrict__ fb_list,
@@ -481,10 +511,10 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
       nx = cx + lane / 9 - 1;
       ny = cy + (lane / 3) % 3 - 1;
       nz = cz + lane % 3 - 1;
-      const CellEntry* e = table_find(table, cell_key(gp, nx, ny, nz), gp.table_mask);
-      if (e) {
-        c_start = e->start;
-        c_cnt = e->end - e->start;
+      int st, en;
+      if (table.find(cell_key(gp, nx, ny, nz), st, en)) {
+        c_start = st;
+        c_cnt = en - st;
       }
     }
     int incl = c_cnt;  // inclusive warp scan of candidate counts
@@ -607,8 +637,7 @@ __device__ __forceinline__ void warp_best(Best& b) {
 // centers.
 __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
                                   const double* __restrict__ pos, GridParams gp,
-                                  const CellEntry* __restrict__ table,
-                                  const double4* __restrict__ spos,
+                                  CellIndex table, const double4* __restrict__ spos,
                                   const int32_t* __restrict__ fb_list, const int32_t* fb_count,
                                   int32_t* __restrict__ assign, int32_t* __restrict__ far_list,
                                   int32_t* __restrict__ far_count,
@@ -1122,6 +1151,17 @@ int bits_for(uint64_t max_value) {
   return b;
 }
 
+// cells of the dense packed key space, and whether a direct cell index over it
+// is small enough (8 bytes per cell)
+int64_t dense_cells(const GridParams& gp) {
+  return int64_t(gp.dims[0] + 4) * int64_t(gp.dims[1] + 4) * int64_t(gp.dims[2] + 4);
+}
+bool dense_cells_ok(const GridParams& gp, int64_t m) {
+  if (!gp.packed) return false;
+  const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
+  return cells <= 8.0 * double(m) + 65536.0;
+}
+
 // radix bits of the dense packed cell keys (cell_key)
 int packed_key_bits(const GridParams& gp) {
   const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
@@ -1504,8 +1544,17 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                  cpos.get(), crec_all.get() + p.center_off, keys.get(), ids.get());
       VPG_CUDA(cudaMemsetAsync(assign_c, 0, sizeof(int32_t) * p.n, s));
     } else {
-      DBuf<CellEntry> table(gp.table_mask + 1, s);
-      VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+      DBuf<CellEntry> table;
+      DBuf<int2> dense;
+      const bool use_dense = dense_cells_ok(gp, m);
+      if (use_dense) {
+        dense.alloc(size_t(dense_cells(gp)), s);
+        VPG_CUDA(cudaMemsetAsync(dense.get(), 0, dense.bytes(), s));
+      } else {
+        table.alloc(gp.table_mask + 1, s);
+        VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+      }
+      const CellIndex cidx{table.get(), use_dense ? dense.get() : nullptr, gp.table_mask};
       VPG_LAUNCH(k_center_setup, grid_for(m, block), block, 0, s, d_local.get(), m, rows_p,
                  p.row_off, rec.pos, gp, cpos.get(), crec_all.get() + p.center_off, keys.get(),
                  ids.get());
@@ -1514,9 +1563,12 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                                                sids.get(), m, 0, end_bits, s);
       }, s);
       VPG_LAUNCH(k_center_table, grid_for(m, block), block, 0, s, skeys.get(), sids.get(),
-                 cpos.get(), m, gp, spos.get(), table.get());
-      VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
-                 table.get());
+                 cpos.get(), m, gp, spos.get(), use_dense ? nullptr : table.get());
+      if (use_dense)
+        VPG_LAUNCH(k_center_dense, grid_for(m, block), block, 0, s, skeys.get(), m, dense.get());
+      else
+        VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
+                   table.get());
       // part A layout order (the table no longer needs skeys/sids)
       VPG_LAUNCH(k_center_morton, grid_for(m, block), block, 0, s, cpos.get(), m, gp, keys.get(),
                  ids.get());
@@ -1530,14 +1582,14 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       }, s);
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
-                 rec.pos, gp, table.get(), spos.get(), pids_sorted, run_start, run_len,
+                 rec.pos, gp, cidx, spos.get(), pids_sorted, run_start, run_len,
                  scalars.get() + 1, assign_c, fb_list, scalars.get());
       int32_t* far_list = scratch_of<int32_t>(s, "far_list", p.n + 1);
       auto* far_d = scratch_of<unsigned long long>(s, "far_d", p.n + 1);
       int32_t* far_j = scratch_of<int32_t>(s, "far_j", p.n + 1);
       VPG_CUDA(cudaMemsetAsync(far_count.get(), 0, sizeof(int32_t), s));
       VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, rows_p, p.row_off, rec.pos, gp,
-                 table.get(), spos.get(), fb_list, scalars.get(), assign_c, far_list,
+                 cidx, spos.get(), fb_list, scalars.get(), assign_c, far_list,
                  far_count.get(), far_d, far_j);
       // points beyond the shell budget: tiled exact scan (grid sized for the
       // worst case; blocks past the list's end exit at once)
@@ -1985,25 +2037,37 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
   DBuf<unsigned long long> keys(m, s), skeys(m, s);
   DBuf<int32_t> ids(m, s), sids(m, s);
   DBuf<double4> spos(m, s);
-  DBuf<CellEntry> table(gp.table_mask + 1, s);
-  VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+  DBuf<CellEntry> table;
+  DBuf<int2> dense;
+  const bool use_dense = dense_cells_ok(gp, m);
+  if (use_dense) {
+    dense.alloc(size_t(dense_cells(gp)), s);
+    VPG_CUDA(cudaMemsetAsync(dense.get(), 0, dense.bytes(), s));
+  } else {
+    table.alloc(gp.table_mask + 1, s);
+    VPG_CUDA(cudaMemsetAsync(table.get(), 0xFF, table.bytes(), s));
+  }
+  const CellIndex cidx{table.get(), use_dense ? dense.get() : nullptr, gp.table_mask};
   VPG_LAUNCH(k_center_keys, grid_for(m, block), block, 0, s, cpos, m, gp, keys.get(), ids.get());
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), skeys.get(), ids.get(), sids.get(), m,
-                                           0, 64, s);
+                                           0, gp.packed ? packed_key_bits(gp) : 64, s);
   }, s);
   VPG_LAUNCH(k_center_table, grid_for(m, block), block, 0, s, skeys.get(), sids.get(), cpos, m, gp,
-             spos.get(), table.get());
-  VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
-             table.get());
+             spos.get(), use_dense ? nullptr : table.get());
+  if (use_dense)
+    VPG_LAUNCH(k_center_dense, grid_for(m, block), block, 0, s, skeys.get(), m, dense.get());
+  else
+    VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
+               table.get());
   VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, nullptr, 0, pos, gp,
-             table.get(), spos.get(), pids_sorted, run_start, run_len, scalars.get() + 1, assign,
+             cidx, spos.get(), pids_sorted, run_start, run_len, scalars.get() + 1, assign,
              fb_list, scalars.get());
   int32_t* far_list = scratch_of<int32_t>(s, "an_far_list", n + 1);
   auto* far_d = scratch_of<unsigned long long>(s, "an_far_d", n + 1);
   int32_t* far_j = scratch_of<int32_t>(s, "an_far_j", n + 1);
   VPG_CUDA(cudaMemsetAsync(far_count.get(), 0, sizeof(int32_t), s));
-  VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, nullptr, 0, pos, gp, table.get(),
+  VPG_LAUNCH(k_assign_fallback, sm_count() * 8, 256, 0, s, nullptr, 0, pos, gp, cidx,
              spos.get(), fb_list, scalars.get(), assign, far_list, far_count.get(), far_d, far_j);
   for (int pass = 0; pass < 2; ++pass)
     VPG_LAUNCH(k_far_tiles, sm_count() * 4, 256, 0, s, nullptr, 0, pos, spos.get(), m, far_list,
