@@ -711,9 +711,11 @@ k_far_tiles(const int32_t* rows, int64_t row_off, const double* __restrict__ pos
   __shared__ double4 tile[256];
   const int nf = *far_count;
   const int groups = (nf + 255) / 256;
-  const int64_t per = (int64_t(m) + kFarSlices - 1) / kFarSlices;
-  for (int blk = blockIdx.x; blk < groups * kFarSlices; blk += gridDim.x) {
-    const int grp = blk / kFarSlices, slice = blk % kFarSlices;
+  // few far points: cut the centers into more slices so every block works
+  const int slices = groups > 0 ? max(kFarSlices, int(gridDim.x) / groups) : kFarSlices;
+  const int64_t per = (int64_t(m) + slices - 1) / slices;
+  for (int blk = blockIdx.x; blk < groups * slices; blk += gridDim.x) {
+    const int grp = blk / slices, slice = blk % slices;
     const int pi = grp * 256 + threadIdx.x;
     const bool active = pi < nf;
     double px = 0, py = 0, pz = 0, target = 0;
