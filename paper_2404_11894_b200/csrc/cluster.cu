@@ -1701,7 +1701,30 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     VPG_CUDA(cudaMemcpyAsync(h_mask_total.get(), mask_total.get(),
                              sizeof(int64_t) * (1 + 3 * (kBulkPieces + 1)), cudaMemcpyDeviceToHost, s));
     count_transfer(0, 16 + 8 * (1 + 3 * (kBulkPieces + 1)));
-    VPG_CUDA(cudaStreamSynchronize(s));
+    // the staging below runs on the side stream from here; part A goes on s
+    // now, before the host learns the staging sizes
+    cudaStream_t side = side_stream();
+    cudaEvent_t sized;
+    VPG_CUDA(cudaEventCreateWithFlags(&sized, cudaEventDisableTiming));
+    VPG_CUDA(cudaEventRecord(sized, s));
+    VPG_CUDA(cudaStreamWaitEvent(side, sized, 0));
+    // ---- part A of this class: permutation, pack, aggregate (device, async)
+    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
+               g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
+               g->clpos.get(), g->cluster_id.get());
+    // part B (split results) may start once this class's rows are placed
+    VPG_CUDA(cudaEventRecord(placed, s));
+    if (with_ops) {
+      // the operator fields may still be in flight (async upload): the
+      // clustering above only needed pos, kind and class_id
+      if (fields_ready && c == 0) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
+      pack_members(g, rec, rows_p ? rows_p + p.row_off : nullptr, p.n, p.row_off, members, s);
+      aggregate_range(g, members, ranges.get() + 2 * c, m, S, s);
+      // children in earlier classes were packed before these parents existed
+      if (c > 0 && rows_p) link_children(g, rec, rows_p + p.row_off, p.n, s);
+    }
+    VPG_CUDA(cudaEventSynchronize(sized));
+    cudaEventDestroy(sized);
     g->info.n_fallback += h_scalars[0];
     const int n_over = h_scalars[2];
     const int64_t staged = n_over > 0 ? h_scalars[3] : 0;
@@ -1715,7 +1738,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     HostBuf<unsigned long long> h_masks(size_t(n_mask) + 1);
     HostBuf<int32_t> h_moved(size_t(staged) + 1);
     // kept until part B applies the deferred first splits
-    auto d_masks_own = std::make_unique<DBuf<unsigned long long>>(size_t(n_mask) + 1, s);
+    auto d_masks_own = std::make_unique<DBuf<unsigned long long>>(size_t(n_mask) + 1, side);
+    d_masks_own->s = s;  // released on s, which joins part B (its last reader)
     cudaEvent_t staged_ready;
     VPG_CUDA(cudaEventCreateWithFlags(&staged_ready, cudaEventDisableTiming));
     // positions, distances and mask rows go in pieces, last groups first (the
@@ -1728,22 +1752,15 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       double* d_xyzd = scratch_of<double>(s, "staged_xyzd", size_t(staged) * 4 + 4);
       unsigned long long* d_masks = d_masks_own->get();
       int32_t* d_moved = scratch_of<int32_t>(s, "first_moved", size_t(staged) + 1);
-      VPG_CUDA(cudaMemsetAsync(d_moved, 0, sizeof(int32_t) * staged, s));
-      VPG_CUDA(cudaMemsetAsync(d_slot, 0x7F, sizeof(int32_t) * n_over, s));
-      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, s, grp_rec, over_seg,
+      VPG_CUDA(cudaMemsetAsync(d_moved, 0, sizeof(int32_t) * staged, side));
+      VPG_CUDA(cudaMemsetAsync(d_slot, 0x7F, sizeof(int32_t) * n_over, side));
+      VPG_LAUNCH(k_gather_oversize, std::min<int64_t>(n_over, 65535), 128, 0, side, grp_rec, over_seg,
                  scalars.get() + 2, over_info.get(), rec.pos, d_srec, d_xyzd, d_xyzd + staged,
                  d_xyzd + 2 * staged, d_xyzd + 3 * staged, d_slot);
-      VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, s, over_seg,
+      VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, side, over_seg,
                  scalars.get() + 2, mask_off, d_xyzd, d_xyzd + staged, d_xyzd + 2 * staged,
                  d_xyzd + 3 * staged, d_masks, d_moved);
-      // the staging goes to the host on a side stream, so part A's kernels
-      // (queued next on s) do not wait behind the copies
-      cudaStream_t side = side_stream();
-      cudaEvent_t gathered;
-      VPG_CUDA(cudaEventCreateWithFlags(&gathered, cudaEventDisableTiming));
-      VPG_CUDA(cudaEventRecord(gathered, s));
-      VPG_CUDA(cudaStreamWaitEvent(side, gathered, 0));
-      cudaEventDestroy(gathered);
+      // the staging goes to the host from the side stream, beside part A
       VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
                                cudaMemcpyDeviceToHost, side));
       VPG_CUDA(cudaMemcpyAsync(h_srec.get(), d_srec, sizeof(int32_t) * staged,
@@ -1769,22 +1786,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       }
       count_transfer(0, 36 * n_over + 40 * staged + 8 * n_mask);
     } else {
-      VPG_CUDA(cudaEventRecord(staged_ready, s));
-    }
-    // ---- part A of this class: permutation, pack, aggregate (device, async)
-    VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
-               g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
-               g->clpos.get(), g->cluster_id.get());
-    // part B (split results) may start once this class's rows are placed
-    VPG_CUDA(cudaEventRecord(placed, s));
-    if (with_ops) {
-      // the operator fields may still be in flight (async upload): the
-      // clustering above only needed pos, kind and class_id
-      if (fields_ready && c == 0) VPG_CUDA(cudaStreamWaitEvent(s, fields_ready, 0));
-      pack_members(g, rec, rows_p ? rows_p + p.row_off : nullptr, p.n, p.row_off, members, s);
-      aggregate_range(g, members, ranges.get() + 2 * c, m, S, s);
-      // children in earlier classes were packed before these parents existed
-      if (c > 0 && rows_p) link_children(g, rec, rows_p + p.row_off, p.n, s);
+      VPG_CUDA(cudaEventRecord(staged_ready, side));
     }
     clk.mark(3);
 
