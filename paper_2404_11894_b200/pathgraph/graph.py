@@ -20,6 +20,10 @@ from paper_2404_11894_b200.pathgraph.clustering import Cluster
 from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
 
 
+# the record fields the build and the solve read on the device (depth never)
+BUILD_FIELDS = tuple(f[0] for f in N.RECORD_FIELDS if f[0] != "depth")
+
+
 class NativeGraph:
     """Owns a vpg_graph handle and keeps the device records it borrows alive."""
 
@@ -37,7 +41,7 @@ class NativeGraph:
         # the clustering needs only pos/kind/class_id: with an upload in flight
         # the native build waits for the other fields itself, just before it
         # first reads them
-        st = records.device(wait="early")
+        st = records.device(wait="early", need=BUILD_FIELDS)
         fields = records.ready_event("all")
         if flags & N.VPG_BUILD_CLUSTERS_ONLY:
             fields = None  # never read; later device() calls wait for them
@@ -47,7 +51,7 @@ class NativeGraph:
             ctypes.byref(st), int(cluster_size), ctypes.byref(state), int(flags), N.stream_handle(),
             fields.cuda_event if fields is not None else None, ctypes.byref(out)))
         state.store_into(rng)
-        return cls(out.value, records.device_tensors(), st, records.n)
+        return cls(out.value, dict(records._dev), st, records.n)
 
     def info(self) -> N.GraphInfo:
         gi = N.GraphInfo()

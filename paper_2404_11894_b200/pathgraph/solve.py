@@ -93,7 +93,8 @@ def splat_output_device(graph, result: SolveResult, aggregate_direct_term: bool 
         raise RuntimeError("the graph was solved again; this SolveResult is stale")
     mode = N.DIRECT_AGGREGATED if aggregate_direct_term else (
         N.DIRECT_EXTRA if extra_direct else N.DIRECT_PT)
-    pst = graph.paths.device()
+    pst = graph.paths.device(need=("rec_start", "rec_count", "cam_weight", "d_cam",
+                                   "extra_direct" if mode == N.DIRECT_EXTRA else "direct0"))
     img = torch.empty((graph.height, graph.width, 3), dtype=torch.float64, device="cuda")
     N.check(N.lib().vpg_splat(g.handle, ctypes.byref(pst), graph.width, graph.height, graph.spp,
                               mode, img.data_ptr(), N.stream_handle()))

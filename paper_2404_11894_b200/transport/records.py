@@ -79,7 +79,7 @@ class _DualSoA:
 
     def _set(self, name, value, width, code):
         arr = np.ascontiguousarray(value, dtype=np.dtype("<" + code))
-        if self._dev is not None:
+        if self._dev is not None and name in self._dev:
             dev = self._dev[name]
             if tuple(dev.shape) == arr.shape:
                 dev.copy_(_torch().from_numpy(arr))  # keep both sides in step
@@ -88,6 +88,7 @@ class _DualSoA:
                 for other, _, _ in self._FIELDS:
                     self._get(other)
                 object.__setattr__(self, "_dev", None)
+                object.__setattr__(self, "_missing", set())
                 object.__setattr__(self, "_struct", None)
                 object.__setattr__(self, "_n", int(arr.shape[0]))
         self._host[name] = arr
@@ -110,12 +111,13 @@ class _DualSoA:
     # fields a consumer may need before the rest (RecordSoA: the clustering's)
     _EARLY: tuple = ()
 
-    def upload_async(self):
+    def upload_async(self, skip=()):
         """Start the host->device copies of a pinned SoA on the copy stream:
         the _EARLY fields first, then the rest, each group closed by an event
         ("early", "all").  Consumers wait on the group they need (device()
         waits on "all"), so compute that needs only the early fields overlaps
-        the rest of the transfer."""
+        the rest of the transfer.  Fields in `skip` stay on the host until a
+        device() call asks for them (the graph solve never reads them)."""
         if self._dev is not None:
             return
         torch = N.require_cuda()
@@ -127,10 +129,11 @@ class _DualSoA:
         copy.wait_stream(main)
         dev, events = {}, {}
         order = [f for f in self._FIELDS if f[0] in self._EARLY] + \
-                [f for f in self._FIELDS if f[0] not in self._EARLY]
+                [f for f in self._FIELDS if f[0] not in self._EARLY and f[0] not in skip]
         with torch.cuda.stream(copy):
             for k, (name, width, code) in enumerate(order):
                 t = self._pinned[name].to("cuda", non_blocking=True)
+                _count_h2d(t)
                 t.record_stream(main)  # used on the main stream: no early reuse
                 dev[name] = t
                 if k + 1 == len(self._EARLY):
@@ -140,6 +143,7 @@ class _DualSoA:
             events["all"].record(copy)
         object.__setattr__(self, "_dev", dev)
         object.__setattr__(self, "_events", events)
+        object.__setattr__(self, "_missing", {f[0] for f in self._FIELDS} - set(dev))
         object.__setattr__(self, "_struct", None)
 
     def ready_event(self, group: str = "all"):
@@ -147,9 +151,11 @@ class _DualSoA:
         ev = self.__dict__.get("_events")
         return ev.get(group, ev.get("all")) if ev else None
 
-    def device(self, stream=None, wait: str = "all"):
-        """Device tensors of every field (uploaded on first use) and the ABI struct.
-        The current stream waits for the field group `wait` of an async upload."""
+    def device(self, stream=None, wait: str = "all", need=None):
+        """Device tensors of the fields in `need` (all by default; uploaded on
+        first use) and the ABI struct (null pointers for fields still on the
+        host).  The current stream waits for the field group `wait` of an
+        async upload."""
         if self._dev is None:
             torch = N.require_cuda()
             if self._pinned is not None:
@@ -159,8 +165,20 @@ class _DualSoA:
                 for name, width, code in self._FIELDS:
                     src = torch.from_numpy(np.ascontiguousarray(self._get(name)))
                     dev[name] = src.to("cuda")
+                    _count_h2d(dev[name])
                 object.__setattr__(self, "_dev", dev)
                 object.__setattr__(self, "_struct", None)
+        missing = self.__dict__.get("_missing") or set()
+        lack = missing if need is None else missing & set(need)
+        if lack:
+            torch = N.require_cuda()
+            for name in sorted(lack):
+                src = self._pinned[name] if self._pinned is not None else \
+                    torch.from_numpy(np.ascontiguousarray(self._get(name)))
+                self._dev[name] = src.to("cuda", non_blocking=self._pinned is not None)
+                _count_h2d(self._dev[name])
+            object.__setattr__(self, "_missing", missing - lack)
+            object.__setattr__(self, "_struct", None)
         ev = self.ready_event(wait)
         if ev is not None:
             _torch().cuda.current_stream().wait_event(ev)
@@ -168,8 +186,8 @@ class _DualSoA:
             st = self._STRUCT()
             st.n = self._n
             for name, _, _ in self._FIELDS:
-                t = self._dev[name]
-                setattr(st, name, t.data_ptr() if t.numel() else None)
+                t = self._dev.get(name)
+                setattr(st, name, t.data_ptr() if t is not None and t.numel() else None)
             object.__setattr__(self, "_struct", st)
         return self._struct
 
@@ -180,13 +198,25 @@ class _DualSoA:
     def drop_host(self):
         """Forget cached host copies of device-resident fields."""
         if self._dev is not None:
-            self._host.clear()
+            for name in list(self._host):
+                if name in self._dev:
+                    del self._host[name]
 
     def host_arrays(self) -> dict:
         return {name: self._get(name) for name, _, _ in self._FIELDS}
 
 
 _COPY = {}
+_H2D = [0]  # bytes this module has copied host -> device (upload accounting)
+
+
+def _count_h2d(t):
+    _H2D[0] += t.numel() * t.element_size()
+
+
+def h2d_bytes() -> int:
+    """Bytes of record / path fields copied to the device so far."""
+    return _H2D[0]
 
 
 def _copy_stream(torch):
