@@ -166,11 +166,19 @@ __device__ __forceinline__ double surface_pdf(const double* __restrict__ geo, in
 // rel. error ~1e-7 on den's fp32 rounding), which is ~1e-6 on the density,
 // far inside the 1e-4 radiance bar, at a quarter of the fp64 issue cost.
 // A pdf is never 0 here unless num is (g = +-1), and then in both.
+// MUFU reciprocal square root without denormal handling (den is a normal
+// number or 0 here)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float hg_pdf(double ax, double ay, double az, double c1, double c2,
                                         float num, double dx, double dy, double dz) {
   const double cs = fma(az, dz, fma(ay, dy, ax * dx));
   const double den = fma(-c2, cs, c1);
-  const float r = rsqrtf(float(den));
+  const float r = rsqrt_ftz(float(den));
   return num * (r * r * r);
 }
 
@@ -186,7 +194,7 @@ __device__ __forceinline__ float hg_pdf32(float ax, float ay, float az, float g,
                                           float g2ca, float dx, float dy, float dz, float cd) {
   const float ux = fmaf(-g, ax, dx), uy = fmaf(-g, ay, dy), uz = fmaf(-g, az, dz);
   const float den = fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, cd + g2ca)));
-  const float r = rsqrtf(den);
+  const float r = rsqrt_ftz(den);
   return num * (r * r * r);
 }
 
@@ -197,15 +205,14 @@ __device__ __forceinline__ float hg_pdf32(float ax, float ay, float az, float g,
 //         (1-|p|^2) (1-|e|^2), S floats each
 //   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
 //          (volume clusters keep them as fp32 in the same region)
-//   pd     S*(S+1) floats (phase-direction pair densities, row-padded; the
-//          emitter-direction ones are recomputed in pass 2b)
+//   (the pair densities are not stored: pass 1 sums them into p-hat, pass 2
+//   evaluates them again for W and D-bar)
 enum AggMode { kSurface = 0, kVol64 = 1, kVol32 = 2 };
 
 template <int kMode>
 __device__ __forceinline__ void aggregate_cluster(
     const Member* __restrict__ mem, int32_t q0, int s, int64_t wb, int64_t n, int S,
-    double* __restrict__ geo, double* __restrict__ wts, float* __restrict__ pd,
-    float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
+    double* __restrict__ geo, double* __restrict__ wts, float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
     float4* __restrict__ coeff_o, float4* __restrict__ rows_o, float4* __restrict__ i0_o) {
   constexpr bool kVol = kMode != kSurface;
   using acc_t = typename std::conditional<kVol, float, double>::type;
@@ -237,7 +244,6 @@ __device__ __forceinline__ void aggregate_cluster(
           const float g = g32[9 * S + l], num = g32[10 * S + l], g2ca = g32[11 * S + l];
           const float a = hg_pdf32(ax, ay, az, g, num, g2ca, dpx, dpy, dpz, cp);
           const float b = hg_pdf32(ax, ay, az, g, num, g2ca, dex, dey, dez, ce);
-          pd[l * (S + 1) + j] = a;
           sp += a;
           se += b;
         }
@@ -250,13 +256,11 @@ __device__ __forceinline__ void aggregate_cluster(
             const double c1 = geo[10 * S + l], c2 = geo[11 * S + l];
             const float a = hg_pdf(ax, ay, az, c1, c2, numf[l], dpx, dpy, dpz);
             const float b = hg_pdf(ax, ay, az, c1, c2, numf[l], dex, dey, dez);
-            pd[l * (S + 1) + j] = a;
             sp += a;
             se += b;
           } else {
             const double a = surface_pdf(geo, S, l, dpx, dpy, dpz);
             const double b = surface_pdf(geo, S, l, dex, dey, dez);
-            pd[l * (S + 1) + j] = float(a);
             sp = __dadd_rn(sp, a);
             se = __dadd_rn(se, b);
           }
@@ -316,15 +320,15 @@ __device__ __forceinline__ void aggregate_cluster(
     const int r = t / P2, h = t % P2;
     acc_t dx = 0, dy = 0, dz = 0;
     if (active) {
-      const float* prow = pd + r * (S + 1);
       const int j0 = h * slice2, j1 = min(s, j0 + slice2);
-      // the emitter-direction density is recomputed rather than kept in
-      // shared memory: half the pair storage, 8 CTAs per SM instead of 5
+      // both densities are recomputed rather than kept in shared memory: no
+      // pair storage, 16 CTAs per SM instead of 8
       if constexpr (kMode == kVol32) {
         const float ax = g32[r], ay = g32[S + r], az = g32[2 * S + r];
         const float g = g32[9 * S + r], num = g32[10 * S + r], g2ca = g32[11 * S + r];
         for (int j = j0; j < j1; ++j) {
-          const float a = prow[j];
+          const float a = hg_pdf32(ax, ay, az, g, num, g2ca, g32[3 * S + j], g32[4 * S + j],
+                                   g32[5 * S + j], g32[12 * S + j]);
           wt[wb + j * s + r] = a * wtsf[j];
           const float b = hg_pdf32(ax, ay, az, g, num, g2ca, g32[6 * S + j], g32[7 * S + j],
                                    g32[8 * S + j], g32[13 * S + j]);
@@ -337,7 +341,8 @@ __device__ __forceinline__ void aggregate_cluster(
         const double c1 = geo[10 * S + r], c2 = geo[11 * S + r];
         const float num = numf[r];
         for (int j = j0; j < j1; ++j) {
-          const float a = prow[j];
+          const float a = hg_pdf(ax, ay, az, c1, c2, num, geo[3 * S + j], geo[4 * S + j],
+                                 geo[5 * S + j]);
           wt[wb + j * s + r] = a * wtsf[j];
           const float b = hg_pdf(ax, ay, az, c1, c2, num, geo[6 * S + j], geo[7 * S + j],
                                  geo[8 * S + j]);
@@ -347,7 +352,7 @@ __device__ __forceinline__ void aggregate_cluster(
         }
       } else {
         for (int j = j0; j < j1; ++j) {
-          const double a = prow[j];
+          const double a = surface_pdf(geo, S, r, geo[3 * S + j], geo[4 * S + j], geo[5 * S + j]);
           wt[wb + j * s + r] = float(a * wts[j]);
           const double b = surface_pdf(geo, S, r, geo[6 * S + j], geo[7 * S + j], geo[8 * S + j]);
           dx += b * wts[S + j] + a * wts[4 * S + j];
@@ -380,7 +385,7 @@ __device__ __forceinline__ void aggregate_cluster(
   }
 }
 
-__global__ void __launch_bounds__(kAggThreads)
+__global__ void __launch_bounds__(kAggThreads, 12)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
             const int64_t* __restrict__ range, int64_t n, int S,
@@ -392,7 +397,6 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
   float* g32 = reinterpret_cast<float*>(geo);
   double* wts = geo + 12 * S + (S + 1) / 2;
-  float* pd = reinterpret_cast<float*>(wts + 7 * S);
   const int tid = threadIdx.x;
 
   const int64_t k_end = range[1];
@@ -460,13 +464,13 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
     }
     __syncthreads();
     if (mode == kVol32)
-      aggregate_cluster<kVol32>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+      aggregate_cluster<kVol32>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
                                 rows_o, i0_o);
     else if (mode == kVol64)
-      aggregate_cluster<kVol64>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+      aggregate_cluster<kVol64>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
                                 rows_o, i0_o);
     else
-      aggregate_cluster<kSurface>(mem, q0, s, wb, n, S, geo, wts, pd, wt, phat, dbar_o, coeff_o,
+      aggregate_cluster<kSurface>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
                                   rows_o, i0_o);
     __syncthreads();
   }
@@ -586,8 +590,7 @@ void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
                      int S, cudaStream_t s) {
   if (max_count <= 0) return;
-  const size_t smem = (size_t(19) * S + (S + 1) / 2) * sizeof(double) +
-                      size_t(S) * (S + 1) * sizeof(float);
+  const size_t smem = (size_t(19) * S + (S + 1) / 2) * sizeof(double);
   VPG_REQUIRE(smem <= kAggSmemMax, VPG_ELIMIT,
               "clusters larger than 160 members (cluster_size > 80) are not supported");
   static bool attr_set = false;
