@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <functional>
+#include <thread>
 #include <vector>
 
 #include "graph.cuh"
@@ -1301,6 +1302,32 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   }
   VPG_CUDA(cudaMemsetAsync(g->clpos.get(), 0xFF, sizeof(int32_t) * n, s));  // -1: not placed
 
+  // The center draw of a single-class record set (the common case) does not
+  // need the class pass: a host thread draws its swap targets speculatively
+  // while the device finds the classes, and the draw is kept when there
+  // turns out to be one class (else discarded, the generator untouched).
+  struct SpecDraw {
+    std::thread th;
+    std::unique_ptr<HostBuf<int32_t>> targets;
+    Pcg64 g;
+    int64_t steps = 0;
+    explicit SpecDraw(const Pcg64& r) : g(r) {}
+    ~SpecDraw() {
+      if (th.joinable()) th.join();
+    }
+  } spec(rng);
+  {
+    const int64_t m_all = (n + K - 1) / K;
+    if (n > 10000 && m_all > n / 50) {
+      spec.steps = n - std::max<int64_t>(n - m_all, 1);
+      spec.targets.reset(new HostBuf<int32_t>(size_t(spec.steps) + 1));
+      spec.th = std::thread([&spec, n] {
+        int32_t* t = spec.targets->get();
+        for (int64_t k = 0; k < spec.steps; ++k) t[k] = int32_t(spec.g.bounded(uint64_t(n - 1 - k)));
+      });
+    }
+  }
+
   // ---- classes (np.unique order of kind<<32 | class_id, graph.py:59)
   const int nbits_words = 2 * kSlotsPerKind / 32;
   DBuf<uint32_t> bitmap(nbits_words + 1, s);
@@ -1506,8 +1533,17 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       // the device resolves the swaps
       const int64_t stop = (p.n - p.m) > 1 ? (p.n - p.m) : 1;
       const int64_t steps = p.n - stop;
-      HostBuf<int32_t> targets(size_t(steps) + 1);
-      for (int64_t k = 0; k < steps; ++k) targets[k] = int32_t(rng.bounded(uint64_t(p.n - 1 - k)));
+      std::unique_ptr<HostBuf<int32_t>> targets_own;
+      if (spec.th.joinable()) spec.th.join();
+      if (spec.targets && n_cls == 1 && spec.steps == steps) {
+        targets_own = std::move(spec.targets);  // the speculative draw is this one
+        rng = spec.g;
+      } else {
+        targets_own.reset(new HostBuf<int32_t>(size_t(steps) + 1));
+        for (int64_t k = 0; k < steps; ++k)
+          (*targets_own)[k] = int32_t(rng.bounded(uint64_t(p.n - 1 - k)));
+      }
+      HostBuf<int32_t>& targets = *targets_own;
       int32_t* d_target = scratch_of<int32_t>(s, "swap_target", steps + 1);
       unsigned long long* d_keys = scratch_of<unsigned long long>(s, "swap_keys", steps + 1);
       unsigned long long* d_sk = scratch_of<unsigned long long>(s, "swap_sorted", steps + 1);
@@ -1525,6 +1561,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                  p.n, p.m, d_local.get());
       VPG_CUDA(cudaStreamSynchronize(s));  // `targets` (pinned) must outlive the copy
     } else {
+      if (spec.th.joinable()) spec.th.join();
       HostBuf<int64_t> picks(m);
       HostBuf<int32_t> picks32(m);
       rng_choice(rng, p.n, p.m, picks.get());
