@@ -1120,11 +1120,43 @@ void to_device(T* d, const std::vector<T>& h, cudaStream_t s) {
 // Host -> device copies that must not queue behind a bulk transfer on the
 // copy engine (the async record upload the build overlaps): the kernel reads
 // the pinned host buffer directly (UVA-mapped) instead of a memcpy.
+// Kernel copy out of pinned host memory (PCIe reads, no copy-engine queue):
+// 16-byte reads when both sides allow it, so fewer requests are in flight.
 __global__ void k_copy_host(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                             int64_t words) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < words;
-       i += int64_t(gridDim.x) * blockDim.x)
-    dst[i] = src[i];
+  const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t head = 0;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const int64_t quads = words / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = tid; i < quads; i += stride) d4[i] = s4[i];
+    head = quads * 4;
+  }
+  for (int64_t i = head + tid; i < words; i += stride) dst[i] = src[i];
+}
+
+// Copy of a pinned host array that a host thread is still writing: chunk c
+// (kReadyChunk words) is read once ready[c] (host memory) is set; the host
+// thread sets it after the chunk's words (release).
+constexpr int64_t kReadyChunk = 8192;
+__global__ void k_copy_when_ready(const uint32_t* __restrict__ src, const int32_t* ready,
+                                  uint32_t* __restrict__ dst, int64_t words) {
+  const int64_t chunks = (words + kReadyChunk - 1) / kReadyChunk;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int v = 0;
+      do {
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
+        if (!v) __nanosleep(500);
+      } while (!v);
+    }
+    __syncthreads();
+    const int64_t b = c * kReadyChunk, e = min(words, b + kReadyChunk);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
 }
 
 struct HostUpload {
@@ -1278,6 +1310,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   for (double& t : g->info.build_ms) t = 0.0;
   StageClock clk(timings, s, g->info.build_ms);
   HostUpload up;
+  std::vector<std::unique_ptr<HostBuf<int32_t>>> up_hold;  // pinned inputs of queued kernels
   Pcg64 rng(*rng_state);
   const int block = 256;
 
@@ -1308,22 +1341,41 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   // turns out to be one class (else discarded, the generator untouched).
   struct SpecDraw {
     std::thread th;
-    std::unique_ptr<HostBuf<int32_t>> targets;
+    std::unique_ptr<HostBuf<int32_t>> targets, ready;  // ready[c]: chunk c written
     Pcg64 g;
     int64_t steps = 0;
+    bool adopted = false;  // the build uses it: rng takes g once the thread ends
     explicit SpecDraw(const Pcg64& r) : g(r) {}
     ~SpecDraw() {
       if (th.joinable()) th.join();
     }
   } spec(rng);
+  // before the host draws again: a speculative draw in use hands over its state
+  auto rng_ready = [&]() {
+    if (spec.th.joinable()) spec.th.join();
+    if (spec.adopted) {
+      rng = spec.g;
+      spec.adopted = false;
+    }
+  };
   {
     const int64_t m_all = (n + K - 1) / K;
     if (n > 10000 && m_all > n / 50) {
       spec.steps = n - std::max<int64_t>(n - m_all, 1);
       spec.targets.reset(new HostBuf<int32_t>(size_t(spec.steps) + 1));
-      spec.th = std::thread([&spec, n] {
+      const int64_t chunks = (spec.steps + kReadyChunk - 1) / kReadyChunk;
+      spec.ready.reset(new HostBuf<int32_t>(size_t(chunks) + 1));
+      std::memset(spec.ready->get(), 0, sizeof(int32_t) * size_t(chunks + 1));
+      spec.th = std::thread([&spec, n, chunks] {
         int32_t* t = spec.targets->get();
-        for (int64_t k = 0; k < spec.steps; ++k) t[k] = int32_t(spec.g.bounded(uint64_t(n - 1 - k)));
+        volatile int32_t* rd = spec.ready->get();
+        for (int64_t c = 0; c < chunks; ++c) {
+          const int64_t e = std::min(spec.steps, (c + 1) * kReadyChunk);
+          for (int64_t k = c * kReadyChunk; k < e; ++k)
+            t[k] = int32_t(spec.g.bounded(uint64_t(n - 1 - k)));
+          std::atomic_thread_fence(std::memory_order_release);
+          rd[c] = 1;
+        }
       });
     }
   }
@@ -1533,22 +1585,23 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       // the device resolves the swaps
       const int64_t stop = (p.n - p.m) > 1 ? (p.n - p.m) : 1;
       const int64_t steps = p.n - stop;
-      std::unique_ptr<HostBuf<int32_t>> targets_own;
-      if (spec.th.joinable()) spec.th.join();
-      if (spec.targets && n_cls == 1 && spec.steps == steps) {
-        targets_own = std::move(spec.targets);  // the speculative draw is this one
-        rng = spec.g;
-      } else {
-        targets_own.reset(new HostBuf<int32_t>(size_t(steps) + 1));
-        for (int64_t k = 0; k < steps; ++k)
-          (*targets_own)[k] = int32_t(rng.bounded(uint64_t(p.n - 1 - k)));
-      }
-      HostBuf<int32_t>& targets = *targets_own;
       int32_t* d_target = scratch_of<int32_t>(s, "swap_target", steps + 1);
       unsigned long long* d_keys = scratch_of<unsigned long long>(s, "swap_keys", steps + 1);
       unsigned long long* d_sk = scratch_of<unsigned long long>(s, "swap_sorted", steps + 1);
       int32_t* d_prev = scratch_of<int32_t>(s, "swap_prev", steps + 1);
-      up.pinned(d_target, targets.get(), size_t(steps), s);
+      if (spec.targets && n_cls == 1 && spec.steps == steps) {
+        // the speculative draw is this one: copy it as the thread writes it
+        spec.adopted = true;
+        VPG_LAUNCH(k_copy_when_ready, 64, 256, 0, s,
+                   reinterpret_cast<const uint32_t*>(spec.targets->get()), spec.ready->get(),
+                   reinterpret_cast<uint32_t*>(d_target), steps);
+      } else {
+        rng_ready();
+        auto t = std::make_unique<HostBuf<int32_t>>(size_t(steps) + 1);
+        for (int64_t k = 0; k < steps; ++k) (*t)[k] = int32_t(rng.bounded(uint64_t(p.n - 1 - k)));
+        up.pinned(d_target, t->get(), size_t(steps), s);
+        up_hold.push_back(std::move(t));
+      }
       VPG_LAUNCH(k_swap_keys, grid_for(steps, block), block, 0, s, d_target, steps, d_keys);
       // by position only (bits 32..): the sort is stable and the keys arrive in
       // step order, so equal positions stay in step order
@@ -1559,9 +1612,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       VPG_LAUNCH(k_swap_links, grid_for(steps, block), block, 0, s, d_sk, steps, p.n, d_prev);
       VPG_LAUNCH(k_swap_resolve, grid_for(steps, block), block, 0, s, d_target, d_sk, d_prev, steps,
                  p.n, p.m, d_local.get());
-      VPG_CUDA(cudaStreamSynchronize(s));  // `targets` (pinned) must outlive the copy
     } else {
-      if (spec.th.joinable()) spec.th.join();
+      rng_ready();
       HostBuf<int64_t> picks(m);
       HostBuf<int32_t> picks32(m);
       rng_choice(rng, p.n, p.m, picks.get());
@@ -1859,6 +1911,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
           VPG_CUDA(cudaEventSynchronize(piece_ready[waited_from]));
         }
       };
+      rng_ready();
       n_splits += split_oversize_soa(
           rng, SplitMembers{h_srec.get(), xyzd, xyzd + staged, xyzd + 2 * staged, xyzd + 3 * staged},
           groups, cslot, max_size, &g->info.split_visits, h_masks.get(), dbg.on ? &st : nullptr,
@@ -1906,6 +1959,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     clk.mark(4);
   }
   g->info.n_splits = n_splits;
+  rng_ready();
   rng.store(rng_state);
 
   // ---- part B: the split results, appended after part A
@@ -2022,6 +2076,10 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     g->hold_host(std::move(ch.deferred));
   }
   for (auto& k : up.keep) g->hold_host(std::move(k));
+  for (auto& b : up_hold) g->hold_host(std::move(b));
+  rng_ready();
+  g->hold_host(std::move(spec.targets));
+  g->hold_host(std::move(spec.ready));
   up.keep.clear();
   VPG_CUDA(cudaEventCreateWithFlags(&g->done_ev, cudaEventDisableTiming));
   VPG_CUDA(cudaEventRecord(g->done_ev, s));
