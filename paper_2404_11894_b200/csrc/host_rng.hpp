@@ -293,6 +293,15 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
           __builtin_prefetch(first_moved + t);
           __builtin_prefetch(id + t);
         }
+        // a large group (> 3/2 of the limit) is likely split again: its
+        // positions and distances are needed too
+        if (2 * ga.size > 3 * max_size)
+          for (int64_t t = ga.begin; t < ga.begin + ga.size; t += 8) {
+            __builtin_prefetch(X + t);
+            __builtin_prefetch(Y + t);
+            __builtin_prefetch(Z + t);
+            __builtin_prefetch(D0 + t);
+          }
       }
     }
     const int64_t new_center = id[b + pick];
