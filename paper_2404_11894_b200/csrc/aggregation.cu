@@ -379,7 +379,10 @@ __device__ __forceinline__ void aggregate_cluster(
       coeff_o[q] = f4(kx, ky, kz);
       rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
                                   __int_as_float(mb.parent));
-      rows_o[2 * q + 1] = f4(wx * bx, wy * by, wz * bz);
+      // w = 1: terminal row (no continuation child writes it), the solve
+      // carries its I over from iteration to iteration
+      rows_o[2 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz),
+                                      (mb.flags & 2u) ? 1.f : 0.f);
       i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
   }

@@ -293,6 +293,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
           const int64_t q = q0 + rr;
           acc_out[q] = make_float4(ac.x, ac.y, ac.z, 0.f);
           const float4 A = srow[2 * (rl + rr)], B = srow[2 * (rl + rr) + 1];
+          if (B.w != 0.f) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
           const int32_t p = __float_as_int(A.w);
           if (p < 0) continue;
           const float nx = fmaf(A.x, ac.x, B.x), ny = fmaf(A.y, ac.y, B.y),
@@ -649,12 +650,12 @@ void solve_begin(vpg_graph* g, const vpg_records& rec, int32_t iterations, doubl
   VPG_CUDA(cudaMemsetAsync(g->red.get(), 0, g->red.bytes(), s));
   VPG_CUDA(cudaMemsetAsync(g->ctl.get(), 0, 4 * sizeof(int32_t), s));
   const int block = 256;
-  if (n > 0) {
+  // the iterations read I_0 from i0 and carry the terminal rows themselves
+  // (rows flagged in rows[].w); only a solve of 0 iterations reads ibuf[0]
+  if (n > 0 && iterations == 0) {
     VPG_LAUNCH(k_fill_f4, grid_for(n, block), block, 0, s, g->ibuf[0].get(), g->i0.get(), n);
-    VPG_LAUNCH(k_fill_f4, grid_for(n, block), block, 0, s, g->ibuf[1].get(), g->i0.get(), n);
-    if (iterations == 0)
-      VPG_LAUNCH(k_own_indirect, grid_for(n, block), block, 0, s, rec, g->perm.get(), n,
-                 g->acc[0].get());
+    VPG_LAUNCH(k_own_indirect, grid_for(n, block), block, 0, s, rec, g->perm.get(), n,
+               g->acc[0].get());
   }
 }
 
@@ -664,7 +665,8 @@ void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
   const SolveLaunch L = solve_launch(g);
   VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->chunk_desc.get(),
              g->cl_meta.get(), g->n_chunks_dev.get(), g->n_stages, L.stage_floats, g->wt.get(),
-             g->rows.get(), g->ibuf[t & 1].get(), g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
+             g->rows.get(), t == 0 ? g->i0.get() : g->ibuf[t & 1].get(),
+             g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
              g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
 }
 
