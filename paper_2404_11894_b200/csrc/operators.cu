@@ -104,6 +104,54 @@ __device__ __forceinline__ void fence_proxy_async() {
 constexpr int kConsumers = 16;
 constexpr int kMaxStages = 4;  // the stage count is chosen per graph (graph.cuh)
 
+// Residual, tol break and 3-growth divergence of iteration t (solve.py:80-94),
+// decided on the device so the loop never waits on the host.
+__device__ void control_step(int t, double tol, const uint32_t* __restrict__ red,
+                             const float* __restrict__ term_max, double* __restrict__ resid,
+                             int32_t* __restrict__ ctl) {
+  if (ctl[1]) return;
+  // red was filled by atomics from every CTA: read it past L1
+  const uint32_t* vred = red;
+  const unsigned nan_bits = __ldcg(vred + t * 8 + 6);
+  double worst = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    // a NaN channel never wins Python's max(worst, q) in the reference
+    if (nan_bits & ((1u | 8u) << c)) continue;
+    const double delta = double(__uint_as_float(__ldcg(vred + t * 8 + c)));
+    double scale = double(fmaxf(__uint_as_float(__ldcg(vred + t * 8 + 3 + c)), term_max[c]));
+    scale = scale > 1e-12 ? scale : 1e-12;
+    const double q = delta / scale;
+    worst = q > worst ? q : worst;
+  }
+  resid[t] = worst;
+  ctl[0] = t + 1;
+  if (t >= 1 && worst > resid[t - 1]) {
+    ctl[2] += 1;
+    if (ctl[2] >= 3) {
+      ctl[3] = 1;
+      ctl[1] = 1;
+      return;
+    }
+  } else {
+    ctl[2] = 0;
+  }
+  if (worst < tol) ctl[1] = 1;
+}
+
+// The last CTA of iteration t to finish (counter red[t*8+7]) runs the control
+// step: no separate control launch between iterations.
+__device__ __forceinline__ void finish_iteration(int t, double tol, uint32_t* __restrict__ red,
+                                                 const float* __restrict__ term_max,
+                                                 double* __restrict__ resid,
+                                                 int32_t* __restrict__ ctl) {
+  __threadfence();
+  const unsigned prev = atomicAdd(&red[t * 8 + 7], 1u);
+  if (prev == gridDim.x - 1) {
+    __threadfence();
+    control_step(t, tol, red, term_max, resid, ctl);
+  }
+}
+
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
 k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
              const int64_t* __restrict__ n_chunks_p, int n_stages, int stage_floats,
@@ -111,10 +159,14 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
              const float4* __restrict__ i_in, float4* __restrict__ i_out,
              const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
              const float4* __restrict__ i0, int t, uint32_t* __restrict__ red,
-             const int32_t* __restrict__ ctl) {
-  if (ctl[1]) return;  // converged or diverged earlier
+             int32_t* __restrict__ ctl, int fused, double tol,
+             const float* __restrict__ term_max, double* __restrict__ resid) {
+  if (ctl[1]) return;  // converged or diverged earlier (every CTA sees the same)
   const int64_t n_chunks = *n_chunks_p;
-  if (int64_t(blockIdx.x) >= n_chunks) return;
+  if (int64_t(blockIdx.x) >= n_chunks) {
+    if (fused && threadIdx.x == 0) finish_iteration(t, tol, red, term_max, resid, ctl);
+    return;
+  }
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // n_stages (<= 4) barriers
   int* done = reinterpret_cast<int*>(smem + 64);                  // n_stages counters
@@ -341,6 +393,10 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
     for (int w2 = 0; w2 < kConsumers; ++w2) nb |= blk_nan[w2];
     if (nb) atomicOr(&red[t * 8 + 6], nb);
   }
+  if (fused) {
+    __syncthreads();  // this CTA's maxima are in
+    if (tid == 0) finish_iteration(t, tol, red, term_max, resid, ctl);
+  }
 }
 
 // W * v per cluster from global memory (aggregate_indirect on an arbitrary
@@ -374,31 +430,7 @@ k_apply_w(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
 __global__ void k_control(int t, double tol, const uint32_t* __restrict__ red,
                           const float* __restrict__ term_max, double* __restrict__ resid,
                           int32_t* __restrict__ ctl) {
-  if (threadIdx.x != 0 || ctl[1]) return;
-  const unsigned nan_bits = red[t * 8 + 6];
-  double worst = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    // a NaN channel never wins Python's max(worst, q) in the reference
-    if (nan_bits & ((1u | 8u) << c)) continue;
-    const double delta = double(__uint_as_float(red[t * 8 + c]));
-    double scale = double(fmaxf(__uint_as_float(red[t * 8 + 3 + c]), term_max[c]));
-    scale = scale > 1e-12 ? scale : 1e-12;
-    const double q = delta / scale;
-    worst = q > worst ? q : worst;
-  }
-  resid[t] = worst;
-  ctl[0] = t + 1;
-  if (t >= 1 && worst > resid[t - 1]) {
-    ctl[2] += 1;
-    if (ctl[2] >= 3) {
-      ctl[3] = 1;
-      ctl[1] = 1;
-      return;
-    }
-  } else {
-    ctl[2] = 0;
-  }
-  if (worst < tol) ctl[1] = 1;
+  if (threadIdx.x == 0) control_step(t, tol, red, term_max, resid, ctl);
 }
 
 // Single-strategy I-bar / coeff (the 0-iteration result, solve.py:41-51).
@@ -659,7 +691,8 @@ void solve_begin(vpg_graph* g, const vpg_records& rec, int32_t iterations, doubl
   }
 }
 
-void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
+namespace {
+void launch_iteration(vpg_graph* g, int32_t t, bool fused, cudaStream_t s) {
   VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
   if (g->n == 0) return;
   const SolveLaunch L = solve_launch(g);
@@ -667,8 +700,14 @@ void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) {
              g->cl_meta.get(), g->n_chunks_dev.get(), g->n_stages, L.stage_floats, g->wt.get(),
              g->rows.get(), t == 0 ? g->i0.get() : g->ibuf[t & 1].get(),
              g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
-             g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get());
+             g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get(),
+             fused ? 1 : 0, g->tol, g->term_max.get(), g->resid.get());
 }
+}  // namespace
+
+// one iteration without its control step (a shard runs the halo exchange and
+// the residual all-reduce in between, then solve_control)
+void solve_step(vpg_graph* g, int32_t t, cudaStream_t s) { launch_iteration(g, t, false, s); }
 
 void solve_control(vpg_graph* g, int32_t t, cudaStream_t s) {
   VPG_REQUIRE(t >= 0 && t < g->iterations, VPG_EINVAL, "iteration index out of range");
@@ -700,8 +739,7 @@ void solve(vpg_graph* g, const vpg_records& rec, int32_t iterations, double tol,
   solve_begin(g, rec, iterations, tol, s);
   const int64_t n = g->n;
   for (int t = 0; t < iterations && n > 0; ++t) {
-    solve_step(g, t, s);
-    solve_control(g, t, s);
+    launch_iteration(g, t, true, s);  // control step in the iteration's last CTA
   }
   solve_end(g, residuals, performed, n == 0, s);
 }
