@@ -127,3 +127,31 @@ def test_device_load_truncated_raises(cuda, tmp_path):
         p.write_bytes(raw[:-cut])
         with pytest.raises(IOError):
             load_records(str(p), device=True)
+
+
+@pytest.mark.gpu
+def test_pinned_solve_uploads_only_what_it_reads(cuda):
+    """solve_from_records on pinned records copies only the fields the build,
+    solve and splat read; the others stay readable on the host and reach the
+    device on first device use (PT image, device save)."""
+    from paper_2404_11894_b200.pathgraph import solve_from_records
+    from paper_2404_11894_b200.transport import records as R
+
+    z = _ref()
+    host = load_records(DUMP)
+    t = load_records(DUMP, pin=True)
+    before = R.h2d_bytes()
+    image, graph, result = solve_from_records(t, int(z["K"]), iterations=int(z["iterations"]),
+                                              tol=0.0, seed=int(z["seed"]))
+    moved = R.h2d_bytes() - before
+    full = sum(a.nbytes for a in host.records.host_arrays().values()) + \
+        sum(a.nbytes for a in host.paths.host_arrays().values())
+    skipped = host.records.depth.nbytes + sum(
+        getattr(host.paths, f).nbytes for f in ("pixel_idx", "direct0_nee", "direct0_phase",
+                                                "pt_estimate", "extra_direct"))
+    assert moved == full - skipped
+    assert_rel(image, z["image"], 1e-4, what="image")
+    np.testing.assert_array_equal(t.records.depth, host.records.depth)
+    # first device use of a skipped field uploads it
+    np.testing.assert_array_equal(t.image, host.image)
+    assert not (t.paths.__dict__.get("_missing") or set()) & {"pt_estimate"}
