@@ -81,6 +81,21 @@ typedef struct vpg_pcg64 {
 } vpg_pcg64;
 
 /* out[0..m) = Generator.choice(n, m, replace=False) (host memory). */
+/* Generator.choice(n, m, replace=False) (clustering.py:51) with the m picks
+ * written to device memory `out` (int32): the tail shuffle's swap targets
+ * drawn on the host (exact stream), the swaps resolved on the device. */
+int vpg_rng_choice_device(vpg_pcg64* state, int64_t n, int64_t m, int32_t* out, void* stream);
+/* The split loop over oversize groups whose members are on the DEVICE (ids
+ * and SoA positions / distances, groups back to back, as vpg_split_groups_soa
+ * takes them on the host): the first splits' bit rows are computed on the
+ * device and the deferred first splits applied there; d_ids ends in final
+ * member order.  Outputs as vpg_split_groups_soa (host arrays). */
+int vpg_split_groups_device(vpg_pcg64* rng, int32_t* d_ids, const double* d_x, const double* d_y,
+                            const double* d_z, const double* d_d0, int64_t n_groups,
+                            const int64_t* sizes, const int64_t* centers, const int64_t* cslot,
+                            int64_t max_size, int64_t cap_groups, int64_t* out_n_groups,
+                            int64_t* out_begin, int64_t* out_size, int64_t* out_center,
+                            int64_t* n_splits, void* stream);
 int vpg_rng_choice(vpg_pcg64* rng, int64_t n, int64_t m, int64_t* out);
 /* out[i] = Generator.integers(k) for i in [0, count) (host memory). */
 int vpg_rng_integers(vpg_pcg64* rng, int64_t k, int64_t count, int64_t* out);

@@ -128,6 +128,10 @@ _SIGNATURES = {
     "vpg_profile_reset": (C.c_int, []),
     "vpg_profile_read": (C.c_int, [C.c_char_p, c_i64, c_p, c_p, c_i64, C.POINTER(c_i64)]),
     "vpg_profile_timeline": (C.c_int, [C.c_char_p, c_i64, c_p, c_p, c_i64, C.POINTER(c_i64)]),
+    "vpg_rng_choice_device": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p, c_p]),
+    "vpg_split_groups_device": (C.c_int, [C.POINTER(Pcg64State), c_p, c_p, c_p, c_p, c_p, c_i64,
+                                          c_p, c_p, c_p, c_i64, c_i64, C.POINTER(c_i64), c_p, c_p,
+                                          c_p, C.POINTER(c_i64), c_p]),
     "vpg_rng_choice": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,

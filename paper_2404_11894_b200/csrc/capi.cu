@@ -264,6 +264,30 @@ int vpg_profile_read(char* names, int64_t names_cap, int64_t* counts, double* to
   });
 }
 
+int vpg_rng_choice_device(vpg_pcg64* state, int64_t n, int64_t m, int32_t* out, void* stream) {
+  return guarded([&] { vpg::choice_device(state, n, m, out, as_stream(stream)); });
+}
+
+int vpg_split_groups_device(vpg_pcg64* rng, int32_t* d_ids, const double* d_x, const double* d_y,
+                            const double* d_z, const double* d_d0, int64_t n_groups,
+                            const int64_t* sizes, const int64_t* centers, const int64_t* cslot,
+                            int64_t max_size, int64_t cap_groups, int64_t* out_n_groups,
+                            int64_t* out_begin, int64_t* out_size, int64_t* out_center,
+                            int64_t* n_splits, void* stream) {
+  return guarded([&] {
+    std::vector<vpg::SplitGroup> groups;
+    vpg::split_groups_device(rng, d_ids, d_x, d_y, d_z, d_d0, n_groups, sizes, centers, cslot,
+                             max_size, groups, n_splits, as_stream(stream));
+    VPG_REQUIRE(int64_t(groups.size()) <= cap_groups, VPG_ELIMIT, "output group capacity exceeded");
+    for (size_t k = 0; k < groups.size(); ++k) {
+      out_begin[k] = groups[k].begin;
+      out_size[k] = groups[k].size;
+      out_center[k] = groups[k].center;
+    }
+    *out_n_groups = int64_t(groups.size());
+  });
+}
+
 int vpg_rng_choice(vpg_pcg64* rng, int64_t n, int64_t m, int64_t* out) {
   return guarded([&] {
     VPG_REQUIRE(n >= 0 && m >= 0 && m <= n, VPG_EINVAL,

@@ -2087,6 +2087,132 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   clk.mark(6);
 }
 
+// The split loop over oversize groups whose members are on the device (SoA x,
+// y, z, d0 and the member ids, groups back to back): the first splits' bit
+// rows and moved counts are computed on the device, the loop runs on the host
+// with the deferred-first-split fast path, and the deferred partitions are
+// applied to the device ids -- the sharded build's equivalent of the build's
+// own split stage.  ids (device) end in final member order.
+void split_groups_device(vpg_pcg64* state, int32_t* d_ids, const double* d_x, const double* d_y,
+                         const double* d_z, const double* d_d0, int64_t n_groups,
+                         const int64_t* sizes, const int64_t* centers, const int64_t* cslot_in,
+                         int64_t max_size, std::vector<SplitGroup>& groups, int64_t* n_splits,
+                         cudaStream_t s) {
+  Pcg64 rng(*state);
+  groups.assign(static_cast<size_t>(n_groups), SplitGroup{0, 0, 0});
+  std::vector<int64_t> cslot(static_cast<size_t>(n_groups));
+  std::vector<int64_t> seg(static_cast<size_t>(n_groups) * 3 + 3), moff(static_cast<size_t>(n_groups) + 1);
+  int64_t total = 0, words = 0;
+  for (int64_t k = 0; k < n_groups; ++k) {
+    groups[k] = SplitGroup{total, sizes[k], centers[k]};
+    cslot[k] = cslot_in[k];
+    seg[3 * k] = 0;
+    seg[3 * k + 1] = sizes[k];
+    seg[3 * k + 2] = total;
+    moff[k] = words;
+    words += sizes[k] * ((sizes[k] + 63) / 64);
+    total += sizes[k];
+  }
+  *n_splits = 0;
+  if (n_groups == 0) {
+    rng.store(state);
+    return;
+  }
+  HostUpload up;
+  DBuf<int64_t> d_seg(seg.size(), s), d_moff(moff.size(), s);
+  DBuf<int32_t> d_n(1, s), d_moved(static_cast<size_t>(total) + 1, s);
+  DBuf<unsigned long long> d_masks(static_cast<size_t>(words) + 1, s);
+  up.put(d_seg.get(), seg.data(), seg.size(), s);
+  up.put(d_moff.get(), moff.data(), moff.size(), s);
+  const int32_t ng32 = int32_t(n_groups);
+  up.put(d_n.get(), &ng32, 1, s);
+  VPG_CUDA(cudaMemsetAsync(d_moved.get(), 0, sizeof(int32_t) * total, s));
+  VPG_LAUNCH(k_first_split_masks, int(std::min<int64_t>(n_groups, 65535)), 256, 0, s, d_seg.get(),
+             d_n.get(), d_moff.get(), d_x, d_y, d_z, d_d0, d_masks.get(), d_moved.get());
+  HostBuf<int32_t> h_ids(static_cast<size_t>(total) + 1), h_moved(static_cast<size_t>(total) + 1);
+  HostBuf<double> h_xyzd(static_cast<size_t>(total) * 4 + 4);
+  HostBuf<unsigned long long> h_masks(static_cast<size_t>(words) + 1);
+  VPG_CUDA(cudaMemcpyAsync(h_ids.get(), d_ids, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, s));
+  const double* src[4] = {d_x, d_y, d_z, d_d0};
+  for (int a = 0; a < 4; ++a)
+    VPG_CUDA(cudaMemcpyAsync(h_xyzd.get() + a * total, src[a], sizeof(double) * total,
+                             cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(h_masks.get(), d_masks.get(), sizeof(unsigned long long) * words,
+                           cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(h_moved.get(), d_moved.get(), sizeof(int32_t) * total,
+                           cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaStreamSynchronize(s));
+  std::vector<DeferredSplit> deferred;
+  double* xyzd = h_xyzd.get();
+  int64_t visits = 0;
+  *n_splits = split_oversize_soa(
+      rng, SplitMembers{h_ids.get(), xyzd, xyzd + total, xyzd + 2 * total, xyzd + 3 * total},
+      groups, cslot, max_size, &visits, h_masks.get(), nullptr, h_moved.get(),
+      2 * max_size <= 3 * kApplyThreads ? &deferred : nullptr);
+  // host order for the splits it made, then the deferred partitions on the device
+  up.pinned(d_ids, h_ids.get(), static_cast<size_t>(total), s);
+  if (!deferred.empty()) {
+    HostBuf<int64_t> hd(deferred.size() * 3);
+    for (size_t k = 0; k < deferred.size(); ++k) {
+      hd[3 * k] = deferred[k].begin;
+      hd[3 * k + 1] = deferred[k].size;
+      hd[3 * k + 2] = deferred[k].row;
+    }
+    DBuf<int64_t> d_def(deferred.size() * 3, s);
+    up.pinned(d_def.get(), hd.get(), deferred.size() * 3, s);
+    VPG_LAUNCH(k_apply_first_splits, int(std::min<size_t>(deferred.size(), 65535)), kApplyThreads,
+               0, s, d_def.get(), int64_t(deferred.size()), d_masks.get(), d_ids);
+    VPG_CUDA(cudaStreamSynchronize(s));
+  } else {
+    VPG_CUDA(cudaStreamSynchronize(s));
+  }
+  // a deferred split's new center is the pick in the original order: the
+  // host's ids for that range are still the original order, so it holds
+  rng.store(state);
+}
+
+// Generator.choice(n, m, replace=False) with the picks left on the device
+// (int32): the tail shuffle's targets are drawn on the host and its swaps
+// resolved on the device as in the build; Floyd's branch (small m) on the
+// host.  Synchronous on return (the host buffers are released).
+void choice_device(vpg_pcg64* state, int64_t n, int64_t m, int32_t* d_out, cudaStream_t s) {
+  VPG_REQUIRE(m >= 0 && m <= n && n < (int64_t(1) << 31), VPG_EINVAL,
+              "Cannot take a larger sample than population when replace is False");
+  if (m == 0) return;
+  Pcg64 rng(*state);
+  const int block = 256;
+  HostUpload up;
+  if (n > 10000 && m > n / 50) {
+    const int64_t stop = (n - m) > 1 ? (n - m) : 1;
+    const int64_t steps = n - stop;
+    HostBuf<int32_t> t(static_cast<size_t>(steps) + 1);
+    for (int64_t k = 0; k < steps; ++k) t[k] = int32_t(rng.bounded(uint64_t(n - 1 - k)));
+    DBuf<int32_t> d_target(size_t(steps) + 1, s), d_prev(size_t(steps) + 1, s);
+    DBuf<unsigned long long> d_keys(size_t(steps) + 1, s), d_sk(size_t(steps) + 1, s);
+    up.pinned(d_target.get(), t.get(), size_t(steps), s);
+    VPG_LAUNCH(k_swap_keys, grid_for(steps, block), block, 0, s, d_target.get(), steps,
+               d_keys.get());
+    const int pos_bits = bits_for(uint64_t(n > 1 ? n - 1 : 1));
+    cub_call([&](void* tmp, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(tmp, b, d_keys.get(), d_sk.get(), int(steps), 32,
+                                            32 + pos_bits, s);
+    }, s);
+    VPG_LAUNCH(k_swap_links, grid_for(steps, block), block, 0, s, d_sk.get(), steps, n,
+               d_prev.get());
+    VPG_LAUNCH(k_swap_resolve, grid_for(steps, block), block, 0, s, d_target.get(), d_sk.get(),
+               d_prev.get(), steps, n, m, d_out);
+    VPG_CUDA(cudaStreamSynchronize(s));
+  } else {
+    std::vector<int64_t> picks(static_cast<size_t>(m));
+    rng_choice(rng, n, m, picks.data());
+    HostBuf<int32_t> p32(static_cast<size_t>(m));
+    for (int64_t j = 0; j < m; ++j) p32[j] = int32_t(picks[j]);
+    up.pinned(d_out, p32.get(), size_t(m), s);
+    VPG_CUDA(cudaStreamSynchronize(s));
+  }
+  rng.store(state);
+}
+
 // Exact nearest center (lowest index on ties) of every point against given
 // centers -- the assignment step of clustering.py:96-148 on its own, for a
 // shard's rows against the replicated centers of a class.  The result does

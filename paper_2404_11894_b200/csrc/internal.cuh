@@ -39,6 +39,13 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
                      int64_t path_begin, const vpg_records& out, cudaStream_t s);
 int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, const double* lo,
                        const double* hi, int32_t* assign, cudaStream_t s);
+struct SplitGroup;
+void split_groups_device(vpg_pcg64* state, int32_t* d_ids, const double* d_x, const double* d_y,
+                         const double* d_z, const double* d_d0, int64_t n_groups,
+                         const int64_t* sizes, const int64_t* centers, const int64_t* cslot_in,
+                         int64_t max_size, std::vector<SplitGroup>& groups, int64_t* n_splits,
+                         cudaStream_t s);
+void choice_device(vpg_pcg64* state, int64_t n, int64_t m, int32_t* d_out, cudaStream_t s);
 void codec_rows(bool unpack, uint8_t* packed, int64_t n, int32_t row_bytes,
                 const vpg_codec_field* fields, int32_t n_fields, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,

@@ -299,13 +299,12 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         my_n = int(rows.numel())
         m = -(-n_c // K)
         # centers: Generator.choice(n, m, replace=False) (clustering.py:51), by
-        # the native bit-exact replica (numpy's own tail shuffle builds an
-        # n-element index array)
-        idx_h = np.empty(m, dtype=np.int64)
+        # the native bit-exact replica (host draws, swaps resolved on the device)
+        idx32 = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
         st0 = N.Pcg64State.from_generator(rng)
-        N.check(lib.vpg_rng_choice(ctypes.byref(st0), n_c, m, idx_h.ctypes.data))
+        N.check(lib.vpg_rng_choice_device(ctypes.byref(st0), n_c, m, idx32.data_ptr(), stream))
         st0.store_into(rng)
-        idx = torch.as_tensor(idx_h, device=dev)
+        idx = idx32[:m].to(torch.int64)
         mine = torch.nonzero((idx >= pref) & (idx < pref + my_n)).reshape(-1)
         c_rows = rows[idx[mine] - pref]
         msg = torch.cat([mine.to(torch.float64).reshape(-1, 1), pos[c_rows],
@@ -374,10 +373,11 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             if hit.numel():
                 kk = torch.searchsorted(over, gj[hit])
                 cslot[kk] = hit  # members ascending: one hit per group
-            ids = np.arange(allm.shape[0], dtype=np.int32)
-            x, y, z, d0 = allm[:, 2:6].t().contiguous().cpu().numpy()  # SoA rows
+            staged = int(allm.shape[0])
+            ids_d = torch.arange(staged, dtype=torch.int32, device=dev)
+            xyzd = allm[:, 2:6].t().contiguous()  # SoA rows, on the device
             st = N.Pcg64State.from_generator(rng)
-            cap = int(allm.shape[0]) + n_over + 1
+            cap = staged + n_over + 1
             o_n = ctypes.c_int64()
             o_b = np.zeros(cap, np.int64)
             o_s = np.zeros(cap, np.int64)
@@ -386,12 +386,12 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             sz_h = osz.cpu().numpy().astype(np.int64)
             cen_h = crec[over].cpu().numpy().astype(np.int64)
             cs_h = cslot.cpu().numpy().astype(np.int64)
-            N.check(lib.vpg_split_groups_soa(ctypes.byref(st), ids.ctypes.data, x.ctypes.data,
-                                             y.ctypes.data, z.ctypes.data, d0.ctypes.data, n_over,
-                                             sz_h.ctypes.data, cen_h.ctypes.data,
-                                             cs_h.ctypes.data, max_size, cap, ctypes.byref(o_n),
-                                             o_b.ctypes.data, o_s.ctypes.data, o_c.ctypes.data,
-                                             ctypes.byref(nspl)))
+            # first splits' bit rows on the device, the loop on the host
+            N.check(lib.vpg_split_groups_device(
+                ctypes.byref(st), ids_d.data_ptr(), xyzd[0].data_ptr(), xyzd[1].data_ptr(),
+                xyzd[2].data_ptr(), xyzd[3].data_ptr(), n_over, sz_h.ctypes.data,
+                cen_h.ctypes.data, cs_h.ctypes.data, max_size, cap, ctypes.byref(o_n),
+                o_b.ctypes.data, o_s.ctypes.data, o_c.ctypes.data, ctypes.byref(nspl), stream))
             st.store_into(rng)
             n_splits += nspl.value
             ng = o_n.value
@@ -400,7 +400,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             # groups are appended
             # the final groups' ranges tile the staged array: each position's
             # group is the last range starting at or before it
-            ids_t = torch.as_tensor(ids.astype(np.int64), device=dev)
+            ids_t = ids_d.to(torch.int64)
             b_t = torch.as_tensor(o_b[:ng], device=dev)
             order_b = torch.argsort(b_t)
             posn = torch.arange(ids_t.numel(), device=dev)

@@ -114,3 +114,18 @@ def test_split_loop_matches_oracle(seed, K):
     assert list(o_cen[:n_out.value]) == ref_centers
     assert g_nat.bit_generator.state == g_ref.bit_generator.state
     assert max(len(x) for x in got) <= 2 * K
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,seed", [(20000, 625, 0), (500, 16, 1), (3_000_000, 93_750, 9)])
+def test_rng_choice_device_matches_numpy(cuda, n, m, seed):
+    g = np.random.default_rng(np.random.SeedSequence([seed, 0xC1A5]))
+    g.integers(5)
+    st = N.Pcg64State.from_generator(g)
+    out = cuda.empty(m, dtype=cuda.int32, device="cuda")
+    N.check(N.lib().vpg_rng_choice_device(ctypes.byref(st), n, m, out.data_ptr(),
+                                          N.stream_handle()))
+    assert np.array_equal(out.cpu().numpy(), g.choice(n, m, replace=False))
+    h = np.random.default_rng(0)
+    st.store_into(h)
+    assert h.bit_generator.state == g.bit_generator.state
