@@ -39,6 +39,7 @@ another shard: exchanges happen between launches.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -262,6 +263,25 @@ class GlobalClusters:
     n_splits: int
 
 
+_TIMING = os.environ.get("VPG_SHARD_TIMING") is not None
+_T = {"t": 0.0}
+
+
+def _tick(label):
+    """VPG_SHARD_TIMING=1: print the wall time since the previous tick (synced)."""
+    if not _TIMING:
+        return
+    import time
+
+    import torch
+
+    torch.cuda.synchronize()
+    now = time.perf_counter()
+    if _T["t"]:
+        print(f"[shard] {label:28s} {1e3 * (now - _T['t']):8.3f} ms", flush=True)
+    _T["t"] = now
+
+
 def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_size: int,
                         rng: np.random.Generator) -> GlobalClusters:
     """cluster_points (clustering.py:28-148) over the shards' records without
@@ -279,6 +299,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
     K = int(cluster_size)
     max_size = 2 * K
     n = int(pos.shape[0])
+    _tick("cd: start")
     keys = (kind.to(torch.int64) << 32) | class_id.to(torch.int64)
     loc_keys = torch.unique(keys) if n else keys[:0]
     cnt = comm.all_gather_ints([int(loc_keys.numel())])[:, 0].tolist()
@@ -300,6 +321,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         m = -(-n_c // K)
         # centers: Generator.choice(n, m, replace=False) (clustering.py:51), by
         # the native bit-exact replica (host draws, swaps resolved on the device)
+        _tick("cd: class rows")
         idx32 = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
         st0 = N.Pcg64State.from_generator(rng)
         N.check(lib.vpg_rng_choice_device(ctypes.byref(st0), n_c, m, idx32.data_ptr(), stream))
@@ -313,6 +335,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         order = got[:, 0].to(torch.int64)
         cpos = torch.empty((m, 3), dtype=torch.float64, device=dev)
         cpos[order] = got[:, 1:4]
+        _tick("cd: centers")
         # class bounding box (sizes the hash grid like the single-device build)
         p_c = pos[rows].contiguous()
         lo = p_c.min(0).values if my_n else torch.full((3,), float("inf"), dtype=torch.float64,
@@ -326,6 +349,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         if my_n:
             N.check(lib.vpg_assign_nearest(p_c.data_ptr(), my_n, cpos.contiguous().data_ptr(), m,
                                            bounds.ctypes.data, assign.data_ptr(), None, stream))
+        _tick("cd: bbox+assign")
         a64 = assign.to(torch.int64)
         hist = torch.bincount(a64, minlength=m) if my_n else torch.zeros(m, dtype=torch.int64,
                                                                             device=dev)
@@ -351,6 +375,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         plain = ~is_over[a64]
         row_cluster[rows[plain]] = cid_of_j[a64[plain]]
         row_rank[rows[plain]] = before[a64[plain]] + lrank[plain]
+        _tick("cd: groups")
         appended = []
         if n_over:
             om = torch.nonzero(is_over[a64]).reshape(-1)
@@ -376,6 +401,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             staged = int(allm.shape[0])
             ids_d = torch.arange(staged, dtype=torch.int32, device=dev)
             xyzd = allm[:, 2:6].t().contiguous()  # SoA rows, on the device
+            _tick("cd: gather oversize")
             st = N.Pcg64State.from_generator(rng)
             cap = staged + n_over + 1
             o_n = ctypes.c_int64()
@@ -393,6 +419,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
                 cen_h.ctypes.data, cs_h.ctypes.data, max_size, cap, ctypes.byref(o_n),
                 o_b.ctypes.data, o_s.ctypes.data, o_c.ctypes.data, ctypes.byref(nspl), stream))
             st.store_into(rng)
+            _tick("cd: split loop")
             n_splits += nspl.value
             ng = o_n.value
             # final groups: members (staged index) in order; cluster ids: the
@@ -434,6 +461,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
     sizes = torch.cat(sizes_all) if sizes_all else torch.zeros(0, dtype=torch.int64, device=dev)
     center_pos = torch.cat(cpos_all) if cpos_all else torch.zeros((0, 3), dtype=torch.float64,
                                                                   device=dev)
+    _tick("cd: mapping")
     return GlobalClusters(sizes, center_pos, row_cluster, row_rank, n_splits)
 
 
@@ -454,16 +482,14 @@ def _torch_dtype(code):
 
 
 def pack_payload(cols: dict, n: int):
-    """Record columns -> (n, W) float64, integer columns bit-cast (exact transport)."""
+    """Record columns -> (n, B) uint8: every column's bytes side by side (exact
+    transport of every dtype, 354 bytes per record)."""
     import torch
 
     parts = []
     for name, width, code in _payload_columns():
-        t = cols[name].reshape(n, width)
-        if code == "f8":
-            parts.append(t)
-        else:
-            parts.append(t.to(torch.int64).view(torch.float64))
+        t = cols[name].reshape(n, width).contiguous()
+        parts.append(t.view(torch.uint8).reshape(n, -1))
     return torch.cat(parts, 1) if parts else None
 
 
@@ -472,11 +498,10 @@ def unpack_payload(p):
 
     out, c = {}, 0
     for name, width, code in _payload_columns():
-        t = p[:, c:c + width]
-        c += width
-        if code != "f8":
-            t = t.contiguous().view(torch.int64).to(_torch_dtype(code))
-        t = t.contiguous()
+        dt = _torch_dtype(code)
+        nb = width * torch.empty((), dtype=dt).element_size()
+        t = p[:, c:c + nb].contiguous().view(dt)
+        c += nb
         out[name] = t if width > 1 else t.reshape(-1)
     return out
 
@@ -528,6 +553,7 @@ class ShardedPathGraph:
         m = int(sizes.numel())
         self.n_clusters_total = m
         self.n_splits = gcl.n_splits
+        _tick("build: clustering")
         plan = plan_owners(sizes, gcl.center_pos, world)
         self.plan = plan
         dest_shard = plan.owner[gcl.row_cluster]
@@ -555,17 +581,35 @@ class ShardedPathGraph:
         grow = torch.arange(g0, g0 + n, dtype=torch.int64, device="cuda")
         cols.update(parent_ipt=parent_ipt, has_child=has_child, grow=grow, par_shard=par_shard,
                     par_row=par_row, dest_row=dest_row)
-        order = torch.argsort(dest_shard, stable=True)
-        send_counts = torch.bincount(dest_shard, minlength=world).tolist() if n else [0] * world
-        sc = torch.tensor(send_counts, dtype=torch.int64, device="cuda").reshape(-1, 1)
-        recv_counts = comm.all_to_all(sc, [1] * world, [1] * world).reshape(-1).tolist()
-        payload = pack_payload(cols, n)
-        got = comm.all_to_all(payload[order], send_counts, recv_counts)
+        _tick("build: plan+cols")
         n_own = int(plan.rows[me])
-        local = torch.empty((n_own, got.shape[1]), dtype=torch.float64, device="cuda")
-        rows_at = got[:, -1].contiguous().view(torch.int64)
-        local[rows_at] = got
-        own = unpack_payload(local)
+        # rows that stay on this shard are placed field by field; only the
+        # others travel, byte-packed, in one all-to-all
+        own = {}
+        for name, width, code in _payload_columns():
+            shape = (n_own, width) if width > 1 else (n_own,)
+            own[name] = torch.empty(shape, dtype=_torch_dtype(code), device="cuda")
+        keep = dest_shard == me
+        li = torch.nonzero(keep).reshape(-1)
+        lr = dest_row[li]
+        for name, _, _ in _payload_columns():
+            own[name][lr] = cols[name][li]
+        if world > 1:
+            ri = torch.nonzero(~keep).reshape(-1)
+            ds = dest_shard[ri]
+            order = torch.argsort(ds, stable=True)
+            send_counts = torch.bincount(ds, minlength=world).tolist() if ri.numel() else [0] * world
+            sc = torch.tensor(send_counts, dtype=torch.int64, device="cuda").reshape(-1, 1)
+            recv_counts = comm.all_to_all(sc, [1] * world, [1] * world).reshape(-1).tolist()
+            sel = ri[order]
+            payload = pack_payload({k: v[sel] for k, v in cols.items()}, int(sel.numel()))
+            got = comm.all_to_all(payload, send_counts, recv_counts)
+            if got is not None and got.shape[0]:
+                recv = unpack_payload(got)
+                rows_at = recv["dest_row"]
+                for name, _, _ in _payload_columns():
+                    own[name][rows_at] = recv[name]
+        _tick("build: records to owners")
         self.own = own
         self.n = n_own
 
@@ -585,6 +629,7 @@ class ShardedPathGraph:
         self.halo_ipt = halo_ipt
         del dest_shard, dest_row
 
+        _tick("build: unpack+halo")
         # operators of this shard's clusters
         own_clusters = plan.order[plan.owner[plan.order] == me]
         cl_sizes = sizes[own_clusters].to(torch.int32).cpu().numpy()
@@ -602,6 +647,7 @@ class ShardedPathGraph:
             self.has_child.data_ptr() if n_own else None, self.halo.n_halo,
             halo_ipt.data_ptr() if self.halo.n_halo else None, stream, ctypes.byref(g)))
         self.handle = g.value
+        _tick("build: build_local")
         # the residual scale covers every shard's terminal rows (solve.py:57-60)
         vw = self.views()
         comm.all_reduce_max_(_view(vw.term_max, (3,), "<f4"))
