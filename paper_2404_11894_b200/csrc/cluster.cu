@@ -1818,8 +1818,10 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       // children in earlier classes were packed before these parents existed
       if (c > 0 && rows_p) link_children(g, rec, rows_p + p.row_off, p.n, s);
     }
+    DebugClock dstage(s);
     VPG_CUDA(cudaEventSynchronize(sized));
     cudaEventDestroy(sized);
+    dstage.mark("stage: sizes known", false);
     g->info.n_fallback += h_scalars[0];
     const int n_over = h_scalars[2];
     const int64_t staged = n_over > 0 ? h_scalars[3] : 0;
@@ -1855,6 +1857,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       VPG_LAUNCH(k_first_split_masks, std::min<int64_t>(n_over, 65535), 256, 0, side, over_seg,
                  scalars.get() + 2, mask_off, d_xyzd, d_xyzd + staged, d_xyzd + 2 * staged,
                  d_xyzd + 3 * staged, d_masks, d_moved);
+      dstage.mark("stage: kernels queued", false);
       // the staging goes to the host from the side stream, beside part A
       VPG_CUDA(cudaMemcpyAsync(info.get(), over_info.get(), sizeof(int64_t) * 4 * n_over,
                                cudaMemcpyDeviceToHost, side));
