@@ -342,7 +342,10 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
         // stable partition by the row's bits; positions and distances move
         // too only when a half will be split again (its d0 = distance to its
         // center: unchanged for the kept half, to the pick for the moved one)
-        const bool again = kept > max_size || moved > max_size;
+        // positions only matter for a half that is split again (the other
+        // half is final: only its ids are read from here on)
+        const bool again_k = kept > max_size, again_m = moved > max_size;
+        const bool again = again_k || again_m;
         int32_t* __restrict__ Mi = mid.data();
         double* __restrict__ MX = mx.data();
         double* __restrict__ MY = my.data();
@@ -353,10 +356,12 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
           const int i = int(t - b);
           const int f = int((row[i >> 6] >> (i & 63)) & 1ull);
           const int32_t idv = id[t];
-          if (again) {
+          if (again_k) {
+            X[wk] = X[t]; Y[wk] = Y[t]; Z[wk] = Z[t]; D0[wk] = D0[t];
+          }
+          if (again_m) {
             const double xv = X[t], yv = Y[t], zv = Z[t];
             const double dx = xv - px, dy = yv - py, dz = zv - pz;
-            X[wk] = xv; Y[wk] = yv; Z[wk] = zv; D0[wk] = D0[t];
             MX[wm] = xv; MY[wm] = yv; MZ[wm] = zv; MD[wm] = (dx * dx + dy * dy) + dz * dz;
           }
           id[wk] = idv;
@@ -367,7 +372,7 @@ inline int64_t split_oversize_soa(Pcg64& g, SplitMembers m, std::vector<SplitGro
           wm += f;
         }
         std::memcpy(id + wk, Mi, sizeof(int32_t) * moved);
-        if (again) {
+        if (again_m) {
           std::memcpy(X + wk, MX, sizeof(double) * moved);
           std::memcpy(Y + wk, MY, sizeof(double) * moved);
           std::memcpy(Z + wk, MZ, sizeof(double) * moved);
