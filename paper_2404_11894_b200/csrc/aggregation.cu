@@ -29,7 +29,7 @@ namespace {
 
 constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 constexpr double kInvPi = 1.0 / 3.14159265358979323846;
-constexpr int kAggThreads = 64;
+constexpr int kAggThreads = 128;
 // HG densities are evaluated all in fp32 for |g| <= kG32 (see hg_pdf32)
 constexpr float kG32 = 0.95f;
 // dynamic shared memory of k_aggregate for the largest supported cluster (2K = 160)
@@ -226,8 +226,7 @@ __device__ __forceinline__ void aggregate_cluster(
   // summing a contiguous slice of l; the slices combine in a fixed order
   // (((p0 + p1) + (p2 + p3))), so p-hat is deterministic.  The loop trip
   // count is uniform so every lane reaches the shuffles.
-  // threads per column: fill the CTA (a power of two <= 4, >= 1)
-  const int P = s * 4 <= kAggThreads ? 4 : (s * 2 <= kAggThreads ? 2 : 1);
+  const int P = s <= 32 ? 4 : 2;
   const int slice = (s + P - 1) / P;
   for (int base = 0; base < P * s; base += blockDim.x) {
     const int t = base + tid;
@@ -268,10 +267,8 @@ __device__ __forceinline__ void aggregate_cluster(
         }
       }
     }
-    if (P >= 2) {
-      sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 1);
-      se += __shfl_xor_sync(0xFFFFFFFFu, se, 1);
-    }
+    sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 1);
+    se += __shfl_xor_sync(0xFFFFFFFFu, se, 1);
     if (P == 4) {
       sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 2);
       se += __shfl_xor_sync(0xFFFFFFFFu, se, 2);
@@ -315,7 +312,7 @@ __device__ __forceinline__ void aggregate_cluster(
   // pass 2: rows: the kernel block (transposed, wt[wb + j*s + r] = W[r, j]),
   // D-bar and the solve vectors, P2 threads per row each covering a slice
   // of the columns, the D-bar sums combined in a fixed order
-  const int P2 = P;
+  const int P2 = s <= 32 ? 4 : 2;
   const int slice2 = (s + P2 - 1) / P2;
   for (int base = 0; base < P2 * s; base += blockDim.x) {
     const int t = base + tid;
@@ -364,11 +361,9 @@ __device__ __forceinline__ void aggregate_cluster(
         }
       }
     }
-    if (P2 >= 2) {
-      dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
-      dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
-      dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
-    }
+    dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
+    dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
+    dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
     if (P2 == 4) {
       dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 2);
       dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
@@ -393,7 +388,7 @@ __device__ __forceinline__ void aggregate_cluster(
   }
 }
 
-__global__ void __launch_bounds__(kAggThreads, 24)
+__global__ void __launch_bounds__(kAggThreads, 12)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
             const int64_t* __restrict__ range, int64_t n, int S,
@@ -607,9 +602,7 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
                                   int(kAggSmemMax)));
     attr_set = true;
   }
-  // a block per cluster (not persistent): blocks of a higher-priority stream
-  // (the build's oversize staging) get SMs as soon as any block retires
-  const int64_t blocks = std::min<int64_t>(max_count, 2147483647LL);
+  const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
   VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, static_cast<const Member*>(members),
              g->cl_off.get(), g->cl_size.get(), g->w_off.get(), range, g->n, S, g->wt.get(),
              g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get());

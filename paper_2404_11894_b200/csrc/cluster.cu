@@ -1230,13 +1230,7 @@ cudaStream_t side_stream(int which = 0) {
   int dev = 0;
   VPG_CUDA(cudaGetDevice(&dev));
   cudaStream_t& st = streams[which][dev];
-  if (!st) {
-    // highest priority: the staging and part B kernels are small and on the
-    // critical path; they take SMs ahead of part A's blocks
-    int lo = 0, hi = 0;
-    VPG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    VPG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
-  }
+  if (!st) VPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   return st;
 }
 
