@@ -217,6 +217,10 @@ int vpg_graph_build(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng
 int vpg_graph_build_wait(const vpg_records* rec, int32_t cluster_size, vpg_pcg64* rng,
                          int32_t flags, void* stream, void* fields_ready, vpg_graph** out);
 int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out);
+/* Re-point the graph at the same records (same n) with more fields on the
+ * device -- e.g. pdf_phase, which only a 0-iteration solve reads, uploaded
+ * after the build. */
+int vpg_graph_set_records(vpg_graph* g, const vpg_records* rec);
 int vpg_graph_free(vpg_graph* g);
 
 /* Host exports (each synchronises `stream`).  All arrays are in record order.

@@ -132,6 +132,7 @@ _SIGNATURES = {
     "vpg_split_groups_device": (C.c_int, [C.POINTER(Pcg64State), c_p, c_p, c_p, c_p, c_p, c_i64,
                                           c_p, c_p, c_p, c_i64, c_i64, C.POINTER(c_i64), c_p, c_p,
                                           c_p, C.POINTER(c_i64), c_p]),
+    "vpg_graph_set_records": (C.c_int, [c_p, C.POINTER(Records)]),
     "vpg_rng_choice": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_rng_integers": (C.c_int, [C.POINTER(Pcg64State), c_i64, c_i64, c_p]),
     "vpg_split_groups": (C.c_int, [C.POINTER(Pcg64State), c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64,

@@ -446,6 +446,13 @@ int vpg_graph_info_get(const vpg_graph* g, vpg_graph_info* out) {
   });
 }
 
+int vpg_graph_set_records(vpg_graph* g, const vpg_records* rec) {
+  return guarded([&] {
+    VPG_REQUIRE(rec->n == g->rec.n, VPG_EINVAL, "records of another size");
+    g->rec = *rec;
+  });
+}
+
 int vpg_graph_free(vpg_graph* g) {
   return guarded([&] { delete g; });
 }

@@ -20,8 +20,12 @@ from paper_2404_11894_b200.pathgraph.clustering import Cluster
 from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
 
 
-# the record fields the build and the solve read on the device (depth never)
-BUILD_FIELDS = tuple(f[0] for f in N.RECORD_FIELDS if f[0] != "depth")
+# the record fields the build and the solve read on the device: never depth;
+# pdf_phase only in a 0-iteration solve (uploaded then, see solve()); normal
+# only for surface records (solve_from_records keeps it on the host when
+# there are none)
+BUILD_FIELDS = tuple(f[0] for f in N.RECORD_FIELDS
+                     if f[0] not in ("depth", "pdf_phase", "normal"))
 
 
 class NativeGraph:
@@ -41,7 +45,9 @@ class NativeGraph:
         # the clustering needs only pos/kind/class_id: with an upload in flight
         # the native build waits for the other fields itself, just before it
         # first reads them
-        st = records.device(wait="early", need=BUILD_FIELDS)
+        need = BUILD_FIELDS if "normal" in (records.__dict__.get("_missing") or ()) \
+            else BUILD_FIELDS + ("normal",)
+        st = records.device(wait="early", need=need)
         fields = records.ready_event("all")
         if flags & N.VPG_BUILD_CLUSTERS_ONLY:
             fields = None  # never read; later device() calls wait for them

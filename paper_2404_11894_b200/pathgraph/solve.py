@@ -69,6 +69,13 @@ def solve(graph, iterations: int = 10, tol: float = 1e-3) -> SolveResult:
     if iterations < 0:
         raise ValueError("iterations must be >= 0")
     g = graph.native
+    if iterations == 0 and graph.records.__dict__.get("_missing"):
+        # the single-strategy I-bar reads pdf_phase (and normals): bring the
+        # fields the build left on the host and re-point the graph at them
+        st = graph.records.device()
+        g.rec_tensors = dict(graph.records._dev)
+        g.rec_struct = st
+        N.check(N.lib().vpg_graph_set_records(g.handle, ctypes.byref(st)))
     res = np.zeros(max(iterations, 1))
     performed = ctypes.c_int32(0)
     rc = N.lib().vpg_solve(g.handle, int(iterations), float(tol), res.ctypes.data,

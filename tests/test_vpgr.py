@@ -146,12 +146,22 @@ def test_pinned_solve_uploads_only_what_it_reads(cuda):
     moved = R.h2d_bytes() - before
     full = sum(a.nbytes for a in host.records.host_arrays().values()) + \
         sum(a.nbytes for a in host.paths.host_arrays().values())
-    skipped = host.records.depth.nbytes + sum(
+    skipped = host.records.depth.nbytes + host.records.pdf_phase.nbytes + sum(
         getattr(host.paths, f).nbytes for f in ("pixel_idx", "direct0_nee", "direct0_phase",
                                                 "pt_estimate", "extra_direct"))
+    if not np.any(host.records.kind):  # no surface records: normals stay on the host
+        skipped += host.records.normal.nbytes
     assert moved == full - skipped
     assert_rel(image, z["image"], 1e-4, what="image")
     np.testing.assert_array_equal(t.records.depth, host.records.depth)
     # first device use of a skipped field uploads it
     np.testing.assert_array_equal(t.image, host.image)
     assert not (t.paths.__dict__.get("_missing") or set()) & {"pt_estimate"}
+    # a 0-iteration solve on the same graph brings pdf_phase over and agrees
+    # with a graph built from fully uploaded records
+    from paper_2404_11894_b200.pathgraph import build_graph, solve
+
+    r0 = solve(graph, iterations=0)
+    full = load_records(DUMP)
+    g2 = build_graph(full, int(z["K"]), seed=int(z["seed"]))
+    np.testing.assert_array_equal(r0.i_bar, solve(g2, iterations=0).i_bar)
