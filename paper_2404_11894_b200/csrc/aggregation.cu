@@ -388,7 +388,7 @@ __device__ __forceinline__ void aggregate_cluster(
   }
 }
 
-__global__ void __launch_bounds__(kAggThreads, 12)
+__global__ void __launch_bounds__(kAggThreads, 10)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
             const int64_t* __restrict__ range, int64_t n, int S,
