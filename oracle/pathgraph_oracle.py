@@ -205,6 +205,13 @@ def build_graph(rec: dict, paths: dict, width, height, spp, K: int, seed: int = 
     rng = np.random.default_rng(np.random.SeedSequence([seed & 0xFFFFFFFF, 0xC1A5]))
     cid, clusters = cluster_points(rec["pos"], class_keys(rec["kind"], rec["class_id"]), K, rng)
     g = Graph(rec, paths, width, height, spp, cid, clusters, next_index(rec["path_idx"]))
+    build_operators(g)
+    return g
+
+
+def build_operators(g: Graph) -> None:
+    """graph.py:94-168 (compute_marginals + _build_operators) over g.clusters."""
+    rec = g.rec
     n = rec["pos"].shape[0]
     g.phat_ind, g.phat_dir_phase, g.phat_dir_emit = np.zeros(n), np.zeros(n), np.zeros(n)
     bins = _by_shape(g)
@@ -249,7 +256,6 @@ def build_graph(rec: dict, paths: dict, width, height, spp, K: int, seed: int = 
         v = np.zeros(0)
     g.w = sp.csr_matrix((v, (r, c)), shape=(n, n))
     g.w.sort_indices()
-    return g
 
 
 # --------------------------------------------------------------- solve
