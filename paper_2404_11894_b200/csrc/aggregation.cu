@@ -596,12 +596,7 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
   const size_t smem = (size_t(19) * S + (S + 1) / 2) * sizeof(double);
   VPG_REQUIRE(smem <= kAggSmemMax, VPG_ELIMIT,
               "clusters larger than 160 members (cluster_size > 80) are not supported");
-  static bool attr_set = false;
-  if (!attr_set) {
-    VPG_CUDA(cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(kAggSmemMax)));
-    attr_set = true;
-  }
+  ensure_dynamic_smem(reinterpret_cast<const void*>(k_aggregate), kAggSmemMax);
   const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
   VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, static_cast<const Member*>(members),
              g->cl_off.get(), g->cl_size.get(), g->w_off.get(), range, g->n, S, g->wt.get(),

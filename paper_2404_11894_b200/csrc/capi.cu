@@ -15,8 +15,6 @@ namespace vpg {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
-std::once_flag g_pool_once;
-int g_sm_count = 0;
 }  // namespace
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -56,23 +54,46 @@ void count_transfer(uint64_t h2d, uint64_t d2h) {
   g_d2h.fetch_add(d2h, std::memory_order_relaxed);
 }
 
+namespace {
+constexpr int kMaxDevices = 64;
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+std::atomic<int> g_sm_counts[kMaxDevices];
+std::once_flag g_pool_once[kMaxDevices];
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_attr;
+}  // namespace
+
+// per device: a process may drive several GPUs (one context per device)
 int sm_count() {
-  if (g_sm_count == 0) {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
-      g_sm_count = v;
-    else
-      g_sm_count = 148;
+  const int dev = current_device();
+  int v = g_sm_counts[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    g_sm_counts[dev].store(v, std::memory_order_relaxed);
   }
-  return g_sm_count;
+  return v;
+}
+
+void ensure_dynamic_smem(const void* func, size_t bytes) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  size_t& have = g_smem_attr[{dev, func}];
+  if (bytes > have) {
+    VPG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    have = bytes;
+  }
 }
 
 void* dalloc(size_t bytes, cudaStream_t s) {
-  std::call_once(g_pool_once, [] {
-    int dev = 0;
+  const int dev = current_device();
+  std::call_once(g_pool_once[dev], [dev] {
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }

@@ -1139,22 +1139,37 @@ __global__ void k_copy_host(const uint32_t* __restrict__ src, uint32_t* __restri
 
 // Copy of a pinned host array that a host thread is still writing: chunk c
 // (kReadyChunk words) is read once ready[c] (host memory) is set; the host
-// thread sets it after the chunk's words (release).
+// thread sets it after the chunk's words (release).  The words are read with
+// ld.relaxed.sys (never the non-coherent path: the host writes them while the
+// kernel runs), and the wait is bounded: a host thread that has not
+// published a chunk within kReadyTimeoutNs aborts the launch (an error on the
+// stream, never a hung GPU).
 constexpr int64_t kReadyChunk = 8192;
-__global__ void k_copy_when_ready(const uint32_t* __restrict__ src, const int32_t* ready,
+constexpr unsigned long long kReadyTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__global__ void k_copy_when_ready(const uint32_t* src, const int32_t* ready,
                                   uint32_t* __restrict__ dst, int64_t words) {
   const int64_t chunks = (words + kReadyChunk - 1) / kReadyChunk;
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     if (threadIdx.x == 0) {
       int v = 0;
+      unsigned long long t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       do {
         asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
-        if (!v) __nanosleep(500);
+        if (!v) {
+          __nanosleep(500);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > kReadyTimeoutNs) __trap();
+        }
       } while (!v);
     }
     __syncthreads();
     const int64_t b = c * kReadyChunk, e = min(words, b + kReadyChunk);
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) dst[i] = src[i];
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      uint32_t w;
+      asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(w) : "l"(src + i) : "memory");
+      dst[i] = w;
+    }
     __syncthreads();
   }
 }
@@ -2010,6 +2025,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   }
   DBuf<int64_t> d_b(size_t(nb) * 8 + 8, sb);
   DBuf<int32_t> d_split(size_t(split_total) + 1, sb);
+  // link_children reads d_split on s after part B: free it on s (s waits
+  // for b_done, so every use on sb precedes the free in s's order)
+  d_split.s = s;
   DBuf<int64_t> range_b(2, sb);
   if (nb) {
     int64_t ob = 0, os = 0;

@@ -154,5 +154,7 @@ inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
 }
 
 int sm_count();
+// cudaFuncAttributeMaxDynamicSharedMemorySize, raised once per (device, kernel)
+void ensure_dynamic_smem(const void* func, size_t bytes);
 
 }  // namespace vpg

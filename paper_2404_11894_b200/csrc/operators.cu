@@ -655,12 +655,7 @@ SolveLaunch solve_launch(const vpg_graph* g) {
   L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + 16 * smax + 4;
   L.smem = 128 + size_t(g->n_stages) * L.stage_floats * sizeof(float);
   VPG_REQUIRE(L.smem <= kSolveSmem, VPG_ELIMIT, "clusters too large for the staged solve");
-  static size_t smem_set = 0;
-  if (L.smem > smem_set) {
-    VPG_CUDA(cudaFuncSetAttribute(k_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(L.smem)));
-    smem_set = L.smem;
-  }
+  ensure_dynamic_smem(reinterpret_cast<const void*>(k_solve_iter), L.smem);
   L.grid = sm_count();  // persistent; CTAs past the (device-side) chunk count exit
   return L;
 }

@@ -386,7 +386,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
             allm = comm.all_gather_rows(mem, comm.all_gather_ints([int(om.numel())])[:, 0])
             gj = allm[:, 0].to(torch.int64)
             gr = allm[:, 1].to(torch.int64)
-            srt2 = torch.argsort(gj * (1 << 40) + gr)
+            srt2 = group_member_order(gj, gr)
             allm, gj, gr = allm[srt2], gj[srt2], gr[srt2]
             crec = torch.empty(m, dtype=torch.int64, device=dev)
             crec[order] = got[:, 4].to(torch.int64)
@@ -463,6 +463,17 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
                                                                   device=dev)
     _tick("cd: mapping")
     return GlobalClusters(sizes, center_pos, row_cluster, row_rank, n_splits)
+
+
+def group_member_order(gj, gr):
+    """Permutation ordering staged oversize members by (group gj, global row
+    gr), both ascending (the split loop's `ostart`/`over` layout).  Two stable
+    sorts instead of one packed int64 key: a packed `gj << 40 | gr` overflows
+    once a class has 2^23 centers (C5 scale)."""
+    import torch
+
+    by_row = torch.argsort(gr, stable=True)
+    return by_row[torch.argsort(gj[by_row], stable=True)]
 
 
 # ------------------------------------------------------------ record payload

@@ -188,3 +188,20 @@ def test_pixel_ranges_cover_every_pixel_once():
 def test_morton_order_is_z_order():
     q = torch.tensor([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1], [2, 0, 0]])
     assert S.morton3(q).tolist() == [0, 1, 2, 4, 7, 8]
+
+
+def test_group_member_order_beyond_2_pow_23_centers():
+    """Oversize members sort by (group, global row) even when a class has more
+    than 2^23 centers and rows beyond 2^40 (a packed gj<<40|gr key wraps)."""
+    import torch
+
+    from paper_2404_11894_b200.pathgraph.sharded import group_member_order
+
+    rng = np.random.default_rng(7)
+    n = 20000
+    gj = torch.as_tensor(rng.integers(0, 1 << 25, n) | np.where(rng.random(n) < 0.5, 1 << 24, 0))
+    gr = torch.as_tensor(rng.integers(0, 1 << 41, n))
+    gj[:50] = (1 << 25) - 1  # the top groups: a packed key would make them negative
+    o = group_member_order(gj, gr)
+    expect = np.lexsort((gr.numpy(), gj.numpy()))
+    assert np.array_equal(o.numpy(), expect)
