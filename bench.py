@@ -2,21 +2,24 @@
 """Benchmark: graph vertices propagated/s (build + K iterations) and ms/frame.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
-                    [--workload C2] [--cpu-sample 96]
+                    [--workload C4] [--cpu-sample 64]
 
 One step = one pass of the hot path over the workload's record set already
 resident in HBM: build_graph (exact clustering, marginals, operator blocks)
 + solve(iterations=K_iter, tol=0).  `value` = vertices * N / step time.
 `e2e` = the same metric through the reference-facing API with HOST buffers
 (solve_from_records on pinned host records: H2D, build, solve, splat, image
-D2H inside the timed region).  The workload (BASELINE.json configs[1] = C2)
-is traced by the CUDA tracer once, outside the timed region; the synthetic
-fbm cloud is procedural (no dataset).  Inputs (2.4 GB of records, 1.2 GB of
-kernel blocks) are far larger than the 126 MB L2.
+D2H inside the timed region).  The workload is C4 (BASELINE.json configs[3]:
+512^3 fbm smoke, 1024x1024, 16 spp, 16 iterations, ~75 M vertices), the
+largest configuration that fits one GPU; it is traced by the CUDA tracer once,
+outside the timed region; the synthetic smoke is procedural (no dataset).
+Inputs (22 GB of records) are far larger than the 126 MB L2.
 
 --impl reference times the reference algorithm's CPU restatement (oracle/,
-numpy) on a bounded sample of the same workload traced by the oracle's C
-tracer restatement, on the host cores.
+numpy, with the reference's own control structure: per-cell candidate loop,
+one nonzero() per center) on a bounded sample of the same workload (the C4
+scene at 64x64, 16 spp) traced by the oracle's C tracer restatement, on the
+host cores.
 """
 
 from __future__ import annotations
@@ -48,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default="C4")
     ap.add_argument("--cpu-sample", type=int, default=64,
                     help="square resolution of the CPU-baseline sample of the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -151,14 +154,16 @@ def cpu_baseline(wl, cfg, sample_res, trace_fn, steps=1):
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        g = O.build_graph(rec, paths, sample_res, sample_res, cfg.spp, cfg.cluster_size, cfg.seed)
+        g = O.build_graph(rec, paths, sample_res, sample_res, cfg.spp, cfg.cluster_size, cfg.seed,
+                          faithful=True)
         O.solve(g, cfg.iterations, 0.0)
         times.append(time.perf_counter() - t0)
     t = min(times)
     return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{wl.name} scene at {sample_res}x{sample_res}, {cfg.spp} spp: {n} vertices, "
                       f"build + {cfg.iterations} iterations in {t:.2f} s (oracle/pathgraph_oracle.py, "
-                      f"numpy, best of {steps})"}, n, t
+                      f"numpy, the reference's per-cell / per-center loops, best of {steps}; "
+                      f"single-threaded like the reference's graph stages)"}, n, t
 
 
 def device_trace_sample(scene, cfg):
@@ -186,17 +191,21 @@ def run_reference(args):
     from oracle import pathgraph_oracle as O
 
     n = rec["pos"].shape[0]
-    for _ in range(args.warmup):
-        g = O.build_graph(rec, paths, res, res, cfg.spp, cfg.cluster_size, cfg.seed)
+    def step():
+        g = O.build_graph(rec, paths, res, res, cfg.spp, cfg.cluster_size, cfg.seed, faithful=True)
         O.solve(g, cfg.iterations, 0.0)
+
+    for _ in range(args.warmup):
+        step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        g = O.build_graph(rec, paths, res, res, cfg.spp, cfg.cluster_size, cfg.seed)
-        O.solve(g, cfg.iterations, 0.0)
+        step()
     dt = (time.perf_counter() - t0) / args.steps
     value = n / dt
     sample = (f"{wl.name} scene at {res}x{res}, {cfg.spp} spp ({n} vertices, traced by "
-              f"oracle/tracer_oracle.c); build + {cfg.iterations} iterations per step")
+              f"oracle/tracer_oracle.c); build + {cfg.iterations} iterations per step "
+              f"(numpy restatement with the reference's per-cell / per-center loops; "
+              f"single-threaded like the reference's graph stages)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,

@@ -97,6 +97,50 @@ def nearest_center(pts: np.ndarray, centers: np.ndarray) -> np.ndarray:
     return best_j
 
 
+def nearest_center_per_cell(pts: np.ndarray, centers: np.ndarray) -> np.ndarray:
+    """The same assignment as nearest_center, computed with the reference's own
+    control structure (clustering.py:96-148): a Python loop over the occupied
+    cells, the 27-cell candidate list per cell, brute force for the rest.
+    Used where the reference's CPU COST is what is being measured (bench.py's
+    reference arm); nearest_center is the fast checker."""
+    n, m = pts.shape[0], centers.shape[0]
+    if m == 1:
+        return np.zeros(n, dtype=np.int64)
+    lo = pts.min(axis=0)
+    volume = float(np.prod(np.maximum(pts.max(axis=0) - lo, 1e-12)))
+    cell = max((volume / m) ** (1.0 / 3.0), 1e-9)
+    table: dict = {}
+    for j, key in enumerate(map(tuple, np.floor((centers - lo) / cell).astype(np.int64))):
+        table.setdefault(key, []).append(j)
+    pc = np.floor((pts - lo) / cell).astype(np.int64)
+    order = np.lexsort((pc[:, 2], pc[:, 1], pc[:, 0]))
+    pcs = pc[order]
+    cuts = np.concatenate(([0], np.flatnonzero(np.any(pcs[1:] != pcs[:-1], axis=1)) + 1, [n]))
+    assign = np.full(n, -1, dtype=np.int64)
+    rest = []
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        rows = order[b:e]
+        x, y, z = pcs[b]
+        cand = sorted(j for dx in (-1, 0, 1) for dy in (-1, 0, 1) for dz in (-1, 0, 1)
+                      for j in table.get((x + dx, y + dy, z + dz), ()))
+        if not cand:
+            rest.append(rows)
+            continue
+        cand = np.asarray(cand, dtype=np.int64)
+        d2 = _sq_dist(pts[rows][:, None, :], centers[cand][None, :, :])
+        k = np.argmin(d2, axis=1)
+        assign[rows] = cand[k]
+        far = np.sqrt(d2[np.arange(rows.shape[0]), k]) >= cell
+        if far.any():
+            rest.append(rows[far])
+    if rest:
+        rows = np.concatenate(rest)
+        for s in range(0, rows.shape[0], 4096):
+            chunk = rows[s:s + 4096]
+            assign[chunk] = np.argmin(_sq_dist(pts[chunk][:, None, :], centers[None, :, :]), axis=1)
+    return assign
+
+
 def _split_loop(pts, groups, centers, K, rng):
     """LIFO split of groups larger than 2K (clustering.py:58-85)."""
     limit = 2 * K
@@ -126,8 +170,12 @@ def _split_loop(pts, groups, centers, K, rng):
             stack.append(len(groups) - 1)
 
 
-def cluster_points(positions, keys, K: int, rng: np.random.Generator):
-    """(cluster_id, [Cluster]) per compatibility class (clustering.py:28-93)."""
+def cluster_points(positions, keys, K: int, rng: np.random.Generator, faithful: bool = False):
+    """(cluster_id, [Cluster]) per compatibility class (clustering.py:28-93).
+
+    faithful=True follows the reference's control structure and its cost
+    (per-cell candidate loop, one nonzero() per center for the groups,
+    clustering.py:54-55) -- same result."""
     if K < 1:
         raise ValueError("cluster size K must be >= 1")
     pos = np.asarray(positions, dtype=np.float64)
@@ -140,10 +188,14 @@ def cluster_points(positions, keys, K: int, rng: np.random.Generator):
         n = rows.shape[0]
         m = (n + K - 1) // K
         picks = rng.choice(n, size=m, replace=False)
-        assign = nearest_center(pts, pts[picks])
-        order = np.argsort(assign, kind="stable")
-        bounds = np.searchsorted(assign[order], np.arange(m + 1))
-        groups = [order[bounds[c]:bounds[c + 1]] for c in range(m)]
+        if faithful:
+            assign = nearest_center_per_cell(pts, pts[picks])
+            groups = [np.flatnonzero(assign == c) for c in range(m)]
+        else:
+            assign = nearest_center(pts, pts[picks])
+            order = np.argsort(assign, kind="stable")
+            bounds = np.searchsorted(assign[order], np.arange(m + 1))
+            groups = [order[bounds[c]:bounds[c + 1]] for c in range(m)]
         centers = [int(x) for x in picks]
         _split_loop(pts, groups, centers, K, rng)
         for g, c in zip(groups, centers):
@@ -200,10 +252,12 @@ def _by_shape(graph: Graph):
     return {k: np.vstack(v) for k, v in bins.items()}
 
 
-def build_graph(rec: dict, paths: dict, width, height, spp, K: int, seed: int = 0) -> Graph:
+def build_graph(rec: dict, paths: dict, width, height, spp, K: int, seed: int = 0,
+                faithful: bool = False) -> Graph:
     """graph.py:56-69 with graph.py:94-168."""
     rng = np.random.default_rng(np.random.SeedSequence([seed & 0xFFFFFFFF, 0xC1A5]))
-    cid, clusters = cluster_points(rec["pos"], class_keys(rec["kind"], rec["class_id"]), K, rng)
+    cid, clusters = cluster_points(rec["pos"], class_keys(rec["kind"], rec["class_id"]), K, rng,
+                                   faithful)
     g = Graph(rec, paths, width, height, spp, cid, clusters, next_index(rec["path_idx"]))
     build_operators(g)
     return g

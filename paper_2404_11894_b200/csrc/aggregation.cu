@@ -134,7 +134,7 @@ __global__ void k_child_links(vpg_records rec, const int32_t* __restrict__ clpos
     const int64_t r = list[i];
     if (r + 1 >= n || rec.path_idx[r + 1] != rec.path_idx[r]) continue;
     const int32_t q = clpos[r], qc = clpos[r + 1];
-    if (q >= 0 && qc >= 0) reinterpret_cast<int32_t*>(rows)[8 * int64_t(qc) + 3] = q;
+    if (q >= 0 && qc >= 0) set_row_parent(rows, qc, q);
   }
 }
 
@@ -146,7 +146,7 @@ __global__ void k_parent_links(vpg_records rec, const int32_t* __restrict__ clpo
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
        r += int64_t(gridDim.x) * blockDim.x) {
     const int32_t par = (r > 0 && rec.path_idx[r - 1] == rec.path_idx[r]) ? clpos[r - 1] : -1;
-    reinterpret_cast<int32_t*>(rows)[8 * int64_t(clpos[r]) + 3] = par;
+    set_row_parent(rows, clpos[r], par);
   }
 }
 
@@ -329,7 +329,7 @@ __device__ __forceinline__ void aggregate_cluster(
         for (int j = j0; j < j1; ++j) {
           const float a = hg_pdf32(ax, ay, az, g, num, g2ca, g32[3 * S + j], g32[4 * S + j],
                                    g32[5 * S + j], g32[12 * S + j]);
-          wt[wb + j * s + r] = a * wtsf[j];
+          // no W store: the solve recomputes these blocks (row_hg / col_hg)
           const float b = hg_pdf32(ax, ay, az, g, num, g2ca, g32[6 * S + j], g32[7 * S + j],
                                    g32[8 * S + j], g32[13 * S + j]);
           dx += b * wtsf[S + j] + a * wtsf[4 * S + j];
@@ -377,12 +377,27 @@ __device__ __forceinline__ void aggregate_cluster(
       const int64_t q = q0 + r;
       dbar_o[q] = f4(bx, by, bz);
       coeff_o[q] = f4(kx, ky, kz);
-      rows_o[2 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
-                                  __int_as_float(mb.parent));
-      // w = 1: terminal row (no continuation child writes it), the solve
-      // carries its I over from iteration to iteration
-      rows_o[2 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz),
-                                      (mb.flags & 2u) ? 1.f : 0.f);
+      // row layout (graph.cuh): {a, link}, {b, 1/phat_ind}, {HG anchor, g},
+      // {phase direction, 1 - |d|^2}; link = (parent + 1) * 2 + terminal
+      // (terminal: no continuation child writes the row, the solve carries
+      // its I over from iteration to iteration)
+      rows_o[4 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
+                                  __int_as_float(row_link(mb.parent, mb.flags & 2u)));
+      float iw, ax, ay, az, g, dx3, dy3, dz3, cd;
+      if constexpr (kMode == kVol32) {
+        iw = wtsf[r];
+        ax = g32[r]; ay = g32[S + r]; az = g32[2 * S + r]; g = g32[9 * S + r];
+        dx3 = g32[3 * S + r]; dy3 = g32[4 * S + r]; dz3 = g32[5 * S + r]; cd = g32[12 * S + r];
+      } else {
+        iw = kVol ? wtsf[r] : float(wts[r]);
+        ax = float(geo[r]); ay = float(geo[S + r]); az = float(geo[2 * S + r]);
+        g = float(mb.g);
+        dx3 = float(geo[3 * S + r]); dy3 = float(geo[4 * S + r]); dz3 = float(geo[5 * S + r]);
+        cd = 0.f;
+      }
+      rows_o[4 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz), iw);
+      rows_o[4 * q + 2] = make_float4(ax, ay, az, g);
+      rows_o[4 * q + 3] = make_float4(dx3, dy3, dz3, cd);
       i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
   }
@@ -394,7 +409,7 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int64_t* __restrict__ range, int64_t n, int S,
             float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
             float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
-            float4* __restrict__ i0_o) {
+            float4* __restrict__ i0_o, uint8_t* __restrict__ cl_mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* geo = reinterpret_cast<double*>(smem);
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
@@ -426,6 +441,8 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
     const bool surface = __any_sync(0xFFFFFFFFu, fl & 4u);
     const bool need64 = __any_sync(0xFFFFFFFFu, fl & 8u);
     const int mode = surface ? kSurface : (need64 ? kVol64 : kVol32);
+    // 1: W block stored (Lambertian / |g| > kG32), 0: recomputed by the solve
+    if (tid == 0) cl_mode[k] = mode == kVol32 ? 0 : 1;
     for (int l = tid; l < s; l += blockDim.x) {
       const Member& mb = mem[q0 + l];
       const double g = mb.g;
@@ -442,11 +459,14 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
         g32[7 * S + l] = float(mb.ey);
         g32[8 * S + l] = float(mb.ez);
         g32[9 * S + l] = float(g);
-        g32[10 * S + l] = float(num);
+        g32[10 * S + l] = hg_num_f32(float(g));  // the solve's own fp32 normalisation
         const double na = fma(mb.ax, mb.ax, fma(mb.ay, mb.ay, mb.az * mb.az));
         const double np = fma(mb.px, mb.px, fma(mb.py, mb.py, mb.pz * mb.pz));
         const double ne = fma(mb.ex, mb.ex, fma(mb.ey, mb.ey, mb.ez * mb.ez));
-        g32[11 * S + l] = float(g2 * (1.0 - na));
+        // g^2 (1 - |a|^2) is ~1e-16 for the unit anchors: left out here and in
+        // the solve's recomputed blocks, so both evaluate the same W
+        (void)na;
+        g32[11 * S + l] = 0.f;
         g32[12 * S + l] = float(1.0 - np);
         g32[13 * S + l] = float(1.0 - ne);
       } else {
@@ -485,7 +505,7 @@ __global__ void k_set_parents(const int32_t* __restrict__ parent, int64_t n,
                               float4* __restrict__ rows) {
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
        q += int64_t(gridDim.x) * blockDim.x)
-    reinterpret_cast<int32_t*>(rows)[8 * q + 3] = parent[q];
+    set_row_parent(rows, q, parent[q]);
 }
 
 // I_0 of the halo slots: the remote parent's i_pt (solve.py:72, I_0 = i_pt).
@@ -509,13 +529,17 @@ __global__ void k_cluster_of_rows(const int32_t* __restrict__ cl_off, int64_t m,
 }
 
 // Solve chunks (see graph.cuh): cost prefix and the first cluster of each chunk.
-__global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, int64_t m,
-                             int64_t* __restrict__ cost) {
+// cost[k]: staged floats of cluster k (its W block only when stored, the
+// row data, I and the previous W*I); wcost[k]: its staged W floats.
+__global__ void k_chunk_cost(const int32_t* __restrict__ cl_off, const uint8_t* __restrict__ cl_mode,
+                             int64_t m, int64_t* __restrict__ cost, int64_t* __restrict__ wcost) {
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k <= m;
        k += int64_t(gridDim.x) * blockDim.x) {
-    if (k == m) { cost[k] = 0; continue; }
+    if (k == m) { cost[k] = 0; wcost[k] = 0; continue; }
     const int64_t s = cl_off[k + 1] - cl_off[k];
-    cost[k] = ((s * s + 3) & ~int64_t(3)) + 16 * s + 4;
+    const int64_t w = cl_mode[k] ? ((s * s + 3) & ~int64_t(3)) : 0;
+    cost[k] = w + kRowFloats * s + 4;
+    wcost[k] = w;
   }
 }
 
@@ -540,30 +564,30 @@ __global__ void k_chunk_first(const int64_t* __restrict__ cst, int64_t m, int64_
 // Chunk descriptors (one 32-byte load per chunk for the solve's producer) and
 // the per-cluster table staged with each chunk.  Cluster k is in chunk
 // floor(cst[k] / chunk_floats) (chunk_first[c] = first k with cst[k] >= c F).
+// Chunk descriptors: {k0, nk, q0, R} and {staged W floats, 0, 0, 0}.
 __global__ void k_chunk_desc(const int32_t* __restrict__ first, const int64_t* __restrict__ n_chunks_p,
-                             const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off,
+                             const int32_t* __restrict__ cl_off, const int64_t* __restrict__ wcs,
                              int4* __restrict__ desc) {
   const int64_t n_chunks = *n_chunks_p;
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_chunks;
        c += int64_t(gridDim.x) * blockDim.x) {
     const int32_t k0 = first[c], k1 = first[c + 1];
-    const int64_t w0 = w_off[k0];
     const int32_t q0 = cl_off[k0];
-    desc[2 * c] = make_int4(int(uint32_t(uint64_t(w0))), int(uint32_t(uint64_t(w0) >> 32)), k0,
-                            k1 - k0);
-    desc[2 * c + 1] = make_int4(q0, cl_off[k1] - q0, int(w_off[k1] - w0), 0);
+    desc[2 * c] = make_int4(k0, k1 - k0, q0, cl_off[k1] - q0);
+    desc[2 * c + 1] = make_int4(int(wcs[k1] - wcs[k0]), 0, 0, 0);
   }
 }
 
-__global__ void k_cluster_meta(const int64_t* __restrict__ cst, int64_t m, int64_t chunk_floats,
-                               const int32_t* __restrict__ first,
+// Per cluster: {first row - chunk's q0, staged W offset, size, W stored}.
+__global__ void k_cluster_meta(const int64_t* __restrict__ cst, const int64_t* __restrict__ wcs,
+                               int64_t m, int64_t chunk_floats, const int32_t* __restrict__ first,
                                const int32_t* __restrict__ cl_off,
-                               const int64_t* __restrict__ w_off, int4* __restrict__ meta) {
+                               const uint8_t* __restrict__ cl_mode, int4* __restrict__ meta) {
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < m;
        k += int64_t(gridDim.x) * blockDim.x) {
     const int32_t k0 = first[cst[k] / chunk_floats];
-    meta[k] = make_int4(cl_off[k] - cl_off[k0], int(w_off[k] - w_off[k0]), cl_off[k + 1] - cl_off[k],
-                        0);
+    meta[k] = make_int4(cl_off[k] - cl_off[k0], int(wcs[k] - wcs[k0]), cl_off[k + 1] - cl_off[k],
+                        int(cl_mode[k]));
   }
 }
 
@@ -578,7 +602,8 @@ void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s) {
   for (auto* v : {&g->dbar, &g->coeff, &g->acc[0], &g->acc[1]}) v->alloc(size_t(n + 1), s);
   // I vectors carry the halo slots after the n rows
   for (auto* v : {&g->i0, &g->ibuf[0], &g->ibuf[1]}) v->alloc(size_t(n + g->n_halo + 1), s);
-  g->rows.alloc(size_t(2 * n + 2), s);
+  g->rows.alloc(size_t(4 * n + 4), s);
+  g->cl_mode.alloc(size_t(n + 1), s);
   g->term_max.alloc(4, s);
   VPG_CUDA(cudaMemsetAsync(g->term_max.get(), 0, 4 * sizeof(float), s));
 }
@@ -600,7 +625,8 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
   const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
   VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, static_cast<const Member*>(members),
              g->cl_off.get(), g->cl_size.get(), g->w_off.get(), range, g->n, S, g->wt.get(),
-             g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get());
+             g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get(),
+             g->cl_mode.get());
 }
 
 void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
@@ -621,12 +647,16 @@ void finalize_operators_async(vpg_graph* g, const vpg_records& rec, cudaStream_t
   // solve chunks: cost prefix over the clusters (internal order)
   int64_t* cost = scratch_of<int64_t>(s, "chunk_cost", size_t(m) + 1);
   int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
-  VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), m, cost);
+  int64_t* wcost = scratch_of<int64_t>(s, "chunk_wcost", size_t(m) + 1);
+  int64_t* wcs = scratch_of<int64_t>(s, "chunk_wcs", size_t(m) + 1);
+  VPG_LAUNCH(k_chunk_cost, grid_for(m + 1, 256), 256, 0, s, g->cl_off.get(), g->cl_mode.get(), m,
+             cost, wcost);
   size_t bytes = 0;
   VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cost, cst, int(m + 1), s));
   void* tmp = scratch(s, "cub_temp", bytes + 256);
   VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cost, cst, int(m + 1), s));
-  count_launch(1);
+  VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, wcost, wcs, int(m + 1), s));
+  count_launch(2);
 }
 
 void finalize_chunks(vpg_graph* g, cudaStream_t s) {
@@ -634,7 +664,7 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {
   // the largest chunk (<= kChunkFloatsMax) with which 3, else 2, else 1
   // stages of chunk + the largest cluster's table, blocks and rows fit
   const int64_t smax = std::max<int64_t>(1, g->max_cluster);
-  const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + 16 * smax + 4;
+  const int64_t extra = ((smax * smax + 3) & ~int64_t(3)) + kRowFloats * smax + 4;
   g->n_stages = 0;
   for (int st = 3; st >= 1 && !g->n_stages; --st) {
     const int64_t room = int64_t((kSolveSmem - 128) / (sizeof(float) * st)) - extra;
@@ -644,8 +674,8 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {
     }
   }
   VPG_REQUIRE(g->n_stages > 0, VPG_ELIMIT, "clusters too large for the staged solve");
-  // sum over clusters of pad4(s^2) + 16 s + 4 <= smax n + 16 n + 7 m
-  const int64_t bound = smax * n + 16 * n + 7 * m;
+  // sum over clusters of pad4(s^2) + kRowFloats s + 4 <= smax n + kRowFloats n + 7 m
+  const int64_t bound = smax * n + kRowFloats * n + 7 * m;
   g->chunk_cap = bound / g->chunk_floats + 2;
   g->chunk_first.alloc(size_t(g->chunk_cap + 1), s);
   g->chunk_desc.alloc(size_t(2 * g->chunk_cap + 2), s);
@@ -657,12 +687,13 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {
     return;
   }
   const int64_t* cst = scratch_of<int64_t>(s, "chunk_cst", size_t(m) + 1);
+  const int64_t* wcs = scratch_of<int64_t>(s, "chunk_wcs", size_t(m) + 1);
   VPG_LAUNCH(k_chunk_first, grid_for(g->chunk_cap + 1, 256), 256, 0, s, cst, m, g->chunk_cap,
              int64_t(g->chunk_floats), g->chunk_first.get(), g->n_chunks_dev.get());
   VPG_LAUNCH(k_chunk_desc, grid_for(g->chunk_cap, 256), 256, 0, s, g->chunk_first.get(),
-             g->n_chunks_dev.get(), g->cl_off.get(), g->w_off.get(), g->chunk_desc.get());
-  VPG_LAUNCH(k_cluster_meta, grid_for(m, 256), 256, 0, s, cst, m, int64_t(g->chunk_floats),
-             g->chunk_first.get(), g->cl_off.get(), g->w_off.get(), g->cl_meta.get());
+             g->n_chunks_dev.get(), g->cl_off.get(), wcs, g->chunk_desc.get());
+  VPG_LAUNCH(k_cluster_meta, grid_for(m, 256), 256, 0, s, cst, wcs, m, int64_t(g->chunk_floats),
+             g->chunk_first.get(), g->cl_off.get(), g->cl_mode.get(), g->cl_meta.get());
 }
 
 void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,

@@ -18,20 +18,30 @@
 //                        (graph.py:143-148), columns implicit
 //   phat[3][N]   double  phat_ind / phat_dir_phase / phat_dir_emit, cluster-major
 //   Solve vectors, cluster-major (xyz = RGB):
-//     rows[q]  RowStatic {a = w_cont*coeff, b = w_cont*D-bar, par}: 32 bytes,
-//              par = position of the continuation parent (record r-1 on the
-//              same path), -1 for a path's first record.  Row q propagates
-//              into par:  I[par] = w_cont*(coeff*(W I)[q] + D-bar[q]) = a*acc + b
+//     rows[4q..4q+3]  64 bytes per row:
+//              {a = w_cont*coeff, link}, {b = w_cont*D-bar, 1/phat_ind},
+//              {HG anchor -omega_out (float), g}, {phase_dir (float), 1 - |d|^2}
+//              link = (par + 1) * 2 + terminal, par = position of the
+//              continuation parent (record r-1 on the same path), -1 for a
+//              path's first record; terminal = no continuation child.  Row q
+//              propagates into par:  I[par] = w_cont*(coeff*(W I)[q] + D-bar[q])
+//              = a*acc + b.  The last two float4 are what the solve needs to
+//              recompute W[r, j] = num(g_r) (|d_j - g_r a_r|^2 + 1 - |d_j|^2)^-3/2
+//              / phat_ind[j] for clusters whose W block is not stored
+//   cl_mode[k] uint8   1: cluster k's W block is stored in wt (Lambertian
+//              members or |g| > 0.95, fp64 densities); 0: the solve recomputes
+//              it in fp32 from the row data (the aggregate's fp32 HG path)
 //     i0 = i_pt, dbar = D-bar, coeff (float4)
 //   ibuf[2], acc[2]: double-buffered I and W*I (acc = i_bar / coeff).
 //   chunk_first[c]: first cluster of solve chunk c; chunks cut the cost prefix
 //     sum(pad4(s^2) + 16 s + 4) floats at multiples of chunk_floats, so one
 //     chunk's cluster table, kernel blocks and row data fit a shared-memory
 //     stage (TMA bulk copies).
-//   chunk_desc[c]: {w0, k0, nk, q0, R, wc}: the chunk's first W float, first
-//     cluster, cluster count, first row, row count, W floats -- one load.
-//   cl_meta[k]: {first row - chunk's q0, W offset - chunk's w0, size, 0}, staged
-//     with the chunk so a consumer never reads cluster metadata from HBM.
+//   chunk_desc[c]: {k0, nk, q0, R}, {wc, 0, 0, 0}: first cluster, cluster
+//     count, first row, row count, staged W floats (stored blocks only) --
+//     one 32-byte load.
+//   cl_meta[k]: {first row - chunk's q0, staged W offset, size, cl_mode},
+//     staged with the chunk so a consumer never reads cluster metadata from HBM.
 #pragma once
 #include <memory>
 #include <vector>
@@ -47,7 +57,8 @@ struct vpg_graph {
   vpg::DBuf<float> wt;
   vpg::DBuf<double> phat;
   vpg::DBuf<float4> i0, dbar, coeff, ibuf[2], acc[2];
-  vpg::DBuf<float4> rows;  // 2 float4 per row: (a.xyz, par bits), (b.xyz, 0)
+  vpg::DBuf<float4> rows;  // 4 float4 per row (see above)
+  vpg::DBuf<uint8_t> cl_mode;  // per cluster: 1 = W block stored, 0 = recomputed
   vpg::DBuf<int32_t> chunk_first;
   vpg::DBuf<int4> chunk_desc;  // 2 int4 per chunk (see above)
   vpg::DBuf<int4> cl_meta;
@@ -110,6 +121,26 @@ namespace vpg {
 constexpr int kChunkFloatsMax = 16384;
 constexpr int kChunkFloatsMin = 2048;
 constexpr size_t kSolveSmem = 226 * 1024;
+// staged floats per row in a solve chunk: 16 row data + 4 I + 4 previous W*I
+constexpr int kRowFloats = 24;
+// row link word: (parent + 1) * 2 + terminal (parent in [-1, 2^31 - 2])
+__host__ __device__ __forceinline__ int32_t row_link(int32_t parent, bool terminal) {
+  return int32_t((uint32_t(parent + 1) << 1) | (terminal ? 1u : 0u));
+}
+__host__ __device__ __forceinline__ int32_t link_parent(int32_t link) {
+  return int32_t(uint32_t(link) >> 1) - 1;
+}
+__host__ __device__ __forceinline__ bool link_terminal(int32_t link) { return link & 1; }
+// HG normalisation (1 - g^2) / 4pi in fp32, shared by the aggregate's fp32 HG
+// path and the solve's recomputed blocks (bit-identical W in both)
+__host__ __device__ __forceinline__ float hg_num_f32(float g) {
+  return float(1.0 / (4.0 * 3.14159265358979323846)) * fmaf(-g, g, 1.f);
+}
+// set row q's parent, keeping its terminal bit
+__device__ __forceinline__ void set_row_parent(float4* rows, int64_t q, int32_t parent) {
+  int32_t* w = reinterpret_cast<int32_t*>(rows) + 16 * q + 3;
+  *w = row_link(parent, link_terminal(*w));
+}
 // cluster.cu: the whole build (clusters, layout, and the operator passes
 // below, overlapped with the host split loop); `with_operators` = false for
 // cluster_points.

@@ -85,6 +85,32 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------- recomputed HG kernel blocks
+// Clusters with cl_mode 0 (volume members, |g| <= 0.95: the aggregate's fp32
+// HG path) store no W block; W[r, j] = num(g_r) hg3(r, j) / phat_ind[j] is
+// recomputed from the row data (graph.cuh): anchor a_r and g_r (rows[4q+2]),
+// phase direction d_j and 1 - |d_j|^2 (rows[4q+3]), 1/phat_ind[j]
+// (rows[4q+1].w).  hg3 = (|d - g a|^2 + 1 - |d|^2)^-3/2, the aggregate's
+// hg_pdf32 without the g^2 (1 - |a|^2) term (~1e-16 for the unit anchors).
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float hg3(const float4 ha, const float4 dc) {
+  const float ux = fmaf(-ha.w, ha.x, dc.x), uy = fmaf(-ha.w, ha.y, dc.y),
+              uz = fmaf(-ha.w, ha.z, dc.z);
+  const float r = rsqrt_ftz(fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, dc.w))));
+  return r * r * r;
+}
+// W[r, j] exactly as the aggregate's fp32 path evaluates it:
+// (num_r * hg3) * (1 / phat_ind[j])
+__device__ __forceinline__ float w_recomputed(const float4* __restrict__ rows, int64_t qr,
+                                              int64_t qj) {
+  const float4 ha = rows[4 * qr + 2];
+  return (hg_num_f32(ha.w) * hg3(ha, rows[4 * qj + 3])) * rows[4 * qj + 1].w;
+}
+
 // One fixed-point iteration t (solve.py:78-83) over TMA-staged chunks.
 //
 // A persistent CTA per SM walks its chunks (see graph.cuh) with a producer
@@ -101,7 +127,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 //    to HBM, with the residual maxima of solve.py:54-61.  The old I[par] is
 //    recomputed from the previous W*I (same arithmetic as when it was stored)
 //    instead of gathered.
-constexpr int kConsumers = 16;
+constexpr int kConsumers = 24;
 constexpr int kMaxStages = 4;  // the stage count is chosen per graph (graph.cuh)
 
 // Residual, tol break and 3-growth divergence of iteration t (solve.py:80-94),
@@ -155,7 +181,8 @@ __device__ __forceinline__ void finish_iteration(int t, double tol, uint32_t* __
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1)
 k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
              const int64_t* __restrict__ n_chunks_p, int n_stages, int stage_floats,
-             const float* __restrict__ wt, const float4* __restrict__ rows,
+             const float* __restrict__ wt, const int64_t* __restrict__ w_off,
+             const float4* __restrict__ rows,
              const float4* __restrict__ i_in, float4* __restrict__ i_out,
              const float4* __restrict__ acc_prev, float4* __restrict__ acc_out,
              const float4* __restrict__ i0, int t, uint32_t* __restrict__ red,
@@ -208,14 +235,14 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
           finished = true;
           break;
         }
-        const uint32_t w0lo = __shfl_sync(0xFFFFFFFFu, uint32_t(d0.x), j);
-        const uint32_t w0hi = __shfl_sync(0xFFFFFFFFu, uint32_t(d0.y), j);
-        const int nk = __shfl_sync(0xFFFFFFFFu, d0.w, j);
-        const int k0 = __shfl_sync(0xFFFFFFFFu, d0.z, j);
-        const int q0 = __shfl_sync(0xFFFFFFFFu, d1.x, j);
-        const int R = __shfl_sync(0xFFFFFFFFu, d1.y, j);
-        const int wc = __shfl_sync(0xFFFFFFFFu, d1.z, j);
+        const int k0 = __shfl_sync(0xFFFFFFFFu, d0.x, j);
+        const int nk = __shfl_sync(0xFFFFFFFFu, d0.y, j);
+        const int q0 = __shfl_sync(0xFFFFFFFFu, d0.z, j);
+        const int R = __shfl_sync(0xFFFFFFFFu, d0.w, j);
+        const int wc = __shfl_sync(0xFFFFFFFFu, d1.x, j);
         const int st = int(i % n_stages);
+        uint64_t* bar = &full[st];
+        float* buf = stage0 + st * int64_t(stage_floats);
         if (lane == 0) {
           if (i >= n_stages) {
             // the stage's previous chunk must be fully consumed
@@ -223,29 +250,39 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
             done[st] = 0;
             fence_proxy_async();  // consumers' generic reads before the async refill
           }
-          uint64_t* bar = &full[st];
-          float* buf = stage0 + st * int64_t(stage_floats);
           // the stage's previous phase has completed (its chunk was consumed), so
           // a consumer that sees issued == i waits on this chunk's phase
           *reinterpret_cast<volatile int*>(&issued[st]) = int(i);
           if (nk == 0) {
             mbar_arrive(bar);
           } else {
-            const int64_t w0 = int64_t((uint64_t(w0hi) << 32) | w0lo);
             const uint32_t mb = uint32_t(nk) * 16u, wb = uint32_t(wc) * 4u,
-                           rb = uint32_t(R) * 32u, ib = uint32_t(R) * 16u;
+                           rb = uint32_t(R) * 64u, ib = uint32_t(R) * 16u;
             mbar_expect_tx(bar, mb + wb + rb + ib + (t > 0 ? ib : 0u));
             bulk_g2s(buf, meta + k0, mb, bar);
-            float* p = buf + 4 * nk;
-            if (wb) bulk_g2s(p, wt + w0, wb, bar);
-            p += wc;
-            bulk_g2s(p, rows + 2 * int64_t(q0), rb, bar);
-            p += 8 * R;
+            float* p = buf + 4 * nk + wc;
+            bulk_g2s(p, rows + 4 * int64_t(q0), rb, bar);
+            p += 16 * R;
             bulk_g2s(p, i_in + q0, ib, bar);
             if (t > 0) bulk_g2s(p + 4 * R, acc_prev + q0, ib, bar);
           }
+          prev_nk[st] = nk;
         }
-        if (lane == 0) prev_nk[st] = nk;
+        if (wc > 0) {
+          // stored W blocks (Lambertian / high-g clusters), one copy per
+          // cluster issued by the lanes in parallel after lane 0 has claimed
+          // the stage and announced the chunk's bytes
+          __syncwarp();
+          fence_proxy_async();
+          for (int kk = lane; kk < nk; kk += 32) {
+            const int4 mk = meta[k0 + kk];
+            if (mk.w) {
+              const int64_t sz = mk.z;
+              bulk_g2s(buf + 4 * nk + mk.y, wt + w_off[k0 + kk],
+                       uint32_t(((sz * sz + 3) & ~int64_t(3)) * 4), bar);
+            }
+          }
+        }
       }
       if (finished) break;
     }
@@ -259,10 +296,10 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
       const int64_t c = blockIdx.x;
       if (c < n_chunks) {
         const int4 d0 = desc[2 * c], d1 = desc[2 * c + 1];
-        nk = d0.w;
-        cq0 = d1.x;
-        R = d1.y;
-        wc = d1.z;
+        nk = d0.y;
+        cq0 = d0.z;
+        R = d0.w;
+        wc = d1.x;
       }
     }
     for (;;) {
@@ -284,10 +321,10 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         const int64_t c2 = blockIdx.x + ci * G;
         if (c2 < n_chunks) {
           const int4 d0 = desc[2 * c2], d1 = desc[2 * c2 + 1];
-          nk = d0.w;
-          cq0 = d1.x;
-          R = d1.y;
-          wc = d1.z;
+          nk = d0.y;
+          cq0 = d0.z;
+          R = d0.w;
+          wc = d1.x;
         }
       }
       if (finished) break;
@@ -302,16 +339,52 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
       const int4 mk = reinterpret_cast<const int4*>(buf)[x - cbase];
       const float* wbase = buf + 4 * nk;
       const float4* srow = reinterpret_cast<const float4*>(wbase + wc);
-      const float4* sin = reinterpret_cast<const float4*>(wbase + wc + 8 * int64_t(R));
-      const float4* sprev = reinterpret_cast<const float4*>(wbase + wc + 12 * int64_t(R));
+      const float4* sin = reinterpret_cast<const float4*>(wbase + wc + 16 * int64_t(R));
+      const float4* sprev = reinterpret_cast<const float4*>(wbase + wc + 20 * int64_t(R));
       const int rl = mk.x;
       const int s = mk.z;
+      const bool stored = mk.w != 0;
       const int64_t q0 = int64_t(cq0) + rl;
       const float* w = wbase + mk.y;
+      const float4* crow = srow + 4 * rl;  // this cluster's row data
       for (int rc = 0; rc < s; rc += 64) {
         const int r0 = rc + lane, r1 = rc + lane + 32;
         float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
-        if (s - rc <= 32) {
+        if (!stored) {
+          // W recomputed (w_recomputed's arithmetic, so the same W as the
+          // aggregate evaluated): acc_r = sum_j ((num_r hg3(r, j)) / phat_ind[j]) I_j
+          const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 ha0 = r0 < s ? crow[4 * r0 + 2] : z4;
+          const float n0 = hg_num_f32(ha0.w);
+          if (s - rc <= 32) {
+#pragma unroll 4
+            for (int j = 0; j < s; ++j) {
+              const float4 dc = crow[4 * j + 3];
+              const float iw = crow[4 * j + 1].w;
+              const float4 ij = sin[rl + j];
+              const float wv = (n0 * hg3(ha0, dc)) * iw;
+              acc0.x = fmaf(wv, ij.x, acc0.x);
+              acc0.y = fmaf(wv, ij.y, acc0.y);
+              acc0.z = fmaf(wv, ij.z, acc0.z);
+            }
+          } else {
+            const float4 ha1 = r1 < s ? crow[4 * r1 + 2] : z4;
+            const float n1 = hg_num_f32(ha1.w);
+#pragma unroll 2
+            for (int j = 0; j < s; ++j) {
+              const float4 dc = crow[4 * j + 3];
+              const float iw = crow[4 * j + 1].w;
+              const float4 ij = sin[rl + j];
+              const float w0v = (n0 * hg3(ha0, dc)) * iw, w1v = (n1 * hg3(ha1, dc)) * iw;
+              acc0.x = fmaf(w0v, ij.x, acc0.x);
+              acc0.y = fmaf(w0v, ij.y, acc0.y);
+              acc0.z = fmaf(w0v, ij.z, acc0.z);
+              acc1.x = fmaf(w1v, ij.x, acc1.x);
+              acc1.y = fmaf(w1v, ij.y, acc1.y);
+              acc1.z = fmaf(w1v, ij.z, acc1.z);
+            }
+          }
+        } else if (s - rc <= 32) {
           // one row per lane (most clusters: s <= 2K = 64, mean K)
           const float* colr = w + r0;
 #pragma unroll 4
@@ -344,9 +417,10 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
           const float3 ac = h ? acc1 : acc0;
           const int64_t q = q0 + rr;
           acc_out[q] = make_float4(ac.x, ac.y, ac.z, 0.f);
-          const float4 A = srow[2 * (rl + rr)], B = srow[2 * (rl + rr) + 1];
-          if (B.w != 0.f) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
-          const int32_t p = __float_as_int(A.w);
+          const float4 A = crow[4 * rr], B = crow[4 * rr + 1];
+          const int32_t link = __float_as_int(A.w);
+          if (link_terminal(link)) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
+          const int32_t p = link_parent(link);
           if (p < 0) continue;
           const float nx = fmaf(A.x, ac.x, B.x), ny = fmaf(A.y, ac.y, B.y),
                       nz = fmaf(A.z, ac.z, B.z);
@@ -404,18 +478,21 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
 constexpr int kItWarps = 8;
 __global__ void __launch_bounds__(kItWarps * 32)
 k_apply_w(const int32_t* __restrict__ cl_off, const int64_t* __restrict__ w_off, int64_t m,
-          const float* __restrict__ wt, const float4* __restrict__ v_in, float4* __restrict__ out) {
+          const float* __restrict__ wt, const uint8_t* __restrict__ cl_mode,
+          const float4* __restrict__ rows, const float4* __restrict__ v_in,
+          float4* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = int64_t(gridDim.x) * kItWarps;
   for (int64_t k = int64_t(blockIdx.x) * kItWarps + (threadIdx.x >> 5); k < m; k += nwarps) {
     const int32_t q0 = cl_off[k];
     const int s = cl_off[k + 1] - q0;
     const float* w = wt + w_off[k];
+    const bool stored = cl_mode[k] != 0;
     for (int r = lane; r < s; r += 32) {
       float3 acc = make_float3(0.f, 0.f, 0.f);
       for (int j = 0; j < s; ++j) {
         const float4 vj = v_in[q0 + j];
-        const float wv = w[int64_t(j) * s + r];
+        const float wv = stored ? w[int64_t(j) * s + r] : w_recomputed(rows, q0 + r, q0 + j);
         acc.x = fmaf(wv, vj.x, acc.x);
         acc.y = fmaf(wv, vj.y, acc.y);
         acc.z = fmaf(wv, vj.z, acc.z);
@@ -538,7 +615,8 @@ __global__ void k_export_csr(const int32_t* __restrict__ cluster_id,
                              const int32_t* __restrict__ internal_of, const int32_t* __restrict__ clpos,
                              const int32_t* __restrict__ cl_off, const int32_t* __restrict__ cl_size,
                              const int64_t* __restrict__ w_off, const int32_t* __restrict__ perm,
-                             const float* __restrict__ wt, const int64_t* __restrict__ indptr,
+                             const float* __restrict__ wt, const uint8_t* __restrict__ cl_mode,
+                             const float4* __restrict__ rows, const int64_t* __restrict__ indptr,
                              int64_t n, int64_t* __restrict__ indices, double* __restrict__ data) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -548,9 +626,11 @@ __global__ void k_export_csr(const int32_t* __restrict__ cluster_id,
     const int s = cl_size[k];
     const int rl = clpos[r] - q0;
     const int64_t base = indptr[r];
+    const bool stored = cl_mode[k] != 0;
     for (int j = lane; j < s; j += 32) {
       indices[base + j] = perm[q0 + j];
-      data[base + j] = double(wt[w_off[k] + int64_t(j) * s + rl]);
+      data[base + j] = double(stored ? wt[w_off[k] + int64_t(j) * s + rl]
+                                     : w_recomputed(rows, q0 + rl, q0 + j));
     }
   }
 }
@@ -652,7 +732,7 @@ SolveLaunch solve_launch(const vpg_graph* g) {
   // stage = one chunk (g->chunk_floats) plus the largest cluster's blocks + rows
   SolveLaunch L;
   const int smax = std::max(1, g->max_cluster);
-  L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + 16 * smax + 4;
+  L.stage_floats = g->chunk_floats + ((smax * smax + 3) & ~3) + kRowFloats * smax + 4;
   L.smem = 128 + size_t(g->n_stages) * L.stage_floats * sizeof(float);
   VPG_REQUIRE(L.smem <= kSolveSmem, VPG_ELIMIT, "clusters too large for the staged solve");
   ensure_dynamic_smem(reinterpret_cast<const void*>(k_solve_iter), L.smem);
@@ -693,7 +773,7 @@ void launch_iteration(vpg_graph* g, int32_t t, bool fused, cudaStream_t s) {
   const SolveLaunch L = solve_launch(g);
   VPG_LAUNCH(k_solve_iter, L.grid, (kConsumers + 1) * 32, L.smem, s, g->chunk_desc.get(),
              g->cl_meta.get(), g->n_chunks_dev.get(), g->n_stages, L.stage_floats, g->wt.get(),
-             g->rows.get(), t == 0 ? g->i0.get() : g->ibuf[t & 1].get(),
+             g->w_off.get(), g->rows.get(), t == 0 ? g->i0.get() : g->ibuf[t & 1].get(),
              g->ibuf[(t + 1) & 1].get(), g->acc[t & 1].get(),
              g->acc[(t + 1) & 1].get(), g->i0.get(), t, g->red.get(), g->ctl.get(),
              fused ? 1 : 0, g->tol, g->term_max.get(), g->resid.get());
@@ -769,7 +849,8 @@ void aggregate_indirect(const vpg_graph* g, const vpg_records& rec, const double
   DBuf<float4> vin(n, s), vout(n, s);
   VPG_LAUNCH(k_gather_rec3, grid_for(n, block), block, 0, s, incoming, g->perm.get(), n, vin.get());
   VPG_LAUNCH(k_apply_w, iterate_grid(g->m), kItWarps * 32, 0, s, g->cl_off.get(),
-             g->w_off.get(), g->m, g->wt.get(), vin.get(), vout.get());
+             g->w_off.get(), g->m, g->wt.get(), g->cl_mode.get(), g->rows.get(), vin.get(),
+             vout.get());
   VPG_LAUNCH(k_scatter_rec3, grid_for(n, block), block, 0, s, vout.get(), g->clpos.get(),
              rec.coeff, n, out);
 }
@@ -848,7 +929,8 @@ void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, dou
       DBuf<double> dat(size_t(g->nnz) + 1, s);
       VPG_LAUNCH(k_export_csr, grid_for(n * 32, block), block, 0, s, g->cluster_id.get(),
                  g->internal_of.get(), g->clpos.get(), g->cl_off.get(), g->cl_size.get(),
-                 g->w_off.get(), g->perm.get(), g->wt.get(), ip.get(), n, ind.get(), dat.get());
+                 g->w_off.get(), g->perm.get(), g->wt.get(), g->cl_mode.get(), g->rows.get(),
+                 ip.get(), n, ind.get(), dat.get());
       if (indices) VPG_CUDA(cudaMemcpyAsync(indices, ind.get(), g->nnz * 8, cudaMemcpyDeviceToHost, s));
       if (data) VPG_CUDA(cudaMemcpyAsync(data, dat.get(), g->nnz * 8, cudaMemcpyDeviceToHost, s));
       VPG_CUDA(cudaStreamSynchronize(s));

@@ -119,3 +119,14 @@ def test_tracer_oracle_matches_reference_records(name):
         np.testing.assert_allclose(v, ref_rec[f], rtol=1e-12, atol=0, err_msg=f)
     for f in ("cam_weight", "d_cam", "direct0", "pt_estimate"):
         np.testing.assert_allclose(paths[f], ref_paths[f], rtol=1e-12, atol=0, err_msg=f)
+
+
+def test_faithful_clustering_equals_fast_clustering():
+    """The cost-faithful variant (the reference's per-cell loop and per-center
+    groups, used by bench.py's reference arm) gives the reference's clusters."""
+    z = golden("c1_16")
+    rec, paths = O.load_golden_records(z)
+    for K in (32, 8):
+        g = O.build_graph(rec, paths, int(z["width"]), int(z["height"]), int(z["spp"]), K,
+                          int(z["seed"]), faithful=True)
+        assert np.array_equal(g.cluster_id, z[f"K{K}_cluster_id"])
