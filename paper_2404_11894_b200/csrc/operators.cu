@@ -138,13 +138,14 @@ __device__ void control_step(int t, double tol, const uint32_t* __restrict__ red
   if (ctl[1]) return;
   // red was filled by atomics from every CTA: read it past L1
   const uint32_t* vred = red;
-  const unsigned nan_bits = __ldcg(vred + t * 8 + 6);
   double worst = 0.0;
   for (int c = 0; c < 3; ++c) {
-    // a NaN channel never wins Python's max(worst, q) in the reference
-    if (nan_bits & ((1u | 8u) << c)) continue;
-    const double delta = double(__uint_as_float(__ldcg(vred + t * 8 + c)));
-    double scale = double(fmaxf(__uint_as_float(__ldcg(vred + t * 8 + 3 + c)), term_max[c]));
+    // maxima of non-negative values as float bits: above +inf means NaN,
+    // and a NaN channel never wins Python's max(worst, q) in the reference
+    const uint32_t db = __ldcg(vred + t * 8 + c), sb = __ldcg(vred + t * 8 + 3 + c);
+    if (db > 0x7F800000u || sb > 0x7F800000u) continue;
+    const double delta = double(__uint_as_float(db));
+    double scale = double(fmaxf(__uint_as_float(sb), term_max[c]));
     scale = scale > 1e-12 ? scale : 1e-12;
     const double q = delta / scale;
     worst = q > worst ? q : worst;
@@ -200,8 +201,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
   int* next_item = reinterpret_cast<int*>(smem + 96);
   int* issued = reinterpret_cast<int*>(smem + 104);               // n_stages chunk ids
   float* stage0 = reinterpret_cast<float*>(smem + 128);
-  __shared__ float blk[kConsumers][6];
-  __shared__ unsigned blk_nan[kConsumers];
+  __shared__ uint32_t blk[kConsumers][6];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
     for (int st = 0; st < n_stages; ++st) {
@@ -288,8 +288,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
     }
   } else {
     // ----------------------------------------------------------- consumers
-    float dmax[3] = {0.f, 0.f, 0.f}, smax[3] = {0.f, 0.f, 0.f};
-    unsigned nan_bits = 0;  // numpy's max propagates NaN per channel: remember it
+    uint32_t dmax[3] = {0u, 0u, 0u}, smax[3] = {0u, 0u, 0u};  // float bits (see epilogue)
     int64_t ci = 0, cbase = 0, waited = -1;  // current chunk (local index), its first item
     int nk = 0, R = 0, wc = 0, cq0 = 0;      // of chunk ci
     {
@@ -336,24 +335,55 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         waited = ci;
       }
       const float* buf = stage0 + st * int64_t(stage_floats);
-      const int4 mk = reinterpret_cast<const int4*>(buf)[x - cbase];
+      const int4* smeta = reinterpret_cast<const int4*>(buf);
+      const int4 mk = smeta[x - cbase];
       const float* wbase = buf + 4 * nk;
       const float4* srow = reinterpret_cast<const float4*>(wbase + wc);
       const float4* sin = reinterpret_cast<const float4*>(wbase + wc + 16 * int64_t(R));
       const float4* sprev = reinterpret_cast<const float4*>(wbase + wc + 20 * int64_t(R));
-      const int rl = mk.x;
-      const int s = mk.z;
-      const bool stored = mk.w != 0;
-      const int64_t q0 = int64_t(cq0) + rl;
-      const float* w = wbase + mk.y;
-      const float4* crow = srow + 4 * rl;  // this cluster's row data
-      for (int rc = 0; rc < s; rc += 64) {
-        const int r0 = rc + lane, r1 = rc + lane + 32;
-        float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
-        if (!stored) {
-          // W recomputed (w_recomputed's arithmetic, so the same W as the
-          // aggregate evaluated): acc_r = sum_j ((num_r hg3(r, j)) / phat_ind[j]) I_j
-          const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      // row rr (position in its cluster, rows from crow / q0) with its
+      // W*I: acc_out, the terminal carry, the scatter into the parent and
+      // the residual maxima.  The maxima are kept as IEEE bit patterns of
+      // non-negative values: an integer max orders NaN above +inf, so a NaN
+      // propagates like numpy's max (solve.py:54-61).
+      auto epilogue = [&](const float4* crow, int rl, int64_t q0, int rr, float ax, float ay,
+                          float az) {
+        const int64_t q = q0 + rr;
+        acc_out[q] = make_float4(ax, ay, az, 0.f);
+        const float4 A = crow[4 * rr], B = crow[4 * rr + 1];
+        const int32_t link = __float_as_int(A.w);
+        if (link_terminal(link)) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
+        const int32_t p = link_parent(link);
+        if (p < 0) return;
+        const float nx = fmaf(A.x, ax, B.x), ny = fmaf(A.y, ay, B.y), nz = fmaf(A.z, az, B.z);
+        float4 old;
+        if (t == 0) {
+          old = i0[p];
+        } else {
+          const float4 pa = sprev[rl + rr];
+          old = make_float4(fmaf(A.x, pa.x, B.x), fmaf(A.y, pa.y, B.y), fmaf(A.z, pa.z, B.z), 0.f);
+        }
+        i_out[p] = make_float4(nx, ny, nz, 0.f);
+        dmax[0] = max(dmax[0], __float_as_uint(fabsf(nx - old.x)));
+        dmax[1] = max(dmax[1], __float_as_uint(fabsf(ny - old.y)));
+        dmax[2] = max(dmax[2], __float_as_uint(fabsf(nz - old.z)));
+        smax[0] = max(smax[0], __float_as_uint(fabsf(nx)));
+        smax[1] = max(smax[1], __float_as_uint(fabsf(ny)));
+        smax[2] = max(smax[2], __float_as_uint(fabsf(nz)));
+      };
+      const int items = 1;
+      if (mk.w == 0) {
+        // W recomputed with w_recomputed's operations (so the same W the
+        // aggregate evaluated), accumulated in column order; lane = row
+        // (two rows per lane for clusters of more than 32)
+        const int rl = mk.x;
+        const int s = mk.z;
+        const int64_t q0 = int64_t(cq0) + rl;
+        const float4* crow = srow + 4 * rl;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int rc = 0; rc < s; rc += 64) {
+          const int r0 = rc + lane, r1 = rc + lane + 32;
+          float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
           const float4 ha0 = r0 < s ? crow[4 * r0 + 2] : z4;
           const float n0 = hg_num_f32(ha0.w);
           if (s - rc <= 32) {
@@ -384,88 +414,63 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
               acc1.z = fmaf(w1v, ij.z, acc1.z);
             }
           }
-        } else if (s - rc <= 32) {
-          // one row per lane (most clusters: s <= 2K = 64, mean K)
-          const float* colr = w + r0;
-#pragma unroll 4
-          for (int j = 0; j < s; ++j) {
-            const float4 ij = sin[rl + j];
-            const float w0v = r0 < s ? colr[j * s] : 0.f;
-            acc0.x = fmaf(w0v, ij.x, acc0.x);
-            acc0.y = fmaf(w0v, ij.y, acc0.y);
-            acc0.z = fmaf(w0v, ij.z, acc0.z);
-          }
-        } else {
-#pragma unroll 4
-          for (int j = 0; j < s; ++j) {
-            const float4 ij = sin[rl + j];
-            const float* col = w + j * s;
-            const float w0v = r0 < s ? col[r0] : 0.f;
-            const float w1v = r1 < s ? col[r1] : 0.f;
-            acc0.x = fmaf(w0v, ij.x, acc0.x);
-            acc0.y = fmaf(w0v, ij.y, acc0.y);
-            acc0.z = fmaf(w0v, ij.z, acc0.z);
-            acc1.x = fmaf(w1v, ij.x, acc1.x);
-            acc1.y = fmaf(w1v, ij.y, acc1.y);
-            acc1.z = fmaf(w1v, ij.z, acc1.z);
-          }
+          if (r0 < s) epilogue(crow, rl, q0, r0, acc0.x, acc0.y, acc0.z);
+          if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x, acc1.y, acc1.z);
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int rr = h ? r1 : r0;
-          if (rr >= s) continue;
-          const float3 ac = h ? acc1 : acc0;
-          const int64_t q = q0 + rr;
-          acc_out[q] = make_float4(ac.x, ac.y, ac.z, 0.f);
-          const float4 A = crow[4 * rr], B = crow[4 * rr + 1];
-          const int32_t link = __float_as_int(A.w);
-          if (link_terminal(link)) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
-          const int32_t p = link_parent(link);
-          if (p < 0) continue;
-          const float nx = fmaf(A.x, ac.x, B.x), ny = fmaf(A.y, ac.y, B.y),
-                      nz = fmaf(A.z, ac.z, B.z);
-          float4 old;
-          if (t == 0) {
-            old = i0[p];
+      } else {
+        // stored W block (Lambertian / |g| > 0.95 clusters), lane = row
+        const int rl = mk.x;
+        const int s = mk.z;
+        const int64_t q0 = int64_t(cq0) + rl;
+        const float* w = wbase + mk.y;
+        const float4* crow = srow + 4 * rl;
+        for (int rc = 0; rc < s; rc += 64) {
+          const int r0 = rc + lane, r1 = rc + lane + 32;
+          float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
+          if (s - rc <= 32) {
+            const float* colr = w + r0;
+#pragma unroll 4
+            for (int j = 0; j < s; ++j) {
+              const float4 ij = sin[rl + j];
+              const float w0v = r0 < s ? colr[j * s] : 0.f;
+              acc0.x = fmaf(w0v, ij.x, acc0.x);
+              acc0.y = fmaf(w0v, ij.y, acc0.y);
+              acc0.z = fmaf(w0v, ij.z, acc0.z);
+            }
           } else {
-            const float4 pa = sprev[rl + rr];
-            old = make_float4(fmaf(A.x, pa.x, B.x), fmaf(A.y, pa.y, B.y), fmaf(A.z, pa.z, B.z), 0.f);
+#pragma unroll 4
+            for (int j = 0; j < s; ++j) {
+              const float4 ij = sin[rl + j];
+              const float* col = w + j * s;
+              const float w0v = r0 < s ? col[r0] : 0.f;
+              const float w1v = r1 < s ? col[r1] : 0.f;
+              acc0.x = fmaf(w0v, ij.x, acc0.x);
+              acc0.y = fmaf(w0v, ij.y, acc0.y);
+              acc0.z = fmaf(w0v, ij.z, acc0.z);
+              acc1.x = fmaf(w1v, ij.x, acc1.x);
+              acc1.y = fmaf(w1v, ij.y, acc1.y);
+              acc1.z = fmaf(w1v, ij.z, acc1.z);
+            }
           }
-          i_out[p] = make_float4(nx, ny, nz, 0.f);
-          const float dv[3] = {fabsf(nx - old.x), fabsf(ny - old.y), fabsf(nz - old.z)};
-          const float sv[3] = {fabsf(nx), fabsf(ny), fabsf(nz)};
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            if (dv[ch] != dv[ch]) nan_bits |= 1u << ch;
-            if (sv[ch] != sv[ch]) nan_bits |= 8u << ch;
-            dmax[ch] = fmaxf(dmax[ch], dv[ch]);
-            smax[ch] = fmaxf(smax[ch], sv[ch]);
-          }
+          if (r0 < s) epilogue(crow, rl, q0, r0, acc0.x, acc0.y, acc0.z);
+          if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x, acc1.y, acc1.z);
         }
       }
       __syncwarp();
-      if (lane == 0) atomicAdd(&done[st], 1);
+      if (lane == 0) atomicAdd(&done[st], items);
     }
-    for (int off = 16; off; off >>= 1) nan_bits |= __shfl_xor_sync(0xFFFFFFFFu, nan_bits, off);
-    float v[6] = {dmax[0], dmax[1], dmax[2], smax[0], smax[1], smax[2]};
+    uint32_t v[6] = {dmax[0], dmax[1], dmax[2], smax[0], smax[1], smax[2]};
 #pragma unroll
     for (int q = 0; q < 6; ++q)
-      for (int off = 16; off; off >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xFFFFFFFFu, v[q], off));
-    if (lane == 0) {
+      for (int off = 16; off; off >>= 1) v[q] = max(v[q], __shfl_xor_sync(0xFFFFFFFFu, v[q], off));
+    if (lane == 0)
       for (int q = 0; q < 6; ++q) blk[wid][q] = v[q];
-      blk_nan[wid] = nan_bits;
-    }
   }
   __syncthreads();
   if (tid < 6) {
-    float x = 0.f;
-    for (int w2 = 0; w2 < kConsumers; ++w2) x = fmaxf(x, blk[w2][tid]);
-    if (x > 0.f) atomicMax(&red[t * 8 + tid], __float_as_uint(x));
-  }
-  if (tid == 6) {
-    unsigned nb = 0;
-    for (int w2 = 0; w2 < kConsumers; ++w2) nb |= blk_nan[w2];
-    if (nb) atomicOr(&red[t * 8 + 6], nb);
+    uint32_t x = 0u;
+    for (int w2 = 0; w2 < kConsumers; ++w2) x = max(x, blk[w2][tid]);
+    if (x) atomicMax(&red[t * 8 + tid], x);
   }
   if (fused) {
     __syncthreads();  // this CTA's maxima are in

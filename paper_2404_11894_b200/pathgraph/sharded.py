@@ -22,7 +22,7 @@ bit-identical results to the single-GPU path for any shard count:
            arithmetic on the same members as the single-GPU build.
   solve    per iteration (solve.py:78-94) rows whose continuation parent
            lives on another shard write into halo slots, one all-to-all
-           delivers them to the parent's shard, and the 7 residual words are
+           delivers them to the parent's shard, and the 6 residual words are
            max-reduced, so every shard takes the same tol / divergence
            decision.  This is the path's only per-iteration exchange:
            f_cross x 16 B per row instead of an all-gather of I.
@@ -48,8 +48,7 @@ from paper_2404_11894_b200 import _native as N
 from paper_2404_11894_b200.harness.config import RenderConfig
 from paper_2404_11894_b200.scenecore.flatten import pack_scene
 
-_FLOAT_WORDS = 6   # residual maxima per iteration (solve.py:54-61)
-_NAN_WORD = 6      # per-channel NaN flags
+_RESIDUAL_WORDS = 6  # residual maxima per iteration (solve.py:54-61), float bits
 
 
 # --------------------------------------------------------------- collectives
@@ -682,19 +681,15 @@ class ShardedPathGraph:
         N.check(lib.vpg_solve_begin(self.handle, int(iterations), float(tol), stream))
         v = self.views()
         rows = self.n + self.halo.n_halo
-        red_f = _view(v.red, ((iterations + 1) * 8,), "<f4")
+        # the residual maxima are IEEE bit patterns of non-negative floats
+        # (NaN above +inf): an integer max reduces them across the shards
         red_i = _view(v.red, ((iterations + 1) * 8,), "<i4")
-        bit = torch.arange(6, device="cuda", dtype=torch.int32)
         for t in range(iterations):
             N.check(lib.vpg_solve_step(self.handle, t, stream))
             if self.comm.world > 1:
                 i_out = _view(v.ibuf[(t + 1) & 1], (rows, 4), "<f4")
                 self.halo.exchange(i_out)
-                words = red_f[t * 8:t * 8 + _FLOAT_WORDS]
-                self.comm.all_reduce_max_(words)
-                nan = (red_i[t * 8 + _NAN_WORD] >> bit) & 1
-                self.comm.all_reduce_max_(nan)
-                red_i[t * 8 + _NAN_WORD] = (nan << bit).sum().to(torch.int32)
+                self.comm.all_reduce_max_(red_i[t * 8:t * 8 + _RESIDUAL_WORDS])
             N.check(lib.vpg_solve_control(self.handle, t, stream))
         res = np.zeros(max(iterations, 1))
         performed = ctypes.c_int32(0)
