@@ -413,6 +413,14 @@ int vpg_pack_rows(void* packed, int64_t n, int32_t row_bytes, const vpg_codec_fi
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream);
 
+/* reconstruct_path_estimate (transport/reconstruct.py:52-72) for `count`
+ * paths: path_ids (device int64, or NULL for paths 0..count-1); outputs
+ * estimate (count,3) float64 = d_cam + the backward walk over the path's
+ * records, and max_ipt_diff (count,) float64 = max |stored i_pt - recomputed
+ * incoming| (device). */
+int vpg_reconstruct_paths(const vpg_records* rec, const vpg_paths* paths, const int64_t* path_ids,
+                          int64_t count, double* estimate, double* max_ipt_diff, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -633,4 +633,11 @@ int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_p
   return guarded([&] { vpg::extra_direct(*scene, *rec, *paths, seed, n_extra, as_stream(stream)); });
 }
 
+int vpg_reconstruct_paths(const vpg_records* rec, const vpg_paths* paths, const int64_t* path_ids,
+                          int64_t count, double* estimate, double* max_ipt_diff, void* stream) {
+  return guarded([&] {
+    vpg::reconstruct_paths(*rec, *paths, path_ids, count, estimate, max_ipt_diff, as_stream(stream));
+  });
+}
+
 }  // extern "C"

@@ -48,6 +48,8 @@ void split_groups_device(vpg_pcg64* state, int32_t* d_ids, const double* d_x, co
 void choice_device(vpg_pcg64* state, int64_t n, int64_t m, int32_t* d_out, cudaStream_t s);
 void codec_rows(bool unpack, uint8_t* packed, int64_t n, int32_t row_bytes,
                 const vpg_codec_field* fields, int32_t n_fields, cudaStream_t s);
+void reconstruct_paths(const vpg_records& rec, const vpg_paths& pth, const int64_t* ids,
+                       int64_t count, double* est, double* diff, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
                   int n_extra, cudaStream_t s);
 }  // namespace vpg

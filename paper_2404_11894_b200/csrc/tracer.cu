@@ -1071,6 +1071,68 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
              kGatherWarps * 32, 0, s, scratch, n, slot_of, out);
 }
 
+// reconstruct_path_estimate (transport/reconstruct.py:52-72): a path's PT
+// estimate rebuilt from its records alone, walking them backward with the
+// recorded pdfs, weights and raw radiances; the stored i_pt is only
+// cross-checked (max |i_pt - recomputed incoming|).  Thread per path, fp64,
+// the reference's operation order (this file is built with -fmad=false).
+namespace {
+__device__ __forceinline__ double rec_strategy(const vpg_records& R, int64_t row, double dx,
+                                               double dy, double dz) {
+  // phase_pdf_at / the scalar part of scatter_kernel (reconstruct.py:18-36)
+  if (R.kind[row] == 0) {
+    const double ax = -R.omega_out[row * 3], ay = -R.omega_out[row * 3 + 1],
+                 az = -R.omega_out[row * 3 + 2];
+    return hg_pdf(ax * dx + ay * dy + az * dz, R.g[row]);
+  }
+  const double c = R.normal[row * 3] * dx + R.normal[row * 3 + 1] * dy + R.normal[row * 3 + 2] * dz;
+  return (c > 0.0 ? c : 0.0) * (1.0 / 3.14159265358979323846);
+}
+
+__global__ void k_reconstruct(const vpg_records R, const vpg_paths P, const int64_t* __restrict__ ids,
+                              int64_t count, double* __restrict__ est, double* __restrict__ diff) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = ids ? ids[i] : i;
+    const int64_t start = P.rec_start[p];
+    const int32_t cnt = P.rec_count[p];
+    double inc[3] = {0.0, 0.0, 0.0};
+    double worst = 0.0;
+    for (int k = cnt - 1; k >= 0; --k) {
+      const int64_t row = start + k;
+      for (int c = 0; c < 3; ++c) worst = fmax(worst, fabs(R.i_pt[row * 3 + c] - inc[c]));
+      // local_direct_estimate (reconstruct.py:39-49)
+      const double ex = R.emit_dir[row * 3], ey = R.emit_dir[row * 3 + 1], ez = R.emit_dir[row * 3 + 2];
+      const double px = R.phase_dir[row * 3], py = R.phase_dir[row * 3 + 1], pz = R.phase_dir[row * 3 + 2];
+      const double rho_e = rec_strategy(R, row, ex, ey, ez);
+      const double rho_p = rec_strategy(R, row, px, py, pz);
+      const double den_e = R.emit_delta[row] ? 0.0 : R.pdf_emit[row] + rho_e;
+      const double den_p = R.pdf_phase[row] + R.pdf_emit_at_phase[row];
+      const double pdf_p = R.pdf_phase[row];
+      for (int c = 0; c < 3; ++c) {
+        const double co = R.coeff[row * 3 + c];
+        const double f_e = co * rho_e, f_p = co * rho_p;
+        const double nee = R.emit_delta[row] ? f_e * R.d_emit[row * 3 + c]
+                                             : f_e * R.d_emit[row * 3 + c] / den_e;
+        const double phase = f_p * R.d_phase[row * 3 + c] / den_p;
+        const double dbar = nee + phase;
+        const double ratio = pdf_p > 0.0 ? f_p / pdf_p : 0.0;
+        inc[c] = R.w_cont[row * 3 + c] * (dbar + ratio * inc[c]);
+      }
+    }
+    for (int c = 0; c < 3; ++c) est[i * 3 + c] = P.d_cam[p * 3 + c] + inc[c];
+    diff[i] = worst;
+  }
+}
+}  // namespace
+
+void reconstruct_paths(const vpg_records& rec, const vpg_paths& pth, const int64_t* ids,
+                       int64_t count, double* est, double* diff, cudaStream_t s) {
+  VPG_REQUIRE(count >= 0, VPG_EINVAL, "negative path count");
+  if (!count) return;
+  VPG_LAUNCH(k_reconstruct, grid_for(count, 128), 128, 0, s, rec, pth, ids, count, est, diff);
+}
+
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
                   int n_extra, cudaStream_t s) {
   check_scene(sc);

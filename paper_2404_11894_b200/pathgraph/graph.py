@@ -17,7 +17,7 @@ import numpy as np
 
 from paper_2404_11894_b200 import _native as N
 from paper_2404_11894_b200.pathgraph.clustering import Cluster
-from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
+from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput, as_trace
 
 
 # the record fields the build and the solve read on the device: never depth;
@@ -194,11 +194,16 @@ def build_graph(out: TraceOutput, cluster_size: int, seed: int = 0, timings: boo
     """
     if cluster_size < 1:
         raise ValueError("cluster size K must be >= 1")
+    foreign = not isinstance(out, TraceOutput)  # e.g. the reference's own TraceOutput
+    trace = as_trace(out)
     rng = np.random.default_rng(np.random.SeedSequence([seed & 0xFFFFFFFF, 0xC1A5]))
     flags = N.VPG_BUILD_TIMINGS if timings else 0
-    native = NativeGraph.build(out.records, cluster_size, rng, flags)
-    graph = PathGraph(out.records, out.paths, out.width, out.height, out.spp, native=native)
-    out.records._set_cluster_provider(lambda: native.export_clusters()[0])
+    native = NativeGraph.build(trace.records, cluster_size, rng, flags)
+    graph = PathGraph(trace.records, trace.paths, trace.width, trace.height, trace.spp,
+                      native=native)
+    trace.records._set_cluster_provider(lambda: native.export_clusters()[0])
+    if foreign:
+        out.records.cluster_id = trace.records.cluster_id  # graph.py:62 mutates the input
     return graph
 
 

@@ -100,7 +100,12 @@ def pack_scene(scene: Scene) -> PackedScene:
                 st.em_pos[j][a] = float(d[a])
         else:
             st.em_type[j] = 1
-            q = scene.area_emitter_surface(j).params
+            # the emitter's quad (types.py area_emitter_surface), found by
+            # field access so any scene object with the reference's fields works
+            q = next((sf.params for sf in scene.surfaces
+                      if sf.material == "emitter" and sf.emitter_index == j), None)
+            if q is None:
+                raise SceneError(f"area emitter {j} has no surface")
             for a in range(9):
                 st.em_quad[j][a] = float(q[a])
             u, v = np.asarray(q[3:6], dtype=np.float64), np.asarray(q[6:9], dtype=np.float64)
@@ -120,7 +125,10 @@ def pack_scene(scene: Scene) -> PackedScene:
         st.med_g[k] = float(m.phase_g)
         for a in range(6):
             st.med_bounds[k][a] = float(m.bounds[a])
-        st.med_majorant[k] = float(m.majorant)
+        # Medium.majorant (types.py:95-101) from the fields
+        top = float(max(m.sigma_t))
+        st.med_majorant[k] = top if m.kind == "homogeneous" else \
+            float(np.max(m.density)) * float(m.density_scale) * top
         st.med_scale[k] = float(m.density_scale)
         if m.kind == "grid":
             vol = np.ascontiguousarray(m.density, dtype=np.float32)

@@ -369,6 +369,43 @@ class TraceOutput:
         self._image = value
 
 
+# ------------------------------------------------ the reference's own objects
+def as_records(obj) -> RecordSoA:
+    """A RecordSoA for `obj`: ours as is, or any object carrying the
+    reference's record fields as arrays (volpg.transport.records.RecordSoA,
+    records.py:75-126) -- copied into a host RecordSoA."""
+    if isinstance(obj, RecordSoA):
+        return obj
+    try:
+        return RecordSoA(**{name: np.asarray(getattr(obj, name)) for name, _, _ in N.RECORD_FIELDS})
+    except AttributeError as exc:
+        raise TypeError(f"not a record set: {type(obj).__name__} lacks {exc}") from None
+
+
+def as_paths(obj) -> PathSoA:
+    """PathSoA for ours or the reference's path table (records.py:143-176)."""
+    if isinstance(obj, PathSoA):
+        return obj
+    try:
+        return PathSoA(**{name: np.asarray(getattr(obj, name)) for name, _, _ in N.PATH_FIELDS})
+    except AttributeError as exc:
+        raise TypeError(f"not a path table: {type(obj).__name__} lacks {exc}") from None
+
+
+def as_trace(obj) -> TraceOutput:
+    """TraceOutput for ours or the reference's (records.py:179-188): a
+    volpg TraceOutput is wrapped (its arrays copied once to host SoAs); the
+    caller writes results back where the reference mutates it (build_graph
+    sets records.cluster_id, graph.py:62)."""
+    if isinstance(obj, TraceOutput):
+        return obj
+    for a in ("records", "paths", "width", "height", "spp"):
+        if not hasattr(obj, a):
+            raise TypeError(f"not a trace: {type(obj).__name__} has no {a!r}")
+    return TraceOutput(getattr(obj, "image", None), as_records(obj.records), as_paths(obj.paths),
+                       obj.width, obj.height, obj.spp)
+
+
 def splat_pt_image(paths: PathSoA, width: int, height: int, spp: int) -> np.ndarray:
     """Per-pixel mean of the PT estimates in sample order, on the device."""
     torch = N.require_cuda()
