@@ -1,7 +1,8 @@
 """Command line over the device pipeline (the reference declares
 `volpg render|mse|convergence|iterations`, pyproject.toml:20,
 but ships no cli module).  Scenes are the built-in configurations (C1-C5 of
-BASELINE.json, `mixed`); images are written as PFM.
+BASELINE.json, `mixed`, and the SPEC.md acceptance scenes `fogbox` and
+`gridpuff`); images are written as PFM.
 
     python -m paper_2404_11894_b200.harness.cli render --scene C1 --mode pg --spp 4 --out pg.pfm
     python -m paper_2404_11894_b200.harness.cli mse pg.pfm ref.pfm
@@ -24,8 +25,12 @@ def _scene(name: str, res):
 
     if name == "mixed":
         return S.scene_mixed(res or (12, 12))
+    if name == "fogbox":
+        return S.scene_fogbox(res or (128, 128))
+    if name == "gridpuff":
+        return S.scene_gridpuff(res or (256, 256))
     if name not in S.WORKLOADS:
-        raise ValueError(f"unknown scene {name!r} (C1-C5 or mixed)")
+        raise ValueError(f"unknown scene {name!r} (C1-C5, mixed, fogbox or gridpuff)")
     return S.WORKLOADS[name].scene(res)
 
 

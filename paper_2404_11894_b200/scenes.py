@@ -109,6 +109,31 @@ def scene_c3(res=(512, 512)) -> Scene:
     return Scene(_camera(32.0, res), [med], [quad], [light])
 
 
+def scene_fogbox(res=(128, 128), half: float = 0.5) -> Scene:
+    """SPEC.md acceptance scene FogBox: homogeneous cube, sigma_s 1.8,
+    sigma_a 0.2, HG g = 0.5, one area light.  The SPEC leaves the cube's size
+    open: the default is the unit cube (optical depth 2 across); at half = 1
+    (optical depth 4) the reference's own fixed-point iteration diverges from
+    128x128 at 1 spp (tests/test_gpu_acceptance.py checks the device diverges
+    with it)."""
+    quad, light = _area_light()
+    h = float(half)
+    med = Medium("homogeneous", (2.0, 2.0, 2.0), (1.8, 1.8, 1.8), 0.5, (-h, -h, -h, h, h, h),
+                 name="fogbox")
+    return Scene(_camera(32.0, res), [med], [quad], [light])
+
+
+def scene_gridpuff(res=(256, 256), grid_n: int = 32, half: float = 0.5) -> Scene:
+    """SPEC.md acceptance scene GridPuff: FogBox as a constant-density grid
+    (delta / ratio tracking instead of the closed forms)."""
+    quad, light = _area_light()
+    dens = np.ones((grid_n, grid_n, grid_n), dtype=np.float32)
+    h = float(half)
+    med = Medium("grid", (2.0, 2.0, 2.0), (1.8, 1.8, 1.8), 0.5, (-h, -h, -h, h, h, h),
+                 name="gridpuff", density=dens)
+    return Scene(_camera(32.0, res), [med], [quad], [light])
+
+
 DOME = [  # (origin, edge_u, edge_v) of the five inward-facing sky quads (SURVEY §8d)
     ((-6.0, 6.0, -6.0), (12.0, 0.0, 0.0), (0.0, 0.0, 12.0)),
     ((-6.0, -6.0, 6.0), (0.0, 12.0, 0.0), (12.0, 0.0, 0.0)),
