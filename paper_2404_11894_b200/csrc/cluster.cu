@@ -1165,7 +1165,15 @@ __global__ void k_copy_when_ready(const uint32_t* src, const int32_t* ready,
     }
     __syncthreads();
     const int64_t b = c * kReadyChunk, e = min(words, b + kReadyChunk);
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    // 16-byte relaxed loads (chunk starts are 16-byte aligned), a word tail
+    const int64_t e4 = b + ((e - b) & ~int64_t(3));
+    for (int64_t i = b + 4 * int64_t(threadIdx.x); i < e4; i += 4 * int64_t(blockDim.x)) {
+      uint4 w;
+      asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(src + i) : "memory");
+      *reinterpret_cast<uint4*>(dst + i) = w;
+    }
+    for (int64_t i = e4 + threadIdx.x; i < e; i += blockDim.x) {
       uint32_t w;
       asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(w) : "l"(src + i) : "memory");
       dst[i] = w;
