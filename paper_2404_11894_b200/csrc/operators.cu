@@ -374,32 +374,40 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
       const int items = 1;
       if (mk.w == 0) {
         // W recomputed with w_recomputed's operations (so the same W the
-        // aggregate evaluated), accumulated in column order; lane = row
-        // (two rows per lane for clusters of more than 32)
+        // aggregate evaluated).  Rows go to lanes in passes chosen to keep
+        // the lanes busy: 64 rows as two per lane, 17..32 rows one per lane,
+        // and up to 16 rows as column slices -- P = 32 / pow2(rows) lanes per
+        // row, each summing every P-th column, combined by xor shuffles.
         const int rl = mk.x;
         const int s = mk.z;
         const int64_t q0 = int64_t(cq0) + rl;
         const float4* crow = srow + 4 * rl;
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int rc = 0; rc < s; rc += 64) {
-          const int r0 = rc + lane, r1 = rc + lane + 32;
-          float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
-          const float4 ha0 = r0 < s ? crow[4 * r0 + 2] : z4;
-          const float n0 = hg_num_f32(ha0.w);
-          if (s - rc <= 32) {
+        // one row (ha, num n) over columns j0, j0 + dj, ... < s
+        auto one_row = [&](const float4 ha, float n, int j0, int dj) {
+          float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll 4
-            for (int j = 0; j < s; ++j) {
-              const float4 dc = crow[4 * j + 3];
-              const float iw = crow[4 * j + 1].w;
-              const float4 ij = sin[rl + j];
-              const float wv = (n0 * hg3(ha0, dc)) * iw;
-              acc0.x = fmaf(wv, ij.x, acc0.x);
-              acc0.y = fmaf(wv, ij.y, acc0.y);
-              acc0.z = fmaf(wv, ij.z, acc0.z);
-            }
-          } else {
+          for (int j = j0; j < s; j += dj) {
+            const float4 dc = crow[4 * j + 3];
+            const float iw = crow[4 * j + 1].w;
+            const float4 ij = sin[rl + j];
+            const float wv = (n * hg3(ha, dc)) * iw;
+            acc.x = fmaf(wv, ij.x, acc.x);
+            acc.y = fmaf(wv, ij.y, acc.y);
+            acc.z = fmaf(wv, ij.z, acc.z);
+          }
+          return acc;
+        };
+        int rc = 0;
+        while (rc < s) {
+          const int rem = s - rc;
+          if (rem > 48) {
+            // two rows per lane, the column data loaded once for both
+            const int r0 = rc + lane, r1 = rc + lane + 32;
+            const float4 ha0 = crow[4 * r0 + 2];
             const float4 ha1 = r1 < s ? crow[4 * r1 + 2] : z4;
-            const float n1 = hg_num_f32(ha1.w);
+            const float n0 = hg_num_f32(ha0.w), n1 = hg_num_f32(ha1.w);
+            float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
 #pragma unroll 2
             for (int j = 0; j < s; ++j) {
               const float4 dc = crow[4 * j + 3];
@@ -413,9 +421,34 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
               acc1.y = fmaf(w1v, ij.y, acc1.y);
               acc1.z = fmaf(w1v, ij.z, acc1.z);
             }
+            epilogue(crow, rl, q0, r0, acc0.x, acc0.y, acc0.z);
+            if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x, acc1.y, acc1.z);
+            rc += 64;
+          } else if (rem > 16) {
+            // one row per lane (32 rows; 17..32 at the end)
+            const int r = rc + lane;
+            const bool on = lane < rem;
+            const float4 ha = on ? crow[4 * r + 2] : z4;
+            const float3 acc = one_row(ha, hg_num_f32(ha.w), 0, 1);
+            if (on) epilogue(crow, rl, q0, r, acc.x, acc.y, acc.z);
+            rc += rem > 32 ? 32 : rem;
+          } else {
+            // <= 16 rows: P lanes per row on every P-th column
+            const int w2 = rem <= 1 ? 1 : (rem <= 2 ? 2 : (rem <= 4 ? 4 : (rem <= 8 ? 8 : 16)));
+            const int P = 32 / w2;
+            const int rr = lane & (w2 - 1), h = lane / w2;
+            const bool on = rr < rem;
+            const int r = rc + rr;
+            const float4 ha = on ? crow[4 * r + 2] : z4;
+            float3 acc = on ? one_row(ha, hg_num_f32(ha.w), h, P) : make_float3(0.f, 0.f, 0.f);
+            for (int off = w2; off < 32; off <<= 1) {
+              acc.x += __shfl_xor_sync(0xFFFFFFFFu, acc.x, off);
+              acc.y += __shfl_xor_sync(0xFFFFFFFFu, acc.y, off);
+              acc.z += __shfl_xor_sync(0xFFFFFFFFu, acc.z, off);
+            }
+            if (on && h == 0) epilogue(crow, rl, q0, r, acc.x, acc.y, acc.z);
+            rc += rem;
           }
-          if (r0 < s) epilogue(crow, rl, q0, r0, acc0.x, acc0.y, acc0.z);
-          if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x, acc1.y, acc1.z);
         }
       } else {
         // stored W block (Lambertian / |g| > 0.95 clusters), lane = row
