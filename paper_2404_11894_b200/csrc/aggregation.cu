@@ -403,6 +403,120 @@ __device__ __forceinline__ void aggregate_cluster(
   }
 }
 
+// fp32 HG clusters (volume members, |g| <= kG32) with the member data packed
+// as float4 rows so every pair costs two shared-memory loads per density:
+//   A4[l] = {anchor, g}, NM[l] = num(g), P4[j] = {phase_dir, 1 - |d|^2},
+//   E4[j] = {emit_dir, 1 - |e|^2}, WE4[j] = {d_emit / phat_dir_emit, 1/phat_ind},
+//   WP4[j] = {d_phase / phat_dir_phase, 0}.
+// The densities are hg_pdf32 with the g^2 (1 - |a|^2) term at 0 (hg32): the
+// same W the solve recomputes (operators.cu w_recomputed).
+__device__ __forceinline__ float hg32(const float4 a, float num, const float4 d) {
+  const float ux = fmaf(-a.w, a.x, d.x), uy = fmaf(-a.w, a.y, d.y), uz = fmaf(-a.w, a.z, d.z);
+  const float r = rsqrt_ftz(fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, d.w))));
+  return num * (r * r * r);
+}
+
+__device__ __forceinline__ void aggregate_v32(
+    const Member* __restrict__ mem, int32_t q0, int s, int64_t n, const float4* __restrict__ A4,
+    const float* __restrict__ NM, const float4* __restrict__ P4, const float4* __restrict__ E4,
+    float4* __restrict__ WE4, float4* __restrict__ WP4, double* __restrict__ phat,
+    float4* __restrict__ dbar_o, float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
+    float4* __restrict__ i0_o) {
+  const int tid = threadIdx.x;
+  const double ks = double(s);
+  // pass 1: columns (P threads each, fixed combination order), p-hat, weights
+  const int P = s <= 32 ? 4 : 2;
+  const int slice = (s + P - 1) / P;
+  for (int base = 0; base < P * s; base += blockDim.x) {
+    const int t = base + tid;
+    const bool active = t < P * s;
+    const int j = t / P, h = t % P;
+    float sp = 0.f, se = 0.f;
+    if (active) {
+      const int l0 = h * slice, l1 = min(s, l0 + slice);
+      const float4 pj = P4[j], ej = E4[j];
+      for (int l = l0; l < l1; ++l) {
+        const float4 a = A4[l];
+        const float num = NM[l];
+        sp += hg32(a, num, pj);
+        se += hg32(a, num, ej);
+      }
+    }
+    sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 1);
+    se += __shfl_xor_sync(0xFFFFFFFFu, se, 1);
+    if (P == 4) {
+      sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 2);
+      se += __shfl_xor_sync(0xFFFFFFFFu, se, 2);
+    }
+    if (active && h == 0) {
+      const Member& mb = mem[q0 + j];
+      const double p_ind = double(sp);
+      const double p_dp = __dadd_rn(p_ind, __dmul_rn(ks, mb.pdf_eap));
+      const double p_de = (mb.flags & 1u) ? ks : __dadd_rn(double(se), __dmul_rn(ks, mb.pdf_e));
+      const int64_t q = q0 + j;
+      phat[q] = p_ind;
+      phat[n + q] = p_dp;
+      phat[2 * n + q] = p_de;
+      const bool inc_p = isfinite(p_ind) && p_ind > 0.0;
+      const bool inc_e = isfinite(p_de) && p_de > 0.0;
+      const bool ok_dp = inc_p && isfinite(p_dp) && p_dp > 0.0;
+      const double ie = inc_e ? __ddiv_rn(1.0, p_de) : 0.0;
+      const double ip = ok_dp ? __ddiv_rn(1.0, p_dp) : 0.0;
+      const double iw = inc_p ? __ddiv_rn(1.0, p_ind) : 0.0;
+      WE4[j] = make_float4(float(double(mb.de[0]) * ie), float(double(mb.de[1]) * ie),
+                           float(double(mb.de[2]) * ie), float(iw));
+      WP4[j] = make_float4(float(double(mb.dp[0]) * ip), float(double(mb.dp[1]) * ip),
+                           float(double(mb.dp[2]) * ip), 0.f);
+    }
+  }
+  __syncthreads();
+  // pass 2: rows -- D-bar and the solve's row data (no W block: recomputed)
+  const int P2 = s <= 32 ? 4 : 2;
+  const int slice2 = (s + P2 - 1) / P2;
+  for (int base = 0; base < P2 * s; base += blockDim.x) {
+    const int t = base + tid;
+    const bool active = t < P2 * s;
+    const int r = t / P2, h = t % P2;
+    float dx = 0.f, dy = 0.f, dz = 0.f;
+    if (active) {
+      const int j0 = h * slice2, j1 = min(s, j0 + slice2);
+      const float4 a = A4[r];
+      const float num = NM[r];
+      for (int j = j0; j < j1; ++j) {
+        const float pa = hg32(a, num, P4[j]);
+        const float pb = hg32(a, num, E4[j]);
+        const float4 we = WE4[j], wp = WP4[j];
+        dx += pb * we.x + pa * wp.x;
+        dy += pb * we.y + pa * wp.y;
+        dz += pb * we.z + pa * wp.z;
+      }
+    }
+    dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 1);
+    dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 1);
+    dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 1);
+    if (P2 == 4) {
+      dx += __shfl_xor_sync(0xFFFFFFFFu, dx, 2);
+      dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
+      dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 2);
+    }
+    if (active && h == 0) {
+      const Member& mb = mem[q0 + r];
+      const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
+      const double bx = kx * double(dx), by = ky * double(dy), bz = kz * double(dz);
+      const double wx = mb.wc[0], wy = mb.wc[1], wz = mb.wc[2];
+      const int64_t q = q0 + r;
+      dbar_o[q] = f4(bx, by, bz);
+      coeff_o[q] = f4(kx, ky, kz);
+      rows_o[4 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
+                                  __int_as_float(row_link(mb.parent, mb.flags & 2u)));
+      rows_o[4 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz), WE4[r].w);
+      rows_o[4 * q + 2] = A4[r];
+      rows_o[4 * q + 3] = P4[r];
+      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kAggThreads, 10)
 k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int32_t* __restrict__ cl_size, const int64_t* __restrict__ w_off,
@@ -415,6 +529,13 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
   float* g32 = reinterpret_cast<float*>(geo);
   double* wts = geo + 12 * S + (S + 1) / 2;
+  // fp32 HG clusters: packed float4 member data in the same space
+  float4* A4 = reinterpret_cast<float4*>(geo);
+  float4* P4 = A4 + S;
+  float4* E4 = P4 + S;
+  float* NM = reinterpret_cast<float*>(E4 + S);  // 52 S bytes <= the 96 S of geo
+  float4* WE4 = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(wts) + 15) & ~uintptr_t(15));
+  float4* WP4 = WE4 + S;  // 32 S + 15 bytes <= the 56 S of wts
   const int tid = threadIdx.x;
 
   const int64_t k_end = range[1];
@@ -449,26 +570,15 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
       const double g2 = __dmul_rn(g, g);
       const double num = __dmul_rn(kInv4Pi, __dsub_rn(1.0, g2));
       if (mode == kVol32) {
-        g32[l] = float(mb.ax);
-        g32[S + l] = float(mb.ay);
-        g32[2 * S + l] = float(mb.az);
-        g32[3 * S + l] = float(mb.px);
-        g32[4 * S + l] = float(mb.py);
-        g32[5 * S + l] = float(mb.pz);
-        g32[6 * S + l] = float(mb.ex);
-        g32[7 * S + l] = float(mb.ey);
-        g32[8 * S + l] = float(mb.ez);
-        g32[9 * S + l] = float(g);
-        g32[10 * S + l] = hg_num_f32(float(g));  // the solve's own fp32 normalisation
-        const double na = fma(mb.ax, mb.ax, fma(mb.ay, mb.ay, mb.az * mb.az));
+        // g^2 (1 - |a|^2) is ~1e-16 for the unit anchors: left out here and in
+        // the solve's recomputed blocks, so both evaluate the same W; num is
+        // the solve's own fp32 normalisation
         const double np = fma(mb.px, mb.px, fma(mb.py, mb.py, mb.pz * mb.pz));
         const double ne = fma(mb.ex, mb.ex, fma(mb.ey, mb.ey, mb.ez * mb.ez));
-        // g^2 (1 - |a|^2) is ~1e-16 for the unit anchors: left out here and in
-        // the solve's recomputed blocks, so both evaluate the same W
-        (void)na;
-        g32[11 * S + l] = 0.f;
-        g32[12 * S + l] = float(1.0 - np);
-        g32[13 * S + l] = float(1.0 - ne);
+        A4[l] = make_float4(float(mb.ax), float(mb.ay), float(mb.az), float(g));
+        P4[l] = make_float4(float(mb.px), float(mb.py), float(mb.pz), float(1.0 - np));
+        E4[l] = make_float4(float(mb.ex), float(mb.ey), float(mb.ez), float(1.0 - ne));
+        NM[l] = hg_num_f32(float(g));
       } else {
         geo[l] = mb.ax;
         geo[S + l] = mb.ay;
@@ -487,8 +597,7 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
     }
     __syncthreads();
     if (mode == kVol32)
-      aggregate_cluster<kVol32>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
-                                rows_o, i0_o);
+      aggregate_v32(mem, q0, s, n, A4, NM, P4, E4, WE4, WP4, phat, dbar_o, coeff_o, rows_o, i0_o);
     else if (mode == kVol64)
       aggregate_cluster<kVol64>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
                                 rows_o, i0_o);
