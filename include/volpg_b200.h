@@ -413,6 +413,12 @@ int vpg_pack_rows(void* packed, int64_t n, int32_t row_bytes, const vpg_codec_fi
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream);
 
+/* vpg_extra_direct over a slice of the frame's path table whose first row is
+ * path `path_begin` of the frame (a shard's pixel range): the per-path
+ * streams are keyed by the frame's path index (kernels.py:532-536). */
+int vpg_extra_direct_range(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
+                           int64_t path_begin, int64_t seed, int32_t n_extra, void* stream);
+
 /* reconstruct_path_estimate (transport/reconstruct.py:52-72) for `count`
  * paths: path_ids (device int64, or NULL for paths 0..count-1); outputs
  * estimate (count,3) float64 = d_cam + the backward walk over the path's

@@ -178,6 +178,8 @@ _SIGNATURES = {
     "vpg_solve_end": (C.c_int, [c_p, c_p, C.POINTER(c_i32), c_p]),
     "vpg_splat_arrays": (C.c_int, [C.POINTER(Paths), c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p,
                                    c_p]),
+    "vpg_extra_direct_range": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(Records),
+                                         C.POINTER(Paths), c_i64, c_i64, c_i32, c_p]),
     "vpg_reconstruct_paths": (C.c_int, [C.POINTER(Records), C.POINTER(Paths), c_p, c_i64, c_p, c_p,
                                         c_p]),
 }

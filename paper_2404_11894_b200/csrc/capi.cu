@@ -633,6 +633,13 @@ int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_p
   return guarded([&] { vpg::extra_direct(*scene, *rec, *paths, seed, n_extra, as_stream(stream)); });
 }
 
+int vpg_extra_direct_range(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
+                           int64_t path_begin, int64_t seed, int32_t n_extra, void* stream) {
+  return guarded([&] {
+    vpg::extra_direct(*scene, *rec, *paths, seed, n_extra, as_stream(stream), path_begin);
+  });
+}
+
 int vpg_reconstruct_paths(const vpg_records* rec, const vpg_paths* paths, const int64_t* path_ids,
                           int64_t count, double* estimate, double* max_ipt_diff, void* stream) {
   return guarded([&] {

@@ -51,5 +51,5 @@ void codec_rows(bool unpack, uint8_t* packed, int64_t n, int32_t row_bytes,
 void reconstruct_paths(const vpg_records& rec, const vpg_paths& pth, const int64_t* ids,
                        int64_t count, double* est, double* diff, cudaStream_t s);
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
-                  int n_extra, cudaStream_t s);
+                  int n_extra, cudaStream_t s, int64_t path_begin = 0);
 }  // namespace vpg

@@ -983,8 +983,8 @@ __global__ void __launch_bounds__(128) k_trace_image(const vpg_scene sc, const v
 
 // extra_direct_kernel (kernels.py:499-553)
 __global__ void __launch_bounds__(128) k_extra_direct(const vpg_scene sc, const vpg_records rec,
-                                                      const vpg_paths pth, int64_t seed,
-                                                      int n_extra) {
+                                                      const vpg_paths pth, int64_t path_begin,
+                                                      int64_t seed, int n_extra) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pth.n;
        p += int64_t(gridDim.x) * blockDim.x) {
     if (pth.rec_count[p] == 0) {
@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(128) k_extra_direct(const vpg_scene sc, const 
     const double g = rec.g[r0];
     const bool volume = rec.kind[r0] == 0;
     double acc[3] = {pth.direct0_nee[p * 3], pth.direct0_nee[p * 3 + 1], pth.direct0_nee[p * 3 + 2]};
-    Rng rng = make_stream(seed, p, kSaltExtra);
+    Rng rng = make_stream(seed, path_begin + p, kSaltExtra);  // the frame's path index
     for (int i = 0; i < n_extra; ++i) {
       const EmitterSample es = sample_emitter(sc, v, rng);
       const double rho_e = volume ? hg_pdf(a.x * es.w.x + a.y * es.w.y + a.z * es.w.z, g)
@@ -1134,10 +1134,11 @@ void reconstruct_paths(const vpg_records& rec, const vpg_paths& pth, const int64
 }
 
 void extra_direct(const vpg_scene& sc, const vpg_records& rec, const vpg_paths& pth, int64_t seed,
-                  int n_extra, cudaStream_t s) {
+                  int n_extra, cudaStream_t s, int64_t path_begin) {
   check_scene(sc);
   VPG_REQUIRE(n_extra >= 0, VPG_EINVAL, "n_extra must be >= 0");
-  VPG_LAUNCH(k_extra_direct, trace_grid(pth.n), 128, 0, s, sc, rec, pth, seed, n_extra);
+  VPG_REQUIRE(path_begin >= 0, VPG_EINVAL, "path_begin must be >= 0");
+  VPG_LAUNCH(k_extra_direct, trace_grid(pth.n), 128, 0, s, sc, rec, pth, path_begin, seed, n_extra);
 }
 
 }  // namespace vpg

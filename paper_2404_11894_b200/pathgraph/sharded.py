@@ -118,6 +118,40 @@ class ShardComm:
         self.dist.all_gather(parts, v, group=self.group)
         return torch.stack(parts).cpu().numpy()
 
+    def exclusive_scan(self, v):
+        """(sum of v over the shards before this one, sum over all shards) for
+        an integer vector of equal length on every shard.  Shards own
+        contiguous blocks of the vector: one all-to-all sends each block to its
+        owner, which scans it across the shards and returns every shard its
+        prefix and the total (3 m words moved per shard instead of the
+        world * m of an all-gather)."""
+        import torch
+
+        m = int(v.shape[0])
+        if self.world == 1:
+            return torch.zeros_like(v), v.clone()
+        if self.world == 2:  # the all-gather is already as small
+            rows = self.all_gather_rows(v.reshape(1, -1), [1, 1])
+            return rows[: self.rank].sum(0), rows.sum(0)
+        w = self.world
+        cuts = [m * k // w for k in range(w + 1)]
+        sizes = [cuts[k + 1] - cuts[k] for k in range(w)]
+        # to owner k: my slice [cuts[k], cuts[k+1])
+        got = self.all_to_all(v, sizes, [sizes[self.rank]] * w)
+        mine = got.reshape(w, sizes[self.rank])
+        total = mine.sum(0)
+        before = torch.cumsum(mine, 0) - mine          # row r: sum over shards < r
+        back = torch.cat([before, total.reshape(1, -1).expand(w, -1)], 1)  # (w, 2 * my size)
+        ret = self.all_to_all(back.reshape(-1), [2 * sizes[self.rank]] * w,
+                              [2 * sz for sz in sizes])
+        pre, tot = [], []
+        at = 0
+        for sz in sizes:
+            pre.append(ret[at:at + sz])
+            tot.append(ret[at + sz:at + 2 * sz])
+            at += 2 * sz
+        return torch.cat(pre), torch.cat(tot)
+
     def all_reduce_max_(self, t):
         """In-place elementwise max over the shards."""
         if self.world == 1:
@@ -352,9 +386,9 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         a64 = assign.to(torch.int64)
         hist = torch.bincount(a64, minlength=m) if my_n else torch.zeros(m, dtype=torch.int64,
                                                                             device=dev)
-        hists = comm.all_gather_rows(hist.reshape(1, -1), [1] * world)  # (world, m)
-        gsize = hists.sum(0)
-        before = hists[:me].sum(0)
+        # group sizes and this shard's offset in every group: an exclusive
+        # scan across the shards (no (world, m) all-gather)
+        before, gsize = comm.exclusive_scan(hist)
         # rank of each row among its group's members (ascending global row)
         srt = torch.argsort(a64, stable=True)
         first = torch.cumsum(hist, 0) - hist
@@ -781,6 +815,7 @@ class ShardedRender:
     graph: ShardedPathGraph
     n_records: int        # this shard's traced records
     n_records_total: int
+    pt_image: np.ndarray = None  # the frame's PT image (render_pg's pt_image)
 
 
 def render_pg_sharded(scene, config: RenderConfig, comm: ShardComm | None = None,
@@ -790,19 +825,83 @@ def render_pg_sharded(scene, config: RenderConfig, comm: ShardComm | None = None
     from paper_2404_11894_b200.transport.tracer import trace_records_device
 
     comm = comm or ShardComm()
-    if config.extra_direct_samples > 0:
-        raise ValueError("extra_direct_samples is not supported on the sharded path")
     packed = pack_scene(scene)
     w, h, spp = packed.width, packed.height, int(config.spp)
     ranges = pixel_ranges(w * h, comm.world)
     p0, p1 = ranges[comm.rank]
     recs, paths, n_rec = trace_records_device(scene, config, ((p0 * spp), (p1 - p0) * spp))
+    rst, pst = _structs(recs, paths, n_rec, (p1 - p0) * spp)
+    if config.extra_direct_samples > 0:
+        # record_extra_direct (pipeline.py:28-29) on this shard's paths, keyed
+        # by the frame's path index
+        N.check(N.lib().vpg_extra_direct_range(
+            ctypes.byref(packed.device()), ctypes.byref(rst), ctypes.byref(pst), p0 * spp,
+            int(np.int64(config.seed)), int(config.extra_direct_samples), N.stream_handle()))
+    else:
+        paths["extra_direct"].copy_(paths["direct0"])
+    if config.dump_records:
+        _dump_frame(comm, config.dump_records, recs, paths, n_rec, w, h, spp)
     g = ShardedPathGraph.build(comm, recs, n_rec, config.cluster_size, seed=config.seed)
     g.pix_ranges = ranges
     sol = g.solve(config.iterations, config.tol)
-    mode = N.DIRECT_AGGREGATED if config.aggregate_direct else N.DIRECT_PT
+    if config.residual_csv and comm.rank == 0:
+        from paper_2404_11894_b200.pathgraph.solve import write_residual_csv
+
+        write_residual_csv(config.residual_csv, sol.residuals)
+    if config.aggregate_direct:
+        mode = N.DIRECT_AGGREGATED
+    else:
+        mode = N.DIRECT_EXTRA if config.extra_direct_samples > 0 else N.DIRECT_PT
     img = g.splat(paths, recs, (p0, p1), w, h, spp, mode)
+    # splat_pt_image (records.py:259-265) of this shard's pixels, gathered
+    import torch
+
+    pt = torch.zeros(((p1 - p0) + 1, 3), dtype=torch.float64, device="cuda")
+    if p1 > p0:
+        N.check(N.lib().vpg_splat_pt(ctypes.byref(pst), p1 - p0, 1, spp, pt.data_ptr(),
+                                     N.stream_handle()))
+    pt_full = comm.all_gather_rows(pt[:p1 - p0], [b - a for a, b in ranges]).reshape(h, w, 3)
     total = int(g.row_off[-1])
     return ShardedRender(image=img.cpu().numpy(), residuals=sol.residuals,
                          iterations=sol.iterations, graph=g if keep_graph else None,
-                         n_records=n_rec, n_records_total=total)
+                         n_records=n_rec, n_records_total=total,
+                         pt_image=pt_full.cpu().numpy())
+
+
+def _structs(recs: dict, paths: dict, n_rec: int, n_paths: int):
+    """vpg_records / vpg_paths views of a shard's device tensors."""
+    rst, pst = N.Records(), N.Paths()
+    rst.n, pst.n = n_rec, n_paths
+    for name, _, _ in N.RECORD_FIELDS:
+        t = recs[name]
+        setattr(rst, name, t.data_ptr() if t.numel() else None)
+    for name, _, _ in N.PATH_FIELDS:
+        t = paths[name]
+        setattr(pst, name, t.data_ptr() if t.numel() else None)
+    return rst, pst
+
+
+def _dump_frame(comm, path, recs, paths, n_rec, w, h, spp):
+    """save_records (records.py:191-217) of the whole frame: the shards'
+    records in shard order are the frame's (contiguous path ranges), path
+    rows re-based to frame record offsets; rank 0 writes the file."""
+    import torch
+
+    from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput, save_records
+
+    counts = comm.all_gather_ints([n_rec])[:, 0]
+    base = int(counts[: comm.rank].sum())
+    n_paths = int(paths["rec_start"].shape[0])
+    pcounts = comm.all_gather_ints([n_paths])[:, 0]
+    rec_all, path_all = {}, {}
+    for name, _, _ in N.RECORD_FIELDS:
+        rec_all[name] = comm.all_gather_rows(recs[name][:n_rec], counts)
+    for name, _, _ in N.PATH_FIELDS:
+        t = paths[name]
+        if name == "rec_start":
+            t = t + base
+        path_all[name] = comm.all_gather_rows(t, pcounts)
+    if comm.rank == 0:
+        out = TraceOutput(None, RecordSoA(**{k: v.cpu().numpy() for k, v in rec_all.items()}),
+                          PathSoA(**{k: v.cpu().numpy() for k, v in path_all.items()}), w, h, spp)
+        save_records(path, out)

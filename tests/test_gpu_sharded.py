@@ -106,3 +106,54 @@ def test_sharded_render_is_bit_identical(cuda, name, world):
     np.testing.assert_array_equal(got["incoming"], ref.result.incoming)
     np.testing.assert_array_equal(got["i_bar"], ref.result.i_bar)
     np.testing.assert_array_equal(got["residuals"], np.array(ref.result.residuals))
+
+
+def _feature_config(tmp, tag):
+    from paper_2404_11894_b200.harness.config import RenderConfig
+
+    return RenderConfig(mode="pg", spp=2, max_depth=16, seed=3, cluster_size=16, iterations=5,
+                        tol=0.0, extra_direct_samples=3,
+                        residual_csv=os.path.join(tmp, f"res_{tag}.csv"),
+                        dump_records=os.path.join(tmp, f"dump_{tag}.vpgr"))
+
+
+def _feature_worker(rank, world, port, tmp):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_11894_b200 import scenes as S
+        from paper_2404_11894_b200.pathgraph.sharded import ShardComm, render_pg_sharded
+
+        out = render_pg_sharded(S.scene_mixed((14, 14)), _feature_config(tmp, "sharded"),
+                                ShardComm(), keep_graph=False)
+        if rank == 0:
+            np.savez(os.path.join(tmp, "sharded.npz"), image=out.image, pt=out.pt_image)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_render_pg_config_features(cuda):
+    """render_pg's config flags on the sharded path (pipeline.py:28-36):
+    extra_direct_samples (streams keyed by the frame's path index),
+    dump_records (the whole frame, rank 0), residual_csv, and the PT image --
+    all equal to the single-GPU render_pg, over 2 shards."""
+    import torch.multiprocessing as mp
+
+    from paper_2404_11894_b200 import scenes as S
+    from paper_2404_11894_b200.pathgraph import render_pg
+
+    with tempfile.TemporaryDirectory() as d:
+        ref = render_pg(S.scene_mixed((14, 14)), _feature_config(d, "single"))
+        mp.spawn(_feature_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        got = np.load(os.path.join(d, "sharded.npz"))
+        np.testing.assert_array_equal(got["image"], ref.image)
+        np.testing.assert_array_equal(got["pt"], ref.pt_image)
+        assert open(os.path.join(d, "res_sharded.csv")).read() == \
+            open(os.path.join(d, "res_single.csv")).read()
+        assert open(os.path.join(d, "dump_sharded.vpgr"), "rb").read() == \
+            open(os.path.join(d, "dump_single.vpgr"), "rb").read()

@@ -205,3 +205,36 @@ def test_group_member_order_beyond_2_pow_23_centers():
     o = group_member_order(gj, gr)
     expect = np.lexsort((gr.numpy(), gj.numpy()))
     assert np.array_equal(o.numpy(), expect)
+
+
+def _scan_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = S.ShardComm()
+        bad = []
+        for m in (1, 5, 1000, 1003):
+            v = torch.as_tensor(np.random.default_rng(rank * 100 + m).integers(0, 50, m))
+            before, total = comm.exclusive_scan(v)
+            parts = [torch.empty_like(v) for _ in range(world)]
+            dist.all_gather(parts, v)
+            want_b = sum(parts[:rank], torch.zeros_like(v))
+            want_t = sum(parts, torch.zeros_like(v))
+            if not (torch.equal(before, want_b) and torch.equal(total, want_t)):
+                bad.append(m)
+        out_q.put((rank, bad))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_exclusive_scan_of_group_sizes(world):
+    """The group-size exchange of the distributed clustering (all-to-all scan
+    instead of an all-gather): every shard gets the sum over the shards
+    before it and the total."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.spawn(_scan_worker, args=(world, _free_port(), q), nprocs=world, join=True)
+    res = [q.get() for _ in range(world)]
+    assert all(not bad for _, bad in res), res
