@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="run the row-partitioned multi-GPU path even at N=1 (default for N>1)")
+    ap.add_argument("--no-sharded-n1", action="store_true",
+                    help="skip the N=1 measurement of the sharded path beside the native one")
     return ap.parse_args()
 
 
@@ -356,6 +358,15 @@ def run_native(args):
            "ms_per_step": e2e_s * 1e3,
            "path": "pathgraph.pipeline.solve_from_records(host pinned records) -> image (host)"}
 
+    # ---- the N > 1 code path (pathgraph/sharded.py) at N = 1 on the same
+    # records, so a scaling curve can be read against either N = 1 point
+    sharded_n1 = None
+    if world == 1 and not args.no_sharded_n1:
+        try:
+            sharded_n1 = sharded_step_n1(trace, cfg, args.steps, args.warmup, stream)
+        except Exception as exc:  # never lose the GPU line over the side measurement
+            sharded_n1 = {"error": repr(exc)}
+
     # ---- CPU baseline (rank 0, N = 1 only): the oracle on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -403,12 +414,49 @@ def run_native(args):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "sharded_n1": sharded_n1,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def sharded_step_n1(trace, cfg, steps, warmup, stream):
+    """The sharded path's build + solve (what bench.py runs for N > 1) on one
+    GPU over the same device records: ms/step and vertices/s."""
+    import torch
+
+    from paper_2404_11894_b200.pathgraph.sharded import ShardComm, ShardedPathGraph
+
+    from paper_2404_11894_b200 import _native as N
+
+    N.release_cached()  # the native build's scratch / pool memory back for torch
+    comm = ShardComm()
+    recs = trace.records.device_tensors()
+    n = trace.records.n
+
+    def step():
+        g = ShardedPathGraph.build(comm, recs, n, cfg.cluster_size, seed=cfg.seed)
+        g.solve(cfg.iterations, 0.0)
+        return g
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"value": n / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "warmup": warmup,
+            "path": "pathgraph/sharded.py ShardedPathGraph.build + solve at world 1 "
+                    "(the code path of the N > 1 runs)"}
 
 
 # ------------------------------------------------------------- sharded arm

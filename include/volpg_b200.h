@@ -413,6 +413,11 @@ int vpg_pack_rows(void* packed, int64_t n, int32_t row_bytes, const vpg_codec_fi
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream);
 
+/* Frees the library's cached device memory (scratch buffers and the free
+ * part of the stream-ordered pool) after a device synchronisation; graphs
+ * alive keep their own buffers. */
+int vpg_release_cached(void);
+
 /* vpg_extra_direct over a slice of the frame's path table whose first row is
  * path `path_begin` of the frame (a shard's pixel range): the per-path
  * streams are keyed by the frame's path index (kernels.py:532-536). */

@@ -178,6 +178,7 @@ _SIGNATURES = {
     "vpg_solve_end": (C.c_int, [c_p, c_p, C.POINTER(c_i32), c_p]),
     "vpg_splat_arrays": (C.c_int, [C.POINTER(Paths), c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p,
                                    c_p]),
+    "vpg_release_cached": (C.c_int, []),
     "vpg_extra_direct_range": (C.c_int, [C.POINTER(SceneStruct), C.POINTER(Records),
                                          C.POINTER(Paths), c_i64, c_i64, c_i32, c_p]),
     "vpg_reconstruct_paths": (C.c_int, [C.POINTER(Records), C.POINTER(Paths), c_p, c_i64, c_p, c_p,
@@ -245,6 +246,15 @@ def profile_timeline():
                                      C.byref(n)))
     keys = names.value.decode().split("\n")
     return [(keys[i], float(st[i]), float(du[i])) for i in range(min(n.value, cap))]
+
+
+def release_cached() -> None:
+    """Free the library's scratch buffers and trimmed pool memory (and torch's
+    cache) so the HBM is available to other allocators."""
+    import torch
+
+    check(lib().vpg_release_cached())
+    torch.cuda.empty_cache()
 
 
 def launch_count() -> int:

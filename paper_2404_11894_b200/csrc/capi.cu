@@ -121,6 +121,23 @@ std::map<std::pair<cudaStream_t, std::string>, std::pair<void*, size_t>>& g_scra
 }
 }  // namespace
 
+// Frees every scratch buffer and returns the stream-ordered pool's free
+// memory to the device (after a device sync): for callers that need the HBM
+// for something else between builds.
+void release_cached() {
+  VPG_CUDA(cudaDeviceSynchronize());
+  {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    for (auto& kv : g_scratch())
+      if (kv.second.first) cudaFree(kv.second.first);
+    g_scratch().clear();
+  }
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    VPG_CUDA(cudaMemPoolTrimTo(pool, 0));
+}
+
 void* scratch(cudaStream_t s, const char* tag, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_scratch_mu);
   auto& e = g_scratch()[{s, std::string(tag)}];
@@ -631,6 +648,10 @@ int vpg_scatter_records(const double* scratch, int64_t n, const int64_t* rec_sta
 int vpg_extra_direct(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,
                      int64_t seed, int32_t n_extra, void* stream) {
   return guarded([&] { vpg::extra_direct(*scene, *rec, *paths, seed, n_extra, as_stream(stream)); });
+}
+
+int vpg_release_cached(void) {
+  return guarded([&] { vpg::release_cached(); });
 }
 
 int vpg_extra_direct_range(const vpg_scene* scene, const vpg_records* rec, const vpg_paths* paths,

@@ -154,6 +154,8 @@ inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
 }
 
 int sm_count();
+// free the scratch buffers and trim the allocation pool (vpg_release_cached)
+void release_cached();
 // cudaFuncAttributeMaxDynamicSharedMemorySize, raised once per (device, kernel)
 void ensure_dynamic_smem(const void* func, size_t bytes);
 
