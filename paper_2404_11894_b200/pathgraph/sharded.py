@@ -636,8 +636,16 @@ class ShardedPathGraph:
         keep = dest_shard == me
         li = torch.nonzero(keep).reshape(-1)
         lr = dest_row[li]
+        # placed in destination order: a gather of the sources (random reads)
+        # and sequential writes instead of a random scatter
+        lr, by_row = torch.sort(lr)
+        li = li[by_row]
+        whole = lr.numel() == n_own  # every owned row is local (one shard)
         for name, _, _ in _payload_columns():
-            own[name][lr] = cols[name][li]
+            if whole:
+                torch.index_select(cols[name], 0, li, out=own[name])
+            else:
+                own[name][lr] = cols[name][li]
         if world > 1:
             ri = torch.nonzero(~keep).reshape(-1)
             ds = dest_shard[ri]
