@@ -30,7 +30,7 @@ namespace {
 constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 constexpr double kInvPi = 1.0 / 3.14159265358979323846;
 constexpr int kAggThreads = 128;
-// HG densities are evaluated all in fp32 for |g| <= kG32 (see hg_pdf32)
+// HG densities are evaluated all in fp32 for |g| <= kG32 (see hg32)
 constexpr float kG32 = 0.95f;
 // dynamic shared memory of k_aggregate for the largest supported cluster (2K = 160)
 constexpr size_t kAggSmemMax = 226 * 1024;
@@ -182,32 +182,15 @@ __device__ __forceinline__ float hg_pdf(double ax, double ay, double az, double 
   return num * (r * r * r);
 }
 
-// HG density with every operand fp32, for |g| <= kG32: den = 1 + g^2 - 2g cos
-// is evaluated as |d - g a|^2 + (1 - |d|^2) + g^2 (1 - |a|^2), an identity
-// for any vectors (the corrections are ~1e-16 for the unit directions the
-// tracer writes and exact for a zero direction), in which nothing cancels:
-// for |g| <= 0.95 the components of d - g a are >= ~0.05 in the forward
-// peak, so the fp32 rounding of the inputs costs < 1e-5 relative on the
-// density (measured ~1e-6), inside the 1e-4 radiance bar.  Larger |g| keeps
-// the fp64 cosine and denominator (hg_pdf above).
-__device__ __forceinline__ float hg_pdf32(float ax, float ay, float az, float g, float num,
-                                          float g2ca, float dx, float dy, float dz, float cd) {
-  const float ux = fmaf(-g, ax, dx), uy = fmaf(-g, ay, dy), uz = fmaf(-g, az, dz);
-  const float den = fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, cd + g2ca)));
-  const float r = rsqrt_ftz(den);
-  return num * (r * r * r);
-}
-
 // Dynamic shared memory for clusters of up to S members:
 //   geo   12*S doubles: ax ay az px py pz ex ey ez | HG num c1 c2 (num also
-//         as fp32 after them); mode kVol32 keeps its fp32 operands in the same
-//         region instead: ax ay az px py pz ex ey ez g num g^2(1-|a|^2)
-//         (1-|p|^2) (1-|e|^2), S floats each
+//         as fp32 after them); the fp32 HG clusters (aggregate_v32) keep
+//         their packed float4 rows in the same region instead
 //   wts    7*S doubles: 1/phat_ind, d_emit/phat_dir_emit (3), d_phase/phat_dir_phase (3)
 //          (volume clusters keep them as fp32 in the same region)
 //   (the pair densities are not stored: pass 1 sums them into p-hat, pass 2
 //   evaluates them again for W and D-bar)
-enum AggMode { kSurface = 0, kVol64 = 1, kVol32 = 2 };
+enum AggMode { kSurface = 0, kVol64 = 1, kVol32 = 2 };  // kVol32: aggregate_v32
 
 template <int kMode>
 __device__ __forceinline__ void aggregate_cluster(
@@ -218,7 +201,6 @@ __device__ __forceinline__ void aggregate_cluster(
   using acc_t = typename std::conditional<kVol, float, double>::type;
   const int tid = threadIdx.x;
   const float* numf = reinterpret_cast<const float*>(geo + 12 * S);  // S floats after geo
-  const float* g32 = reinterpret_cast<const float*>(geo);            // kVol32 operands
   float* wtsf = reinterpret_cast<float*>(wts);
   const double ks = double(s);
 
@@ -235,19 +217,7 @@ __device__ __forceinline__ void aggregate_cluster(
     acc_t sp = 0, se = 0;
     if (active) {
       const int l0 = h * slice, l1 = min(s, l0 + slice);
-      if constexpr (kMode == kVol32) {
-        const float dpx = g32[3 * S + j], dpy = g32[4 * S + j], dpz = g32[5 * S + j];
-        const float dex = g32[6 * S + j], dey = g32[7 * S + j], dez = g32[8 * S + j];
-        const float cp = g32[12 * S + j], ce = g32[13 * S + j];
-        for (int l = l0; l < l1; ++l) {
-          const float ax = g32[l], ay = g32[S + l], az = g32[2 * S + l];
-          const float g = g32[9 * S + l], num = g32[10 * S + l], g2ca = g32[11 * S + l];
-          const float a = hg_pdf32(ax, ay, az, g, num, g2ca, dpx, dpy, dpz, cp);
-          const float b = hg_pdf32(ax, ay, az, g, num, g2ca, dex, dey, dez, ce);
-          sp += a;
-          se += b;
-        }
-      } else {
+      {
         const double dpx = geo[3 * S + j], dpy = geo[4 * S + j], dpz = geo[5 * S + j];
         const double dex = geo[6 * S + j], dey = geo[7 * S + j], dez = geo[8 * S + j];
         for (int l = l0; l < l1; ++l) {
@@ -323,20 +293,7 @@ __device__ __forceinline__ void aggregate_cluster(
       const int j0 = h * slice2, j1 = min(s, j0 + slice2);
       // both densities are recomputed rather than kept in shared memory: no
       // pair storage, 16 CTAs per SM instead of 8
-      if constexpr (kMode == kVol32) {
-        const float ax = g32[r], ay = g32[S + r], az = g32[2 * S + r];
-        const float g = g32[9 * S + r], num = g32[10 * S + r], g2ca = g32[11 * S + r];
-        for (int j = j0; j < j1; ++j) {
-          const float a = hg_pdf32(ax, ay, az, g, num, g2ca, g32[3 * S + j], g32[4 * S + j],
-                                   g32[5 * S + j], g32[12 * S + j]);
-          // no W store: the solve recomputes these blocks (row_hg / col_hg)
-          const float b = hg_pdf32(ax, ay, az, g, num, g2ca, g32[6 * S + j], g32[7 * S + j],
-                                   g32[8 * S + j], g32[13 * S + j]);
-          dx += b * wtsf[S + j] + a * wtsf[4 * S + j];
-          dy += b * wtsf[2 * S + j] + a * wtsf[5 * S + j];
-          dz += b * wtsf[3 * S + j] + a * wtsf[6 * S + j];
-        }
-      } else if constexpr (kMode == kVol64) {
+      if constexpr (kMode == kVol64) {
         const double ax = geo[r], ay = geo[S + r], az = geo[2 * S + r];
         const double c1 = geo[10 * S + r], c2 = geo[11 * S + r];
         const float num = numf[r];
@@ -383,18 +340,13 @@ __device__ __forceinline__ void aggregate_cluster(
       // its I over from iteration to iteration)
       rows_o[4 * q] = make_float4(float(wx * kx), float(wy * ky), float(wz * kz),
                                   __int_as_float(row_link(mb.parent, mb.flags & 2u)));
-      float iw, ax, ay, az, g, dx3, dy3, dz3, cd;
-      if constexpr (kMode == kVol32) {
-        iw = wtsf[r];
-        ax = g32[r]; ay = g32[S + r]; az = g32[2 * S + r]; g = g32[9 * S + r];
-        dx3 = g32[3 * S + r]; dy3 = g32[4 * S + r]; dz3 = g32[5 * S + r]; cd = g32[12 * S + r];
-      } else {
-        iw = kVol ? wtsf[r] : float(wts[r]);
-        ax = float(geo[r]); ay = float(geo[S + r]); az = float(geo[2 * S + r]);
-        g = float(mb.g);
-        dx3 = float(geo[3 * S + r]); dy3 = float(geo[4 * S + r]); dz3 = float(geo[5 * S + r]);
-        cd = 0.f;
-      }
+      // (the fp32 HG clusters are aggregated by aggregate_v32; these rows'
+      // anchor / direction slots are not read by the solve)
+      const float iw = kVol ? wtsf[r] : float(wts[r]);
+      const float ax = float(geo[r]), ay = float(geo[S + r]), az = float(geo[2 * S + r]);
+      const float g = float(mb.g);
+      const float dx3 = float(geo[3 * S + r]), dy3 = float(geo[4 * S + r]),
+                  dz3 = float(geo[5 * S + r]), cd = 0.f;
       rows_o[4 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz), iw);
       rows_o[4 * q + 2] = make_float4(ax, ay, az, g);
       rows_o[4 * q + 3] = make_float4(dx3, dy3, dz3, cd);
@@ -403,13 +355,20 @@ __device__ __forceinline__ void aggregate_cluster(
   }
 }
 
-// fp32 HG clusters (volume members, |g| <= kG32) with the member data packed
-// as float4 rows so every pair costs two shared-memory loads per density:
+// fp32 HG clusters (volume members, |g| <= kG32).  Every operand is fp32:
+// den = 1 + g^2 - 2g cos is evaluated as |d - g a|^2 + (1 - |d|^2) (+ g^2
+// (1 - |a|^2), ~1e-16 for the unit anchors and left out), an identity in
+// which nothing cancels: for |g| <= 0.95 the components of d - g a are
+// >= ~0.05 in the forward peak, so the fp32 rounding of the inputs costs
+// < 1e-5 relative on the density (measured ~1e-6), inside the 1e-4 radiance
+// bar; larger |g| keeps the fp64 cosine and denominator (hg_pdf above).  The
+// member data is packed as float4 rows so every pair costs two shared-memory
+// loads per density:
 //   A4[l] = {anchor, g}, NM[l] = num(g), P4[j] = {phase_dir, 1 - |d|^2},
 //   E4[j] = {emit_dir, 1 - |e|^2}, WE4[j] = {d_emit / phat_dir_emit, 1/phat_ind},
 //   WP4[j] = {d_phase / phat_dir_phase, 0}.
-// The densities are hg_pdf32 with the g^2 (1 - |a|^2) term at 0 (hg32): the
-// same W the solve recomputes (operators.cu w_recomputed).
+// hg32 is the same arithmetic as the solve's recomputed W (operators.cu
+// w_recomputed), so both see the same W bit for bit.
 __device__ __forceinline__ float hg32(const float4 a, float num, const float4 d) {
   const float ux = fmaf(-a.w, a.x, d.x), uy = fmaf(-a.w, a.y, d.y), uz = fmaf(-a.w, a.z, d.z);
   const float r = rsqrt_ftz(fmaf(ux, ux, fmaf(uy, uy, fmaf(uz, uz, d.w))));
@@ -527,7 +486,6 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
   extern __shared__ __align__(16) unsigned char smem[];
   double* geo = reinterpret_cast<double*>(smem);
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
-  float* g32 = reinterpret_cast<float*>(geo);
   double* wts = geo + 12 * S + (S + 1) / 2;
   // fp32 HG clusters: packed float4 member data in the same space
   float4* A4 = reinterpret_cast<float4*>(geo);
