@@ -13,7 +13,11 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libvolpg_b200.so")
+# VPG_LIB_VARIANT=name loads _lib/variants/libvolpg_b200_<name>.so (build
+# experiments: tools/build_variant.py); the default is the in-tree build
+_VARIANT = os.environ.get("VPG_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, "_lib", "libvolpg_b200.so") if not _VARIANT else \
+    os.path.join(_HERE, "_lib", "variants", f"libvolpg_b200_{_VARIANT}.so")
 
 VPG_OK, VPG_EINVAL, VPG_ECUDA, VPG_EDIVERGED, VPG_ENOMEM, VPG_ELIMIT = 0, -1, -2, -3, -4, -5
 VPG_BUILD_TIMINGS = 1
