@@ -383,18 +383,24 @@ __device__ __forceinline__ void aggregate_v32(
     float4* __restrict__ i0_o) {
   const int tid = threadIdx.x;
   const double ks = double(s);
+  // column sums, then row sums, handed from the passes to their per-member
+  // epilogues (free space after WP4 in the weights region: 16 S bytes)
+  float2* SS = reinterpret_cast<float2*>(WP4 + s);
+  float4* DS = reinterpret_cast<float4*>(WP4 + s);
   // pass 1: columns (P threads each, fixed combination order), p-hat, weights
   const int P = s <= 32 ? 4 : 2;
-  const int slice = (s + P - 1) / P;
   for (int base = 0; base < P * s; base += blockDim.x) {
     const int t = base + tid;
     const bool active = t < P * s;
     const int j = t / P, h = t % P;
     float sp = 0.f, se = 0.f;
     if (active) {
-      const int l0 = h * slice, l1 = min(s, l0 + slice);
+      // thread h takes every P-th member (strided, not a contiguous slice:
+      // the P threads of a column then read consecutive rows of A4 -- no
+      // shared-memory bank conflicts); the P partial sums combine in a fixed
+      // order, so p-hat stays deterministic
       const float4 pj = P4[j], ej = E4[j];
-      for (int l = l0; l < l1; ++l) {
+      for (int l = h; l < s; l += P) {
         const float4 a = A4[l];
         const float num = NM[l];
         sp += hg32(a, num, pj);
@@ -407,7 +413,14 @@ __device__ __forceinline__ void aggregate_v32(
       sp += __shfl_xor_sync(0xFFFFFFFFu, sp, 2);
       se += __shfl_xor_sync(0xFFFFFFFFu, se, 2);
     }
-    if (active && h == 0) {
+    if (active && h == 0) SS[j] = make_float2(sp, se);
+  }
+  __syncthreads();
+  // the per-member marginals and weights, one member per thread (fp64
+  // divisions: with P lanes per column most of a warp would idle here)
+  for (int j = tid; j < s; j += blockDim.x) {
+    {
+      const float sp = SS[j].x, se = SS[j].y;
       const Member& mb = mem[q0 + j];
       const double p_ind = double(sp);
       const double p_dp = __dadd_rn(p_ind, __dmul_rn(ks, mb.pdf_eap));
@@ -431,17 +444,15 @@ __device__ __forceinline__ void aggregate_v32(
   __syncthreads();
   // pass 2: rows -- D-bar and the solve's row data (no W block: recomputed)
   const int P2 = s <= 32 ? 4 : 2;
-  const int slice2 = (s + P2 - 1) / P2;
   for (int base = 0; base < P2 * s; base += blockDim.x) {
     const int t = base + tid;
     const bool active = t < P2 * s;
     const int r = t / P2, h = t % P2;
     float dx = 0.f, dy = 0.f, dz = 0.f;
     if (active) {
-      const int j0 = h * slice2, j1 = min(s, j0 + slice2);
       const float4 a = A4[r];
       const float num = NM[r];
-      for (int j = j0; j < j1; ++j) {
+      for (int j = h; j < s; j += P2) {  // strided columns (see pass 1)
         const float pa = hg32(a, num, P4[j]);
         const float pb = hg32(a, num, E4[j]);
         const float4 we = WE4[j], wp = WP4[j];
@@ -458,7 +469,13 @@ __device__ __forceinline__ void aggregate_v32(
       dy += __shfl_xor_sync(0xFFFFFFFFu, dy, 2);
       dz += __shfl_xor_sync(0xFFFFFFFFu, dz, 2);
     }
-    if (active && h == 0) {
+    if (active && h == 0) DS[r] = make_float4(dx, dy, dz, 0.f);
+  }
+  __syncthreads();
+  // D-bar and the row data, one member per thread
+  for (int r = tid; r < s; r += blockDim.x) {
+    {
+      const float dx = DS[r].x, dy = DS[r].y, dz = DS[r].z;
       const Member& mb = mem[q0 + r];
       const double kx = mb.coeff[0], ky = mb.coeff[1], kz = mb.coeff[2];
       const double bx = kx * double(dx), by = ky * double(dy), bz = kz * double(dz);
