@@ -1,7 +1,7 @@
 // Build of the aggregation operators (graph.py:94-168) on the device.
 //
 //   k_pack_members  one coalesced pass over the records (record order) that
-//                   transposes what the operators need into a 192-byte
+//                   transposes what the operators need into a 160-byte
 //                   member struct at the record's cluster-major position
 //                   (full-sector scattered writes instead of ~17 scattered
 //                   field reads per member), plus the continuation parent and
@@ -42,12 +42,12 @@ struct __align__(32) Member {
   double g, pdf_eap, pdf_e;
   float de[3], dp[3];  // d_emit, d_phase
   float coeff[3], wc[3];
-  float ipt[3];
   uint32_t flags;  // 1 emit_delta, 2 terminal (no continuation child), 4 surface, 8 |g| > kG32
   int32_t parent;  // cluster-major row of the continuation parent, -1 none / not yet known
-  uint32_t pad[7];
+  uint32_t pad[2];
 };
-static_assert(sizeof(Member) == 192, "Member must stay 6 sectors");
+// five full sectors (i_pt goes straight to i0 from the pack)
+static_assert(sizeof(Member) == 160, "Member must stay 5 sectors");
 
 __device__ __forceinline__ double dot3(double ax, double ay, double az, double bx, double by,
                                        double bz) {
@@ -63,7 +63,7 @@ __device__ __forceinline__ float4 f4(double x, double y, double z) {
 __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpos,
                                const int32_t* __restrict__ list, int64_t list_n, int64_t off,
                                Member* __restrict__ out, float* __restrict__ term_max,
-                               const uint8_t* __restrict__ has_child) {
+                               const uint8_t* __restrict__ has_child, float4* __restrict__ i0) {
   const int64_t n = rec.n;
   const int lane = threadIdx.x & 31;
   float tmax[3] = {0.f, 0.f, 0.f};
@@ -97,7 +97,6 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
       m.dp[c] = float(rec.d_phase[r * 3 + c]);
       m.coeff[c] = float(rec.coeff[r * 3 + c]);
       m.wc[c] = float(rec.w_cont[r * 3 + c]);
-      m.ipt[c] = float(rec.i_pt[r * 3 + c]);
     }
     // no continuation child (records.py:128-140); shard-local records carry it
     const bool terminal = has_child ? !has_child[r]
@@ -108,10 +107,14 @@ __global__ void k_pack_members(vpg_records rec, const int32_t* __restrict__ clpo
     // placed; a parent placed later (a split group) links its children in
     // k_child_links.  Shard-local builds get theirs from k_set_parents.
     m.parent = (!has_child && r > 0 && rec.path_idx[r - 1] == rec.path_idx[r]) ? clpos[r - 1] : -1;
-    for (int k = 0; k < 7; ++k) m.pad[k] = 0;
+    m.pad[0] = m.pad[1] = 0;
     out[q] = m;
+    // I_0 = i_pt (solve.py:72)
+    const float ipt[3] = {float(rec.i_pt[r * 3]), float(rec.i_pt[r * 3 + 1]),
+                          float(rec.i_pt[r * 3 + 2])};
+    i0[q] = make_float4(ipt[0], ipt[1], ipt[2], 0.f);
     if (terminal)
-      for (int c = 0; c < 3; ++c) tmax[c] = fmaxf(tmax[c], fabsf(m.ipt[c]));
+      for (int c = 0; c < 3; ++c) tmax[c] = fmaxf(tmax[c], fabsf(ipt[c]));
   }
   for (int c = 0; c < 3; ++c) {
     float v = tmax[c];
@@ -196,7 +199,7 @@ template <int kMode>
 __device__ __forceinline__ void aggregate_cluster(
     const Member* __restrict__ mem, int32_t q0, int s, int64_t wb, int64_t n, int S,
     double* __restrict__ geo, double* __restrict__ wts, float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
-    float4* __restrict__ coeff_o, float4* __restrict__ rows_o, float4* __restrict__ i0_o) {
+    float4* __restrict__ coeff_o, float4* __restrict__ rows_o) {
   constexpr bool kVol = kMode != kSurface;
   using acc_t = typename std::conditional<kVol, float, double>::type;
   const int tid = threadIdx.x;
@@ -350,7 +353,6 @@ __device__ __forceinline__ void aggregate_cluster(
       rows_o[4 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz), iw);
       rows_o[4 * q + 2] = make_float4(ax, ay, az, g);
       rows_o[4 * q + 3] = make_float4(dx3, dy3, dz3, cd);
-      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
   }
 }
@@ -379,8 +381,7 @@ __device__ __forceinline__ void aggregate_v32(
     const Member* __restrict__ mem, int32_t q0, int s, int64_t n, const float4* __restrict__ A4,
     const float* __restrict__ NM, const float4* __restrict__ P4, const float4* __restrict__ E4,
     float4* __restrict__ WE4, float4* __restrict__ WP4, double* __restrict__ phat,
-    float4* __restrict__ dbar_o, float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
-    float4* __restrict__ i0_o) {
+    float4* __restrict__ dbar_o, float4* __restrict__ coeff_o, float4* __restrict__ rows_o) {
   const int tid = threadIdx.x;
   const double ks = double(s);
   // column sums, then row sums, handed from the passes to their per-member
@@ -488,7 +489,6 @@ __device__ __forceinline__ void aggregate_v32(
       rows_o[4 * q + 1] = make_float4(float(wx * bx), float(wy * by), float(wz * bz), WE4[r].w);
       rows_o[4 * q + 2] = A4[r];
       rows_o[4 * q + 3] = P4[r];
-      i0_o[q] = make_float4(mb.ipt[0], mb.ipt[1], mb.ipt[2], 0.f);
     }
   }
 }
@@ -499,7 +499,7 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
             const int64_t* __restrict__ range, int64_t n, int S,
             float* __restrict__ wt, double* __restrict__ phat, float4* __restrict__ dbar_o,
             float4* __restrict__ coeff_o, float4* __restrict__ rows_o,
-            float4* __restrict__ i0_o, uint8_t* __restrict__ cl_mode) {
+            uint8_t* __restrict__ cl_mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* geo = reinterpret_cast<double*>(smem);
   float* numf = reinterpret_cast<float*>(geo + 12 * S);
@@ -572,13 +572,13 @@ k_aggregate(const Member* __restrict__ mem, const int32_t* __restrict__ cl_off,
     }
     __syncthreads();
     if (mode == kVol32)
-      aggregate_v32(mem, q0, s, n, A4, NM, P4, E4, WE4, WP4, phat, dbar_o, coeff_o, rows_o, i0_o);
+      aggregate_v32(mem, q0, s, n, A4, NM, P4, E4, WE4, WP4, phat, dbar_o, coeff_o, rows_o);
     else if (mode == kVol64)
       aggregate_cluster<kVol64>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
-                                rows_o, i0_o);
+                                rows_o);
     else
       aggregate_cluster<kSurface>(mem, q0, s, wb, n, S, geo, wts, wt, phat, dbar_o, coeff_o,
-                                  rows_o, i0_o);
+                                  rows_o);
     __syncthreads();
   }
 }
@@ -696,7 +696,7 @@ void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int
                   int64_t off, void* members, cudaStream_t s, const uint8_t* has_child) {
   if (list_n <= 0) return;
   VPG_LAUNCH(k_pack_members, grid_for(list_n, 256), 256, 0, s, rec, g->clpos.get(), list, list_n,
-             off, static_cast<Member*>(members), g->term_max.get(), has_child);
+             off, static_cast<Member*>(members), g->term_max.get(), has_child, g->i0.get());
 }
 
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
@@ -709,8 +709,7 @@ void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, in
   const int64_t blocks = std::min<int64_t>(max_count, int64_t(sm_count()) * 16);
   VPG_LAUNCH(k_aggregate, int(blocks), kAggThreads, smem, s, static_cast<const Member*>(members),
              g->cl_off.get(), g->cl_size.get(), g->w_off.get(), range, g->n, S, g->wt.get(),
-             g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->i0.get(),
-             g->cl_mode.get());
+             g->phat.get(), g->dbar.get(), g->coeff.get(), g->rows.get(), g->cl_mode.get());
 }
 
 void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
