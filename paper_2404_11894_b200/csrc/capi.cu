@@ -544,6 +544,7 @@ int vpg_graph_views_get(const vpg_graph* g, vpg_graph_views* v) {
     v->n_halo = g->n_halo;
     v->perm = g->perm.get();
     v->clpos = g->clpos.get();
+    vpg::ensure_cluster_ids(g, as_stream(nullptr));
     v->cluster_id = g->cluster_id.get();
     v->cl_off = g->cl_off.get();
     v->cl_size = g->cl_size.get();

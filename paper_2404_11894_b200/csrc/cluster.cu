@@ -1092,7 +1092,7 @@ __global__ void k_fill_perm(const int64_t* __restrict__ range, const int32_t* __
       const int32_t r = from[t];
       perm[q0 + t] = r;
       clpos[r] = q0 + t;
-      cluster_id[r] = ref;
+      if (cluster_id) cluster_id[r] = ref;
     }
   }
 }
@@ -1340,6 +1340,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   g->perm.alloc(n, s);
   g->clpos.alloc(n, s);
   g->cluster_id.alloc(n, s);
+  g->cluster_id_ready = false;  // filled on first export (ensure_cluster_ids)
   if (n == 0) {
     g->m = 0;
     for (auto* v : {&g->cl_off, &g->cl_size, &g->cl_center, &g->ref_of, &g->internal_of}) {
@@ -1823,7 +1824,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     // ---- part A of this class: permutation, pack, aggregate (device, async)
     VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, s, ranges.get() + 2 * c, g->cl_off.get(),
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, nullptr, g->perm.get(),
-               g->clpos.get(), g->cluster_id.get());
+               g->clpos.get(), static_cast<int32_t*>(nullptr));
     // part B (split results) may start once this class's rows are placed
     VPG_CUDA(cudaEventRecord(placed, s));
     if (with_ops) {
@@ -2061,7 +2062,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   if (nb) {
     VPG_LAUNCH(k_fill_perm, sm_count() * 8, 256, 0, sb, range_b.get(), g->cl_off.get(),
                g->cl_size.get(), a_src.get(), g->ref_of.get(), grp_rec, d_split.get(),
-               g->perm.get(), g->clpos.get(), g->cluster_id.get());
+               g->perm.get(), g->clpos.get(), static_cast<int32_t*>(nullptr));
     if (with_ops) {
       pack_members(g, rec, d_split.get(), split_total, 0, members, sb);
       aggregate_range(g, members, range_b.get(), nb, S, sb);

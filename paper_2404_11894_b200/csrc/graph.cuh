@@ -72,6 +72,9 @@ struct vpg_graph {
   vpg::DBuf<int32_t> ctl;
   int32_t red_cap = 0;
   int32_t performed = -1;  // -1 = no solve yet
+  // cluster_id (record -> reference cluster number) is only read by exports:
+  // the build leaves it to vpg::ensure_cluster_ids on first use
+  mutable bool cluster_id_ready = true;
   double tol = 0.0;        // of the solve in progress (vpg_solve_begin)
   int32_t iterations = 0;
   // shard-local graphs (vpg_graph_build_local): rows whose continuation
@@ -162,6 +165,8 @@ void link_children(vpg_graph* g, const vpg_records& rec, const int32_t* list, in
 // chunk table, descriptors and cluster table on the device (no host sync;
 // g->max_cluster must bound the largest cluster)
 void finalize_chunks(vpg_graph* g, cudaStream_t s);
+// operators.cu: fill g->cluster_id if the build deferred it
+void ensure_cluster_ids(const vpg_graph* g, cudaStream_t s);
 // shard-local graph from a given cluster partition (records already
 // cluster-major, clusters back to back), explicit parents and child flags
 void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,

@@ -899,8 +899,32 @@ void propagate(const vpg_records& rec, const double* lbar, double* out, int line
   VPG_LAUNCH(k_propagate, grid_for(rec.n, 256), 256, 0, s, rec, lbar, linear, out);
 }
 
+namespace {
+// record -> reference cluster number, warp per cluster (exports only)
+__global__ void k_cluster_ids(const int32_t* __restrict__ cl_off, const int32_t* __restrict__ cl_size,
+                              const int32_t* __restrict__ ref_of, const int32_t* __restrict__ perm,
+                              int64_t m, int32_t* __restrict__ cluster_id) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < m; k += warps) {
+    const int32_t q0 = cl_off[k], sz = cl_size[k], ref = ref_of[k];
+    for (int32_t t = lane; t < sz; t += 32) cluster_id[perm[q0 + t]] = ref;
+  }
+}
+}  // namespace
+
+void ensure_cluster_ids(const vpg_graph* g, cudaStream_t s) {
+  if (g->cluster_id_ready) return;
+  if (g->n > 0)
+    VPG_LAUNCH(k_cluster_ids, grid_for(g->m * 32, 256), 256, 0, s, g->cl_off.get(),
+               g->cl_size.get(), g->ref_of.get(), g->perm.get(), g->m,
+               const_cast<int32_t*>(g->cluster_id.get()));
+  g->cluster_id_ready = true;
+}
+
 void export_clusters(const vpg_graph* g, int64_t* cluster_id, int64_t* cl_off, int64_t* members,
                      int64_t* centers, cudaStream_t s) {
+  ensure_cluster_ids(g, s);
   const int64_t n = g->n, m = g->m;
   const int block = 256;
   if (cluster_id && n) {
@@ -943,6 +967,7 @@ void export_marginals(const vpg_graph* g, double* p0, double* p1, double* p2, cu
 
 void export_operators(const vpg_graph* g, int64_t* indptr, int64_t* indices, double* data,
                       double* d_bar, cudaStream_t s) {
+  ensure_cluster_ids(g, s);
   const int64_t n = g->n;
   if (n == 0) {
     if (indptr) indptr[0] = 0;
