@@ -695,7 +695,9 @@ void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s) {
 void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
                   int64_t off, void* members, cudaStream_t s, const uint8_t* has_child) {
   if (list_n <= 0) return;
-  VPG_LAUNCH(k_pack_members, grid_for(list_n, 256), 256, 0, s, rec, g->clpos.get(), list, list_n,
+  // one record per thread (not a persistent grid): short blocks, so the
+  // high-priority staging kernels on the side streams interleave at once
+  VPG_LAUNCH(k_pack_members, grid_for(list_n, 256, 1 << 30), 256, 0, s, rec, g->clpos.get(), list, list_n,
              off, static_cast<Member*>(members), g->term_max.get(), has_child, g->i0.get());
 }
 

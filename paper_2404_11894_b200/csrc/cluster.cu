@@ -1253,7 +1253,14 @@ cudaStream_t side_stream(int which = 0) {
   int dev = 0;
   VPG_CUDA(cudaGetDevice(&dev));
   cudaStream_t& st = streams[which][dev];
-  if (!st) VPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  if (!st) {
+    // the highest priority: the oversize staging and part B feed the host
+    // split loop and the critical path, their blocks go first whenever an
+    // SM frees up
+    int lo = 0, hi = 0;
+    VPG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VPG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+  }
   return st;
 }
 
