@@ -418,7 +418,6 @@ __global__ void k_swap_resolve(const int32_t* __restrict__ target,
 }
 
 // ------------------------------------------------ cell-sorted assignment
-constexpr int kCandCap = 128;  // candidate centers staged per warp
 constexpr long long kShellBudget = 4096;  // cells one fallback point may enumerate
 constexpr int kAssignWarps = 8;
 
@@ -445,27 +444,43 @@ __global__ void k_point_keys(const int32_t* rows, int64_t row_off, int64_t n,
 // Counting sort of the points by cell (dense packed keys): count, scan,
 // scatter.  Points of one cell land in arbitrary order, which the assignment
 // does not see (each point's nearest center is exact on its own).
+constexpr int kOctShift = 29;  // octant bits in the cell-sorted point ids
+
+// Also the point's octant in its cell (bit a: the upper half along axis a),
+// carried into cell order for the assignment's batches.
+__device__ __forceinline__ int cell_and_octant(double p, double lo, double cell, long long& c) {
+  const double t = __ddiv_rn(__dsub_rn(p, lo), cell);
+  c = (long long)floor(t);
+  return int((long long)floor(2.0 * t) & 1);  // 2t is exact
+}
+
 __global__ void k_cell_count(const int32_t* rows, int64_t row_off, int64_t n,
                              const double* __restrict__ pos, GridParams gp,
-                             int32_t* __restrict__ counts, int32_t* __restrict__ pkey) {
+                             int32_t* __restrict__ counts, int32_t* __restrict__ pkey,
+                             uint8_t* __restrict__ poct) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = class_row(rows, row_off, i);
-    const int32_t key = int32_t(cell_key(gp, cell_coord(pos[r * 3], gp.lo[0], gp.cell),
-                                         cell_coord(pos[r * 3 + 1], gp.lo[1], gp.cell),
-                                         cell_coord(pos[r * 3 + 2], gp.lo[2], gp.cell)));
+    long long x, y, z;
+    const int o = cell_and_octant(pos[r * 3], gp.lo[0], gp.cell, x) |
+                  (cell_and_octant(pos[r * 3 + 1], gp.lo[1], gp.cell, y) << 1) |
+                  (cell_and_octant(pos[r * 3 + 2], gp.lo[2], gp.cell, z) << 2);
+    const int32_t key = int32_t(cell_key(gp, x, y, z));
     pkey[i] = key;
+    if (poct) poct[i] = uint8_t(o);
     atomicAdd(&counts[key], 1);
   }
 }
 
+// poct (n < 2^29): the octant rides in bits 29..31 of the sorted ids
 __global__ void k_cell_scatter(int64_t n, const int32_t* __restrict__ pkey,
-                               const int32_t* __restrict__ offs, int32_t* __restrict__ counts,
-                               int32_t* __restrict__ sorted_ids) {
+                               const uint8_t* __restrict__ poct, const int32_t* __restrict__ offs,
+                               int32_t* __restrict__ counts, int32_t* __restrict__ sorted_ids) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t key = pkey[i];
-    sorted_ids[offs[key] + atomicSub(&counts[key], 1) - 1] = int32_t(i);
+    const int32_t at = offs[key] + atomicSub(&counts[key], 1) - 1;
+    sorted_ids[at] = int32_t(uint32_t(i) | (poct ? uint32_t(poct[i]) << kOctShift : 0u));
   }
 }
 
@@ -485,126 +500,250 @@ __global__ void k_cell_runs(const int32_t* __restrict__ cells, const int32_t* __
   }
 }
 
+// Neighbour cell v of the visit order (k = 9 dx + 3 dy + dz, offsets d - 1):
+// the home cell, the 6 faces, then the 12 edges and the 8 corners.
+__host__ __device__ constexpr int visit_cell(int v) {
+  switch (v) {
+    case 0: return 13;
+    case 1: return 4;   case 2: return 10;  case 3: return 12;  case 4: return 14;
+    case 5: return 16;  case 6: return 22;
+    case 7: return 1;   case 8: return 3;   case 9: return 5;   case 10: return 7;
+    case 11: return 9;  case 12: return 11; case 13: return 15; case 14: return 17;
+    case 15: return 19; case 16: return 21; case 17: return 23; case 18: return 25;
+    case 19: return 0;  case 20: return 2;  case 21: return 6;  case 22: return 8;
+    case 23: return 18; case 24: return 20; case 25: return 24; default: return 26;
+  }
+}
+__constant__ uint8_t kVisitOrder[27] = {13, 4,  10, 12, 14, 16, 22, 1, 3,  5,  7,  9,  11, 15,
+                                        17, 19, 21, 23, 25, 0,  2,  6, 8, 18, 20, 24, 26};
+constexpr int kNearCells = 7;   // home + faces: always scanned
+constexpr int kCandCap = 240;   // candidate centers staged per warp
+constexpr int kRunCap = 256;    // points put in octant order at a time
+
+// (out of line: only hashed grids need it, and three inlined divisions per
+// call site would bloat the assignment loop out of the instruction cache)
+__device__ __noinline__ bool center_in_cell(double cx, double cy, double cz, const GridParams& gp,
+                                            long long x, long long y, long long z) {
+  return cell_coord(cx, gp.lo[0], gp.cell) == x && cell_coord(cy, gp.lo[1], gp.cell) == y &&
+         cell_coord(cz, gp.lo[2], gp.cell) == z;
+}
+
+__device__ __forceinline__ int octant_of(double x, double y, double z, const GridParams& gp,
+                                         long long cx, long long cy, long long cz,
+                                         double inv_cell) {
+  return int((x - gp.lo[0]) * inv_cell - double(cx) >= 0.5) |
+         (int((y - gp.lo[1]) * inv_cell - double(cy) >= 0.5) << 1) |
+         (int((z - gp.lo[2]) * inv_cell - double(cz) >= 0.5) << 2);
+}
+
 // One warp per run of points sharing a cell (points sorted by cell): lanes
-// 0..26 look up the 27 neighbour cells once, the candidate centers are staged
-// in shared memory, and every point of the run scans the same candidate set
-// -- exactly the reference's per-cell candidate list (clustering.py:121-137).
-__global__ void __launch_bounds__(kAssignWarps * 32)
+// 0..26 look up the 27 neighbour cells once, in visit order -- exactly the
+// reference's per-cell candidate list (clustering.py:121-137).  The run's
+// points are taken kRunCap at a time in octant order, then 32 at a time scan
+// the home cell and the faces, and of the 20 edge and corner cells only those
+// some lane can still reach: a cell is skipped when, for every lane, the
+// point's distance to the cell's box (in cell units, fp32, shrunk by a margin
+// far above the rounding of the cell indices) exceeds its best squared
+// distance so far, so all its centers are strictly farther and the
+// lexicographic (d2, center) minimum over the 27 cells is unchanged.  Octant
+// order makes the 32 points of a batch neighbours, so they skip the same
+// cells.  The candidates are staged in shared memory once per run, or, for a
+// crowded neighbourhood (more than kCandCap), cell by cell for each batch.
+__global__ void __launch_bounds__(kAssignWarps * 32, 3)
 k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ pos, GridParams gp,
                CellIndex table, const double4* __restrict__ spos,
-               const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ run_start,
-               const int32_t* __restrict__ run_len, const int32_t* __restrict__ n_runs,
-               int32_t* __restrict__ assign, int32_t* __restrict__ fb_list,
-               int32_t* __restrict__ fb_count) {
-  __shared__ double4 cand[kAssignWarps][kCandCap];
+               const int32_t* __restrict__ sorted_ids, int oct_in_ids,
+               const int32_t* __restrict__ run_start, const int32_t* __restrict__ run_len,
+               const int32_t* __restrict__ n_runs, int32_t* __restrict__ assign,
+               int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  constexpr float kMargin = 1e-4f;  // cells
+  extern __shared__ __align__(16) unsigned char assign_smem[];
+  double4* cand = reinterpret_cast<double4*>(assign_smem) + (threadIdx.x >> 5) * kCandCap;
+  int32_t* run_ids = reinterpret_cast<int32_t*>(assign_smem + sizeof(double4) * kCandCap *
+                                                                  kAssignWarps) +
+                     (threadIdx.x >> 5) * kRunCap;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int runs = *n_runs;
   const int warps = gridDim.x * kAssignWarps;
+  const double inv_cell = 1.0 / gp.cell;
+  const double inv_cell2 = inv_cell * inv_cell;
   for (int run = blockIdx.x * kAssignWarps + wid; run < runs; run += warps) {
     const int32_t b = run_start[run], len = run_len[run];
-    const int64_t r0 = class_row(rows, row_off, sorted_ids[b]);
+    const uint32_t id_mask = oct_in_ids ? (1u << kOctShift) - 1u : 0xFFFFFFFFu;
+    const int64_t r0 = class_row(rows, row_off, int32_t(sorted_ids[b] & id_mask));
     const long long cx = cell_coord(pos[r0 * 3], gp.lo[0], gp.cell);
     const long long cy = cell_coord(pos[r0 * 3 + 1], gp.lo[1], gp.cell);
     const long long cz = cell_coord(pos[r0 * 3 + 2], gp.lo[2], gp.cell);
-    long long nx = 0, ny = 0, nz = 0;
     int c_start = 0, c_cnt = 0;
     if (lane < 27) {
-      nx = cx + lane / 9 - 1;
-      ny = cy + (lane / 3) % 3 - 1;
-      nz = cz + lane % 3 - 1;
+      const int k = visit_cell(lane);
       int st, en;
-      if (table.find(cell_key(gp, nx, ny, nz), st, en)) {
+      if (table.find(cell_key(gp, cx + k / 9 - 1, cy + (k / 3) % 3 - 1, cz + k % 3 - 1), st, en)) {
         c_start = st;
         c_cnt = en - st;
       }
     }
-    int incl = c_cnt;  // inclusive warp scan of candidate counts
+    const unsigned nonempty = __ballot_sync(kFull, c_cnt > 0);
+    int incl = c_cnt;  // inclusive warp scan of candidate counts (visit order)
     for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+      const int v = __shfl_up_sync(kFull, incl, off);
       if (lane >= off) incl += v;
     }
-    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    if (total <= kCandCap) {
-      for (int t = 0; t < c_cnt; ++t) {
-        const double4 c = spos[c_start + t];
-        // hashed keys: a colliding cell's centers are filtered out here
-        const bool keep = gp.packed || (cell_coord(c.x, gp.lo[0], gp.cell) == nx &&
-                                        cell_coord(c.y, gp.lo[1], gp.cell) == ny &&
-                                        cell_coord(c.z, gp.lo[2], gp.cell) == nz);
-        cand[wid][incl - c_cnt + t] = keep ? c : make_double4(INFINITY, INFINITY, INFINITY,
-                                                              __longlong_as_double(0x7FFFFFFFLL));
-      }
-      __syncwarp();
-      for (int t = lane; t < len; t += 32) {
-        const int32_t i = sorted_ids[b + t];
-        const int64_t r = class_row(rows, row_off, i);
-        const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
-        Best best{INFINITY, 0x7FFFFFFF};
-        for (int q = 0; q < total; ++q) {
-          const double4 c = cand[wid][q];
-          const int j = int(__double_as_longlong(c.w));
-          if (j == 0x7FFFFFFF) continue;
-          best_update(best, dist2_exact(px, py, pz, c.x, c.y, c.z), j);
-        }
-        if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
-          fb_list[atomicAdd(fb_count, 1)] = i;
-          assign[i] = -1;
-        } else {
-          assign[i] = best.j;
-        }
-      }
-      __syncwarp();
-    } else {
-      // crowded neighbourhood (dense regions): 32 points at a time scan the
-      // candidate list in shared-memory chunks staged by the whole warp --
-      // candidate idx belongs to neighbour cell k = #lanes whose inclusive
-      // count is <= idx.  The lexicographic (d2, center) minimum does not
-      // depend on the chunking.
-      for (int pb = 0; pb < len; pb += 32) {
-        const int t = pb + lane;
-        const bool active = t < len;
-        int32_t i = 0;
-        double px = 0.0, py = 0.0, pz = 0.0;
-        if (active) {
-          i = sorted_ids[b + t];
-          const int64_t r = class_row(rows, row_off, i);
-          px = pos[r * 3];
-          py = pos[r * 3 + 1];
-          pz = pos[r * 3 + 2];
-        }
-        Best best{INFINITY, 0x7FFFFFFF};
-        for (int base = 0; base < total; base += kCandCap) {
-          const int cnt = total - base < kCandCap ? total - base : kCandCap;
-          __syncwarp();
-          for (int rd = 0; rd < cnt; rd += 32) {
-            const int idx = base + rd + lane;
-            int k = 0;
+    const int total = __shfl_sync(kFull, incl, 31);
+    const bool staged = total <= kCandCap;
+    // copy candidates [i0, i0 + cnt) of the visit order into cand[0 ..):
+    // index idx is in visit cell v = #lanes whose inclusive count is <= idx;
+    // with hashed keys a colliding cell's centers become +inf
+    auto stage = [&](int i0, int cnt) {
+#pragma unroll 1
+      for (int t0 = 0; t0 < cnt; t0 += 32) {  // warp-uniform: the shuffles need every lane
+        const int t = t0 + lane;
+        const int idx = i0 + t;
+        int v = 0;
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-              const int v = __shfl_sync(0xFFFFFFFFu, incl, k + step - 1);
-              if (v <= idx) k += step;
-            }
-            const int k_start = __shfl_sync(0xFFFFFFFFu, c_start, k);
-            const int k_first = __shfl_sync(0xFFFFFFFFu, incl - c_cnt, k);
-            if (rd + lane < cnt) {
-              const double4 c = spos[k_start + (idx - k_first)];
-              const bool keep = gp.packed ||
-                                (cell_coord(c.x, gp.lo[0], gp.cell) == cx + k / 9 - 1 &&
-                                 cell_coord(c.y, gp.lo[1], gp.cell) == cy + (k / 3) % 3 - 1 &&
-                                 cell_coord(c.z, gp.lo[2], gp.cell) == cz + k % 3 - 1);
-              cand[wid][rd + lane] = keep ? c : make_double4(INFINITY, INFINITY, INFINITY,
-                                                             __longlong_as_double(0x7FFFFFFFLL));
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int c = __shfl_sync(kFull, incl, v + step - 1);
+          if (c <= idx) v += step;
+        }
+        const int first = __shfl_sync(kFull, incl - c_cnt, v);
+        const int from = __shfl_sync(kFull, c_start, v) + (idx - first);
+        if (t >= cnt) continue;
+        double4 c = spos[from];
+        if (!gp.packed) {
+          const int k = kVisitOrder[v];
+          if (!center_in_cell(c.x, c.y, c.z, gp, cx + k / 9 - 1, cy + (k / 3) % 3 - 1,
+                              cz + k % 3 - 1))
+            c = make_double4(INFINITY, INFINITY, INFINITY, __longlong_as_double(0x7FFFFFFFLL));
+        }
+        cand[t] = c;
+      }
+    };
+    if (staged) {
+      stage(0, total);
+      __syncwarp();
+    }
+    const int c_first = incl - c_cnt;  // visit-order offset of each cell
+#pragma unroll 1
+    for (int s0 = 0; s0 < len; s0 += kRunCap) {
+      const int seg = len - s0 < kRunCap ? len - s0 : kRunCap;
+      // the segment's point ids into run_ids, octant by octant (a counting
+      // sort; lanes 0..7 hold the octant counts, then their bases)
+      int base = 0;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < seg; c0 += 32) {
+          int o = 8;
+          int32_t id = 0;
+          if (c0 + lane < seg) {
+            id = sorted_ids[b + s0 + c0 + lane];
+            if (oct_in_ids) {
+              o = int(uint32_t(id) >> kOctShift);
+              id = int32_t(uint32_t(id) & id_mask);
+            } else {
+              const int64_t r = class_row(rows, row_off, id);
+              o = octant_of(pos[r * 3], pos[r * 3 + 1], pos[r * 3 + 2], gp, cx, cy, cz, inv_cell);
             }
           }
-          __syncwarp();
-          if (active)
-            for (int q = 0; q < cnt; ++q) {
-              const double4 c = cand[wid][q];
-              const int j = int(__double_as_longlong(c.w));
-              if (j == 0x7FFFFFFF) continue;
-              best_update(best, dist2_exact(px, py, pz, c.x, c.y, c.z), j);
-            }
+          if (pass == 1) {
+            const unsigned peers = __match_any_sync(kFull, o);
+            const int at = __shfl_sync(kFull, base, o & 7) + __popc(peers & ((1u << lane) - 1u));
+            if (o < 8) run_ids[at] = id;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int cnt = __popc(__ballot_sync(kFull, o == q));
+            if (lane == q) base += cnt;
+          }
         }
+        if (pass == 0) {
+          const int hist = base;
+          for (int off = 1; off < 8; off <<= 1) {
+            const int v = __shfl_up_sync(kFull, base, off);
+            if (lane >= off) base += v;
+          }
+          base -= hist;
+        }
+      }
+      __syncwarp();
+      // the next batch's point is loaded while this one scans
+      int32_t ni = 0;
+      double nx = 0.0, ny = 0.0, nz = 0.0;
+      auto load_point = [&](int pb) {
+        if (pb + lane < seg) {
+          ni = run_ids[pb + lane];
+          const int64_t r = class_row(rows, row_off, ni);
+          nx = pos[r * 3];
+          ny = pos[r * 3 + 1];
+          nz = pos[r * 3 + 2];
+        }
+      };
+      load_point(0);
+#pragma unroll 1
+      for (int pb = 0; pb < seg; pb += 32) {
+        const bool active = pb + lane < seg;
+        const int32_t i = ni;
+        const double px = nx, py = ny, pz = nz;
+        if (pb + 32 < seg) load_point(pb + 32);
+        Best best{INFINITY, 0x7FFFFFFF};
+        auto scan = [&](int q0, int cnt) {
+#pragma unroll 4
+          for (int q = q0; q < q0 + cnt; ++q) {
+            const double4 c = cand[q];
+            best_update(best, dist2_exact(px, py, pz, c.x, c.y, c.z),
+                        int(__double_as_longlong(c.w)));
+          }
+        };
+        // visit the cells whose bits are set: staged, or copied cell by cell
+        // (crowded)
+        auto visit = [&](unsigned cells) {
+          while (cells) {
+            const int v = __ffs(cells) - 1;
+            cells &= cells - 1;
+            const int kb = __shfl_sync(kFull, c_first, v), kc = __shfl_sync(kFull, c_cnt, v);
+            if (staged) {
+              scan(kb, kc);
+            } else {
+              for (int t0 = 0; t0 < kc; t0 += kCandCap) {
+                const int cnt = kc - t0 < kCandCap ? kc - t0 : kCandCap;
+                __syncwarp();
+                stage(kb + t0, cnt);
+                __syncwarp();
+                scan(0, cnt);
+              }
+            }
+          }
+        };
+        // home cell and faces
+        visit(nonempty & ((1u << kNearCells) - 1u));
+        // edges and corners some lane can still reach
+        unsigned need = 0;
+        if (active) {
+          float sq[3][2];
+          const double t[3] = {(px - gp.lo[0]) * inv_cell - double(cx),
+                               (py - gp.lo[1]) * inv_cell - double(cy),
+                               (pz - gp.lo[2]) * inv_cell - double(cz)};
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float lo_gap = fmaxf(float(t[a]) - kMargin, 0.f);
+            const float hi_gap = fmaxf(float(1.0 - t[a]) - kMargin, 0.f);
+            sq[a][0] = lo_gap * lo_gap;
+            sq[a][1] = hi_gap * hi_gap;
+          }
+          const float reach = float(best.d2 * inv_cell2) * 1.0001f;
+#pragma unroll
+          for (int v = kNearCells; v < 27; ++v) {
+            const int k = visit_cell(v);
+            const int dx = k / 9, dy = (k / 3) % 3, dz = k % 3;
+            float lb = 0.f;
+            if (dx != 1) lb += sq[0][dx >> 1];
+            if (dy != 1) lb += sq[1][dy >> 1];
+            if (dz != 1) lb += sq[2][dz >> 1];
+            if (!(lb > reach)) need |= 1u << v;
+          }
+        }
+        visit(__reduce_or_sync(kFull, need) & nonempty);
         if (active) {
           if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
             fb_list[atomicAdd(fb_count, 1)] = i;
@@ -618,6 +757,8 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
     }
   }
 }
+constexpr size_t kAssignSmem = (sizeof(double4) * kCandCap + sizeof(int32_t) * kRunCap) *
+                               kAssignWarps;
 
 __device__ __forceinline__ void warp_best(Best& b) {
   for (int off = 16; off; off >>= 1) {
@@ -1559,6 +1700,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
     // center draw, overlap the host RNG
     unsigned long long *pkeys = nullptr, *pkeys_sorted = nullptr;
     int32_t *pids = nullptr, *pids_sorted = nullptr, *run_start = nullptr, *run_len = nullptr;
+    uint8_t* poct = nullptr;  // octants (counting sort of < 2^29 points only)
     int end_bits = 64;
     if (m > 1) {
       pkeys = scratch_of<unsigned long long>(s, "pkeys", p.n);
@@ -1577,12 +1719,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
         int32_t* offs = scratch_of<int32_t>(s, "cell_offs", size_t(nc) + 1);
         int32_t* pkey = reinterpret_cast<int32_t*>(pkeys);
         VPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nc + 1), s));
+        if (p.n < (int64_t(1) << kOctShift)) poct = scratch_of<uint8_t>(s, "cell_oct", p.n);
         VPG_LAUNCH(k_cell_count, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
-                   rec.pos, gp, counts, pkey);
+                   rec.pos, gp, counts, pkey, poct);
         cub_call([&](void* t, size_t& b) {
           return cub::DeviceScan::ExclusiveSum(t, b, counts, offs, int(nc + 1), s);
         }, s);
-        VPG_LAUNCH(k_cell_scatter, grid_for(p.n, block), block, 0, s, p.n, pkey, offs, counts,
+        VPG_LAUNCH(k_cell_scatter, grid_for(p.n, block), block, 0, s, p.n, pkey, poct, offs, counts,
                    pids_sorted);
         int32_t* sel = reinterpret_cast<int32_t*>(pkeys_sorted);
         cub::CountingInputIterator<int32_t> ci(0);
@@ -1703,8 +1846,9 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                                                sids.get(), m, 0, morton_bits, s);
       }, s);
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
-      VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, rows_p, p.row_off,
-                 rec.pos, gp, cidx, spos.get(), pids_sorted, run_start, run_len,
+      ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
+      VPG_LAUNCH(k_assign_cells, sm_count() * 3, kAssignWarps * 32, kAssignSmem, s, rows_p, p.row_off,
+                 rec.pos, gp, cidx, spos.get(), pids_sorted, int(poct != nullptr), run_start, run_len,
                  scalars.get() + 1, assign_c, fb_list, scalars.get());
       int32_t* far_list = scratch_of<int32_t>(s, "far_list", p.n + 1);
       auto* far_d = scratch_of<unsigned long long>(s, "far_d", p.n + 1);
@@ -2322,8 +2466,10 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
   else
     VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
                table.get());
-  VPG_LAUNCH(k_assign_cells, sm_count() * 8, kAssignWarps * 32, 0, s, nullptr, 0, pos, gp,
-             cidx, spos.get(), pids_sorted, run_start, run_len, scalars.get() + 1, assign,
+  ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
+  VPG_LAUNCH(k_assign_cells, sm_count() * 3, kAssignWarps * 32, kAssignSmem, s, nullptr, 0, pos, gp,
+             cidx, spos.get(), pids_sorted, 0, run_start, run_len,
+             scalars.get() + 1, assign,
              fb_list, scalars.get());
   int32_t* far_list = scratch_of<int32_t>(s, "an_far_list", n + 1);
   auto* far_d = scratch_of<unsigned long long>(s, "an_far_d", n + 1);
