@@ -352,7 +352,9 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         acc_out[q] = make_float4(ax, ay, az, 0.f);
         const float4 A = crow[4 * rr], B = crow[4 * rr + 1];
         const int32_t link = __float_as_int(A.w);
-        if (link_terminal(link)) i_out[q] = sin[rl + rr];  // terminal row: I stays i_pt
+        // a terminal row's I stays i_pt: written into both I buffers by the
+        // first two iterations, never touched again
+        if (t < 2 && link_terminal(link)) i_out[q] = i0[q];
         const int32_t p = link_parent(link);
         if (p < 0) return;
         const float nx = fmaf(A.x, ax, B.x), ny = fmaf(A.y, ay, B.y), nz = fmaf(A.z, az, B.z);
@@ -373,8 +375,9 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
       };
       const int items = 1;
       if (mk.w == 0) {
-        // W recomputed with w_recomputed's operations (so the same W the
-        // aggregate evaluated).  Rows go to lanes in passes chosen to keep
+        // W recomputed from the row data: num_r hg3(r, j) / phat_ind[j], the
+        // aggregate's fp32 HG terms (the products grouped per row and per
+        // column instead of per pair).  Rows go to lanes in passes chosen to keep
         // the lanes busy: 64 rows as two per lane, 17..32 rows one per lane,
         // and up to 16 rows as column slices -- P = 32 / pow2(rows) lanes per
         // row, each summing every P-th column, combined by xor shuffles.
@@ -383,20 +386,47 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         const int64_t q0 = int64_t(cq0) + rl;
         const float4* crow = srow + 4 * rl;
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        // one row (ha, num n) over columns j0, j0 + dj, ... < s
+        if (s == 1) {
+          // a lone record: W = phat * (1 / phat), evaluated exactly as the
+          // aggregate did, so that at K = 1 the fixed point (the PT
+          // estimate, reached at once) shows no fp32 noise growth
+          if (lane == 0) {
+            const float4 ha = crow[2], ij = sin[rl];
+            const float wv = (hg_num_f32(ha.w) * hg3(ha, crow[3])) * crow[1].w;
+            epilogue(crow, rl, q0, 0, wv * ij.x, wv * ij.y, wv * ij.z);
+          }
+          __syncwarp();
+          if (lane == 0) atomicAdd(&done[st], 1);
+          continue;
+        }
+        // W[r, j] I_j = num_r hg3(r, j) (1/phat_ind[j] I_j): the column
+        // factor is applied to the staged I once per column (in place: only
+        // this cluster reads these rows of I), num_r once per row
+        {
+          float4* icol = const_cast<float4*>(sin) + rl;
+          for (int j = lane; j < s; j += 32) {
+            const float iw = crow[4 * j + 1].w;
+            float4 v = icol[j];
+            v.x *= iw;
+            v.y *= iw;
+            v.z *= iw;
+            icol[j] = v;
+          }
+          __syncwarp();
+        }
+        // one row (anchor ha) over columns j0, j0 + dj, ... < s, times num n
         auto one_row = [&](const float4 ha, float n, int j0, int dj) {
           float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll 4
           for (int j = j0; j < s; j += dj) {
             const float4 dc = crow[4 * j + 3];
-            const float iw = crow[4 * j + 1].w;
             const float4 ij = sin[rl + j];
-            const float wv = (n * hg3(ha, dc)) * iw;
-            acc.x = fmaf(wv, ij.x, acc.x);
-            acc.y = fmaf(wv, ij.y, acc.y);
-            acc.z = fmaf(wv, ij.z, acc.z);
+            const float h = hg3(ha, dc);
+            acc.x = fmaf(h, ij.x, acc.x);
+            acc.y = fmaf(h, ij.y, acc.y);
+            acc.z = fmaf(h, ij.z, acc.z);
           }
-          return acc;
+          return make_float3(acc.x * n, acc.y * n, acc.z * n);
         };
         int rc = 0;
         while (rc < s) {
@@ -411,18 +441,17 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
 #pragma unroll 2
             for (int j = 0; j < s; ++j) {
               const float4 dc = crow[4 * j + 3];
-              const float iw = crow[4 * j + 1].w;
               const float4 ij = sin[rl + j];
-              const float w0v = (n0 * hg3(ha0, dc)) * iw, w1v = (n1 * hg3(ha1, dc)) * iw;
-              acc0.x = fmaf(w0v, ij.x, acc0.x);
-              acc0.y = fmaf(w0v, ij.y, acc0.y);
-              acc0.z = fmaf(w0v, ij.z, acc0.z);
-              acc1.x = fmaf(w1v, ij.x, acc1.x);
-              acc1.y = fmaf(w1v, ij.y, acc1.y);
-              acc1.z = fmaf(w1v, ij.z, acc1.z);
+              const float h0 = hg3(ha0, dc), h1 = hg3(ha1, dc);
+              acc0.x = fmaf(h0, ij.x, acc0.x);
+              acc0.y = fmaf(h0, ij.y, acc0.y);
+              acc0.z = fmaf(h0, ij.z, acc0.z);
+              acc1.x = fmaf(h1, ij.x, acc1.x);
+              acc1.y = fmaf(h1, ij.y, acc1.y);
+              acc1.z = fmaf(h1, ij.z, acc1.z);
             }
-            epilogue(crow, rl, q0, r0, acc0.x, acc0.y, acc0.z);
-            if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x, acc1.y, acc1.z);
+            epilogue(crow, rl, q0, r0, acc0.x * n0, acc0.y * n0, acc0.z * n0);
+            if (r1 < s) epilogue(crow, rl, q0, r1, acc1.x * n1, acc1.y * n1, acc1.z * n1);
             rc += 64;
           } else if (rem > 16) {
             // one row per lane (32 rows; 17..32 at the end)
@@ -440,13 +469,14 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
             const bool on = rr < rem;
             const int r = rc + rr;
             const float4 ha = on ? crow[4 * r + 2] : z4;
-            float3 acc = on ? one_row(ha, hg_num_f32(ha.w), h, P) : make_float3(0.f, 0.f, 0.f);
+            float3 acc = on ? one_row(ha, 1.f, h, P) : make_float3(0.f, 0.f, 0.f);
             for (int off = w2; off < 32; off <<= 1) {
               acc.x += __shfl_xor_sync(0xFFFFFFFFu, acc.x, off);
               acc.y += __shfl_xor_sync(0xFFFFFFFFu, acc.y, off);
               acc.z += __shfl_xor_sync(0xFFFFFFFFu, acc.z, off);
             }
-            if (on && h == 0) epilogue(crow, rl, q0, r, acc.x, acc.y, acc.z);
+            const float n = hg_num_f32(ha.w);
+            if (on && h == 0) epilogue(crow, rl, q0, r, acc.x * n, acc.y * n, acc.z * n);
             rc += rem;
           }
         }
