@@ -383,8 +383,8 @@ int vpg_trace_fill(const vpg_scene* scene, const vpg_trace_cfg* cfg, const vpg_r
  * record per slot, VPG_SCRATCH_DOUBLES doubles each (a slot-major layout, so
  * a path's stores land in its own slot).  vpg_scatter_records then writes the
  * n = *counter scratch records, in path order (row = rec_start[path -
- * path_begin] + depth), into the SoA `out`.  Any max_depth (a path's slots
- * are linked in a scratch list for the backward i_pt sweep). */
+ * path_begin] + depth), into the SoA `out`, and runs the backward i_pt sweep
+ * (kernels.py:393-408) over them there.  Any max_depth. */
 #define VPG_SCRATCH_DOUBLES 40
 int vpg_trace_capture(const vpg_scene* scene, const vpg_trace_cfg* cfg, double* scratch,
                       int64_t capacity, uint64_t* counter, int64_t* counts, const vpg_paths* paths,

@@ -466,13 +466,13 @@ struct PathResult {
 
 // ------------------------------------------------------- kernels.py
 // Capture mode: records go to scratch slots handed out by a warp-aggregated
-// counter (paths interleave); the path keeps its slot list for the backward
-// sweep and a scatter pass later moves records into path order.
+// counter (paths interleave); a scatter pass later moves them into path
+// order and runs the backward i_pt sweep there (k_ipt_sweep), so the tracing
+// kernel never walks a path's records back through memory.
 struct Capture {
   unsigned long long* counter;
   int64_t capacity;
-  int32_t* link;  // per slot: slot of the same path's previous record, -1 for its first
-  double* aos;    // capacity x kScratchDoubles: one record per slot (see RecView)
+  double* aos;  // capacity x kScratchDoubles: one record per slot (see RecView)
 };
 
 // Record fields.  The capture scratch holds one record per slot, structure
@@ -749,8 +749,6 @@ __device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg
   if (kMode == kCapture) {
     const int64_t got = claim_slot(cap);
     row = got < cap.capacity ? got : -1;
-    // the backward sweep walks the path's slots through the link list
-    if (row >= 0) cap.link[row] = int32_t(st.last_row);
     st.last_row = row;
   }
   if (kStore && row >= 0) {
@@ -796,7 +794,22 @@ __device__ bool path_bounce(PathState<kMode>& st, const vpg_scene& sc, const vpg
   return true;
 }
 
-// Backward i_pt sweep (kernels.py:393-408) and the path-table row.
+// One record's step of the backward i_pt sweep (kernels.py:393-408): i_pt
+// holds the record's direct term until the sweep replaces it with the
+// incoming radiance from the next record; returns this record's outgoing.
+__device__ __forceinline__ void sweep_record(double* ip, const double* kcp, const double* wcp,
+                                             double pp, double* in) {
+  for (int c = 0; c < 3; ++c) {
+    const double dbar = ip[c];
+    ip[c] = in[c];
+    const double kc = kcp[c];
+    const double fpp = pp > 0.0 ? kc * pp / pp : 0.0;
+    in[c] = wcp[c] * (dbar + fpp * in[c]);
+  }
+}
+
+// Backward i_pt sweep (fill mode; capture mode sweeps in k_ipt_sweep) and the
+// path-table row.
 template <int kMode>
 __device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, const vpg_paths& pth,
                                const Capture& cap) {
@@ -809,24 +822,12 @@ __device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, con
   const double* camw = st.camw;
   const double* d0n = st.d0n;
   const double* d0p = st.d0p;
-  if (kStore && n_rec > 0) {  // backward sweep (kernels.py:393-408)
+  if (kMode == kFill && n_rec > 0) {  // backward sweep (kernels.py:393-408)
     double in[3] = {0.0, 0.0, 0.0};
-    int64_t row = st.last_row;
     for (int kk = n_rec - 1; kk >= 0; --kk) {
-      if (kMode != kCapture) row = st.rec_offset + kk;
-      else if (kk < n_rec - 1) row = cap.link[row];
-      if (row < 0) break;  // overflowed capture: the host retries with room
-      const double pp = *rv.f(kFPdfPhase, row);
-      double* ip = rv.f(kFIpt, row);
-      const double* kcp = rv.f(kFCoeff, row);
-      const double* wcp = rv.f(kFWcont, row);
-      for (int c = 0; c < 3; ++c) {
-        const double dbar = ip[c];
-        ip[c] = in[c];
-        const double kc = kcp[c];
-        const double fpp = pp > 0.0 ? kc * pp / pp : 0.0;
-        in[c] = wcp[c] * (dbar + fpp * in[c]);
-      }
+      const int64_t row = st.rec_offset + kk;
+      sweep_record(rv.f(kFIpt, row), rv.f(kFCoeff, row), rv.f(kFWcont, row),
+                   *rv.f(kFPdfPhase, row), in);
     }
   }
   if (kMode != kOff) {
@@ -846,7 +847,7 @@ template <int kMode>
 __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, int64_t px,
                                 int64_t py, int64_t path_id, int64_t rec_offset,
                                 const vpg_records& rec, const vpg_paths& pth, int64_t slot,
-                                const Capture& cap = Capture{nullptr, 0, nullptr, nullptr}) {
+                                const Capture& cap = Capture{nullptr, 0, nullptr}) {
   PathState<kMode> st;
   path_begin(st, sc, cfg, px, py, path_id, rec_offset, slot);
   while (path_bounce(st, sc, cfg, rec, cap)) {
@@ -963,6 +964,53 @@ k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __res
   }
 }
 
+// The backward i_pt sweep of the captured records, now in path order: the
+// thread at a path's last row walks the path's rows back (same operations
+// and order as path_end's fill-mode sweep, so the same bits).  One thread per
+// row and no grid stride: the blocks in flight cover one contiguous window of
+// rows (a grid-stride walk over the 75 M-row arrays thrashes the TLB).
+__global__ void k_ipt_sweep(const vpg_records rec, int64_t n) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const int64_t* __restrict__ pidx = rec.path_idx;
+  double* __restrict__ ipt = rec.i_pt;
+  const double* __restrict__ coeff = rec.coeff;
+  const double* __restrict__ wc = rec.w_cont;
+  const double* __restrict__ pdf = rec.pdf_phase;
+  const int64_t pid = pidx[r];
+  if (r + 1 < n && pidx[r + 1] == pid) return;
+  int64_t first = r;  // the path's first row
+  while (first > 0 && pidx[first - 1] == pid) --first;
+  // each row's fields are loaded before the previous row's results are
+  // stored (the loads of a row do not wait on the stores of the one after)
+  struct Row {
+    double ip[3], kc[3], w[3], pp;
+  };
+  auto load = [&](int64_t row, Row& x) {
+    for (int c = 0; c < 3; ++c) {
+      x.ip[c] = ipt[row * 3 + c];
+      x.kc[c] = coeff[row * 3 + c];
+      x.w[c] = wc[row * 3 + c];
+    }
+    x.pp = pdf[row];
+  };
+  double in[3] = {0.0, 0.0, 0.0};
+  Row cur, nxt;
+  load(r, cur);
+  for (int64_t row = r; row >= first; --row) {
+    if (row > first) load(row - 1, nxt);
+    double out[3];
+    for (int c = 0; c < 3; ++c) {  // sweep_record's operations
+      const double dbar = cur.ip[c];
+      out[c] = in[c];
+      const double fpp = cur.pp > 0.0 ? cur.kc[c] * cur.pp / cur.pp : 0.0;
+      in[c] = cur.w[c] * (dbar + fpp * in[c]);
+    }
+    for (int c = 0; c < 3; ++c) ipt[row * 3 + c] = out[c];
+    cur = nxt;
+  }
+}
+
 // record-free image (render_image_kernel): thread per pixel, samples in order
 __global__ void __launch_bounds__(128) k_trace_image(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                      double* __restrict__ image) {
@@ -1055,9 +1103,8 @@ void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratc
   VPG_REQUIRE(capacity >= 0 && capacity < (int64_t(1) << 31), VPG_ELIMIT,
               "capture scratch capacity must be below 2^31 slots");
   VPG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
-  int32_t* link = scratch_of<int32_t>(s, "capture_link", size_t(capacity) + 1);
   VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts,
-             vpg_records{}, pth, Capture{counter, capacity, link, scratch});
+             vpg_records{}, pth, Capture{counter, capacity, scratch});
 }
 
 void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
@@ -1069,6 +1116,7 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
              slot_of);
   VPG_LAUNCH(k_gather_records, int((n + 127) / 128 < sm_count() * 8 ? (n + 127) / 128 : sm_count() * 8),
              kGatherWarps * 32, 0, s, scratch, n, slot_of, out);
+  VPG_LAUNCH(k_ipt_sweep, int((n + 255) / 256), 256, 0, s, out, n);
 }
 
 // reconstruct_path_estimate (transport/reconstruct.py:52-72): a path's PT
