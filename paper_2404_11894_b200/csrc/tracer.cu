@@ -167,6 +167,34 @@ __device__ V3 surface_normal_at(const vpg_scene& sc, int i, const V3& x) {
 }
 
 // ---------------------------------------------------------- medium.py
+// Division by a divisor known ahead: with y = RN(1/b), q = RN(a y),
+// r = a - b q (exact, one FMA) and RN(q + r y) is the correctly rounded a / b
+// (Markstein's theorem: y within half an ulp of 1/b, q within an ulp of a/b;
+// no overflow or underflow, which the tracking quantities never reach).  So
+// the tracking loops divide with one DMUL and two DFMA instead of a full
+// division sequence each step, bit for bit the same quotients.
+struct Divisor {
+  double b, y;
+  __device__ explicit Divisor(double d) : b(d), y(1.0 / d) {}  // IEEE division: RN(1/d)
+  __device__ __forceinline__ double div(double a) const {
+    const double q = __dmul_rn(a, y);
+    return __fma_rn(__fma_rn(-b, q, a), y, q);
+  }
+};
+
+__device__ __forceinline__ double grid_density_div(const vpg_scene& sc, int k, const V3& x,
+                                                   const Divisor* ext) {
+  const double* bd = sc.med_bounds[k];
+  const int nx = sc.grid_dims[k][0], ny = sc.grid_dims[k][1], nz = sc.grid_dims[k][2];
+  long long ix = (long long)(ext[0].div(x.x - bd[0]) * nx);
+  long long iy = (long long)(ext[1].div(x.y - bd[1]) * ny);
+  long long iz = (long long)(ext[2].div(x.z - bd[2]) * nz);
+  ix = ix < 0 ? 0 : (ix > nx - 1 ? nx - 1 : ix);
+  iy = iy < 0 ? 0 : (iy > ny - 1 ? ny - 1 : iy);
+  iz = iz < 0 ? 0 : (iz > nz - 1 ? nz - 1 : iz);
+  return double(__ldg(sc.grid_data + sc.grid_offset[k] + (iz * ny + iy) * nx + ix));
+}
+
 __device__ double grid_density(const vpg_scene& sc, int k, const V3& x) {
   const double* bd = sc.med_bounds[k];
   const int nx = sc.grid_dims[k][0], ny = sc.grid_dims[k][1], nz = sc.grid_dims[k][2];
@@ -207,15 +235,18 @@ __device__ Flight flight_one_medium(const vpg_scene& sc, int k, const V3& o, con
   const double mu = sc.med_majorant[k];
   if (mu <= 0.0) return f;
   const double scale = sc.med_scale[k];
+  const double* bd = sc.med_bounds[k];
+  const Divisor dmu(mu), three(3.0);
+  const Divisor ext[3] = {Divisor(bd[3] - bd[0]), Divisor(bd[4] - bd[1]), Divisor(bd[5] - bd[2])};
   double t = a;
   while (true) {
     const double u = rng.next();
-    t += -log1p(-u) / mu;
+    t += dmu.div(-log1p(-u));
     if (t >= b) return f;
     const V3 x{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
-    const double dens = grid_density(sc, k, x) * scale;
+    const double dens = grid_density_div(sc, k, x, ext) * scale;
     const double s0 = st[0] * dens, s1 = st[1] * dens, s2 = st[2] * dens;
-    const double sbar = (s0 + s1 + s2) / 3.0;
+    const double sbar = three.div(s0 + s1 + s2);
     const double u2 = rng.next();
     if (u2 * mu < sbar) {
       const double inv = 1.0 / sbar;
@@ -224,10 +255,11 @@ __device__ Flight flight_one_medium(const vpg_scene& sc, int k, const V3& o, con
       f.t = t;
       return f;
     }
-    const double denom = mu - sbar;
-    f.w[0] *= (mu - s0) / denom;
-    f.w[1] *= (mu - s1) / denom;
-    f.w[2] *= (mu - s2) / denom;
+    // sbar < mu here (u2 < 1), so the divisor is positive
+    const Divisor den(mu - sbar);
+    f.w[0] *= den.div(mu - s0);
+    f.w[1] *= den.div(mu - s1);
+    f.w[2] *= den.div(mu - s2);
   }
 }
 
@@ -244,14 +276,17 @@ __device__ void transmittance_one_medium(const vpg_scene& sc, int k, const V3& o
   const double mu = sc.med_majorant[k];
   if (mu <= 0.0) return;
   const double scale = sc.med_scale[k];
+  const double* bd = sc.med_bounds[k];
+  const Divisor dmu(mu);
+  const Divisor ext[3] = {Divisor(bd[3] - bd[0]), Divisor(bd[4] - bd[1]), Divisor(bd[5] - bd[2])};
   double t = a;
   while (true) {
     const double u = rng.next();
-    t += -log1p(-u) / mu;
+    t += dmu.div(-log1p(-u));
     if (t >= b) return;
     const V3 x{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
-    const double dens = grid_density(sc, k, x) * scale;
-    for (int c = 0; c < 3; ++c) w[c] *= 1.0 - st[c] * dens / mu;
+    const double dens = grid_density_div(sc, k, x, ext) * scale;
+    for (int c = 0; c < 3; ++c) w[c] *= 1.0 - dmu.div(st[c] * dens);
     if (w[0] == 0.0 && w[1] == 0.0 && w[2] == 0.0) {
       w[0] = w[1] = w[2] = 0.0;
       return;
