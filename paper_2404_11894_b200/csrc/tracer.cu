@@ -890,9 +890,18 @@ __device__ PathResult trace_one(const vpg_scene& sc, const vpg_trace_cfg& cfg, i
   return path_end(st, rec, pth, cap);
 }
 
+// The record-tracing kernels are latency-bound (density reads, fp64
+// chains): 64 registers and 32 warps per SM (spilling to L1) beat 128
+// registers and 16 warps (C4 capture 190 vs 235 ms, C2 22.3 vs 24.7 ms).  The
+// record-free image kernel (a pixel's samples in order per thread) measured
+// 10 % slower so, and keeps the compiler's choice.
+#ifndef VPG_TRACE_MINB
+#define VPG_TRACE_MINB 8
+#endif
+
 // count / fill over paths [path_begin, path_begin + path_count)
 template <int kMode>
-__global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const vpg_trace_cfg cfg,
+__global__ void __launch_bounds__(128, VPG_TRACE_MINB) k_trace_paths(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                      int64_t* __restrict__ counts,
                                                      const vpg_records rec, const vpg_paths pth) {
   const int64_t spp = cfg.spp;
@@ -912,7 +921,7 @@ __global__ void __launch_bounds__(128) k_trace_paths(const vpg_scene sc, const v
 // A lane whose path ends starts its next path at once (the loop advances
 // every lane by one bounce per iteration), so lanes do not idle until the
 // longest path of their warp has finished.
-__global__ void __launch_bounds__(128, 4) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
+__global__ void __launch_bounds__(128, VPG_TRACE_MINB) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                        int64_t* __restrict__ counts,
                                                        const vpg_records scratch,
                                                        const vpg_paths pth, Capture cap) {
