@@ -517,8 +517,17 @@ __host__ __device__ constexpr int visit_cell(int v) {
 __constant__ uint8_t kVisitOrder[27] = {13, 4,  10, 12, 14, 16, 22, 1, 3,  5,  7,  9,  11, 15,
                                         17, 19, 21, 23, 25, 0,  2,  6, 8, 18, 20, 24, 26};
 constexpr int kNearCells = 7;   // home + faces: always scanned
-constexpr int kCandCap = 240;   // candidate centers staged per warp
-constexpr int kRunCap = 256;    // points put in octant order at a time
+#ifndef VPG_ASSIGN_CAND
+#define VPG_ASSIGN_CAND 240
+#endif
+#ifndef VPG_ASSIGN_RUN
+#define VPG_ASSIGN_RUN 256
+#endif
+#ifndef VPG_ASSIGN_MINB
+#define VPG_ASSIGN_MINB 3
+#endif
+constexpr int kCandCap = VPG_ASSIGN_CAND;  // candidate centers staged per warp
+constexpr int kRunCap = VPG_ASSIGN_RUN;    // points put in octant order at a time
 
 // (out of line: only hashed grids need it, and three inlined divisions per
 // call site would bloat the assignment loop out of the instruction cache)
@@ -549,7 +558,7 @@ __device__ __forceinline__ int octant_of(double x, double y, double z, const Gri
 // order makes the 32 points of a batch neighbours, so they skip the same
 // cells.  The candidates are staged in shared memory once per run, or, for a
 // crowded neighbourhood (more than kCandCap), cell by cell for each batch.
-__global__ void __launch_bounds__(kAssignWarps * 32, 3)
+__global__ void __launch_bounds__(kAssignWarps * 32, VPG_ASSIGN_MINB)
 k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ pos, GridParams gp,
                CellIndex table, const double4* __restrict__ spos,
                const int32_t* __restrict__ sorted_ids, int oct_in_ids,
@@ -1847,7 +1856,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       }, s);
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
-      VPG_LAUNCH(k_assign_cells, sm_count() * 3, kAssignWarps * 32, kAssignSmem, s, rows_p, p.row_off,
+      VPG_LAUNCH(k_assign_cells, sm_count() * VPG_ASSIGN_MINB, kAssignWarps * 32, kAssignSmem, s, rows_p, p.row_off,
                  rec.pos, gp, cidx, spos.get(), pids_sorted, int(poct != nullptr), run_start, run_len,
                  scalars.get() + 1, assign_c, fb_list, scalars.get());
       int32_t* far_list = scratch_of<int32_t>(s, "far_list", p.n + 1);
@@ -2467,7 +2476,7 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
     VPG_LAUNCH(k_center_table_ends, grid_for(m, block), block, 0, s, skeys.get(), m, gp,
                table.get());
   ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
-  VPG_LAUNCH(k_assign_cells, sm_count() * 3, kAssignWarps * 32, kAssignSmem, s, nullptr, 0, pos, gp,
+  VPG_LAUNCH(k_assign_cells, sm_count() * VPG_ASSIGN_MINB, kAssignWarps * 32, kAssignSmem, s, nullptr, 0, pos, gp,
              cidx, spos.get(), pids_sorted, 0, run_start, run_len,
              scalars.get() + 1, assign,
              fb_list, scalars.get());
