@@ -502,7 +502,7 @@ struct PathResult {
 // ------------------------------------------------------- kernels.py
 // Capture mode: records go to scratch slots handed out by a warp-aggregated
 // counter (paths interleave); a scatter pass later moves them into path
-// order and runs the backward i_pt sweep there (k_ipt_sweep), so the tracing
+// order and runs the backward i_pt sweep there (k_gather_records), so the tracing
 // kernel never walks a path's records back through memory.
 struct Capture {
   unsigned long long* counter;
@@ -843,7 +843,7 @@ __device__ __forceinline__ void sweep_record(double* ip, const double* kcp, cons
   }
 }
 
-// Backward i_pt sweep (fill mode; capture mode sweeps in k_ipt_sweep) and the
+// Backward i_pt sweep (fill mode; capture mode sweeps in k_gather_records) and the
 // path-table row.
 template <int kMode>
 __device__ PathResult path_end(PathState<kMode>& st, const vpg_records& rec, const vpg_paths& pth,
@@ -964,13 +964,20 @@ __global__ void k_slot_of_row(const double* __restrict__ aos, int64_t n,
 }
 
 // Path-ordered SoA records from the slot-major scratch: a warp stages 32
-// records (10 full sectors each) in shared memory, then writes every field
-// of its 32 consecutive rows coalesced (lane = row).
+// records (10 full sectors each) in shared memory, runs the backward i_pt
+// sweep of every path lying inside those 32 rows there, then writes every
+// field of its rows coalesced (lane = row).  A path reaching back before the
+// window's first row is listed (its end row) for k_ipt_sweep_listed.
 constexpr int kGatherWarps = 4;
 constexpr int kSlotStride = VPG_SCRATCH_DOUBLES + 1;  // odd stride: conflict-free row reads
+__device__ __forceinline__ long long slot_path(const double* __restrict__ aos,
+                                               const int32_t* __restrict__ slot_of, int64_t row) {
+  return __double_as_longlong(aos[int64_t(slot_of[row]) * VPG_SCRATCH_DOUBLES + kFPath]);
+}
 __global__ void __launch_bounds__(kGatherWarps * 32)
 k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __restrict__ slot_of,
-                 const vpg_records dst) {
+                 const vpg_records dst, int32_t* __restrict__ listed,
+                 int32_t* __restrict__ n_listed) {
   __shared__ double buf[kGatherWarps][32 * kSlotStride];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* b = buf[wid];
@@ -980,6 +987,26 @@ k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __res
     for (int idx = lane; idx < cnt * VPG_SCRATCH_DOUBLES; idx += 32) {
       const int j = idx / VPG_SCRATCH_DOUBLES, w = idx - j * VPG_SCRATCH_DOUBLES;
       b[j * kSlotStride + w] = __ldcs(aos + int64_t(slot_of[base + j]) * VPG_SCRATCH_DOUBLES + w);
+    }
+    __syncwarp();
+    if (lane < cnt) {
+      const long long pid = __double_as_longlong(b[lane * kSlotStride + kFPath]);
+      const long long next =
+          lane + 1 < cnt ? __double_as_longlong(b[(lane + 1) * kSlotStride + kFPath])
+                         : (base + cnt < n ? slot_path(aos, slot_of, base + cnt) : -1);
+      if (next != pid) {  // the path ends at this row
+        int j = lane;
+        while (j > 0 && __double_as_longlong(b[(j - 1) * kSlotStride + kFPath]) == pid) --j;
+        if (j == 0 && base > 0 && slot_path(aos, slot_of, base - 1) == pid) {
+          listed[atomicAdd(n_listed, 1)] = int32_t(base + lane);
+        } else {
+          double in[3] = {0.0, 0.0, 0.0};
+          for (int row = lane; row >= j; --row) {
+            double* q = b + row * kSlotStride;
+            sweep_record(q + kFIpt, q + kFCoeff, q + kFWcont, q[kFPdfPhase], in);
+          }
+        }
+      }
     }
     __syncwarp();
     if (lane < cnt) {
@@ -1008,21 +1035,21 @@ k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __res
   }
 }
 
-// The backward i_pt sweep of the captured records, now in path order: the
-// thread at a path's last row walks the path's rows back (same operations
-// and order as path_end's fill-mode sweep, so the same bits).  One thread per
-// row and no grid stride: the blocks in flight cover one contiguous window of
-// rows (a grid-stride walk over the 75 M-row arrays thrashes the TLB).
-__global__ void k_ipt_sweep(const vpg_records rec, int64_t n) {
-  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (r >= n) return;
+// The backward i_pt sweep of the paths k_gather_records listed (those
+// crossing the start of a 32-row window), over the path-ordered records: the
+// thread of a listed end row walks the path's rows back (same operations and
+// order as path_end's fill-mode sweep, so the same bits).
+__global__ void k_ipt_sweep_listed(const vpg_records rec, const int32_t* __restrict__ listed,
+                                   const int32_t* __restrict__ n_listed) {
+  const int64_t li = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (li >= *n_listed) return;
+  const int64_t r = listed[li];
   const int64_t* __restrict__ pidx = rec.path_idx;
   double* __restrict__ ipt = rec.i_pt;
   const double* __restrict__ coeff = rec.coeff;
   const double* __restrict__ wc = rec.w_cont;
   const double* __restrict__ pdf = rec.pdf_phase;
   const int64_t pid = pidx[r];
-  if (r + 1 < n && pidx[r + 1] == pid) return;
   int64_t first = r;  // the path's first row
   while (first > 0 && pidx[first - 1] == pid) --first;
   // each row's fields are loaded before the previous row's results are
@@ -1158,9 +1185,13 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
   int32_t* slot_of = scratch_of<int32_t>(s, "slot_of_row", size_t(n));
   VPG_LAUNCH(k_slot_of_row, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin,
              slot_of);
+  const int64_t max_listed = (n + 31) / 32 + 1;
+  int32_t* listed = scratch_of<int32_t>(s, "sweep_listed", size_t(max_listed) + 1);
+  VPG_CUDA(cudaMemsetAsync(listed + max_listed, 0, sizeof(int32_t), s));
   VPG_LAUNCH(k_gather_records, int((n + 127) / 128 < sm_count() * 8 ? (n + 127) / 128 : sm_count() * 8),
-             kGatherWarps * 32, 0, s, scratch, n, slot_of, out);
-  VPG_LAUNCH(k_ipt_sweep, int((n + 255) / 256), 256, 0, s, out, n);
+             kGatherWarps * 32, 0, s, scratch, n, slot_of, out, listed, listed + max_listed);
+  VPG_LAUNCH(k_ipt_sweep_listed, int((max_listed + 255) / 256), 256, 0, s, out, listed,
+             listed + max_listed);
 }
 
 // reconstruct_path_estimate (transport/reconstruct.py:52-72): a path's PT
