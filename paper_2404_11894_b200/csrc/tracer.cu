@@ -1174,8 +1174,16 @@ void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratc
   VPG_REQUIRE(capacity >= 0 && capacity < (int64_t(1) << 31), VPG_ELIMIT,
               "capture scratch capacity must be below 2^31 slots");
   VPG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
-  VPG_LAUNCH(k_trace_capture, trace_grid(cfg.path_count), 128, 0, s, sc, cfg, counts,
-             vpg_records{}, pth, Capture{counter, capacity, scratch});
+  // exactly one wave of resident blocks: every lane regenerates paths until
+  // the frame is done, so a second wave would only start on the SMs the
+  // first frees, late (C4: 168 ms with one wave, 189 with two)
+  int per_sm = 0;
+  VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, reinterpret_cast<const void*>(k_trace_capture), 128, 0));
+  const int64_t wave = int64_t(std::max(per_sm, 1)) * sm_count();
+  const int grid = int(std::min<int64_t>(wave, (cfg.path_count + 127) / 128));
+  VPG_LAUNCH(k_trace_capture, std::max(grid, 1), 128, 0, s, sc, cfg, counts, vpg_records{}, pth,
+             Capture{counter, capacity, scratch});
 }
 
 void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
