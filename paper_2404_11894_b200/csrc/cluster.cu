@@ -1425,6 +1425,68 @@ void cub_call(F&& f, cudaStream_t s) {
   count_launch(2);
 }
 
+// The points bucketed by cell for k_assign_cells: ids in cell order (the
+// octant in the top bits when oct_in_ids), one run per occupied cell, the run
+// count in *n_runs (device).  A counting sort over the dense packed cell keys
+// when the padded grid is small; a radix sort of the (hashed) keys otherwise.
+struct PointCells {
+  int32_t *pids_sorted, *run_start, *run_len;
+  bool oct_in_ids;
+};
+PointCells sort_points_by_cell(const int32_t* rows_p, int64_t row_off, int64_t n, const double* pos,
+                               const GridParams& gp, int32_t* n_runs, const std::string& tag,
+                               cudaStream_t s) {
+  const int block = 256;
+  PointCells pc{};
+  auto* pkeys = scratch_of<unsigned long long>(s, (tag + "pkeys").c_str(), n);
+  auto* pkeys_sorted = scratch_of<unsigned long long>(s, (tag + "pkeys_sorted").c_str(), n);
+  int32_t* pids = scratch_of<int32_t>(s, (tag + "pids").c_str(), n);
+  pc.pids_sorted = scratch_of<int32_t>(s, (tag + "pids_sorted").c_str(), n);
+  pc.run_start = scratch_of<int32_t>(s, (tag + "run_start").c_str(), n + 1);
+  pc.run_len = scratch_of<int32_t>(s, (tag + "run_len").c_str(), n + 1);
+  const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
+  if (gp.packed && cells <= 4.0 * double(n) + 4096.0 && cells < 2.0e9) {
+    const int64_t nc = int64_t(cells);
+    int32_t* counts = scratch_of<int32_t>(s, (tag + "cell_counts").c_str(), size_t(nc) + 1);
+    int32_t* offs = scratch_of<int32_t>(s, (tag + "cell_offs").c_str(), size_t(nc) + 1);
+    int32_t* pkey = reinterpret_cast<int32_t*>(pkeys);
+    uint8_t* poct = nullptr;  // octants (fewer than 2^29 points only)
+    if (n < (int64_t(1) << kOctShift)) poct = scratch_of<uint8_t>(s, (tag + "cell_oct").c_str(), n);
+    pc.oct_in_ids = poct != nullptr;
+    VPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nc + 1), s));
+    VPG_LAUNCH(k_cell_count, grid_for(n, block), block, 0, s, rows_p, row_off, n, pos, gp, counts,
+               pkey, poct);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, counts, offs, int(nc + 1), s);
+    }, s);
+    VPG_LAUNCH(k_cell_scatter, grid_for(n, block), block, 0, s, n, pkey, poct, offs, counts,
+               pc.pids_sorted);
+    int32_t* sel = reinterpret_cast<int32_t*>(pkeys_sorted);
+    cub::CountingInputIterator<int32_t> ci(0);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceSelect::If(t, b, ci, sel, n_runs, int(nc), CellNonEmpty{offs}, s);
+    }, s);
+    VPG_LAUNCH(k_cell_runs, grid_for(n, block), block, 0, s, sel, n_runs, offs, pc.run_start,
+               pc.run_len);
+  } else {
+    const int end_bits = gp.packed ? packed_key_bits(gp) : 64;
+    VPG_LAUNCH(k_point_keys, grid_for(n, block), block, 0, s, rows_p, row_off, n, pos, gp, pkeys,
+               pids);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pc.pids_sorted,
+                                             int(n), 0, end_bits, s);
+    }, s);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, pc.run_len, n_runs,
+                                                int(n), s);
+    }, s);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, pc.run_len, pc.run_start, int(n), s);
+    }, s);
+  }
+  return pc;
+}
+
 // VPG_DEBUG_TIMING=1 prints sub-stage wall times of the build to stderr.
 struct DebugClock {
   bool on;
@@ -1707,59 +1769,13 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
 
     // device: cell keys of the points and their sort, independent of the
     // center draw, overlap the host RNG
-    unsigned long long *pkeys = nullptr, *pkeys_sorted = nullptr;
-    int32_t *pids = nullptr, *pids_sorted = nullptr, *run_start = nullptr, *run_len = nullptr;
-    uint8_t* poct = nullptr;  // octants (counting sort of < 2^29 points only)
     int end_bits = 64;
-    if (m > 1) {
-      pkeys = scratch_of<unsigned long long>(s, "pkeys", p.n);
-      pkeys_sorted = scratch_of<unsigned long long>(s, "pkeys_sorted", p.n);
-      pids = scratch_of<int32_t>(s, "pids", p.n);
-      pids_sorted = scratch_of<int32_t>(s, "pids_sorted", p.n);
-      run_start = scratch_of<int32_t>(s, "run_start", p.n + 1);
-      run_len = scratch_of<int32_t>(s, "run_len", p.n + 1);
-      if (gp.packed) end_bits = packed_key_bits(gp);
-      const int64_t nn = p.n;
-      const double cells = double(gp.dims[0] + 4) * double(gp.dims[1] + 4) * double(gp.dims[2] + 4);
-      if (gp.packed && cells <= 4.0 * double(p.n) + 4096.0 && cells < 2.0e9) {
-        // counting sort over the dense cell keys
-        const int64_t nc = int64_t(cells);
-        int32_t* counts = scratch_of<int32_t>(s, "cell_counts", size_t(nc) + 1);
-        int32_t* offs = scratch_of<int32_t>(s, "cell_offs", size_t(nc) + 1);
-        int32_t* pkey = reinterpret_cast<int32_t*>(pkeys);
-        VPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nc + 1), s));
-        if (p.n < (int64_t(1) << kOctShift)) poct = scratch_of<uint8_t>(s, "cell_oct", p.n);
-        VPG_LAUNCH(k_cell_count, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
-                   rec.pos, gp, counts, pkey, poct);
-        cub_call([&](void* t, size_t& b) {
-          return cub::DeviceScan::ExclusiveSum(t, b, counts, offs, int(nc + 1), s);
-        }, s);
-        VPG_LAUNCH(k_cell_scatter, grid_for(p.n, block), block, 0, s, p.n, pkey, poct, offs, counts,
-                   pids_sorted);
-        int32_t* sel = reinterpret_cast<int32_t*>(pkeys_sorted);
-        cub::CountingInputIterator<int32_t> ci(0);
-        cub_call([&](void* t, size_t& b) {
-          return cub::DeviceSelect::If(t, b, ci, sel, scalars.get() + 1, int(nc), CellNonEmpty{offs},
-                                       s);
-        }, s);
-        VPG_LAUNCH(k_cell_runs, grid_for(p.n, block), block, 0, s, sel, scalars.get() + 1, offs,
-                   run_start, run_len);
-      } else {
-        VPG_LAUNCH(k_point_keys, grid_for(p.n, block), block, 0, s, rows_p, p.row_off, p.n,
-                   rec.pos, gp, pkeys, pids);
-        cub_call([&](void* t, size_t& b) {
-          return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted,
-                                                 int(nn), 0, end_bits, s);
-        }, s);
-        cub_call([&](void* t, size_t& b) {
-          return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
-                                                    scalars.get() + 1, int(nn), s);
-        }, s);
-        cub_call([&](void* t, size_t& b) {
-          return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(nn), s);
-        }, s);
-      }
-    }
+    if (gp.packed) end_bits = packed_key_bits(gp);
+    PointCells pc{};
+    if (m > 1) pc = sort_points_by_cell(rows_p, p.row_off, p.n, rec.pos, gp, scalars.get() + 1, "", s);
+    int32_t* pids_sorted = pc.pids_sorted;
+    int32_t* run_start = pc.run_start;
+    int32_t* run_len = pc.run_len;
 
     // m centers = Generator.choice(n, m) (clustering.py:51)
     DBuf<int32_t> d_local(m, s);
@@ -1857,7 +1873,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
       VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, sizeof(int32_t), s));
       ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
       VPG_LAUNCH(k_assign_cells, sm_count() * VPG_ASSIGN_MINB, kAssignWarps * 32, kAssignSmem, s, rows_p, p.row_off,
-                 rec.pos, gp, cidx, spos.get(), pids_sorted, int(poct != nullptr), run_start, run_len,
+                 rec.pos, gp, cidx, spos.get(), pids_sorted, int(pc.oct_in_ids), run_start, run_len,
                  scalars.get() + 1, assign_c, fb_list, scalars.get());
       int32_t* far_list = scratch_of<int32_t>(s, "far_list", p.n + 1);
       auto* far_d = scratch_of<unsigned long long>(s, "far_d", p.n + 1);
@@ -2428,27 +2444,8 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
   DBuf<int32_t> scalars(4, s);
   DBuf<int32_t> far_count(1, s);
   VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, scalars.bytes(), s));
-  unsigned long long* pkeys = scratch_of<unsigned long long>(s, "an_pkeys", n);
-  unsigned long long* pkeys_sorted = scratch_of<unsigned long long>(s, "an_pkeys_sorted", n);
-  int32_t* pids = scratch_of<int32_t>(s, "an_pids", n);
-  int32_t* pids_sorted = scratch_of<int32_t>(s, "an_pids_sorted", n);
-  int32_t* run_start = scratch_of<int32_t>(s, "an_run_start", n + 1);
-  int32_t* run_len = scratch_of<int32_t>(s, "an_run_len", n + 1);
   int32_t* fb_list = scratch_of<int32_t>(s, "an_fb_list", n + 1);
-  VPG_LAUNCH(k_point_keys, grid_for(n, block), block, 0, s, nullptr, 0, n, pos, gp, pkeys, pids);
-  int end_bits = 64;
-  if (gp.packed) end_bits = packed_key_bits(gp);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, pkeys, pkeys_sorted, pids, pids_sorted, int(n), 0,
-                                           end_bits, s);
-  }, s);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceRunLengthEncode::Encode(t, b, pkeys_sorted, pkeys, run_len,
-                                              scalars.get() + 1, int(n), s);
-  }, s);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, run_len, run_start, int(n), s);
-  }, s);
+  const PointCells pc = sort_points_by_cell(nullptr, 0, n, pos, gp, scalars.get() + 1, "an_", s);
   DBuf<unsigned long long> keys(m, s), skeys(m, s);
   DBuf<int32_t> ids(m, s), sids(m, s);
   DBuf<double4> spos(m, s);
@@ -2477,7 +2474,7 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
                table.get());
   ensure_dynamic_smem(reinterpret_cast<const void*>(k_assign_cells), kAssignSmem);
   VPG_LAUNCH(k_assign_cells, sm_count() * VPG_ASSIGN_MINB, kAssignWarps * 32, kAssignSmem, s, nullptr, 0, pos, gp,
-             cidx, spos.get(), pids_sorted, 0, run_start, run_len,
+             cidx, spos.get(), pc.pids_sorted, int(pc.oct_in_ids), pc.run_start, pc.run_len,
              scalars.get() + 1, assign,
              fb_list, scalars.get());
   int32_t* far_list = scratch_of<int32_t>(s, "an_far_list", n + 1);

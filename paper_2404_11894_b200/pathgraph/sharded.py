@@ -390,7 +390,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         # scan across the shards (no (world, m) all-gather)
         before, gsize = comm.exclusive_scan(hist)
         # rank of each row among its group's members (ascending global row)
-        srt = torch.argsort(a64, stable=True)
+        srt = torch.sort(assign, stable=True).indices  # 32-bit keys: a 4-pass radix sort
         first = torch.cumsum(hist, 0) - hist
         lrank = torch.empty(my_n, dtype=torch.int64, device=dev)
         lrank[srt] = torch.arange(my_n, device=dev) - first[a64[srt]]
