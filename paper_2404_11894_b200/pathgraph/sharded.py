@@ -390,10 +390,10 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         # scan across the shards (no (world, m) all-gather)
         before, gsize = comm.exclusive_scan(hist)
         # rank of each row among its group's members (ascending global row)
-        srt = torch.sort(assign, stable=True).indices  # 32-bit keys: a 4-pass radix sort
+        sv, srt = torch.sort(assign, stable=True)  # 32-bit keys: a 4-pass radix sort
         first = torch.cumsum(hist, 0) - hist
         lrank = torch.empty(my_n, dtype=torch.int64, device=dev)
-        lrank[srt] = torch.arange(my_n, device=dev) - first[a64[srt]]
+        lrank[srt] = torch.arange(my_n, device=dev) - first[sv.to(torch.int64)]
         over = torch.nonzero(gsize > max_size).reshape(-1)
         n_over = int(over.numel())
         # reference numbering: non-empty groups in center order, then the
@@ -405,9 +405,13 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         cl_pos = cpos[nonempty].clone()
         is_over = torch.zeros(m, dtype=torch.bool, device=dev)
         is_over[over] = True
+        # rows of the groups that need no split: cluster and rank at once
+        # (dense where/index_copy, no boolean indexing and its host syncs;
+        # the oversize groups' rows stay -1 until the split loop below)
         plain = ~is_over[a64]
-        row_cluster[rows[plain]] = cid_of_j[a64[plain]]
-        row_rank[rows[plain]] = before[a64[plain]] + lrank[plain]
+        minus = torch.full_like(lrank, -1)
+        row_cluster.index_copy_(0, rows, torch.where(plain, cid_of_j[a64], minus))
+        row_rank.index_copy_(0, rows, torch.where(plain, before[a64] + lrank, minus))
         _tick("cd: groups")
         appended = []
         if n_over:
@@ -636,15 +640,17 @@ class ShardedPathGraph:
         keep = dest_shard == me
         li = torch.nonzero(keep).reshape(-1)
         lr = dest_row[li]
-        # placed in destination order: a gather of the sources (random reads)
-        # and sequential writes instead of a random scatter
-        lr, by_row = torch.sort(lr)
-        li = li[by_row]
         whole = lr.numel() == n_own  # every owned row is local (one shard)
-        for name, _, _ in _payload_columns():
-            if whole:
-                torch.index_select(cols[name], 0, li, out=own[name])
-            else:
+        if whole:
+            # placed in destination order: the destination rows are a
+            # permutation, so its inverse (one scatter of indices) turns the
+            # move into gathers of the sources (random reads, sequential writes)
+            src = torch.empty(n_own, dtype=torch.int64, device="cuda")
+            src[lr] = li
+            for name, _, _ in _payload_columns():
+                torch.index_select(cols[name], 0, src, out=own[name])
+        else:
+            for name, _, _ in _payload_columns():
                 own[name][lr] = cols[name][li]
         if world > 1:
             ri = torch.nonzero(~keep).reshape(-1)
