@@ -127,7 +127,10 @@ __device__ __forceinline__ float w_recomputed(const float4* __restrict__ rows, i
 //    to HBM, with the residual maxima of solve.py:54-61.  The old I[par] is
 //    recomputed from the previous W*I (same arithmetic as when it was stored)
 //    instead of gathered.
-constexpr int kConsumers = 24;
+#ifndef VPG_SOLVE_CONSUMERS
+#define VPG_SOLVE_CONSUMERS 24
+#endif
+constexpr int kConsumers = VPG_SOLVE_CONSUMERS;
 constexpr int kMaxStages = 4;  // the stage count is chosen per graph (graph.cuh)
 
 // Residual, tol break and 3-growth divergence of iteration t (solve.py:80-94),
