@@ -1,7 +1,9 @@
 """GPU tracer vs the reference tracer's records and images (same splitmix64
-streams, fp64, no FMA): record counts per path equal, record values equal up
-to the last-ulp differences of the device libm, PT images within a tight
-RMSE band of the reference's CPU render at equal spp."""
+streams, fp64, no FMA): every path's record count equal, record values equal
+up to the last-ulp differences of the device libm (largest relative
+difference ~3e-12 on the golden scenes, ~5e-11 against the C oracle; see
+tools/tracer_parity_stats.py), PT images within a tight RMSE band of the
+reference's CPU render at equal spp."""
 
 import numpy as np
 import pytest
@@ -46,9 +48,9 @@ def test_records_match_reference_tracer(cuda, name):
     ref_rec, ref_paths = O.load_golden_records(z)
     cnt, ref_cnt = out.paths.rec_count, ref_paths["rec_count"]
     same = cnt == ref_cnt
-    # a path may only diverge when a random draw lands within an ulp of a
-    # branch threshold; require >= 99.5% identical record counts
-    assert same.mean() >= 0.995, f"{(~same).sum()} of {cnt.size} paths differ in length"
+    # every path takes the reference's branches (a divergence would need a
+    # draw within an ulp of a threshold; none on these scenes)
+    assert same.all(), f"{(~same).sum()} of {cnt.size} paths differ in length"
     rows = np.concatenate([np.arange(s, s + c) for s, c in
                            zip(out.paths.rec_start[same], cnt[same])]) if same.any() else []
     ref_rows = np.concatenate([np.arange(s, s + c) for s, c in
@@ -57,14 +59,16 @@ def test_records_match_reference_tracer(cuda, name):
         assert np.array_equal(getattr(out.records, f)[rows], ref_rec[f][ref_rows]), f
     worst = {f: float(_rel(getattr(out.records, f)[rows], ref_rec[f][ref_rows]).max(initial=0))
              for f in VEC}
-    # per-record values agree to ~1e-13 except where an ulp flip of a
-    # transcendental propagated; the 99.9th percentile must be tight
+    # values are not all bit-identical (CUDA's log1p / exp / sin / cos
+    # differ from glibc's by an ulp now and then: ~60 % of the phase
+    # directions match bit for bit); the largest relative difference over
+    # every record of these scenes is ~3e-12 (tools/tracer_parity_stats.py)
     for f in VEC:
         r = _rel(getattr(out.records, f)[rows], ref_rec[f][ref_rows])
-        assert np.quantile(r, 0.999) < 1e-9, (f, worst)
+        assert float(r.max(initial=0)) < 1e-10, (f, worst)
     for f in ("cam_weight", "d_cam", "direct0", "pt_estimate"):
         r = _rel(getattr(out.paths, f)[same], ref_paths[f][same])
-        assert np.quantile(r, 0.999) < 1e-9, f
+        assert np.quantile(r, 0.999) < 1e-10 and float(r.max(initial=0)) < 1e-8, f
 
 
 @pytest.mark.parametrize("name", list(TRACE_CASES))
@@ -179,13 +183,12 @@ def test_device_pipeline_matches_oracles(cuda, name):
     out = render_pt(scene, cfg, with_records=True)
     ref_rec, ref_paths = T.trace_records(scene, cfg)
     same = out.paths.rec_count == ref_paths["rec_count"]
-    assert same.mean() >= 0.995, f"{(~same).sum()} paths differ in length"
-    if same.all():  # identical record sets: the graph must match the oracle exactly
-        for f in INT:
-            assert np.array_equal(getattr(out.records, f), ref_rec[f]), f
-        for f in VEC:
-            r = _rel(getattr(out.records, f), ref_rec[f])
-            assert np.quantile(r, 0.999) < 1e-9, f
+    assert same.all(), f"{(~same).sum()} paths differ in length"
+    for f in INT:
+        assert np.array_equal(getattr(out.records, f), ref_rec[f]), f
+    for f in VEC:  # libm ulp differences only: ~5e-11 at most on these scenes
+        r = _rel(getattr(out.records, f), ref_rec[f])
+        assert float(r.max(initial=0)) < 1e-9, f
     w, h = scene.camera.resolution
     g = build_graph(out, 16, seed=seed)
     res = solve(g, iterations=8, tol=0.0)
