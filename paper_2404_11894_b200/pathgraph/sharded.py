@@ -315,6 +315,23 @@ def _tick(label):
     _T["t"] = now
 
 
+def _local_class_keys(keys):
+    """np.unique of this shard's class keys (kind << 32 | class_id), ascending:
+    one min/max pass when every row has the same key (the usual single
+    class), a presence map over the key range when it is small, else a sort."""
+    import torch
+
+    lo, hi = torch.aminmax(keys)
+    lo, hi = int(lo), int(hi)
+    if lo == hi:
+        return keys[:1].clone()
+    if hi - lo < 1 << 20:
+        seen = torch.zeros(hi - lo + 1, dtype=torch.bool, device=keys.device)
+        seen.index_fill_(0, keys - lo, True)
+        return torch.nonzero(seen).reshape(-1) + lo
+    return torch.unique(keys)
+
+
 def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_size: int,
                         rng: np.random.Generator) -> GlobalClusters:
     """cluster_points (clustering.py:28-148) over the shards' records without
@@ -334,7 +351,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
     n = int(pos.shape[0])
     _tick("cd: start")
     keys = (kind.to(torch.int64) << 32) | class_id.to(torch.int64)
-    loc_keys = torch.unique(keys) if n else keys[:0]
+    loc_keys = _local_class_keys(keys) if n else keys[:0]
     cnt = comm.all_gather_ints([int(loc_keys.numel())])[:, 0].tolist()
     all_keys = comm.all_gather_rows(loc_keys, cnt)
     classes = sorted(set(int(x) for x in all_keys.cpu().tolist()))
@@ -346,7 +363,10 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
     lib = N.lib()
     stream = N.stream_handle()
     for key in classes:
-        rows = torch.nonzero(keys == key).reshape(-1)  # ascending = ascending global row
+        if len(classes) == 1:  # every row (no class filter, no copy of pos)
+            rows = torch.arange(n, device=dev)
+        else:
+            rows = torch.nonzero(keys == key).reshape(-1)  # ascending = ascending global row
         counts = comm.all_gather_ints([int(rows.numel())])[:, 0]
         n_c = int(counts.sum())
         pref = int(counts[:me].sum())
@@ -370,7 +390,7 @@ def cluster_distributed(comm: ShardComm, pos, kind, class_id, g0: int, cluster_s
         cpos[order] = got[:, 1:4]
         _tick("cd: centers")
         # class bounding box (sizes the hash grid like the single-device build)
-        p_c = pos[rows].contiguous()
+        p_c = pos.contiguous() if len(classes) == 1 else pos[rows].contiguous()
         lo = p_c.min(0).values if my_n else torch.full((3,), float("inf"), dtype=torch.float64,
                                                          device=dev)
         hi = p_c.max(0).values if my_n else torch.full((3,), -float("inf"), dtype=torch.float64,
