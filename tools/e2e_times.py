@@ -8,15 +8,16 @@ from paper_2404_11894_b200.transport import render_pt
 from paper_2404_11894_b200.transport.records import PathSoA, RecordSoA, TraceOutput
 from paper_2404_11894_b200.pathgraph.pipeline import solve_from_records
 
-wl = WORKLOADS["C2"]
+wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 cfg = RenderConfig(spp=wl.spp, max_depth=wl.max_depth, seed=0)
 tr = render_pt(wl.scene(), cfg, with_records=True)
+W, H = tr.width, tr.height
 hr = RecordSoA(**tr.records.host_arrays()).pin_memory()
 hp = PathSoA(**tr.paths.host_arrays()).pin_memory()
 del tr
 
 def fresh():
-    t = TraceOutput(None, RecordSoA(**hr.host_arrays()), PathSoA(**hp.host_arrays()), 512, 512, 8)
+    t = TraceOutput(None, RecordSoA(**hr.host_arrays()), PathSoA(**hp.host_arrays()), W, H, wl.spp)
     t.records._pinned = hr._pinned
     t.paths._pinned = hp._pinned
     return t
@@ -31,7 +32,7 @@ for rep in range(3):
 for rep in range(3):
     t = fresh()
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    img, g, r = solve_from_records(t, 32, iterations=10, tol=0.0)
+    img, g, r = solve_from_records(t, 32, iterations=wl.iterations, tol=0.0)
     torch.cuda.synchronize(); t1 = time.perf_counter()
     print(f"solve_from_records: {(t1-t0)*1e3:.1f} ms")
     del g, r, t
