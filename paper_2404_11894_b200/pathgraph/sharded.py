@@ -57,10 +57,12 @@ class ShardComm:
 
     NCCL exchanges device tensors directly; any other backend (gloo) stages
     through host memory.  With one process (or no initialised group) every
-    call is a local no-op, so the same code runs a single shard.
+    call is a local no-op, so the same code runs a single shard --
+    `loopback=True` sends them through the group anyway (a one-rank NCCL group
+    then runs every NCCL call of the N > 1 path on one GPU).
     """
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, loopback=False):
         import torch.distributed as dist
 
         self.group = group
@@ -72,6 +74,8 @@ class ShardComm:
         else:
             self.dist, self.rank, self.world, self.backend = None, 0, 1, "none"
         self.staged = self.backend != "nccl"
+        # skip the collectives only for a single rank that is not looped back
+        self.local = self.world == 1 and not (loopback and self.dist is not None)
 
     def _out(self, t):
         return t.cpu() if self.staged else t
@@ -82,7 +86,7 @@ class ShardComm:
 
         send_counts = [int(c) for c in send_counts]
         recv_counts = [int(c) for c in recv_counts]
-        if self.world == 1:
+        if self.local:
             return send.clone()
         src = self._out(send.contiguous())
         out = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype,
@@ -95,7 +99,7 @@ class ShardComm:
         import torch
 
         counts = [int(c) for c in counts]
-        if self.world == 1:
+        if self.local:
             return t.clone()
         mx = max(max(counts), 1)
         pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -110,7 +114,7 @@ class ShardComm:
         import torch
 
         v = torch.tensor([int(x) for x in values], dtype=torch.int64)
-        if self.world == 1:
+        if self.local:
             return v.numpy()[None, :]
         dev = "cpu" if self.staged else "cuda"
         v = v.to(dev)
@@ -128,7 +132,7 @@ class ShardComm:
         import torch
 
         m = int(v.shape[0])
-        if self.world == 1:
+        if self.local:
             return torch.zeros_like(v), v.clone()
         if self.world == 2:  # the all-gather is already as small
             rows = self.all_gather_rows(v.reshape(1, -1), [1, 1])
@@ -154,7 +158,7 @@ class ShardComm:
 
     def all_reduce_max_(self, t):
         """In-place elementwise max over the shards."""
-        if self.world == 1:
+        if self.local:
             return t
         src = self._out(t)
         self.dist.all_reduce(src, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -268,7 +272,7 @@ class HaloExchange:
 
     def exchange(self, i_out):
         """i_out: (n + n_halo, C) — send the halo rows, write the received ones."""
-        if self.comm.world == 1:
+        if self.comm.local:
             return
         got = self.comm.all_to_all(i_out[self.n:self.n + self.n_halo], self.send_counts,
                                    self.recv_counts)
@@ -557,7 +561,8 @@ def pack_payload(cols: dict, n: int):
     parts = []
     for name, width, code in _payload_columns():
         t = cols[name].reshape(n, width).contiguous()
-        parts.append(t.view(torch.uint8).reshape(n, -1))
+        # explicit row width: a shard may send no rows at all
+        parts.append(t.view(torch.uint8).reshape(n, width * t.element_size()))
     return torch.cat(parts, 1) if parts else None
 
 
@@ -568,7 +573,12 @@ def unpack_payload(p):
     for name, width, code in _payload_columns():
         dt = _torch_dtype(code)
         nb = width * torch.empty((), dtype=dt).element_size()
-        t = p[:, c:c + nb].contiguous().view(dt)
+        if p.shape[0] == 0:  # no rows (a view of 0 bytes cannot change dtype)
+            t = torch.empty((0, width), dtype=dt, device=p.device)
+        else:
+            # through 1-D: a single row counts as contiguous whatever its
+            # stride, and a dtype view needs the row stride to divide
+            t = p[:, c:c + nb].contiguous().view(-1).view(dt).reshape(p.shape[0], width)
         c += nb
         out[name] = t if width > 1 else t.reshape(-1)
     return out
@@ -672,7 +682,7 @@ class ShardedPathGraph:
         else:
             for name, _, _ in _payload_columns():
                 own[name][lr] = cols[name][li]
-        if world > 1:
+        if not comm.local:
             ri = torch.nonzero(~keep).reshape(-1)
             ds = dest_shard[ri]
             order = torch.argsort(ds, stable=True)
@@ -754,7 +764,7 @@ class ShardedPathGraph:
         red_i = _view(v.red, ((iterations + 1) * 8,), "<i4")
         for t in range(iterations):
             N.check(lib.vpg_solve_step(self.handle, t, stream))
-            if self.comm.world > 1:
+            if not self.comm.local:
                 i_out = _view(v.ibuf[(t + 1) & 1], (rows, 4), "<f4")
                 self.halo.exchange(i_out)
                 self.comm.all_reduce_max_(red_i[t * 8:t * 8 + _RESIDUAL_WORDS])

@@ -157,3 +157,47 @@ def test_sharded_render_pg_config_features(cuda):
             open(os.path.join(d, "res_single.csv")).read()
         assert open(os.path.join(d, "dump_sharded.vpgr"), "rb").read() == \
             open(os.path.join(d, "dump_single.vpgr"), "rb").read()
+
+
+def _loopback_worker(rank, world, port, name, out_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    try:
+        from paper_2404_11894_b200.pathgraph.sharded import ShardComm, render_pg_sharded
+
+        comm = ShardComm(loopback=True)
+        assert comm.backend == "nccl" and not comm.staged and not comm.local
+        c = CASES[name]
+        out = render_pg_sharded(_scene(name, c["res"]), _config(c), comm)
+        inc, ibar = out.graph.gather_solution()
+        np.savez(out_path, image=out.image, incoming=inc.cpu().numpy(), i_bar=ibar.cpu().numpy(),
+                 residuals=np.array(out.residuals))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["cloud", "c1floor_k4"])
+def test_nccl_collectives_single_rank_loopback(cuda, name):
+    """Every collective of the N > 1 path through NCCL itself (a one-rank
+    NCCL group with the collectives looped back instead of skipped): device
+    tensors in all_to_all_single / all_gather / all_reduce(MAX) of the
+    residual bit patterns, the exclusive scan, the halo exchange -- the
+    result stays bit-identical to render_pg.  (Two NCCL ranks cannot share
+    the one GPU of the test pool.)"""
+    import torch.multiprocessing as mp
+
+    ref = _single(name)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "loopback.npz")
+        mp.spawn(_loopback_worker, args=(1, _free_port(), name, path), nprocs=1, join=True)
+        got = dict(np.load(path))
+    np.testing.assert_array_equal(got["image"], ref.image)
+    np.testing.assert_array_equal(got["incoming"], ref.result.incoming)
+    np.testing.assert_array_equal(got["i_bar"], ref.result.i_bar)
+    np.testing.assert_array_equal(got["residuals"], np.array(ref.result.residuals))

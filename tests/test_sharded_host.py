@@ -238,3 +238,26 @@ def test_exclusive_scan_of_group_sizes(world):
     mp.spawn(_scan_worker, args=(world, _free_port(), q), nprocs=world, join=True)
     res = [q.get() for _ in range(world)]
     assert all(not bad for _, bad in res), res
+
+
+@pytest.mark.parametrize("n", [0, 1, 7])
+def test_record_payload_round_trip(n):
+    """The byte payload the owner all-to-all moves: every column's bytes back
+    exactly, including a shard that sends no rows."""
+    import torch
+
+    from paper_2404_11894_b200.pathgraph.sharded import (_payload_columns, _torch_dtype,
+                                                          pack_payload, unpack_payload)
+
+    g = torch.Generator().manual_seed(n)
+    cols = {}
+    for name, width, code in _payload_columns():
+        dt = _torch_dtype(code)
+        shape = (n, width) if width > 1 else (n,)
+        if dt.is_floating_point:
+            cols[name] = torch.randn(shape, generator=g, dtype=dt)
+        else:
+            cols[name] = torch.randint(0, 100, shape, generator=g).to(dt)
+    back = unpack_payload(pack_payload(cols, n))
+    for name, width, _ in _payload_columns():
+        assert torch.equal(back[name].reshape(cols[name].shape), cols[name]), name
