@@ -576,9 +576,10 @@ def unpack_payload(p):
         if p.shape[0] == 0:  # no rows (a view of 0 bytes cannot change dtype)
             t = torch.empty((0, width), dtype=dt, device=p.device)
         else:
-            # through 1-D: a single row counts as contiguous whatever its
-            # stride, and a dtype view needs the row stride to divide
-            t = p[:, c:c + nb].contiguous().view(-1).view(dt).reshape(p.shape[0], width)
+            # a fresh copy: a single row counts as contiguous whatever its
+            # stride and offset, and a dtype view needs both aligned
+            t = p[:, c:c + nb].clone(memory_format=torch.contiguous_format)
+            t = t.view(-1).view(dt).reshape(p.shape[0], width)
         c += nb
         out[name] = t if width > 1 else t.reshape(-1)
     return out
