@@ -514,8 +514,14 @@ __host__ __device__ constexpr int visit_cell(int v) {
     case 23: return 18; case 24: return 20; case 25: return 24; default: return 26;
   }
 }
-__constant__ uint8_t kVisitOrder[27] = {13, 4,  10, 12, 14, 16, 22, 1, 3,  5,  7,  9,  11, 15,
-                                        17, 19, 21, 23, 25, 0,  2,  6, 8, 18, 20, 24, 26};
+// the same order for runtime indices
+#define VPG_V(i) uint8_t(visit_cell(i))
+__constant__ uint8_t kVisitOrder[27] = {
+    VPG_V(0),  VPG_V(1),  VPG_V(2),  VPG_V(3),  VPG_V(4),  VPG_V(5),  VPG_V(6),
+    VPG_V(7),  VPG_V(8),  VPG_V(9),  VPG_V(10), VPG_V(11), VPG_V(12), VPG_V(13),
+    VPG_V(14), VPG_V(15), VPG_V(16), VPG_V(17), VPG_V(18), VPG_V(19), VPG_V(20),
+    VPG_V(21), VPG_V(22), VPG_V(23), VPG_V(24), VPG_V(25), VPG_V(26)};
+#undef VPG_V
 constexpr int kNearCells = 7;   // home + faces: always scanned
 #ifndef VPG_ASSIGN_CAND
 #define VPG_ASSIGN_CAND 240
