@@ -921,7 +921,11 @@ __global__ void __launch_bounds__(128, VPG_TRACE_MINB) k_trace_paths(const vpg_s
 // A lane whose path ends starts its next path at once (the loop advances
 // every lane by one bounce per iteration), so lanes do not idle until the
 // longest path of their warp has finished.
-__global__ void __launch_bounds__(128, VPG_TRACE_MINB) k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
+#ifndef VPG_TRACE_BLOCK
+#define VPG_TRACE_BLOCK 128
+#endif
+__global__ void __launch_bounds__(VPG_TRACE_BLOCK, VPG_TRACE_MINB * 128 / VPG_TRACE_BLOCK)
+k_trace_capture(const vpg_scene sc, const vpg_trace_cfg cfg,
                                                        int64_t* __restrict__ counts,
                                                        const vpg_records scratch,
                                                        const vpg_paths pth, Capture cap) {
@@ -1179,10 +1183,11 @@ void trace_capture(const vpg_scene& sc, const vpg_trace_cfg& cfg, double* scratc
   // first frees, late (C4: 168 ms with one wave, 189 with two)
   int per_sm = 0;
   VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, reinterpret_cast<const void*>(k_trace_capture), 128, 0));
+      &per_sm, reinterpret_cast<const void*>(k_trace_capture), VPG_TRACE_BLOCK, 0));
   const int64_t wave = int64_t(std::max(per_sm, 1)) * sm_count();
-  const int grid = int(std::min<int64_t>(wave, (cfg.path_count + 127) / 128));
-  VPG_LAUNCH(k_trace_capture, std::max(grid, 1), 128, 0, s, sc, cfg, counts, vpg_records{}, pth,
+  const int grid =
+      int(std::min<int64_t>(wave, (cfg.path_count + VPG_TRACE_BLOCK - 1) / VPG_TRACE_BLOCK));
+  VPG_LAUNCH(k_trace_capture, std::max(grid, 1), VPG_TRACE_BLOCK, 0, s, sc, cfg, counts, vpg_records{}, pth,
              Capture{counter, capacity, scratch});
 }
 
