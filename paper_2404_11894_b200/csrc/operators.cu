@@ -127,6 +127,13 @@ __device__ __forceinline__ float w_recomputed(const float4* __restrict__ rows, i
 //    to HBM, with the residual maxima of solve.py:54-61.  The old I[par] is
 //    recomputed from the previous W*I (same arithmetic as when it was stored)
 //    instead of gathered.
+#ifndef VPG_SOLVE_UNROLL1
+#define VPG_SOLVE_UNROLL1 4  // column loop, one row per lane
+#endif
+#ifndef VPG_SOLVE_UNROLL2
+#define VPG_SOLVE_UNROLL2 2  // column loop, two rows per lane
+#endif
+constexpr int kSolveUnroll1 = VPG_SOLVE_UNROLL1, kSolveUnroll2 = VPG_SOLVE_UNROLL2;
 #ifndef VPG_SOLVE_CONSUMERS
 #define VPG_SOLVE_CONSUMERS 24
 #endif
@@ -420,7 +427,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         // one row (anchor ha) over columns j0, j0 + dj, ... < s, times num n
         auto one_row = [&](const float4 ha, float n, int j0, int dj) {
           float3 acc = make_float3(0.f, 0.f, 0.f);
-#pragma unroll 4
+#pragma unroll kSolveUnroll1
           for (int j = j0; j < s; j += dj) {
             const float4 dc = crow[4 * j + 3];
             const float4 ij = sin[rl + j];
@@ -441,7 +448,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
             const float4 ha1 = r1 < s ? crow[4 * r1 + 2] : z4;
             const float n0 = hg_num_f32(ha0.w), n1 = hg_num_f32(ha1.w);
             float3 acc0 = make_float3(0.f, 0.f, 0.f), acc1 = acc0;
-#pragma unroll 2
+#pragma unroll kSolveUnroll2
             for (int j = 0; j < s; ++j) {
               const float4 dc = crow[4 * j + 3];
               const float4 ij = sin[rl + j];
