@@ -304,6 +304,11 @@ struct Best {
   double d2;
   int j;
 };
+// a point sent on to the exact fallback, with its best over the 27 cells
+struct FbEntry {
+  double d2;
+  int32_t i, j;
+};
 __device__ __forceinline__ void best_update(Best& b, double d2, int j) {
   if (d2 < b.d2 || (d2 == b.d2 && j < b.j)) {
     b.d2 = d2;
@@ -570,7 +575,7 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
                const int32_t* __restrict__ sorted_ids, int oct_in_ids,
                const int32_t* __restrict__ run_start, const int32_t* __restrict__ run_len,
                const int32_t* __restrict__ n_runs, int32_t* __restrict__ assign,
-               int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
+               FbEntry* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
   constexpr unsigned kFull = 0xFFFFFFFFu;
   constexpr float kMargin = 1e-4f;  // cells
   extern __shared__ __align__(16) unsigned char assign_smem[];
@@ -761,7 +766,7 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
         visit(__reduce_or_sync(kFull, need) & nonempty);
         if (active) {
           if (best.j == 0x7FFFFFFF || !(__dsqrt_rn(best.d2) < gp.cell)) {
-            fb_list[atomicAdd(fb_count, 1)] = i;
+            fb_list[atomicAdd(fb_count, 1)] = FbEntry{best.d2, i, best.j};
             assign[i] = -1;
           } else {
             assign[i] = best.j;
@@ -795,7 +800,7 @@ __device__ __forceinline__ void warp_best(Best& b) {
 __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
                                   const double* __restrict__ pos, GridParams gp,
                                   CellIndex table, const double4* __restrict__ spos,
-                                  const int32_t* __restrict__ fb_list, const int32_t* fb_count,
+                                  const FbEntry* __restrict__ fb_list, const int32_t* fb_count,
                                   int32_t* __restrict__ assign, int32_t* __restrict__ far_list,
                                   int32_t* __restrict__ far_count,
                                   unsigned long long* __restrict__ far_d,
@@ -804,17 +809,15 @@ __global__ void k_assign_fallback(const int32_t* rows, int64_t row_off,
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *fb_count;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
-    const int64_t i = fb_list[w];
+    const FbEntry e = fb_list[w];
+    const int64_t i = e.i;
     const int64_t r = class_row(rows, row_off, i);
     const double px = pos[r * 3], py = pos[r * 3 + 1], pz = pos[r * 3 + 2];
     const long long cx = cell_coord(px, gp.lo[0], gp.cell);
     const long long cy = cell_coord(py, gp.lo[1], gp.cell);
     const long long cz = cell_coord(pz, gp.lo[2], gp.cell);
-    Best b{INFINITY, 0x7FFFFFFF};
-    if (lane < 27)
-      scan_cell(gp, table, spos, cx + lane / 9 - 1, cy + (lane / 3) % 3 - 1, cz + lane % 3 - 1,
-                px, py, pz, b);
-    warp_best(b);
+    // the 27 cells' best, as k_assign_cells found it
+    Best b{e.d2, e.j};
     bool resolved = false;
     long long spent = 27;  // cells enumerated; beyond kShellBudget the tiled scan is cheaper
     for (int R = 1;; ++R) {
@@ -1707,7 +1710,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   int32_t* grp_rec = scratch_of<int32_t>(s, "grp_rec", n);
   int32_t* assign_all = scratch_of<int32_t>(s, "assign", n);
   int32_t* values = scratch_of<int32_t>(s, "values", n);
-  int32_t* fb_list = scratch_of<int32_t>(s, "fb_list", n);
+  FbEntry* fb_list = scratch_of<FbEntry>(s, "fb_list", n);
   DBuf<int32_t> counts_all(center_total, s), crec_all(center_total, s), gstart_all(center_total, s);
   DBuf<int32_t> ne_prefix_all(center_total + 1, s);
   DBuf<int32_t> scalars(4, s);  // fb count, n_runs, n_over
@@ -2450,7 +2453,7 @@ int64_t assign_nearest(const double* pos, int64_t n, const double* cpos, int m, 
   DBuf<int32_t> scalars(4, s);
   DBuf<int32_t> far_count(1, s);
   VPG_CUDA(cudaMemsetAsync(scalars.get(), 0, scalars.bytes(), s));
-  int32_t* fb_list = scratch_of<int32_t>(s, "an_fb_list", n + 1);
+  FbEntry* fb_list = scratch_of<FbEntry>(s, "an_fb_list", n + 1);
   const PointCells pc = sort_points_by_cell(nullptr, 0, n, pos, gp, scalars.get() + 1, "an_", s);
   DBuf<unsigned long long> keys(m, s), skeys(m, s);
   DBuf<int32_t> ids(m, s), sids(m, s);
