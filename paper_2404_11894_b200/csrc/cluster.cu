@@ -103,6 +103,10 @@ __device__ __forceinline__ uint64_t table_slot(uint64_t key, uint64_t mask) {
 
 __global__ void k_class_bitmap(const uint8_t* __restrict__ kind, const int32_t* __restrict__ cls,
                                int64_t n, uint32_t* bitmap, int32_t* err) {
+  // a thread sets a class's bit only when its slot differs from the last
+  // one it saw, and only while the bit is still clear (the few classes would
+  // otherwise serialise every warp on one word)
+  uint32_t last = ~0u;
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
        r += int64_t(gridDim.x) * blockDim.x) {
     const int k = kind[r];
@@ -112,12 +116,10 @@ __global__ void k_class_bitmap(const uint8_t* __restrict__ kind, const int32_t* 
       continue;
     }
     const uint32_t slot = uint32_t(k * kSlotsPerKind + c);
-    const unsigned peers = __match_any_sync(__activemask(), slot);
-    // one lane per distinct class, and only while its bit is still clear (the
-    // few classes would otherwise serialise every warp on one word)
+    if (slot == last) continue;
+    last = slot;
     const uint32_t bit = 1u << (slot & 31);
-    if ((__ffs(peers) - 1) == int(threadIdx.x & 31) &&
-        !(*reinterpret_cast<volatile uint32_t*>(&bitmap[slot >> 5]) & bit))
+    if (!(*reinterpret_cast<volatile uint32_t*>(&bitmap[slot >> 5]) & bit))
       atomicOr(&bitmap[slot >> 5], bit);
   }
 }
