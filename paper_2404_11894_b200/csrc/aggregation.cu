@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256, VPG_PACK_MINB) k_pack_members(vpg_records
     const int64_t r = list ? int64_t(list[i]) : off + i;
     const int32_t q = clpos[r];
     if (q < 0) continue;
+    VPG_CHECK(q < n);
     Member m;
     const bool volume = rec.kind[r] == 0;
     if (volume) {

@@ -631,6 +631,7 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
         const int first = __shfl_sync(kFull, incl - c_cnt, v);
         const int from = __shfl_sync(kFull, c_start, v) + (idx - first);
         if (t >= cnt) continue;
+        VPG_CHECK(t < kCandCap && v < 27 && from >= 0);
         double4 c = spos[from];
         if (!gp.packed) {
           const int k = kVisitOrder[v];
@@ -671,6 +672,7 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
           if (pass == 1) {
             const unsigned peers = __match_any_sync(kFull, o);
             const int at = __shfl_sync(kFull, base, o & 7) + __popc(peers & ((1u << lane) - 1u));
+            VPG_CHECK(o == 8 || (at >= 0 && at < seg));
             if (o < 8) run_ids[at] = id;
           }
 #pragma unroll
@@ -725,6 +727,7 @@ k_assign_cells(const int32_t* rows, int64_t row_off, const double* __restrict__ 
             cells &= cells - 1;
             const int kb = __shfl_sync(kFull, c_first, v), kc = __shfl_sync(kFull, c_cnt, v);
             if (staged) {
+              VPG_CHECK(kb >= 0 && kb + kc <= total && total <= kCandCap);
               scan(kb, kc);
             } else {
               for (int t0 = 0; t0 < kc; t0 += kCandCap) {

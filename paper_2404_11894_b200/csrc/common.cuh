@@ -41,6 +41,26 @@ void prof_end(int token, cudaStream_t s);
     if (!(cond)) throw ::vpg::Error((code), (msg));  \
   } while (0)
 
+// Device-side bounds checks, compiled in only for the checked build
+// (python tools/build_variant.py checked -DVPG_CHECKED, then the GPU tests
+// with VPG_LIB_VARIANT=checked): compute-sanitizer is not available on the
+// GPU pool, so the kernels assert their own index ranges there.  A failed
+// check prints the condition and traps (the test's launch then errors).
+#ifdef VPG_CHECKED
+#define VPG_CHECK(cond)                                                                    \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("VPG_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             int(blockIdx.x), int(threadIdx.x));                                          \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define VPG_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // Launch wrapper: counts the launch and surfaces configuration errors.
 #define VPG_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
   do {                                                                     \

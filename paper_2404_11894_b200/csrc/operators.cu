@@ -393,6 +393,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         // row, each summing every P-th column, combined by xor shuffles.
         const int rl = mk.x;
         const int s = mk.z;
+        VPG_CHECK(rl >= 0 && s >= 1 && rl + s <= R);  // the cluster's rows are staged
         const int64_t q0 = int64_t(cq0) + rl;
         const float4* crow = srow + 4 * rl;
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -494,6 +495,7 @@ k_solve_iter(const int4* __restrict__ desc, const int4* __restrict__ meta,
         // stored W block (Lambertian / |g| > 0.95 clusters), lane = row
         const int rl = mk.x;
         const int s = mk.z;
+        VPG_CHECK(rl >= 0 && rl + s <= R && mk.y >= 0 && int64_t(mk.y) + int64_t(s) * s <= wc);
         const int64_t q0 = int64_t(cq0) + rl;
         const float* w = wbase + mk.y;
         const float4* crow = srow + 4 * rl;

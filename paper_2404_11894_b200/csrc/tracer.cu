@@ -1002,7 +1002,9 @@ k_gather_records(const double* __restrict__ aos, int64_t n, const int32_t* __res
         int j = lane;
         while (j > 0 && __double_as_longlong(b[(j - 1) * kSlotStride + kFPath]) == pid) --j;
         if (j == 0 && base > 0 && slot_path(aos, slot_of, base - 1) == pid) {
-          listed[atomicAdd(n_listed, 1)] = int32_t(base + lane);
+          const int li = atomicAdd(n_listed, 1);
+          VPG_CHECK(li <= (n + 31) / 32);  // at most one listed path per window
+          listed[li] = int32_t(base + lane);
         } else {
           double in[3] = {0.0, 0.0, 0.0};
           for (int row = lane; row >= j; --row) {
