@@ -1468,12 +1468,12 @@ PointCells sort_points_by_cell(const int32_t* rows_p, int64_t row_off, int64_t n
     if (n < (int64_t(1) << kOctShift)) poct = scratch_of<uint8_t>(s, (tag + "cell_oct").c_str(), n);
     pc.oct_in_ids = poct != nullptr;
     VPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nc + 1), s));
-    VPG_LAUNCH(k_cell_count, grid_for(n, block), block, 0, s, rows_p, row_off, n, pos, gp, counts,
+    VPG_LAUNCH(k_cell_count, grid_for(n, block, 1 << 30), block, 0, s, rows_p, row_off, n, pos, gp, counts,
                pkey, poct);
     cub_call([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, counts, offs, int(nc + 1), s);
     }, s);
-    VPG_LAUNCH(k_cell_scatter, grid_for(n, block), block, 0, s, n, pkey, poct, offs, counts,
+    VPG_LAUNCH(k_cell_scatter, grid_for(n, block, 1 << 30), block, 0, s, n, pkey, poct, offs, counts,
                pc.pids_sorted);
     int32_t* sel = reinterpret_cast<int32_t*>(pkeys_sorted);
     cub::CountingInputIterator<int32_t> ci(0);
@@ -1922,7 +1922,7 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
                                                end_bit, s);
       }, s);
     }
-    VPG_LAUNCH(k_histogram, grid_for(p.n, block), block, 0, s, assign_c, p.n, counts_c);
+    VPG_LAUNCH(k_histogram, grid_for(p.n, block, 1 << 30), block, 0, s, assign_c, p.n, counts_c);
     cub_call([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, counts_c, gstart_c, m, s);
     }, s);

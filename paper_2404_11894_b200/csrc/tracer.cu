@@ -1275,7 +1275,7 @@ void scatter_records(const double* scratch, int64_t n, const int64_t* rec_start,
   if (n <= 0) return;
   VPG_REQUIRE(n < (int64_t(1) << 31), VPG_ELIMIT, "more than 2^31 records per trace");
   int32_t* slot_of = scratch_of<int32_t>(s, "slot_of_row", size_t(n));
-  VPG_LAUNCH(k_slot_of_row, grid_for(n, 256), 256, 0, s, scratch, n, rec_start, path_begin,
+  VPG_LAUNCH(k_slot_of_row, grid_for(n, 256, 1 << 30), 256, 0, s, scratch, n, rec_start, path_begin,
              slot_of);
   const int64_t max_listed = (n + 31) / 32 + 1;
   int32_t* listed = scratch_of<int32_t>(s, "sweep_listed", size_t(max_listed) + 1);
