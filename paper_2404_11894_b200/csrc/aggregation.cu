@@ -683,6 +683,24 @@ __global__ void k_cluster_meta(const int64_t* __restrict__ cst, const int64_t* _
 
 size_t member_bytes() { return sizeof(Member); }
 
+// Whether any record would put its cluster in a stored-W mode (k_aggregate's
+// kSurface / kVol64: a surface record, or |g| > kG32); the build then
+// reserves no W-block storage when none does (19 GB at C4).
+__global__ void k_needs_stored_w(const uint8_t* __restrict__ kind, const double* __restrict__ g,
+                                 int64_t n, int32_t* __restrict__ flag) {
+  bool any = false;
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x)
+    any |= kind[r] != 0 || fabs(g[r]) > double(kG32);
+  if (__any_sync(0xFFFFFFFFu, any) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+void launch_needs_stored_w(const vpg_records& rec, int32_t* flag, cudaStream_t s) {
+  VPG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+  if (rec.n > 0)
+    VPG_LAUNCH(k_needs_stored_w, grid_for(rec.n, 256), 256, 0, s, rec.kind, rec.g, rec.n, flag);
+}
+
 void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s) {
   const int64_t n = g->n;
   g->wt.alloc(size_t(wt_capacity > 0 ? wt_capacity : 1), s);

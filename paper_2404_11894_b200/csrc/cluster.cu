@@ -1676,6 +1676,18 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   VPG_LAUNCH(k_class_stats, grid_for(n, block, sm_count() * 4), block, 0, s, rec.kind,
              rec.class_id, rec.pos, n, d_slots.get(), n_cls, cls_idx.get(), stats.get(),
              stats.get() + n_cls, stats.get() + 4 * n_cls);
+  // whether any cluster can store a W block (only when the record fields
+  // are already resident: with an upload in flight, g is not there yet and
+  // the full reservation stays)
+  DBuf<int32_t> needs_w_dev;
+  int32_t needs_w = 1;
+  if (with_ops && !fields_ready) {
+    needs_w_dev.alloc(1, s);
+    launch_needs_stored_w(rec, needs_w_dev.get(), s);
+    // (to pageable memory: returns once the copy has completed)
+    VPG_CUDA(cudaMemcpyAsync(&needs_w, needs_w_dev.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    count_transfer(0, sizeof(int32_t));
+  }
   std::vector<unsigned long long> h_stats;
   to_host(h_stats, stats.get(), n_cls * 7, s);
 
@@ -1745,8 +1757,10 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
   g->w_off = std::move(a_w);
   void* members = nullptr;
   if (with_ops) {
-    // kernel blocks: sum of pad4(s^2) <= 2K * N + 3 per cluster
-    const int64_t wt_cap = std::min<int64_t>(max_size, n) * n + 4 * (center_total + n) + 16;
+    // kernel blocks: sum of pad4(s^2) <= 2K * N + 3 per cluster, when any
+    // cluster stores one
+    const int64_t wt_cap =
+        needs_w ? std::min<int64_t>(max_size, n) * n + 4 * (center_total + n) + 16 : 16;
     alloc_operator_buffers(g, wt_cap, s);
     members = scratch(s, "members", member_bytes() * size_t(n) + 256);
   }

@@ -152,6 +152,8 @@ void build_graph(vpg_graph* g, const vpg_records& rec, int32_t K, vpg_pcg64* rng
 // aggregation.cu
 size_t member_bytes();
 void alloc_operator_buffers(vpg_graph* g, int64_t wt_capacity, cudaStream_t s);
+// *flag (device) = 1 when some record needs a stored W block (surface, |g| > kG32)
+void launch_needs_stored_w(const vpg_records& rec, int32_t* flag, cudaStream_t s);
 void pack_members(vpg_graph* g, const vpg_records& rec, const int32_t* list, int64_t list_n,
                   int64_t off, void* members, cudaStream_t s, const uint8_t* has_child = nullptr);
 void aggregate_range(vpg_graph* g, const void* members, const int64_t* range, int64_t max_count,
