@@ -865,7 +865,17 @@ void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t*
     VPG_LAUNCH(k_cluster_of_rows, grid_for(m, block), block, 0, s, g->cl_off.get(), m,
                g->cluster_id.get());
   }
-  alloc_operator_buffers(g, std::max<int64_t>(w, 1), s);
+  // W-block storage only when some record can need a stored block (as in
+  // the single-GPU build)
+  int32_t needs_w = 0;
+  if (n > 0) {
+    int32_t* flag = scratch_of<int32_t>(s, "needs_w", 1);
+    launch_needs_stored_w(rec, flag, s);
+    VPG_CUDA(cudaMemcpyAsync(&needs_w, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    count_transfer(0, sizeof(int32_t));
+    VPG_CUDA(cudaStreamSynchronize(s));
+  }
+  alloc_operator_buffers(g, needs_w ? std::max<int64_t>(w, 1) : 16, s);
   if (n > 0) {
     void* members = scratch(s, "members", member_bytes() * size_t(n) + 256);
     pack_members(g, rec, nullptr, n, 0, members, s, has_child);
