@@ -803,6 +803,18 @@ void finalize_chunks(vpg_graph* g, cudaStream_t s) {
              g->chunk_first.get(), g->cl_off.get(), g->cl_mode.get(), g->cl_meta.get());
 }
 
+struct PadSquare {  // a cluster's padded kernel block, pad4(s^2) floats
+  __host__ __device__ int64_t operator()(int32_t sz) const {
+    return (int64_t(sz) * sz + 3) & ~int64_t(3);
+  }
+};
+struct Square {
+  __host__ __device__ int64_t operator()(int32_t sz) const { return int64_t(sz) * sz; }
+};
+struct Widen {
+  __host__ __device__ int64_t operator()(int32_t sz) const { return int64_t(sz); }
+};
+
 void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t* cl_size_host,
                  const int32_t* parent, const uint8_t* has_child, int64_t n_halo,
                  const double* halo_ipt, cudaStream_t s) {
@@ -813,25 +825,53 @@ void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t*
   g->n = n;
   g->m = m;
   g->n_halo = n_halo;
-  // host cluster geometry: offsets, padded kernel-block offsets, sizes
-  std::vector<int32_t> off(m + 1), size(m + 1, 0);
-  std::vector<int64_t> woff(m + 1);
-  int64_t q = 0, w = 0, nnz = 0;
-  int32_t smax = 0;
-  for (int64_t k = 0; k < m; ++k) {
-    const int32_t sz = cl_size_host[k];
-    VPG_REQUIRE(sz >= 1, VPG_EINVAL, "empty cluster in a shard-local partition");
-    off[k] = int32_t(q);
-    size[k] = sz;
-    woff[k] = w;
-    q += sz;
-    w += (int64_t(sz) * sz + 3) & ~int64_t(3);
-    nnz += int64_t(sz) * sz;
-    smax = std::max(smax, sz);
+  // cluster geometry on the device from the sizes: offsets, padded
+  // kernel-block offsets, nnz, the largest and smallest cluster
+  g->cl_off.alloc(m + 1, s);
+  g->cl_size.alloc(m + 1, s);
+  g->w_off.alloc(m + 1, s);
+  VPG_CUDA(cudaMemsetAsync(g->cl_size.get(), 0, sizeof(int32_t) * (m + 1), s));
+  if (m > 0)
+    VPG_CUDA(cudaMemcpyAsync(g->cl_size.get(), cl_size_host, sizeof(int32_t) * m,
+                             cudaMemcpyHostToDevice, s));
+  count_transfer(4 * m, 0);
+  int64_t* geo = scratch_of<int64_t>(s, "local_geometry", 8);  // nnz, smax, smin
+  {
+    const int32_t* sz = g->cl_size.get();
+    cub::TransformInputIterator<int64_t, PadSquare, const int32_t*> pads(sz, PadSquare{});
+    cub::TransformInputIterator<int64_t, Square, const int32_t*> sqs(sz, Square{});
+    cub::TransformInputIterator<int64_t, Widen, const int32_t*> wide(sz, Widen{});
+    size_t b0 = 0, b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b0, sz, g->cl_off.get(), int(m + 1), s));
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b1, pads, g->w_off.get(), int(m + 1), s));
+    VPG_CUDA(cub::DeviceReduce::Sum(nullptr, b2, sqs, geo, int(std::max<int64_t>(m, 1)), s));
+    VPG_CUDA(cub::DeviceReduce::Max(nullptr, b3, wide, geo + 1, int(std::max<int64_t>(m, 1)), s));
+    VPG_CUDA(cub::DeviceReduce::Min(nullptr, b4, wide, geo + 2, int(std::max<int64_t>(m, 1)), s));
+    const size_t bytes = std::max({b0, b1, b2, b3, b4});
+    void* tmp = scratch(s, "cub_temp", bytes + 256);
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b0, sz, g->cl_off.get(), int(m + 1), s));
+    VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b1, pads, g->w_off.get(), int(m + 1), s));
+    if (m > 0) {
+      VPG_CUDA(cub::DeviceReduce::Sum(tmp, b2, sqs, geo, int(m), s));
+      VPG_CUDA(cub::DeviceReduce::Max(tmp, b3, wide, geo + 1, int(m), s));
+      VPG_CUDA(cub::DeviceReduce::Min(tmp, b4, wide, geo + 2, int(m), s));
+    } else {
+      VPG_CUDA(cudaMemsetAsync(geo, 0, 3 * sizeof(int64_t), s));
+    }
+    count_launch(5);
   }
-  VPG_REQUIRE(q == n, VPG_EINVAL, "cluster sizes do not sum to the shard's row count");
-  off[m] = int32_t(q);
-  woff[m] = w;
+  int64_t h_geo[3] = {0, 0, 0};
+  int32_t h_total = 0;
+  int64_t h_w = 0;
+  VPG_CUDA(cudaMemcpyAsync(h_geo, geo, sizeof(h_geo), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_total, g->cl_off.get() + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  VPG_CUDA(cudaMemcpyAsync(&h_w, g->w_off.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  count_transfer(0, sizeof(h_geo) + 12);
+  VPG_CUDA(cudaStreamSynchronize(s));
+  VPG_REQUIRE(m == 0 || h_geo[2] >= 1, VPG_EINVAL, "empty cluster in a shard-local partition");
+  VPG_REQUIRE(int64_t(h_total) == n, VPG_EINVAL, "cluster sizes do not sum to the shard's row count");
+  const int64_t nnz = h_geo[0], w = h_w;
+  const int32_t smax = int32_t(h_geo[1]);
   g->nnz = nnz;
   g->wt_len = w;
   g->max_cluster = smax;
@@ -843,17 +883,7 @@ void build_local(vpg_graph* g, const vpg_records& rec, int64_t m, const int32_t*
   g->perm.alloc(n + 1, s);
   g->clpos.alloc(n + 1, s);
   g->cluster_id.alloc(n + 1, s);
-  g->cl_off.alloc(m + 1, s);
-  g->cl_size.alloc(m + 1, s);
-  g->w_off.alloc(m + 1, s);
   for (auto* v : {&g->cl_center, &g->ref_of, &g->internal_of}) v->alloc(m + 1, s);
-  VPG_CUDA(cudaMemcpyAsync(g->cl_off.get(), off.data(), sizeof(int32_t) * (m + 1),
-                           cudaMemcpyHostToDevice, s));
-  VPG_CUDA(cudaMemcpyAsync(g->cl_size.get(), size.data(), sizeof(int32_t) * (m + 1),
-                           cudaMemcpyHostToDevice, s));
-  VPG_CUDA(cudaMemcpyAsync(g->w_off.get(), woff.data(), sizeof(int64_t) * (m + 1),
-                           cudaMemcpyHostToDevice, s));
-  count_transfer(16 * (m + 1), 0);
   if (n > 0) {
     VPG_LAUNCH(k_iota32, grid_for(n, block), block, 0, s, g->perm.get(), n);
     VPG_LAUNCH(k_iota32, grid_for(n, block), block, 0, s, g->clpos.get(), n);
